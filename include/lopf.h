@@ -1,0 +1,189 @@
+/*
+ * lopf.h — C ABI of the B200-native solver-free consensus ADMM for linearized,
+ * multi-phase, unbalanced distribution OPF (arXiv 2310.09410, Ryu / Byeon / Kim).
+ *
+ * The library (paper_2310_09410_b200/liblopf.so) exposes the two calls the method
+ * needs — a setup call and a solve call — plus getters for parity checking:
+ *
+ *   lopf_setup   CPU, once: validate the network (Table I), assemble
+ *                the linearized OPF LP (eqs. (2)-(5)), decompose it
+ *                component-wise with leaf merging into subsystems
+ *                (A_s, b_s) and 0-1 maps B_s, and precompute
+ *                Abar_s = A_s^T (A_s A_s^T)^-1 A_s - I and bbar_s = A_s^T (A_s A_s^T)^-1 b_s
+ *                (closed_2; Algorithm 1 lines 2-3) and pack them for
+ *                the device.
+ *   lopf_bind    copy the packed problem host -> device into a caller-owned arena.
+ *   lopf_solve   Algorithm 1 on the GPU until (termination)
+ *                 or max_iter: global update closed_1 (PAPER.md:305-310,
+ *                rho restored — DESIGN.md reading C1), local update closed_2, dual update
+ *                ADMM-3, residuals; no host synchronisation per iteration.
+ *   lopf_run     exactly k iterations (the termination test optional) — fixed-K parity.
+ *
+ * Conventions
+ *   - All arrays in / out are plain host pointers unless stated "device".  Setup copies
+ *     every input, so the caller may free its arrays as soon as lopf_setup returns.
+ *   - Phases: bitmask a = 1, b = 2, c = 4.  Per-phase arrays have 3 slots [.. * 3]
+ *     (slot 0 = phase a); slots of absent phases are ignored.  3x3 impedance blocks are
+ *     row-major [.. * 9].
+ *   - Output arrays are caller-allocated and sized from lopf_sizes_get(); everything
+ *     is in CANONICAL order (reading C12); internal device layouts never leak.
+ *   - Device memory: one caller-owned region (e.g. a torch uint8 CUDA tensor) of at least
+ *     lopf_sizes.device_bytes bytes, 256-byte aligned; the library sub-allocates it and
+ *     never frees it.  Streams are cudaStream_t passed as void* (0 = legacy default).
+ *   - No exceptions cross the ABI.  Every call returns a lopf_status; on error
+ *     lopf_last_error() (thread-local) describes it, naming the offending component or
+ *     subsystem.  Reaching max_iter is an OUTCOME (LOPF_MAX_ITER), not an error.
+ *   - A handle is not thread-safe; distinct handles are independent.
+ */
+#ifndef LOPF_H
+#define LOPF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOPF_ABI_VERSION 1
+
+typedef struct lopf_handle lopf_handle;
+
+typedef enum {
+    LOPF_OK = 0,
+    LOPF_E_ARG = 1,            /* bad option / null pointer / size mismatch */
+    LOPF_E_NETWORK = 2,        /* network validation failed */
+    LOPF_E_ORPHAN = 3,         /* a global variable belongs to no subsystem (nu_i = 0) */
+    LOPF_E_INFEASIBLE_SUB = 4, /* a subsystem's equality rows are inconsistent */
+    LOPF_E_RANK = 5,           /* A_s A_s^T not positive definite even after row reduction */
+    LOPF_E_CUDA = 6,           /* CUDA runtime error (message has the CUDA error string) */
+    LOPF_E_NCCL = 7,           /* reserved: multi-GPU partitioned mode */
+    LOPF_E_NUMERIC = 8,        /* non-finite residual detected on the device */
+    LOPF_E_STATE = 9           /* call out of order (e.g. solve before bind) */
+} lopf_status;
+
+typedef enum { LOPF_CONVERGED = 0, LOPF_MAX_ITER = 2 } lopf_outcome;   /* SPEC.md:393 exit codes 0 / 2 */
+
+/* Network, structure of arrays (Table I).  All pointers host, caller-owned. */
+typedef struct {
+    int32_t n_bus, n_line, n_gen, n_load, root_bus;
+    const uint8_t *bus_phases;                                      /* [n_bus] */
+    const double *bus_wmin, *bus_wmax, *bus_gsh, *bus_bsh;          /* [n_bus*3]: w bounds, g^sh, b^sh */
+    const int32_t *line_from, *line_to;                             /* [n_line] bus indices (i = from) */
+    const uint8_t *line_phases;                                     /* [n_line] */
+    const double *line_r, *line_x;                                  /* [n_line*9] 3x3 row-major */
+    const double *line_gs_from, *line_bs_from;                      /* [n_line*3] g^s_eij, b^s_eij */
+    const double *line_gs_to, *line_bs_to;                          /* [n_line*3] g^s_eji, b^s_eji */
+    const double *line_tau;                                         /* [n_line*3] tap ratio > 0 */
+    const double *line_pmin, *line_pmax, *line_qmin, *line_qmax;    /* [n_line*3] flow bounds */
+    const int32_t *gen_bus;                                         /* [n_gen] */
+    const uint8_t *gen_phases;                                      /* [n_gen] */
+    const double *gen_pmin, *gen_pmax, *gen_qmin, *gen_qmax;        /* [n_gen*3] */
+    const int32_t *load_bus;                                        /* [n_load] */
+    const uint8_t *load_phases, *load_conn;                         /* [n_load]; conn 0 wye, 1 delta (3-phase only) */
+    const double *load_alpha, *load_beta, *load_a, *load_b;         /* [n_load*3] VDLM-1/2 data */
+} lopf_network;
+
+typedef struct {
+    double rho;            /* penalty rho > 0 (paper default 100) */
+    double eps_rel;        /* relative tolerance > 0 (paper default 1e-3) */
+    int64_t max_iter;      /* >= 0 */
+    int32_t trace_every;   /* 0: no trace; k > 0: record (t, pres, dres, eps_prim, eps_dual) every k sweeps */
+    int32_t trace_cap;     /* rows of trace kept on the device (0 = default 4096) */
+    int32_t single;        /* 1: one subsystem holding every row (S = 1) */
+    int32_t kernel;        /* 0 auto, 1 streaming (operators in HBM/L2), 2 resident (operators in SMEM) */
+    int32_t block_threads; /* 0 = default */
+    int32_t reserved[5];
+} lopf_options;
+
+typedef struct {
+    int64_t S, n, m, n_copies, p_sym, n_tasks, n_slots, device_bytes;
+    int64_t abar_doubles;  /* doubles of the packed operator pool streamed per iteration */
+    int64_t alg_bytes;     /* algorithmic bytes per iteration (DESIGN.md §5 byte model) */
+    int32_t kernel;        /* kernel actually selected (1 streaming, 2 resident) */
+    int32_t grid;          /* CTAs of the persistent launch (known after bind) */
+    int32_t block;         /* threads per CTA */
+    int32_t max_ns, max_ms;
+    int32_t reserved[3];
+} lopf_sizes;
+
+typedef struct {
+    int32_t outcome;       /* lopf_outcome */
+    int32_t reserved0;
+    int64_t iters;         /* sweeps executed, K */
+    double pres, dres, eps_prim, eps_dual;   /* of the last sweep */
+    double objective;      /* c^T x of the last global x */
+    double solve_ms;       /* device time of the iteration launch (CUDA events) */
+} lopf_result;
+
+/* Fill *o with the paper's defaults: rho 100, eps_rel 1e-3, max_iter 1e6. */
+lopf_status lopf_options_default(lopf_options *o);
+
+/* CPU setup (see top of file).  On success *out owns host copies of everything.
+ * Errors: LOPF_E_ARG, LOPF_E_NETWORK, LOPF_E_ORPHAN, LOPF_E_INFEASIBLE_SUB, LOPF_E_RANK. */
+lopf_status lopf_setup(const lopf_network *net, const lopf_options *opt, lopf_handle **out);
+
+lopf_status lopf_sizes_get(const lopf_handle *h, lopf_sizes *sz);
+
+/* Copy the packed problem into the caller's device arena (device pointer, >= device_bytes,
+ * 256-byte aligned) on `stream`, and reset the iterate to the initial point of PAPER.md:495.
+ * May be called again (e.g. to re-upload for an end-to-end timing). */
+lopf_status lopf_bind(lopf_handle *h, void *device_arena, size_t bytes, void *cuda_stream);
+
+/* Reset the device iterate to the initial point (lambda = 0; x_s = 1 / midpoint / 0). */
+lopf_status lopf_reset(lopf_handle *h, void *cuda_stream);
+
+/* Run until (termination) or max_iter, starting from the current device iterate.
+ * Synchronises `stream` once at the end to fill *res. */
+lopf_status lopf_solve(lopf_handle *h, void *cuda_stream, lopf_result *res);
+
+/* Run exactly k sweeps (test = 0) or at most k sweeps stopping at (termination) (test = 1). */
+lopf_status lopf_run(lopf_handle *h, int64_t k, int32_t test, void *cuda_stream, lopf_result *res);
+
+/* Asynchronous variant for CUDA-graph capture / timing: enqueue the solve on `stream`
+ * without synchronising; fetch the result later with lopf_result_get. */
+lopf_status lopf_solve_async(lopf_handle *h, int64_t max_iter, int32_t test, void *cuda_stream);
+lopf_status lopf_result_get(lopf_handle *h, void *cuda_stream, lopf_result *res);
+
+/* Canonical decomposition: kind (0 BUS, 1 LINE, 2 LEAF), comp (bus or line index),
+ * leaf_bus (-1 unless LEAF), m_s, n_s [S]; sub_ptr [S+1] copy offsets; copy_global [n_copies]. */
+lopf_status lopf_get_decomposition(const lopf_handle *h, int32_t *kind, int32_t *comp, int32_t *leaf_bus,
+                                   int32_t *m_s, int32_t *n_s, int64_t *sub_ptr, int32_t *copy_global);
+
+/* Consensus map global -> copies (I_si): row_ptr [n+1], copy_idx [n_copies]. */
+lopf_status lopf_get_consensus(const lopf_handle *h, int64_t *row_ptr, int32_t *copy_idx);
+
+/* Global variable catalog (canonical order) and LP data: role codes 0 pg 1 qg 2 w 3 pb 4 qb
+ * 5 pd 6 qd 7 p_eij 8 q_eij 9 p_eji 10 q_eji; comp; phase slot; c, lo, hi (+-inf allowed). */
+lopf_status lopf_get_globals(const lopf_handle *h, int32_t *role, int32_t *comp, int32_t *phase,
+                             double *c, double *lo, double *hi);
+
+/* Subsystem s's precomputed operator: abar [n_s*n_s] row-major, bbar [n_s]. */
+lopf_status lopf_get_operator(const lopf_handle *h, int64_t s, double *abar, double *bbar);
+
+/* Subsystem s's dense A_s [m_s*n_s] row-major and b_s [m_s] (after any row reduction m_s may shrink;
+ * *m_out receives the row count). */
+lopf_status lopf_get_subsystem(const lopf_handle *h, int64_t s, double *A, double *b, int32_t *m_out);
+
+/* Device iterate -> host (canonical order): x [n] (last global update), x_loc, lam [n_copies].
+ * Any pointer may be NULL.  Synchronous on `stream`. */
+lopf_status lopf_get_state(lopf_handle *h, void *cuda_stream, double *x, double *x_loc, double *lam);
+
+/* Host -> device iterate (canonical order); x_loc, lam [n_copies] (warm start / resume). */
+lopf_status lopf_set_state(lopf_handle *h, void *cuda_stream, const double *x_loc, const double *lam);
+
+/* Trace rows {t, pres, dres, eps_prim, eps_dual} of the last solve: buf [cap*5]. */
+lopf_status lopf_get_trace(lopf_handle *h, void *cuda_stream, double *buf, int64_t cap, int64_t *n_rows);
+
+void lopf_destroy(lopf_handle *h);
+
+/* Thread-local description of the last error (empty string if none). */
+const char *lopf_last_error(void);
+
+/* Library / ABI version (LOPF_ABI_VERSION). */
+int32_t lopf_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOPF_H */

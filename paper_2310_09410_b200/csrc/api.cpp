@@ -1,0 +1,367 @@
+// C ABI of liblopf (include/lopf.h): argument checking, handle lifetime, device arena binding,
+// launch orchestration and canonical-order getters.  No exception crosses this boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "internal.h"
+
+using namespace lopf;
+
+struct lopf_handle {
+    Net net;
+    Canon cp;
+    Layout lay;
+    lopf_options opt{};
+    void* arena = nullptr;
+    size_t arena_bytes = 0;
+    bool bound = false;
+    bool registered = false;
+    int grid = 0;
+    DevProblem dp{};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+static thread_local std::string g_err;
+
+static lopf_status fail(lopf_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+static lopf_status cuda_fail(cudaError_t e, const char* where) {
+    g_err = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+    return LOPF_E_CUDA;
+}
+#define CUDA_TRY(call, where)                      \
+    do {                                           \
+        cudaError_t _e = (call);                   \
+        if (_e != cudaSuccess) return cuda_fail(_e, where); \
+    } while (0)
+
+static constexpr int kMaxGrid = 4096;
+
+extern "C" {
+
+int32_t lopf_abi_version(void) { return LOPF_ABI_VERSION; }
+
+const char* lopf_last_error(void) { return g_err.c_str(); }
+
+lopf_status lopf_options_default(lopf_options* o) {
+    if (!o) return fail(LOPF_E_ARG, "options pointer is NULL");
+    std::memset(o, 0, sizeof(*o));
+    o->rho = 100.0;
+    o->eps_rel = 1e-3;
+    o->max_iter = 1000000; // reading C21
+    o->trace_cap = 4096;
+    return LOPF_OK;
+}
+
+lopf_status lopf_setup(const lopf_network* net, const lopf_options* opt, lopf_handle** out) {
+    g_err.clear();
+    if (!out) return fail(LOPF_E_ARG, "out handle pointer is NULL");
+    *out = nullptr;
+    lopf_options o;
+    if (opt) o = *opt; else lopf_options_default(&o);
+    if (!(o.rho > 0) || !std::isfinite(o.rho)) return fail(LOPF_E_ARG, "rho must be > 0 (SPEC.md:186)");
+    if (!(o.eps_rel > 0) || !std::isfinite(o.eps_rel)) return fail(LOPF_E_ARG, "eps_rel must be > 0 (SPEC.md:186)");
+    if (o.max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
+    if (o.trace_every < 0) return fail(LOPF_E_ARG, "trace_every must be >= 0");
+    if (o.kernel < 0 || o.kernel > 2) return fail(LOPF_E_ARG, "kernel must be 0 (auto), 1 or 2");
+    lopf_handle* h = new (std::nothrow) lopf_handle();
+    if (!h) return fail(LOPF_E_ARG, "out of host memory");
+    h->opt = o;
+    std::string err;
+    try {
+        lopf_status st = copy_network(net, h->net, err);
+        if (st == LOPF_OK) st = build_canon(h->net, h->opt, h->cp, err);
+        if (st == LOPF_OK) st = pack_streaming(h->cp, h->opt, kMaxGrid, h->lay, err);
+        if (st != LOPF_OK) { delete h; return fail(st, err); }
+    } catch (const std::bad_alloc&) {
+        delete h;
+        return fail(LOPF_E_ARG, "out of host memory during setup");
+    } catch (const std::exception& ex) {
+        delete h;
+        return fail(LOPF_E_ARG, std::string("setup failed: ") + ex.what());
+    }
+    *out = h;
+    return LOPF_OK;
+}
+
+lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
+    if (!h || !sz) return fail(LOPF_E_ARG, "NULL argument");
+    std::memset(sz, 0, sizeof(*sz));
+    const Canon& P = h->cp;
+    sz->S = P.S; sz->n = P.n; sz->m = P.m; sz->n_copies = P.nc;
+    int64_t psym = 0;
+    int mx = 0, mm = 0;
+    for (int64_t s = 0; s < P.S; ++s) {
+        psym += (int64_t)P.n_s[s] * (P.n_s[s] + 1) / 2;
+        mx = std::max(mx, P.n_s[s]);
+        mm = std::max(mm, P.m_raw[s]);
+    }
+    sz->p_sym = psym;
+    sz->max_ns = mx; sz->max_ms = mm;
+    sz->n_tasks = h->lay.n_tasks;
+    sz->n_slots = h->lay.n_slots;
+    sz->device_bytes = (int64_t)h->lay.bytes;
+    sz->abar_doubles = h->lay.abar_doubles;
+    // algorithmic bytes per sweep: packed symmetric Abar + bbar of load-bearing
+    // subsystems + 6 per-copy streams (lambda, x_s rd+wr; u wr+rd) + 4 per-global (x wr+rd, lo, hi)
+    // + c nonzeros, in fp64; plus the int32 copy->global map and CSR.
+    int64_t nbbar = 0;
+    for (int64_t s = 0; s < P.S; ++s) {
+        bool any = false;
+        for (int64_t r = P.b_ptr[s]; r < P.b_ptr[s + 1]; ++r) any |= P.b[r] != 0.0;
+        if (any) nbbar += P.n_s[s];
+    }
+    sz->alg_bytes = 8 * (psym + nbbar + 6 * P.nc + 4 * P.n + h->lay.n_obj) + 4 * (2 * P.nc + P.n + 1);
+    sz->kernel = h->lay.kernel;
+    sz->grid = h->grid;
+    sz->block = kStreamBlock;
+    return LOPF_OK;
+}
+
+lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
+    if (!h || !arena) return fail(LOPF_E_ARG, "NULL argument");
+    if (bytes < h->lay.bytes) return fail(LOPF_E_ARG, "arena smaller than lopf_sizes.device_bytes");
+    if (((uintptr_t)arena) & 255) return fail(LOPF_E_ARG, "arena must be 256-byte aligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!h->registered) {   // pin the host image once so every (re)bind is a DMA from pinned memory
+        if (cudaHostRegister(h->lay.image.data(), h->lay.image.size(), cudaHostRegisterDefault) == cudaSuccess)
+            h->registered = true;
+        else
+            cudaGetLastError();
+    }
+    if (!h->ev0) {
+        CUDA_TRY(cudaEventCreate(&h->ev0), "cudaEventCreate");
+        CUDA_TRY(cudaEventCreate(&h->ev1), "cudaEventCreate");
+    }
+    CUDA_TRY(cudaMemcpyAsync(arena, h->lay.image.data(), h->lay.bytes, cudaMemcpyHostToDevice, s), "bind H2D");
+    const Layout& L = h->lay;
+    uint8_t* b = (uint8_t*)arena;
+    DevProblem& P = h->dp;
+    P.n_tasks = (int32_t)L.n_tasks;
+    P.n_slots = (int32_t)L.n_slots;
+    P.n = h->cp.n;
+    P.tasks = (const int4*)(b + L.off_tasks);
+    P.s_info = (const int32_t*)(b + L.off_info);
+    P.s_g = (const int32_t*)(b + L.off_g);
+    P.s_nbr = (const int4*)(b + L.off_nbr);
+    P.s_bbar = (const double*)(b + L.off_bbar);
+    P.xl = (double*)(b + L.off_xl);
+    P.lam = (double*)(b + L.off_lam);
+    P.u0 = (double*)(b + L.off_u0);
+    P.u1 = (double*)(b + L.off_u1);
+    P.x0 = (const double*)(b + L.off_x0);
+    P.gpar = (const double4*)(b + L.off_gpar);
+    P.seg_ptr = (const int32_t*)(b + L.off_segptr);
+    P.seg_slot = (const int32_t*)(b + L.off_segslot);
+    P.x = (double*)(b + L.off_x);
+    P.abar = (const double*)(b + L.off_abar);
+    P.partial = (double*)(b + L.off_partial);
+    P.ctrl = (DevCtrl*)(b + L.off_ctrl);
+    P.trace = (double*)(b + L.off_trace);
+    P.obj_idx = (const int32_t*)(b + L.off_objidx);
+    P.obj_c = (const double*)(b + L.off_objc);
+    P.n_obj = (int32_t)L.n_obj;
+    P.trace_cap = L.trace_cap;
+    P.trace_every = h->opt.trace_every;
+    P.rho = h->opt.rho;
+    P.inv_rho = 1.0 / h->opt.rho;
+    P.eps_rel = h->opt.eps_rel;
+    std::string err;
+    int grid = 0;
+    lopf_status st = query_grid(&grid, err);
+    if (st != LOPF_OK) return fail(st, err);
+    grid = std::min(grid, kMaxGrid);
+    if (h->opt.reserved[0] > 0) grid = std::min(grid, h->opt.reserved[0]);   // test hook: cap the grid
+    h->grid = grid;
+    P.grid = grid;
+    h->arena = arena;
+    h->arena_bytes = bytes;
+    h->bound = true;
+    return LOPF_OK;
+}
+
+lopf_status lopf_reset(lopf_handle* h, void* stream) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->bound) return fail(LOPF_E_STATE, "lopf_reset before lopf_bind");
+    std::string err;
+    lopf_status st = launch_reset(h->dp, stream, err);
+    return st == LOPF_OK ? LOPF_OK : fail(st, err);
+}
+
+lopf_status lopf_solve_async(lopf_handle* h, int64_t max_iter, int32_t test, void* stream) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->bound) return fail(LOPF_E_STATE, "solve before lopf_bind");
+    if (max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
+    DevProblem P = h->dp;
+    P.max_iter = max_iter;
+    P.test = test ? 1 : 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_TRY(cudaEventRecord(h->ev0, s), "cudaEventRecord");
+    std::string err;
+    lopf_status st = launch_solve(P, h->grid, stream, err);
+    if (st != LOPF_OK) return fail(st, err);
+    CUDA_TRY(cudaEventRecord(h->ev1, s), "cudaEventRecord");
+    return LOPF_OK;
+}
+
+lopf_status lopf_result_get(lopf_handle* h, void* stream, lopf_result* res) {
+    if (!h || !res) return fail(LOPF_E_ARG, "NULL argument");
+    if (!h->bound) return fail(LOPF_E_STATE, "result before lopf_bind");
+    DevCtrl c;
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemcpyAsync(&c, h->dp.ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost, s), "result D2H");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    std::memset(res, 0, sizeof(*res));
+    res->outcome = c.outcome;
+    res->iters = c.iters;
+    res->pres = c.res[0]; res->dres = c.res[1]; res->eps_prim = c.res[2]; res->eps_dual = c.res[3];
+    res->objective = c.objective;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, h->ev0, h->ev1) == cudaSuccess) res->solve_ms = ms;
+    else cudaGetLastError();
+    if (c.numeric) return fail(LOPF_E_NUMERIC, "non-finite residual sum detected on the device at sweep " +
+                                                   std::to_string(c.iters));
+    return LOPF_OK;
+}
+
+lopf_status lopf_run(lopf_handle* h, int64_t k, int32_t test, void* stream, lopf_result* res) {
+    lopf_status st = lopf_solve_async(h, k, test, stream);
+    if (st != LOPF_OK) return st;
+    if (k == 0) {
+        if (res) std::memset(res, 0, sizeof(*res)), res->outcome = LOPF_MAX_ITER;
+        return LOPF_OK;
+    }
+    return res ? lopf_result_get(h, stream, res) : LOPF_OK;
+}
+
+lopf_status lopf_solve(lopf_handle* h, void* stream, lopf_result* res) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    return lopf_run(h, h->opt.max_iter, 1, stream, res);
+}
+
+lopf_status lopf_get_decomposition(const lopf_handle* h, int32_t* kind, int32_t* comp, int32_t* leaf, int32_t* m_s,
+                                   int32_t* n_s, int64_t* sub_ptr, int32_t* copy_global) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    const Canon& P = h->cp;
+    if (kind) std::copy(P.kind.begin(), P.kind.end(), kind);
+    if (comp) std::copy(P.comp.begin(), P.comp.end(), comp);
+    if (leaf) std::copy(P.leaf.begin(), P.leaf.end(), leaf);
+    if (m_s) std::copy(P.m_raw.begin(), P.m_raw.end(), m_s);
+    if (n_s) std::copy(P.n_s.begin(), P.n_s.end(), n_s);
+    if (sub_ptr) std::copy(P.sub_ptr.begin(), P.sub_ptr.end(), sub_ptr);
+    if (copy_global) std::copy(P.copy_global.begin(), P.copy_global.end(), copy_global);
+    return LOPF_OK;
+}
+
+lopf_status lopf_get_consensus(const lopf_handle* h, int64_t* row_ptr, int32_t* copy_idx) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (row_ptr) std::copy(h->cp.seg_ptr.begin(), h->cp.seg_ptr.end(), row_ptr);
+    if (copy_idx) std::copy(h->cp.seg_copy.begin(), h->cp.seg_copy.end(), copy_idx);
+    return LOPF_OK;
+}
+
+lopf_status lopf_get_globals(const lopf_handle* h, int32_t* role, int32_t* comp, int32_t* phase, double* c, double* lo,
+                             double* hi) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    const Canon& P = h->cp;
+    for (int64_t i = 0; i < P.n; ++i) {
+        if (role) role[i] = P.var[i].role;
+        if (comp) comp[i] = P.var[i].comp;
+        if (phase) phase[i] = P.var[i].phase;
+    }
+    if (c) std::copy(P.c.begin(), P.c.end(), c);
+    if (lo) std::copy(P.lo.begin(), P.lo.end(), lo);
+    if (hi) std::copy(P.hi.begin(), P.hi.end(), hi);
+    return LOPF_OK;
+}
+
+lopf_status lopf_get_operator(const lopf_handle* h, int64_t s, double* abar, double* bbar) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    const Canon& P = h->cp;
+    if (s < 0 || s >= P.S) return fail(LOPF_E_ARG, "subsystem index out of range");
+    if (abar) std::copy(P.abar.begin() + P.abar_ptr[s], P.abar.begin() + P.abar_ptr[s + 1], abar);
+    if (bbar) std::copy(P.bbar.begin() + P.sub_ptr[s], P.bbar.begin() + P.sub_ptr[s + 1], bbar);
+    return LOPF_OK;
+}
+
+lopf_status lopf_get_subsystem(const lopf_handle* h, int64_t s, double* A, double* b, int32_t* m_out) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    const Canon& P = h->cp;
+    if (s < 0 || s >= P.S) return fail(LOPF_E_ARG, "subsystem index out of range");
+    if (A) std::copy(P.A.begin() + P.a_ptr[s], P.A.begin() + P.a_ptr[s + 1], A);
+    if (b) std::copy(P.b.begin() + P.b_ptr[s], P.b.begin() + P.b_ptr[s + 1], b);
+    if (m_out) *m_out = P.m_s[s];
+    return LOPF_OK;
+}
+
+lopf_status lopf_get_state(lopf_handle* h, void* stream, double* x, double* x_loc, double* lam) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->bound) return fail(LOPF_E_STATE, "get_state before lopf_bind");
+    cudaStream_t s = (cudaStream_t)stream;
+    const Layout& L = h->lay;
+    std::vector<double> xl(L.n_slots), lm(L.n_slots);
+    if (x) CUDA_TRY(cudaMemcpyAsync(x, h->dp.x, sizeof(double) * h->cp.n, cudaMemcpyDeviceToHost, s), "state D2H");
+    if (x_loc) CUDA_TRY(cudaMemcpyAsync(xl.data(), h->dp.xl, sizeof(double) * L.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
+    if (lam) CUDA_TRY(cudaMemcpyAsync(lm.data(), h->dp.lam, sizeof(double) * L.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    for (int64_t k = 0; k < h->cp.nc; ++k) {
+        if (x_loc) x_loc[k] = xl[L.slot_of_copy[k]];
+        if (lam) lam[k] = lm[L.slot_of_copy[k]];
+    }
+    return LOPF_OK;
+}
+
+lopf_status lopf_set_state(lopf_handle* h, void* stream, const double* x_loc, const double* lam) {
+    if (!h || !x_loc || !lam) return fail(LOPF_E_ARG, "NULL argument");
+    if (!h->bound) return fail(LOPF_E_STATE, "set_state before lopf_bind");
+    cudaStream_t s = (cudaStream_t)stream;
+    const Layout& L = h->lay;
+    std::vector<double> xl(L.n_slots, 0.0), lm(L.n_slots, 0.0), u(L.n_slots, 0.0);
+    const double inv_rho = 1.0 / h->opt.rho;
+    for (int64_t k = 0; k < h->cp.nc; ++k) {
+        const int32_t sl = L.slot_of_copy[k];
+        xl[sl] = x_loc[k];
+        lm[sl] = lam[k];
+        u[sl] = x_loc[k] - lam[k] * inv_rho;
+    }
+    CUDA_TRY(cudaMemcpyAsync(h->dp.xl, xl.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
+    CUDA_TRY(cudaMemcpyAsync(h->dp.lam, lm.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
+    CUDA_TRY(cudaMemcpyAsync(h->dp.u0, u.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
+    CUDA_TRY(cudaMemsetAsync(&h->dp.ctrl->total, 0, sizeof(long long), s), "state memset");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return LOPF_OK;
+}
+
+lopf_status lopf_get_trace(lopf_handle* h, void* stream, double* buf, int64_t cap, int64_t* n_rows) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->bound) return fail(LOPF_E_STATE, "get_trace before lopf_bind");
+    cudaStream_t s = (cudaStream_t)stream;
+    DevCtrl c;
+    CUDA_TRY(cudaMemcpyAsync(&c, h->dp.ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost, s), "trace D2H");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    int64_t rows = std::min<int64_t>(c.trace_rows, cap);
+    if (buf && rows > 0) {
+        CUDA_TRY(cudaMemcpyAsync(buf, h->dp.trace, sizeof(double) * 5 * rows, cudaMemcpyDeviceToHost, s), "trace D2H");
+        CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    }
+    if (n_rows) *n_rows = rows;
+    return LOPF_OK;
+}
+
+void lopf_destroy(lopf_handle* h) {
+    if (!h) return;
+    if (h->registered) cudaHostUnregister(h->lay.image.data());
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    cudaGetLastError();
+    delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+// Internal data structures of liblopf (NOT part of the ABI; see include/lopf.h).
+//
+// Host side (setup.cpp): an independent C++ implementation of the LP assembly
+// (PAPER.md:109-227), the component decomposition and the operator
+// precompute by Cholesky.  Device side (kernels.cu): the fused ADMM
+// sweep.  pack.cpp turns the canonical problem into the device layouts described in
+// DESIGN.md §4.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <vector_types.h>
+
+#include "../../include/lopf.h"
+
+namespace lopf {
+
+enum Role : int8_t { PG = 0, QG, W, PB, QB, PD, QD, PF, QF, PT, QT };
+enum Kind : int32_t { BUS = 0, LINE = 1, LEAF = 2 };
+
+struct Var {
+    int8_t role;
+    int8_t phase;
+    int32_t comp;
+};
+
+// Host copy of the network (validated).
+struct Net {
+    int32_t n_bus = 0, n_line = 0, n_gen = 0, n_load = 0, root = 0;
+    std::vector<uint8_t> bus_ph, line_ph, gen_ph, load_ph, load_conn;
+    std::vector<double> bus_wmin, bus_wmax, bus_gsh, bus_bsh;
+    std::vector<int32_t> line_from, line_to, gen_bus, load_bus;
+    std::vector<double> line_r, line_x, line_gsf, line_bsf, line_gst, line_bst, line_tau;
+    std::vector<double> line_pmin, line_pmax, line_qmin, line_qmax;
+    std::vector<double> gen_pmin, gen_pmax, gen_qmin, gen_qmax;
+    std::vector<double> load_alpha, load_beta, load_a, load_b;
+};
+
+// Canonical problem: globals, subsystems, operators (everything in canonical order).
+struct Canon {
+    int64_t n = 0, m = 0, S = 0, nc = 0;
+    std::vector<Var> var;
+    std::vector<double> c, lo, hi;
+    std::vector<int32_t> kind, comp, leaf, m_s, n_s;      // [S]; m_s after row reduction
+    std::vector<int32_t> m_raw;                            // [S] rows before reduction
+    std::vector<int64_t> sub_ptr;                          // [S+1] copy offsets
+    std::vector<int32_t> copy_global;                      // [nc]
+    std::vector<int64_t> seg_ptr;                          // [n+1]
+    std::vector<int32_t> seg_copy;                         // [nc]
+    std::vector<int64_t> a_ptr;                            // [S+1] offsets of dense A_s (reduced rows)
+    std::vector<double> A, b;                              // dense A_s row-major; b_s (b_ptr = row offsets)
+    std::vector<int64_t> b_ptr;                            // [S+1]
+    std::vector<int64_t> abar_ptr;                         // [S+1] offsets of dense n_s x n_s Abar_s
+    std::vector<double> abar, bbar;                        // bbar [nc]
+    std::vector<double> x0;                                // [nc] initial x_s
+};
+
+// ---- device layout shared by pack.cpp and kernels.cu ---------------------------------------
+// Slot info bit fields (streaming kernel).
+constexpr int kInfoBaseMask = 0xFF;        // slot index of the subsystem's first row in its task (R <= 2)
+constexpr int kInfoValid = 1 << 8;
+constexpr int kInfoFirst = 1 << 9;         // first copy (canonical) of its global: writes x_g
+constexpr int kInfoInline = 1 << 10;       // segment slots stored inline (nu <= 4)
+constexpr int kInfoNuShift = 16;
+
+struct DevCtrl {                           // 256 B, device-resident control block
+    unsigned long long arrive;             // barrier arrivals of this launch
+    unsigned long long flag;               // (iteration << 2) | (stop << 1) | numeric
+    long long total;                       // sweeps since reset (u ping-pong parity)
+    long long iters;                       // sweeps executed by the last launch
+    int outcome, numeric;
+    double res[4];                         // pres, dres, eps_prim, eps_dual of the last sweep
+    double objective;
+    long long trace_rows;
+    double pad[19];
+};
+
+struct DevProblem {                        // kernel argument (pointers into the arena)
+    int32_t n_tasks, n_slots, grid, pad0;
+    int64_t n;
+    const int4* tasks;                     // {slot_off, abar_off, kmax, R}
+    const int32_t* s_info;
+    const int32_t* s_g;
+    const int4* s_nbr;
+    const double* s_bbar;
+    double* xl;
+    double* lam;
+    double* u0;
+    double* u1;
+    const double* x0;                      // initial x_s per slot
+    const double4* gpar;                   // {c/rho, 1/nu, lo, hi} per global
+    const int32_t* seg_ptr;                // [n+1] into seg_slot
+    const int32_t* seg_slot;               // [nc] slots in canonical copy order
+    double* x;                             // [n]
+    const double* abar;                    // packed operator pool
+    double* partial;                       // [grid * 8]
+    DevCtrl* ctrl;
+    double* trace;                         // [trace_cap * 5]
+    const int32_t* obj_idx;                // globals with c != 0
+    const double* obj_c;
+    int32_t n_obj, trace_cap, trace_every, test;
+    double rho, inv_rho, eps_rel;
+    long long max_iter;
+};
+
+// Arena layout: byte offsets of every array (all 256-byte aligned).
+struct Layout {
+    int32_t kernel = 1;
+    int64_t n_tasks = 0, n_slots = 0, abar_doubles = 0, n_obj = 0;
+    size_t off_tasks = 0, off_info = 0, off_g = 0, off_nbr = 0, off_bbar = 0, off_xl = 0, off_lam = 0,
+           off_u0 = 0, off_u1 = 0, off_x0 = 0, off_gpar = 0, off_segptr = 0, off_segslot = 0, off_x = 0, off_abar = 0,
+           off_partial = 0, off_ctrl = 0, off_trace = 0, off_objidx = 0, off_objc = 0;
+    size_t bytes = 0;
+    int32_t max_grid = 0, trace_cap = 0;
+    std::vector<int32_t> slot_of_copy;     // [nc] canonical copy -> slot
+    std::vector<uint8_t> image;            // host image of the whole arena (initial state included)
+};
+
+// setup.cpp
+lopf_status build_canon(const Net& net, const lopf_options& opt, Canon& out, std::string& err);
+lopf_status copy_network(const lopf_network* src, Net& dst, std::string& err);
+// pack.cpp
+lopf_status pack_streaming(const Canon& cp, const lopf_options& opt, int max_grid, Layout& lay, std::string& err);
+void init_state_image(const Canon& cp, Layout& lay);
+// kernels.cu
+constexpr int kStreamBlock = 512;
+lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
+lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err);
+lopf_status query_grid(int* grid, std::string& err);
+
+}  // namespace lopf

@@ -1,0 +1,177 @@
+// Device layout of the streaming kernel.
+//
+// Subsystems are packed into warp TASKS: a task owns 32*R row SLOTS (lane l handles slots
+// l, l+32, ...).  Subsystems with n_s <= 32 are packed floor(32/n_s) to a task, all of one
+// n_s (so a task's column loop has no padding); 32 < n_s <= 64 gives one subsystem per
+// R = 2 task.  The operator pool stores, per task, Abar columns k = 0..kmax-1 as 32*R
+// consecutive doubles (slot-major inside a column), so every column read of a warp is one
+// coalesced 256-byte (R = 1) request.  Per-slot metadata, b-bar and the iterate (x_s, lambda,
+// u ping-pong) are slot-indexed arrays; globals keep {c/rho, 1/nu, lo, hi} as one 32-byte record.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+
+#include <vector_functions.h>
+
+#include "internal.h"
+
+namespace lopf {
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+lopf_status pack_streaming(const Canon& P, const lopf_options& opt, int max_grid, Layout& L, std::string& err) {
+    L = Layout();
+    L.kernel = 1;
+    // ---- tasks ---------------------------------------------------------------------------------
+    std::map<int, std::vector<int64_t>> by_ns;       // n_s -> subsystems (canonical order)
+    for (int64_t s = 0; s < P.S; ++s) {
+        if (P.n_s[s] > 256) {
+            err = "subsystem " + std::to_string(s) + " has n_s = " + std::to_string(P.n_s[s]) +
+                  " > 256 (unsupported by the warp-task layout; the S = 1 path is for small feeders)";
+            return LOPF_E_ARG;
+        }
+        if (P.n_s[s] > 0) by_ns[P.n_s[s]].push_back(s);
+    }
+    struct T { int R, kmax; std::vector<int64_t> subs; };
+    std::vector<T> tasks;
+    for (auto it = by_ns.rbegin(); it != by_ns.rend(); ++it) {   // heavy tasks first
+        const int ns = it->first;
+        const auto& v = it->second;
+        if (ns > 32) {                                            // one subsystem per task, R = 2, 4 or 8
+            const int R = ns <= 64 ? 2 : ns <= 128 ? 4 : 8;
+            for (int64_t s : v) tasks.push_back({R, ns, {s}});
+        } else {
+            const int per = 32 / ns;
+            for (size_t i = 0; i < v.size(); i += per) {
+                T t{1, ns, {}};
+                for (size_t j = i; j < std::min(v.size(), i + (size_t)per); ++j) t.subs.push_back(v[j]);
+                tasks.push_back(std::move(t));
+            }
+        }
+    }
+    L.n_tasks = (int64_t)tasks.size();
+    std::vector<int4> trec(L.n_tasks);
+    int64_t slots = 0, pool = 0;
+    for (int64_t t = 0; t < L.n_tasks; ++t) {
+        trec[t] = make_int4((int)slots, (int)pool, tasks[t].kmax, tasks[t].R);
+        slots += 32 * tasks[t].R;
+        pool += (int64_t)tasks[t].kmax * 32 * tasks[t].R;
+    }
+    if (slots > INT32_MAX || pool > INT32_MAX) { err = "problem too large for 32-bit slot / pool offsets"; return LOPF_E_ARG; }
+    L.n_slots = slots;
+    L.abar_doubles = pool;
+    L.max_grid = max_grid;
+    L.trace_cap = opt.trace_cap > 0 ? opt.trace_cap : 4096;
+
+    // ---- objective terms (c != 0) -----------------------------------------------------------------
+    std::vector<int32_t> obj_idx;
+    std::vector<double> obj_c;
+    for (int64_t i = 0; i < P.n; ++i)
+        if (P.c[i] != 0.0) { obj_idx.push_back((int32_t)i); obj_c.push_back(P.c[i]); }
+    L.n_obj = (int64_t)obj_idx.size();
+
+    // ---- arena offsets --------------------------------------------------------------------------------
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = align256(o + std::max<size_t>(bytes, 1)); return r; };
+    const size_t NS = (size_t)slots, NG = (size_t)P.n, NC = (size_t)P.nc;
+    L.off_tasks = take(sizeof(int4) * L.n_tasks);
+    L.off_info = take(4 * NS);
+    L.off_g = take(4 * NS);
+    L.off_nbr = take(16 * NS);
+    L.off_bbar = take(8 * NS);
+    L.off_xl = take(8 * NS);
+    L.off_lam = take(8 * NS);
+    L.off_u0 = take(8 * NS);
+    L.off_u1 = take(8 * NS);
+    L.off_x0 = take(8 * NS);
+    L.off_gpar = take(32 * NG);
+    L.off_segptr = take(4 * (NG + 1));
+    L.off_segslot = take(4 * NC);
+    L.off_x = take(8 * NG);
+    L.off_abar = take(8 * (size_t)pool);
+    L.off_partial = take(8 * 8 * (size_t)max_grid);
+    L.off_ctrl = take(sizeof(DevCtrl));
+    L.off_trace = take(8 * 5 * (size_t)L.trace_cap);
+    L.off_objidx = take(4 * obj_idx.size());
+    L.off_objc = take(8 * obj_c.size());
+    L.bytes = o;
+    L.image.assign(L.bytes, 0);
+    uint8_t* img = L.image.data();
+    auto at = [&](size_t off) { return img + off; };
+
+    std::memcpy(at(L.off_tasks), trec.data(), sizeof(int4) * trec.size());
+    int32_t* info = (int32_t*)at(L.off_info);
+    int32_t* gs = (int32_t*)at(L.off_g);
+    int4* nbr = (int4*)at(L.off_nbr);
+    double* bbar = (double*)at(L.off_bbar);
+    double* abar = (double*)at(L.off_abar);
+    for (size_t i = 0; i < NS; ++i) { gs[i] = -1; nbr[i] = make_int4(0, 0, 0, 0); }
+
+    L.slot_of_copy.assign(NC, -1);
+    for (int64_t t = 0; t < L.n_tasks; ++t) {
+        const int R = tasks[t].R, P32 = 32 * R, kmax = tasks[t].kmax;
+        int base = 0;
+        for (int64_t s : tasks[t].subs) {
+            const int ns = P.n_s[s];
+            for (int r = 0; r < ns; ++r) {
+                const int64_t slot = trec[t].x + base + r;
+                const int64_t copy = P.sub_ptr[s] + r;
+                L.slot_of_copy[copy] = (int32_t)slot;
+                info[slot] = (base & kInfoBaseMask) | kInfoValid;
+                gs[slot] = P.copy_global[copy];
+                bbar[slot] = P.bbar[copy];
+                const double* Ab = &P.abar[P.abar_ptr[s]];
+                for (int k = 0; k < ns; ++k)      // lane (slot) r computes row r: sum_k Abar[r][k] d[k]
+                    abar[(size_t)trec[t].y + (size_t)k * P32 + base + r] = Ab[(size_t)r * ns + k];
+            }
+            base += ns;
+        }
+        (void)kmax;
+    }
+    // segments: inline neighbour slots (nu <= 4) + CSR fallback; first-copy flag
+    int32_t* segptr = (int32_t*)at(L.off_segptr);
+    int32_t* segslot = (int32_t*)at(L.off_segslot);
+    for (int64_t i = 0; i <= P.n; ++i) segptr[i] = (int32_t)P.seg_ptr[i];
+    for (int64_t q = 0; q < P.nc; ++q) segslot[q] = L.slot_of_copy[P.seg_copy[q]];
+    for (int64_t k = 0; k < P.nc; ++k) {
+        const int32_t slot = L.slot_of_copy[k];
+        const int32_t g = P.copy_global[k];
+        const int64_t s0 = P.seg_ptr[g], nu = P.seg_ptr[g + 1] - s0;
+        info[slot] |= (int)(std::min<int64_t>(nu, 255) << kInfoNuShift);
+        if (P.seg_copy[s0] == k) info[slot] |= kInfoFirst;
+        if (nu <= 4) {
+            info[slot] |= kInfoInline;
+            int v[4] = {0, 0, 0, 0};
+            for (int64_t j = 0; j < nu; ++j) v[j] = segslot[s0 + j];
+            nbr[slot] = make_int4(v[0], v[1], v[2], v[3]);
+        }
+    }
+    double4* gpar = (double4*)at(L.off_gpar);
+    for (int64_t i = 0; i < P.n; ++i) {
+        const double nu = (double)(P.seg_ptr[i + 1] - P.seg_ptr[i]);
+        gpar[i] = make_double4(P.c[i] / opt.rho, 1.0 / nu, P.lo[i], P.hi[i]);
+    }
+    std::memcpy(at(L.off_objidx), obj_idx.data(), 4 * obj_idx.size());
+    std::memcpy(at(L.off_objc), obj_c.data(), 8 * obj_c.size());
+    init_state_image(P, L);
+    return LOPF_OK;
+}
+
+// Initial iterate (Algorithm 1 line 1): x_s = x0, lambda = 0, u = x_s - lambda/rho = x0.
+void init_state_image(const Canon& P, Layout& L) {
+    uint8_t* img = L.image.data();
+    double* xl = (double*)(img + L.off_xl);
+    double* lam = (double*)(img + L.off_lam);
+    double* u0 = (double*)(img + L.off_u0);
+    double* u1 = (double*)(img + L.off_u1);
+    double* x0 = (double*)(img + L.off_x0);
+    for (int64_t i = 0; i < L.n_slots; ++i) xl[i] = lam[i] = u0[i] = u1[i] = x0[i] = 0.0;
+    for (int64_t k = 0; k < P.nc; ++k) {
+        const int32_t s = L.slot_of_copy[k];
+        xl[s] = u0[s] = x0[s] = P.x0[k];
+    }
+    std::memset(img + L.off_ctrl, 0, sizeof(DevCtrl));
+}
+
+}  // namespace lopf

@@ -1,0 +1,167 @@
+"""GPU parity through the C-ABI (marker `gpu`): the sm_100a path against the oracle on the same
+seeded inputs.  Bars (north_star / DESIGN.md §3): decomposition, consensus map and iteration count
+to (termination) bit-exact; iterates after fixed K within 1e-9 relative
+(||y_gpu - y_ora||_inf <= 1e-9 max(1, ||y_ora||_inf) for y in {x, x_loc, lambda}); objective 1e-6."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import feedergen as fg
+import fixtures as fx
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_golden.json")))["configs"]
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+_cache = {}
+
+
+def _problem(shape):
+    if shape not in _cache:
+        f = fg.make_feeder(shape)
+        _cache[shape] = (f, oracle.build_problem(f))
+    return _cache[shape]
+
+
+def _solver(f, **kw):
+    from paper_2310_09410_b200 import Lopf
+    return Lopf.setup(f, **kw).bind("cuda")
+
+
+def _rel(a, b):
+    return float(np.abs(a - b).max() / max(1.0, np.abs(b).max()))
+
+
+def _check_state(h, ref):
+    x, xl, lam = h.get_state()
+    assert _rel(x, ref.x) <= TOL, ("x", _rel(x, ref.x))
+    assert _rel(xl, ref.x_loc) <= TOL, ("x_loc", _rel(xl, ref.x_loc))
+    assert _rel(lam, ref.lam) <= TOL, ("lambda", _rel(lam, ref.lam))
+
+
+@pytest.mark.parametrize("shape,ks", [("13", (1, 10, 100, 1000)), ("123", (1, 10, 1000)), ("8500", (1, 10, 200))])
+def test_fixed_k_iterates(torch_cuda, shape, ks):
+    f, p = _problem(shape)
+    h = _solver(f)
+    done = 0
+    for k in ks:                                   # run(k) continues from the current iterate
+        h.run(k - done)
+        done = k
+        _check_state(h, oracle.run_k(p, k))
+
+
+@pytest.mark.parametrize("shape", ["13", "123", "8500"])
+def test_iterations_to_tolerance_bit_exact(torch_cuda, shape):
+    f, p = _problem(shape)
+    g = GOLD[shape]
+    assert f.sha256() == g["sha256"], "synthetic feeder differs from the golden's"
+    h = _solver(f)
+    r = h.solve()
+    from paper_2310_09410_b200 import CONVERGED
+    assert r.outcome == CONVERGED
+    assert r.iters == g["iters"], (r.iters, g["iters"])
+    assert abs(r.objective - g["objective"]) <= 1e-6 * abs(g["objective"])
+    for a, b in ((r.pres, g["pres"]), (r.dres, g["dres"]), (r.eps_prim, g["eps_prim"]), (r.eps_dual, g["eps_dual"])):
+        assert abs(a - b) <= 1e-6 * max(abs(b), 1e-12)
+    # the final global x satisfies its bounds exactly
+    x, _, _ = h.get_state()
+    assert np.all(x >= p.lp.lo) and np.all(x <= p.lp.hi)
+
+
+@pytest.mark.parametrize("make", [lambda: fx.chain_1ph(4), lambda: fx.two_bus_3ph(fg.DELTA), fx.four_bus])
+def test_fixtures_fixed_k_and_solve(torch_cuda, make):
+    f = make()
+    p = oracle.build_problem(f)
+    h = _solver(f)
+    h.run(300)
+    _check_state(h, oracle.run_k(p, 300))
+    h.reset()
+    r = h.solve()
+    o = oracle.solve(p)
+    assert r.iters == o.iters and abs(r.objective - o.objective) <= 1e-6 * abs(o.objective)
+
+
+def test_single_partition_s1(torch_cuda):
+    """S = 1 (one subsystem of n_s = n > 64: the SMEM-staged large-task path)."""
+    f = fx.four_bus()
+    p = oracle.build_problem(f, single=True)
+    h = _solver(f, single=True)
+    h.run(200)
+    _check_state(h, oracle.run_k(p, 200))
+
+
+@pytest.mark.parametrize("cap", [1, 3, 37])
+def test_grid_size_independence(torch_cuda, cap):
+    """Few CTAs (many tasks per warp, few barrier participants): same K, iterates within tolerance."""
+    f, p = _problem("123")
+    h = _solver(f, grid_cap=cap)
+    h.run(100)
+    _check_state(h, oracle.run_k(p, 100))
+    h.reset()
+    r = h.solve()
+    assert r.iters == GOLD["123"]["iters"]
+
+
+def test_determinism_and_reset(torch_cuda):
+    f, _ = _problem("123")
+    h = _solver(f)
+    h.run(777)
+    a = h.get_state()
+    h.reset()
+    h.run(777)
+    b = h.get_state()
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)                                 # bit-identical reruns
+    h.reset()
+    h.run(0)
+    x0 = oracle.initial_state(_problem("123")[1])
+    _, xl, lam = h.get_state()
+    assert np.array_equal(xl, x0[0]) and not lam.any()
+
+
+def test_set_state_resume(torch_cuda):
+    """lopf_set_state / get_state: resuming from the oracle's iterate at K1 continues the oracle run."""
+    f, p = _problem("13")
+    h = _solver(f)
+    mid = oracle.run_k(p, 400)
+    h.set_state(mid.x_loc, mid.lam)
+    h.run(100)
+    end = oracle.run_k(p, 100, state=(mid.x_loc, mid.lam))
+    _check_state(h, end)
+
+
+def test_trace_and_max_iter(torch_cuda):
+    f, p = _problem("13")
+    from paper_2310_09410_b200 import Lopf, MAX_ITER
+    h = Lopf.setup(f, trace_every=10, max_iter=250).bind("cuda")
+    r = h.solve()
+    assert r.outcome == MAX_ITER and r.iters == 250
+    tr = h.get_trace()
+    o = oracle.solve(p, max_iter=250, trace_every=10)
+    assert tr.shape == (25, 5) and np.array_equal(tr[:, 0], np.arange(10, 251, 10))
+    assert np.allclose(tr[:, 1:], o.trace, rtol=1e-7, atol=1e-12)
+
+
+def test_termination_fires_on_conjunction_only(torch_cuda):
+    """Every traced sweep before K fails the test; sweep K passes both."""
+    f, p = _problem("13")
+    from paper_2310_09410_b200 import Lopf
+    h = Lopf.setup(f, trace_every=1, trace_cap=20000).bind("cuda")
+    r = h.solve()
+    tr = h.get_trace(cap=20000)
+    ok = (tr[:, 1] <= tr[:, 3]) & (tr[:, 2] <= tr[:, 4])
+    assert len(tr) == r.iters and ok[-1] and not ok[:-1].any()
