@@ -238,7 +238,8 @@ def main():
                        "block": int(sz.block), "setup_s": round(setup_s, 3)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "admm_stream_kernel (one persistent launch = one solve)",
+                         "kernel": ("admm_resident_kernel" if sz.kernel == 2 else "admm_stream_kernel")
+                                   + " (one persistent cooperative launch = one solve)",
                          "alg_bytes_per_sweep": int(sz.alg_bytes), "mean_kernel_ms": mean_kern_ms,
                          "us_per_sweep": 1e3 * mean_kern_ms / mean_iters},
             "cpu_baseline": cpu,

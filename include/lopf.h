@@ -93,7 +93,9 @@ typedef struct {
     int32_t single;        /* 1: one subsystem holding every row (S = 1) */
     int32_t kernel;        /* 0 auto, 1 streaming (operators in HBM/L2), 2 resident (operators in SMEM) */
     int32_t block_threads; /* 0 = default */
-    int32_t reserved[5];
+    int32_t max_ctas;      /* resident kernel: CTAs available (one per SM; 0 = 148, the B200 SM count) */
+    int32_t grid_cap;      /* streaming kernel: cap on the persistent grid (0 = occupancy x SMs; test hook) */
+    int32_t reserved[3];
 } lopf_options;
 
 typedef struct {

@@ -23,6 +23,8 @@ struct lopf_handle {
     bool registered = false;
     int grid = 0;
     DevProblem dp{};
+    ResProblem rp{};
+    bool resident() const { return lay.kernel == 2; }
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -78,7 +80,17 @@ lopf_status lopf_setup(const lopf_network* net, const lopf_options* opt, lopf_ha
     try {
         lopf_status st = copy_network(net, h->net, err);
         if (st == LOPF_OK) st = build_canon(h->net, h->opt, h->cp, err);
-        if (st == LOPF_OK) st = pack_streaming(h->cp, h->opt, kMaxGrid, h->lay, err);
+        if (st == LOPF_OK) {
+            if (h->opt.kernel == 2) {
+                st = pack_resident(h->net, h->cp, h->opt, h->lay, err);
+            } else if (h->opt.kernel == 1) {
+                st = pack_streaming(h->cp, h->opt, kMaxGrid, h->lay, err);
+            } else {                                      // auto: operators on chip when they fit
+                std::string e2;
+                st = pack_resident(h->net, h->cp, h->opt, h->lay, e2);
+                if (st != LOPF_OK) st = pack_streaming(h->cp, h->opt, kMaxGrid, h->lay, err);
+            }
+        }
         if (st != LOPF_OK) { delete h; return fail(st, err); }
     } catch (const std::bad_alloc&) {
         delete h;
@@ -120,8 +132,8 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
     }
     sz->alg_bytes = 8 * (psym + nbbar + 6 * P.nc + 4 * P.n + h->lay.n_obj) + 4 * (2 * P.nc + P.n + 1);
     sz->kernel = h->lay.kernel;
-    sz->grid = h->grid;
-    sz->block = kStreamBlock;
+    sz->grid = h->resident() ? h->lay.G : h->grid;
+    sz->block = h->resident() ? kResBlock : kStreamBlock;
     return LOPF_OK;
 }
 
@@ -143,6 +155,45 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     CUDA_TRY(cudaMemcpyAsync(arena, h->lay.image.data(), h->lay.bytes, cudaMemcpyHostToDevice, s), "bind H2D");
     const Layout& L = h->lay;
     uint8_t* b = (uint8_t*)arena;
+    if (h->resident()) {
+        std::string err;
+        int sms = 0, optin = 0;
+        lopf_status st = resident_capacity(&sms, &optin, err);
+        if (st != LOPF_OK) return fail(st, err);
+        if (L.G > sms) return fail(LOPF_E_ARG, "resident layout needs " + std::to_string(L.G) + " CTAs but the device has " +
+                                                   std::to_string(sms) + " SMs (set max_ctas or kernel = 1)");
+        if (L.max_smem + 4096 > optin) return fail(LOPF_E_ARG, "resident layout exceeds the per-CTA shared memory");
+        ResProblem& R = h->rp;
+        R.hdr = (const CtaHdr*)(b + L.off_hdr);
+        R.blobs = b + L.off_blobs;
+        R.xchg = (double*)(b + L.off_xchg);
+        R.partial = (double*)(b + L.off_partial);
+        R.ctrl = (DevCtrl*)(b + L.off_ctrl);
+        R.trace = (double*)(b + L.off_trace);
+        R.x = (double*)(b + L.off_x);
+        R.obj_idx = (const int32_t*)(b + L.off_objidx);
+        R.obj_c = (const double*)(b + L.off_objc);
+        R.x0 = (const double*)(b + L.off_x0r);
+        R.n_exp = L.n_exp;
+        R.G = L.G;
+        R.n_obj = (int32_t)L.n_obj;
+        R.trace_cap = L.trace_cap;
+        R.trace_every = h->opt.trace_every;
+        R.total_slots = L.total_slots;
+        R.max_smem = L.max_smem;
+        R.rho = h->opt.rho;
+        R.inv_rho = 1.0 / h->opt.rho;
+        R.eps_rel = h->opt.eps_rel;
+        h->dp = DevProblem{};
+        h->dp.ctrl = R.ctrl;
+        h->dp.x = R.x;
+        h->dp.trace = R.trace;
+        h->grid = L.G;
+        h->arena = arena;
+        h->arena_bytes = bytes;
+        h->bound = true;
+        return LOPF_OK;
+    }
     DevProblem& P = h->dp;
     P.n_tasks = (int32_t)L.n_tasks;
     P.n_slots = (int32_t)L.n_slots;
@@ -178,7 +229,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     lopf_status st = query_grid(&grid, err);
     if (st != LOPF_OK) return fail(st, err);
     grid = std::min(grid, kMaxGrid);
-    if (h->opt.reserved[0] > 0) grid = std::min(grid, h->opt.reserved[0]);   // test hook: cap the grid
+    if (h->opt.grid_cap > 0) grid = std::min(grid, h->opt.grid_cap);   // test hook: cap the grid
     h->grid = grid;
     P.grid = grid;
     h->arena = arena;
@@ -191,7 +242,7 @@ lopf_status lopf_reset(lopf_handle* h, void* stream) {
     if (!h) return fail(LOPF_E_ARG, "NULL handle");
     if (!h->bound) return fail(LOPF_E_STATE, "lopf_reset before lopf_bind");
     std::string err;
-    lopf_status st = launch_reset(h->dp, stream, err);
+    lopf_status st = h->resident() ? launch_reset_resident(h->rp, stream, err) : launch_reset(h->dp, stream, err);
     return st == LOPF_OK ? LOPF_OK : fail(st, err);
 }
 
@@ -199,13 +250,21 @@ lopf_status lopf_solve_async(lopf_handle* h, int64_t max_iter, int32_t test, voi
     if (!h) return fail(LOPF_E_ARG, "NULL handle");
     if (!h->bound) return fail(LOPF_E_STATE, "solve before lopf_bind");
     if (max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
-    DevProblem P = h->dp;
-    P.max_iter = max_iter;
-    P.test = test ? 1 : 0;
     cudaStream_t s = (cudaStream_t)stream;
     CUDA_TRY(cudaEventRecord(h->ev0, s), "cudaEventRecord");
     std::string err;
-    lopf_status st = launch_solve(P, h->grid, stream, err);
+    lopf_status st;
+    if (h->resident()) {
+        ResProblem R = h->rp;
+        R.max_iter = max_iter;
+        R.test = test ? 1 : 0;
+        st = launch_resident(R, stream, err);
+    } else {
+        DevProblem P = h->dp;
+        P.max_iter = max_iter;
+        P.test = test ? 1 : 0;
+        st = launch_solve(P, h->grid, stream, err);
+    }
     if (st != LOPF_OK) return fail(st, err);
     CUDA_TRY(cudaEventRecord(h->ev1, s), "cudaEventRecord");
     return LOPF_OK;
@@ -301,19 +360,43 @@ lopf_status lopf_get_subsystem(const lopf_handle* h, int64_t s, double* A, doubl
     return LOPF_OK;
 }
 
+// slot-ordered x_s / lambda of the current device iterate (streaming: flat slot arrays; resident:
+// per-CTA blob regions concatenated in global slot order)
+static lopf_status fetch_slots(lopf_handle* h, cudaStream_t s, std::vector<double>& xl, std::vector<double>& lm) {
+    const Layout& L = h->lay;
+    xl.assign(L.n_slots, 0.0);
+    lm.assign(L.n_slots, 0.0);
+    if (!h->resident()) {
+        CUDA_TRY(cudaMemcpyAsync(xl.data(), h->dp.xl, 8 * L.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
+        CUDA_TRY(cudaMemcpyAsync(lm.data(), h->dp.lam, 8 * L.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
+    } else {
+        for (int c = 0; c < L.G; ++c) {
+            const CtaHdr& H = L.hdr[c];
+            const uint8_t* blob = h->rp.blobs + H.blob_off;
+            CUDA_TRY(cudaMemcpyAsync(xl.data() + H.slot_base, blob + H.off_xl, 8 * (size_t)H.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
+            CUDA_TRY(cudaMemcpyAsync(lm.data() + H.slot_base, blob + H.off_lam, 8 * (size_t)H.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return LOPF_OK;
+}
+
 lopf_status lopf_get_state(lopf_handle* h, void* stream, double* x, double* x_loc, double* lam) {
     if (!h) return fail(LOPF_E_ARG, "NULL handle");
     if (!h->bound) return fail(LOPF_E_STATE, "get_state before lopf_bind");
     cudaStream_t s = (cudaStream_t)stream;
     const Layout& L = h->lay;
-    std::vector<double> xl(L.n_slots), lm(L.n_slots);
     if (x) CUDA_TRY(cudaMemcpyAsync(x, h->dp.x, sizeof(double) * h->cp.n, cudaMemcpyDeviceToHost, s), "state D2H");
-    if (x_loc) CUDA_TRY(cudaMemcpyAsync(xl.data(), h->dp.xl, sizeof(double) * L.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
-    if (lam) CUDA_TRY(cudaMemcpyAsync(lm.data(), h->dp.lam, sizeof(double) * L.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
-    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-    for (int64_t k = 0; k < h->cp.nc; ++k) {
-        if (x_loc) x_loc[k] = xl[L.slot_of_copy[k]];
-        if (lam) lam[k] = lm[L.slot_of_copy[k]];
+    if (x_loc || lam) {
+        std::vector<double> xl, lm;
+        lopf_status st = fetch_slots(h, s, xl, lm);
+        if (st != LOPF_OK) return st;
+        for (int64_t k = 0; k < h->cp.nc; ++k) {
+            if (x_loc) x_loc[k] = xl[L.slot_of_copy[k]];
+            if (lam) lam[k] = lm[L.slot_of_copy[k]];
+        }
+    } else {
+        CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     }
     return LOPF_OK;
 }
@@ -323,7 +406,7 @@ lopf_status lopf_set_state(lopf_handle* h, void* stream, const double* x_loc, co
     if (!h->bound) return fail(LOPF_E_STATE, "set_state before lopf_bind");
     cudaStream_t s = (cudaStream_t)stream;
     const Layout& L = h->lay;
-    std::vector<double> xl(L.n_slots, 0.0), lm(L.n_slots, 0.0), u(L.n_slots, 0.0);
+    std::vector<double> xl(L.n_slots, 0.0), lm(L.n_slots, 0.0), u(L.n_slots, 0.0), z(L.n_slots, 0.0);
     const double inv_rho = 1.0 / h->opt.rho;
     for (int64_t k = 0; k < h->cp.nc; ++k) {
         const int32_t sl = L.slot_of_copy[k];
@@ -331,9 +414,19 @@ lopf_status lopf_set_state(lopf_handle* h, void* stream, const double* x_loc, co
         lm[sl] = lam[k];
         u[sl] = x_loc[k] - lam[k] * inv_rho;
     }
-    CUDA_TRY(cudaMemcpyAsync(h->dp.xl, xl.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
-    CUDA_TRY(cudaMemcpyAsync(h->dp.lam, lm.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
-    CUDA_TRY(cudaMemcpyAsync(h->dp.u0, u.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
+    if (!h->resident()) {
+        CUDA_TRY(cudaMemcpyAsync(h->dp.xl, xl.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
+        CUDA_TRY(cudaMemcpyAsync(h->dp.lam, lm.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
+        CUDA_TRY(cudaMemcpyAsync(h->dp.u0, u.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
+    } else {
+        for (int c = 0; c < L.G; ++c) {
+            const CtaHdr& H = L.hdr[c];
+            uint8_t* blob = h->rp.blobs + H.blob_off;
+            const size_t nb = 8 * (size_t)H.n_slots;
+            CUDA_TRY(cudaMemcpyAsync(blob + H.off_xl, xl.data() + H.slot_base, nb, cudaMemcpyHostToDevice, s), "state H2D");
+            CUDA_TRY(cudaMemcpyAsync(blob + H.off_lam, lm.data() + H.slot_base, nb, cudaMemcpyHostToDevice, s), "state H2D");
+        }
+    }
     CUDA_TRY(cudaMemsetAsync(&h->dp.ctrl->total, 0, sizeof(long long), s), "state memset");
     CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     return LOPF_OK;

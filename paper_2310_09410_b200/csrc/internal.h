@@ -104,6 +104,45 @@ struct DevProblem {                        // kernel argument (pointers into the
     long long max_iter;
 };
 
+// ---- resident kernel (operators + iterate in shared memory) -----------------------------------
+// Every CTA owns a DFS-contiguous chunk of subsystems.  Its BLOB (global memory) is copied into
+// SMEM at kernel start; the iterate (x_s, lambda, u) lives in SMEM for the whole launch and is
+// written back at the end.  Offsets are bytes from the blob start.
+constexpr int kResBlock = 512;
+constexpr int kResSmemBudget = 222 * 1024;    // blob + scratch per CTA (227 KB usable on sm_100)
+// sinfo: base (bits 0-5, first slot of the subsystem in its task) | valid (bit 6) | n_s (bits 7-13) | gl (bits 14-31)
+constexpr int kResValid = 1 << 6;
+constexpr int kResNsShift = 7;
+constexpr int kResGlShift = 14;
+
+struct CtaHdr {                               // 128 B, one per CTA
+    int32_t n_tasks, n_slots, n_glob, n_seg, n_expl;
+    int32_t blob_bytes, smem_bytes;
+    int32_t off_abar, off_bbar, off_xl, off_lam, off_gpar, off_tasks, off_sinfo, off_aoff, off_gsegoff, off_gseg,
+        off_gown, off_expl, off_xg;
+    int32_t slot_base;
+    int32_t pad0;
+    long long blob_off;
+    int32_t pad[4];
+};
+
+struct ResProblem {                           // resident kernel argument
+    const CtaHdr* hdr;
+    uint8_t* blobs;
+    double* xchg;                             // [2][n_exp] boundary u values (ping-pong)
+    double* partial;                          // [2][G][8]
+    DevCtrl* ctrl;
+    double* trace;
+    double* x;                                // [n] solution
+    const int32_t* obj_idx;
+    const double* obj_c;
+    const double* x0;                         // [total slots] initial x_s, blob slot order
+    int32_t n_exp, G, n_obj, test;
+    int32_t trace_cap, trace_every, total_slots, max_smem;
+    double rho, inv_rho, eps_rel;
+    long long max_iter;
+};
+
 // Arena layout: byte offsets of every array (all 256-byte aligned).
 struct Layout {
     int32_t kernel = 1;
@@ -113,8 +152,13 @@ struct Layout {
            off_partial = 0, off_ctrl = 0, off_trace = 0, off_objidx = 0, off_objc = 0;
     size_t bytes = 0;
     int32_t max_grid = 0, trace_cap = 0;
-    std::vector<int32_t> slot_of_copy;     // [nc] canonical copy -> slot
+    std::vector<int32_t> slot_of_copy;     // [nc] canonical copy -> slot (resident: global slot id)
     std::vector<uint8_t> image;            // host image of the whole arena (initial state included)
+    // resident kernel
+    int32_t G = 0, n_exp = 0, max_smem = 0, total_slots = 0;
+    size_t off_hdr = 0, off_blobs = 0, off_xchg = 0, off_x0r = 0;
+    std::vector<CtaHdr> hdr;               // host copy of the per-CTA headers
+    std::vector<int32_t> slot_cta;         // [total slots] CTA of a global slot id
 };
 
 // setup.cpp
@@ -123,10 +167,15 @@ lopf_status copy_network(const lopf_network* src, Net& dst, std::string& err);
 // pack.cpp
 lopf_status pack_streaming(const Canon& cp, const lopf_options& opt, int max_grid, Layout& lay, std::string& err);
 void init_state_image(const Canon& cp, Layout& lay);
+// pack_resident.cpp: returns LOPF_E_ARG (with err) when the problem does not fit max_ctas CTAs
+lopf_status pack_resident(const Net& net, const Canon& cp, const lopf_options& opt, Layout& lay, std::string& err);
 // kernels.cu
 constexpr int kStreamBlock = 512;
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
 lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err);
 lopf_status query_grid(int* grid, std::string& err);
+lopf_status launch_resident(const ResProblem& P, void* stream, std::string& err);
+lopf_status launch_reset_resident(const ResProblem& P, void* stream, std::string& err);
+lopf_status resident_capacity(int* sms, int* smem_optin, std::string& err);
 
 }  // namespace lopf

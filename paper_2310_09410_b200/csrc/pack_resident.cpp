@@ -1,0 +1,369 @@
+// Device layout of the SMEM-resident kernel.
+//
+// 1. Subsystems are ordered by a depth-first walk of the feeder from the root (a bus, then each of
+//    its lines followed by the subtree behind it), so a contiguous run of that order is a
+//    connected piece of the network.
+// 2. The order is cut into G chunks of balanced shared-memory footprint (<= kResSmemBudget each);
+//    chunk c is owned by CTA c for the whole solve.
+// 3. Inside a chunk, subsystems are bin-packed (first fit decreasing) into 32-row warp tasks
+//    (n_s > 32: one subsystem per 64-row task); each Abar_s is stored compactly (n_s x n_s, exactly
+//    sum n_s^2 doubles per chunk) and lane r of subsystem s reads Abar_s[k][r] at base_s + k n_s + r.
+// 4. Every global variable with a copy in the chunk gets a local index and a segment list in
+//    canonical copy order whose entries are local slots (u in SMEM) or, for copies owned by other
+//    CTAs, indices into the global exchange buffer (only boundary copies are exchanged).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+
+#include <vector_functions.h>
+
+#include "internal.h"
+
+namespace lopf {
+
+static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+static int32_t a16(int64_t x) { return (int32_t)((x + 15) & ~(int64_t)15); }
+
+// depth-first order of the subsystems from the root bus
+static std::vector<int64_t> dfs_order(const Net& N, const Canon& P) {
+    std::vector<int64_t> order;
+    order.reserve(P.S);
+    if (P.S == 1) { order.push_back(0); return order; }
+    std::vector<int64_t> sub_of_bus(N.n_bus, -1), sub_of_line(N.n_line, -1);
+    for (int64_t s = 0; s < P.S; ++s) {
+        if (P.kind[s] == BUS) sub_of_bus[P.comp[s]] = s;
+        else {
+            sub_of_line[P.comp[s]] = s;
+            if (P.kind[s] == LEAF) sub_of_bus[P.leaf[s]] = s;
+        }
+    }
+    std::vector<std::vector<int32_t>> adj(N.n_bus);
+    for (int e = 0; e < N.n_line; ++e) { adj[N.line_from[e]].push_back(e); adj[N.line_to[e]].push_back(e); }
+    for (auto& a : adj) std::sort(a.begin(), a.end());
+    std::vector<char> emitted(P.S, 0), seen(N.n_bus, 0);
+    auto emit = [&](int64_t s) { if (s >= 0 && !emitted[s]) { emitted[s] = 1; order.push_back(s); } };
+    auto walk = [&](int root) {
+        std::vector<std::pair<int, size_t>> st;
+        st.push_back({root, 0});
+        seen[root] = 1;
+        emit(sub_of_bus[root]);
+        while (!st.empty()) {
+            auto& [b, k] = st.back();
+            if (k >= adj[b].size()) { st.pop_back(); continue; }
+            const int e = adj[b][k++];
+            const int o = N.line_from[e] == b ? N.line_to[e] : N.line_from[e];
+            emit(sub_of_line[e]);
+            if (!seen[o]) {
+                seen[o] = 1;
+                emit(sub_of_bus[o]);
+                st.push_back({o, 0});
+            }
+        }
+    };
+    if (N.n_bus > 0) walk(N.root);
+    for (int b = 0; b < N.n_bus; ++b)
+        if (!seen[b]) walk(b);
+    for (int64_t s = 0; s < P.S; ++s) emit(s);
+    return order;
+}
+
+namespace {
+struct Chunk {
+    std::vector<int64_t> subs;
+};
+struct TaskR {
+    int R, kmax;
+    std::vector<int64_t> subs;
+};
+
+std::vector<TaskR> make_tasks(const Canon& P, const std::vector<int64_t>& subs) {
+    std::vector<int64_t> v;
+    for (int64_t s : subs)
+        if (P.n_s[s] > 0) v.push_back(s);
+    std::stable_sort(v.begin(), v.end(), [&](int64_t a, int64_t b) { return P.n_s[a] > P.n_s[b]; });
+    std::vector<TaskR> tasks;
+    std::vector<int> room;
+    for (int64_t s : v) {
+        const int ns = P.n_s[s];
+        if (ns > 32) { tasks.push_back({2, ns, {s}}); room.push_back(0); continue; }
+        size_t t = 0;
+        for (; t < tasks.size(); ++t)
+            if (tasks[t].R == 1 && room[t] >= ns) break;
+        if (t == tasks.size()) { tasks.push_back({1, 0, {}}); room.push_back(32); }
+        tasks[t].subs.push_back(s);
+        tasks[t].kmax = std::max(tasks[t].kmax, ns);
+        room[t] -= ns;
+    }
+    return tasks;
+}
+
+// exact SMEM bytes of a chunk (blob + xg scratch); mirrors the blob layout built below
+int64_t chunk_bytes(const Canon& P, const std::vector<int64_t>& subs, std::vector<int32_t>& cnt) {
+    auto tasks = make_tasks(P, subs);
+    int64_t NS = 0, pool = 0, NG = 0, NSEG = 0, NX = 0;
+    for (auto& t : tasks) NS += 32 * t.R;
+    for (int64_t s : subs) pool += (int64_t)P.n_s[s] * P.n_s[s];
+    for (int64_t s : subs)
+        for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) {
+            const int32_t g = P.copy_global[k];
+            if (cnt[g]++ == 0) { ++NG; NSEG += P.seg_ptr[g + 1] - P.seg_ptr[g]; }
+        }
+    for (int64_t s : subs)                       // exported copies: globals not entirely inside the chunk
+        for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) {
+            const int32_t g = P.copy_global[k];
+            NX += cnt[g] < P.seg_ptr[g + 1] - P.seg_ptr[g];
+        }
+    for (int64_t s : subs)
+        for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) cnt[P.copy_global[k]] = 0;
+    const int64_t NT = (int64_t)tasks.size();
+    int64_t b = 0;
+    for (int64_t sz : {8 * pool, 8 * NS, 8 * NS, 8 * NS, 32 * NG, 16 * NT, 4 * NS, 4 * NS, 4 * (NG + 1), 4 * NSEG, 4 * NG,
+                       8 * NX, 16 * NG})
+        b = a16(b + sz);
+    return b;
+}
+}  // namespace
+
+lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt, Layout& L, std::string& err) {
+    L = Layout();
+    L.kernel = 2;
+    const int max_ctas = opt.max_ctas > 0 ? opt.max_ctas : 148;
+    for (int64_t s = 0; s < P.S; ++s)
+        if (P.n_s[s] > 64) { err = "resident kernel supports n_s <= 64 (use the streaming kernel)"; return LOPF_E_ARG; }
+    const std::vector<int64_t> order = dfs_order(N, P);
+    std::vector<int32_t> cnt(P.n, 0);
+
+    // ---- choose G and cut the DFS order into chunks of balanced SMEM footprint -----------------------
+    std::vector<int64_t> est(P.S);
+    int64_t total = 0;
+    for (int64_t s = 0; s < P.S; ++s) {
+        est[s] = 8LL * P.n_s[s] * P.n_s[s] + 72LL * P.n_s[s];
+        total += est[s];
+    }
+    const int warps = kResBlock / 32;
+    int G = (int)std::max<int64_t>(1, (total + (kResSmemBudget * 8 / 10) - 1) / (kResSmemBudget * 8 / 10));
+    {   // work heuristic: ~3 warp tasks per warp per sweep before adding CTAs is worth a bigger barrier
+        int64_t approx_tasks = 0;
+        std::map<int, int64_t> cnt;
+        for (int64_t s = 0; s < P.S; ++s) cnt[P.n_s[s]]++;
+        int64_t rows = 0;
+        for (auto& [ns, c] : cnt) rows += (int64_t)ns * c;
+        approx_tasks = (rows + 31) / 32;
+        G = std::max<int>(G, (int)((approx_tasks + 3 * warps - 1) / (3 * warps)));
+    }
+    if (G > max_ctas / 2) G = max_ctas;              // large problems: use every SM
+    std::vector<Chunk> chunks;
+    auto cut = [&](int64_t T, int64_t cap) {
+        chunks.assign(1, Chunk{});
+        int64_t acc = 0;
+        for (int64_t s : order) {
+            if (acc > 0 && (acc + est[s] > T || acc + est[s] > cap)) { chunks.push_back(Chunk{}); acc = 0; }
+            chunks.back().subs.push_back(s);
+            acc += est[s];
+        }
+    };
+    bool done = false;
+    double margin = 0.95;
+    while (!done) {
+        if (G > max_ctas) {
+            err = "problem does not fit in the shared memory of " + std::to_string(max_ctas) + " CTAs";
+            return LOPF_E_ARG;
+        }
+        const int64_t cap = (int64_t)(kResSmemBudget * margin);
+        bool grew = false;
+        for (int64_t T = (total + G - 1) / G;; T = T + T / 32 + 1) {    // smallest balanced target that fits G
+            cut(T, cap);
+            if ((int)chunks.size() <= G) break;
+            if (T > cap) { ++G; grew = true; break; }
+        }
+        if (grew) continue;
+        bool ok = true;
+        for (auto& c : chunks)
+            if (chunk_bytes(P, c.subs, cnt) > kResSmemBudget) { ok = false; break; }
+        if (ok) done = true;
+        else if (margin > 0.5) margin *= 0.95;
+        else ++G;
+    }
+    L.G = (int32_t)chunks.size();
+
+    // ---- copy -> chunk, exported copies -------------------------------------------------------------
+    std::vector<int32_t> copy_chunk(P.nc, -1);
+    for (int c = 0; c < L.G; ++c)
+        for (int64_t s : chunks[c].subs)
+            for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) copy_chunk[k] = c;
+    std::vector<int32_t> xidx(P.nc, -1);
+    int32_t n_exp = 0;
+    for (int64_t g = 0; g < P.n; ++g) {
+        bool multi = false;
+        for (int64_t q = P.seg_ptr[g] + 1; q < P.seg_ptr[g + 1]; ++q)
+            if (copy_chunk[P.seg_copy[q]] != copy_chunk[P.seg_copy[P.seg_ptr[g]]]) multi = true;
+        if (multi)
+            for (int64_t q = P.seg_ptr[g]; q < P.seg_ptr[g + 1]; ++q) xidx[P.seg_copy[q]] = n_exp++;
+    }
+    L.n_exp = n_exp;
+
+    // ---- per-chunk blobs ------------------------------------------------------------------------------------
+    struct Built {
+        CtaHdr h;
+        std::vector<uint8_t> blob;
+        std::vector<double> x0;
+    };
+    std::vector<Built> B(L.G);
+    L.slot_of_copy.assign(P.nc, -1);
+    int32_t slot_base = 0;
+    int max_smem = 0;
+    std::vector<int32_t> gl_of(P.n, -1);
+    for (int c = 0; c < L.G; ++c) {
+        auto tasks = make_tasks(P, chunks[c].subs);
+        CtaHdr& h = B[c].h;
+        std::memset(&h, 0, sizeof(h));
+        int64_t NS = 0, pool = 0;
+        std::vector<int4> trec;
+        for (auto& t : tasks) {
+            trec.push_back(make_int4((int)NS, t.kmax, t.R, 0));
+            NS += 32 * t.R;
+        }
+        std::vector<int64_t> sub_abar;                          // compact operator offsets (doubles)
+        std::vector<int32_t> gl_list;
+        for (size_t t = 0; t < tasks.size(); ++t)
+            for (int64_t s : tasks[t].subs) {
+                sub_abar.push_back(pool);
+                pool += (int64_t)P.n_s[s] * P.n_s[s];
+                for (int r = 0; r < P.n_s[s]; ++r) {
+                    const int32_t g = P.copy_global[P.sub_ptr[s] + r];
+                    if (gl_of[g] < 0) { gl_of[g] = (int32_t)gl_list.size(); gl_list.push_back(g); }
+                }
+            }
+        const int64_t NG = (int64_t)gl_list.size();
+        if (NG >= (1 << (32 - kResGlShift))) { err = "too many globals in one CTA chunk"; return LOPF_E_ARG; }
+        int64_t NSEG = 0;
+        for (int32_t g : gl_list) NSEG += P.seg_ptr[g + 1] - P.seg_ptr[g];
+        int64_t NX = 0;
+        for (auto& t : tasks)
+            for (int64_t s : t.subs)
+                for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) NX += xidx[k] >= 0;
+        const int64_t NT = (int64_t)tasks.size();
+        int32_t o = 0;
+        h.off_abar = o;     o = a16(o + 8 * pool);
+        h.off_bbar = o;     o = a16(o + 8 * NS);
+        h.off_xl = o;       o = a16(o + 8 * NS);
+        h.off_lam = o;      o = a16(o + 8 * NS);
+        h.off_gpar = o;     o = a16(o + 32 * NG);
+        h.off_tasks = o;    o = a16(o + 16 * NT);
+        h.off_sinfo = o;    o = a16(o + 4 * NS);
+        h.off_aoff = o;     o = a16(o + 4 * NS);
+        h.off_gsegoff = o;  o = a16(o + 4 * (NG + 1));
+        h.off_gseg = o;     o = a16(o + 4 * NSEG);
+        h.off_gown = o;     o = a16(o + 4 * NG);
+        h.off_expl = o;     o = a16(o + 8 * NX);
+        h.blob_bytes = o;
+        h.off_xg = o;       o = a16(o + 16 * NG);
+        h.smem_bytes = o;
+        if (h.smem_bytes > kResSmemBudget) { err = "internal: chunk exceeds the SMEM budget"; return LOPF_E_ARG; }
+        h.n_tasks = (int32_t)NT; h.n_slots = (int32_t)NS; h.n_glob = (int32_t)NG; h.n_seg = (int32_t)NSEG;
+        h.n_expl = (int32_t)NX;
+        h.slot_base = slot_base;
+        max_smem = std::max(max_smem, h.smem_bytes);
+        std::vector<uint8_t>& blob = B[c].blob;
+        blob.assign(h.blob_bytes, 0);
+        auto D = [&](int32_t off) { return (double*)(blob.data() + off); };
+        auto I = [&](int32_t off) { return (int32_t*)(blob.data() + off); };
+        std::memcpy(blob.data() + h.off_tasks, trec.data(), 16 * NT);
+        double* abar = D(h.off_abar);
+        int32_t* sinfo = I(h.off_sinfo);
+        int32_t* aoff = I(h.off_aoff);
+        int2* expl = (int2*)(blob.data() + h.off_expl);
+        B[c].x0.assign(NS, 0.0);
+        size_t si = 0;
+        int64_t nx = 0;
+        for (size_t t = 0; t < tasks.size(); ++t) {
+            int base = 0;
+            for (int64_t s : tasks[t].subs) {
+                const int ns = P.n_s[s];
+                const int64_t ab = sub_abar[si++];
+                const double* Ab = &P.abar[P.abar_ptr[s]];
+                for (int64_t q = 0; q < (int64_t)ns * ns; ++q) abar[ab + q] = Ab[q];   // symmetric: col-major = row-major
+                for (int r = 0; r < ns; ++r) {
+                    const int64_t slot = trec[t].x + base + r;
+                    const int64_t copy = P.sub_ptr[s] + r;
+                    const int32_t g = P.copy_global[copy];
+                    sinfo[slot] = (base & 0x3F) | kResValid | (ns << kResNsShift) | (gl_of[g] << kResGlShift);
+                    aoff[slot] = (int32_t)(ab + r);
+                    D(h.off_bbar)[slot] = P.bbar[copy];
+                    D(h.off_xl)[slot] = P.x0[copy];
+                    B[c].x0[slot] = P.x0[copy];
+                    L.slot_of_copy[copy] = slot_base + (int32_t)slot;
+                    if (xidx[copy] >= 0) expl[nx++] = make_int2((int)slot, xidx[copy]);
+                }
+                base += ns;
+            }
+        }
+        double4* gpar = (double4*)(blob.data() + h.off_gpar);
+        int32_t* segoff = I(h.off_gsegoff);
+        int32_t* seg = I(h.off_gseg);
+        int32_t* gown = I(h.off_gown);
+        int32_t q = 0;
+        for (int64_t j = 0; j < NG; ++j) {
+            const int32_t g = gl_list[j];
+            const double nu = (double)(P.seg_ptr[g + 1] - P.seg_ptr[g]);
+            gpar[j] = make_double4(P.c[g] / opt.rho, 1.0 / nu, P.lo[g], P.hi[g]);
+            segoff[j] = q;
+            for (int64_t p = P.seg_ptr[g]; p < P.seg_ptr[g + 1]; ++p) {
+                const int32_t k = P.seg_copy[p];                 // canonical ascending copy order
+                seg[q++] = copy_chunk[k] == c ? (L.slot_of_copy[k] - slot_base) : -(1 + xidx[k]);
+            }
+            gown[j] = copy_chunk[P.seg_copy[P.seg_ptr[g]]] == c ? g : -1;
+        }
+        segoff[NG] = q;
+        for (int32_t g : gl_list) gl_of[g] = -1;
+        slot_base += (int32_t)NS;
+    }
+    L.total_slots = slot_base;
+    L.max_smem = max_smem;
+    L.n_slots = slot_base;
+    for (auto& b : B) L.n_tasks += b.h.n_tasks;
+    int64_t pool_all = 0;
+    for (int64_t s = 0; s < P.S; ++s) pool_all += (int64_t)P.n_s[s] * P.n_s[s];
+    L.abar_doubles = pool_all;
+
+    // ---- objective, arena ---------------------------------------------------------------------------
+    std::vector<int32_t> obj_idx;
+    std::vector<double> obj_c;
+    for (int64_t i = 0; i < P.n; ++i)
+        if (P.c[i] != 0.0) { obj_idx.push_back((int32_t)i); obj_c.push_back(P.c[i]); }
+    L.n_obj = (int64_t)obj_idx.size();
+    L.trace_cap = opt.trace_cap > 0 ? opt.trace_cap : 4096;
+    L.max_grid = L.G;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t r = off; off = a256(off + std::max<size_t>(bytes, 1)); return r; };
+    L.off_hdr = take(sizeof(CtaHdr) * L.G);
+    size_t blobs_total = 0;
+    for (auto& b : B) { b.h.blob_off = (long long)blobs_total; blobs_total = a256(blobs_total + b.blob.size()); }
+    L.off_blobs = take(blobs_total);
+    L.off_xchg = take(8 * 2 * (size_t)std::max(n_exp, 1));
+    L.off_x0r = take(8 * (size_t)L.total_slots);
+    L.off_x = take(8 * (size_t)P.n);
+    L.off_partial = take(8 * 8 * 2 * (size_t)L.G);
+    L.off_ctrl = take(sizeof(DevCtrl));
+    L.off_trace = take(8 * 5 * (size_t)L.trace_cap);
+    L.off_objidx = take(4 * obj_idx.size());
+    L.off_objc = take(8 * obj_c.size());
+    L.bytes = off;
+    L.image.assign(L.bytes, 0);
+    uint8_t* img = L.image.data();
+    L.hdr.resize(L.G);
+    L.slot_cta.assign(L.total_slots, 0);
+    for (int c = 0; c < L.G; ++c) {
+        L.hdr[c] = B[c].h;
+        std::memcpy(img + L.off_blobs + B[c].h.blob_off, B[c].blob.data(), B[c].blob.size());
+        std::memcpy(img + L.off_x0r + 8 * (size_t)B[c].h.slot_base, B[c].x0.data(), 8 * B[c].x0.size());
+        for (int i = 0; i < B[c].h.n_slots; ++i) L.slot_cta[B[c].h.slot_base + i] = c;
+    }
+    std::memcpy(img + L.off_hdr, L.hdr.data(), sizeof(CtaHdr) * L.G);
+    std::memcpy(img + L.off_objidx, obj_idx.data(), 4 * obj_idx.size());
+    std::memcpy(img + L.off_objc, obj_c.data(), 8 * obj_c.size());
+    return LOPF_OK;
+}
+
+}  // namespace lopf

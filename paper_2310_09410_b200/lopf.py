@@ -43,7 +43,8 @@ class Network(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("rho", _f64), ("eps_rel", _f64), ("max_iter", _i64), ("trace_every", _i32), ("trace_cap", _i32),
-                ("single", _i32), ("kernel", _i32), ("block_threads", _i32), ("reserved", _i32 * 5)]
+                ("single", _i32), ("kernel", _i32), ("block_threads", _i32), ("max_ctas", _i32), ("grid_cap", _i32),
+                ("reserved", _i32 * 3)]
 
 
 class Sizes(C.Structure):
@@ -161,13 +162,13 @@ class Lopf:
     @classmethod
     def setup(cls, feeder, rho: float = 100.0, eps_rel: float = 1e-3, max_iter: int = 1_000_000,
               trace_every: int = 0, trace_cap: int = 4096, single: bool = False, kernel: int = 0,
-              grid_cap: int = 0) -> "Lopf":
+              grid_cap: int = 0, max_ctas: int = 0) -> "Lopf":
         lib = load_library()
         o = Options()
         _check(lib.lopf_options_default(C.byref(o)), "lopf_options_default")
         o.rho, o.eps_rel, o.max_iter = float(rho), float(eps_rel), int(max_iter)
         o.trace_every, o.trace_cap, o.single, o.kernel = int(trace_every), int(trace_cap), int(bool(single)), int(kernel)
-        o.reserved[0] = int(grid_cap)
+        o.grid_cap, o.max_ctas = int(grid_cap), int(max_ctas)
         net, keep = _network(feeder)
         h = _vp()
         _check(lib.lopf_setup(C.byref(net), C.byref(o), C.byref(h)), "lopf_setup")

@@ -133,3 +133,15 @@ def test_sizes_byte_model():
     nobj = int((p.lp.c != 0).sum())
     assert s.p_sym == psym
     assert s.alg_bytes == 8 * (psym + nb + 6 * p.dec.n_copies + 4 * p.lp.n + nobj) + 4 * (2 * p.dec.n_copies + p.lp.n + 1)
+
+
+def test_kernel_selection():
+    """auto picks the SMEM-resident kernel when every chunk fits one CTA's shared memory (all
+    three shapes on 148 SMs) and the streaming kernel otherwise (S = 1: n_s > 64)."""
+    for shape, g_max in (("13", 4), ("123", 8), ("8500", 148)):
+        s = Lopf.setup(fg.make_feeder(shape)).sizes
+        assert s.kernel == 2 and 1 <= s.grid <= g_max
+    assert Lopf.setup(fx.four_bus(), single=True).sizes.kernel == 1
+    assert Lopf.setup(fg.make_feeder("123"), kernel=1).sizes.kernel == 1
+    with pytest.raises(LopfError):
+        Lopf.setup(fg.make_feeder("8500"), kernel=2, max_ctas=16)        # does not fit 16 CTAs

@@ -17,6 +17,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_golden.json")))["configs"]
 TOL = 1e-9
+KERNELS = [1, 2]          # 1 streaming (operators in HBM/L2), 2 resident (operators + iterate in SMEM)
 
 
 @pytest.fixture(scope="module")
@@ -53,10 +54,12 @@ def _check_state(h, ref):
     assert _rel(lam, ref.lam) <= TOL, ("lambda", _rel(lam, ref.lam))
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("shape,ks", [("13", (1, 10, 100, 1000)), ("123", (1, 10, 1000)), ("8500", (1, 10, 200))])
-def test_fixed_k_iterates(torch_cuda, shape, ks):
+def test_fixed_k_iterates(torch_cuda, shape, ks, kernel):
     f, p = _problem(shape)
-    h = _solver(f)
+    h = _solver(f, kernel=kernel)
+    assert h.sizes.kernel == kernel
     done = 0
     for k in ks:                                   # run(k) continues from the current iterate
         h.run(k - done)
@@ -64,12 +67,13 @@ def test_fixed_k_iterates(torch_cuda, shape, ks):
         _check_state(h, oracle.run_k(p, k))
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("shape", ["13", "123", "8500"])
-def test_iterations_to_tolerance_bit_exact(torch_cuda, shape):
+def test_iterations_to_tolerance_bit_exact(torch_cuda, shape, kernel):
     f, p = _problem(shape)
     g = GOLD[shape]
     assert f.sha256() == g["sha256"], "synthetic feeder differs from the golden's"
-    h = _solver(f)
+    h = _solver(f, kernel=kernel)
     r = h.solve()
     from paper_2310_09410_b200 import CONVERGED
     assert r.outcome == CONVERGED
@@ -82,11 +86,12 @@ def test_iterations_to_tolerance_bit_exact(torch_cuda, shape):
     assert np.all(x >= p.lp.lo) and np.all(x <= p.lp.hi)
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("make", [lambda: fx.chain_1ph(4), lambda: fx.two_bus_3ph(fg.DELTA), fx.four_bus])
-def test_fixtures_fixed_k_and_solve(torch_cuda, make):
+def test_fixtures_fixed_k_and_solve(torch_cuda, make, kernel):
     f = make()
     p = oracle.build_problem(f)
-    h = _solver(f)
+    h = _solver(f, kernel=kernel)
     h.run(300)
     _check_state(h, oracle.run_k(p, 300))
     h.reset()
@@ -104,11 +109,13 @@ def test_single_partition_s1(torch_cuda):
     _check_state(h, oracle.run_k(p, 200))
 
 
-@pytest.mark.parametrize("cap", [1, 3, 37])
-def test_grid_size_independence(torch_cuda, cap):
-    """Few CTAs (many tasks per warp, few barrier participants): same K, iterates within tolerance."""
+@pytest.mark.parametrize("kw", [dict(kernel=1, grid_cap=1), dict(kernel=1, grid_cap=3), dict(kernel=1, grid_cap=37),
+                                dict(kernel=2, max_ctas=8), dict(kernel=2, max_ctas=148)])
+def test_grid_size_independence(torch_cuda, kw):
+    """Streaming with few CTAs (many tasks per warp) and resident with different chunkings
+    (more boundary exchange): same K, iterates within tolerance."""
     f, p = _problem("123")
-    h = _solver(f, grid_cap=cap)
+    h = _solver(f, **kw)
     h.run(100)
     _check_state(h, oracle.run_k(p, 100))
     h.reset()
@@ -116,9 +123,10 @@ def test_grid_size_independence(torch_cuda, cap):
     assert r.iters == GOLD["123"]["iters"]
 
 
-def test_determinism_and_reset(torch_cuda):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_determinism_and_reset(torch_cuda, kernel):
     f, _ = _problem("123")
-    h = _solver(f)
+    h = _solver(f, kernel=kernel)
     h.run(777)
     a = h.get_state()
     h.reset()
@@ -133,10 +141,11 @@ def test_determinism_and_reset(torch_cuda):
     assert np.array_equal(xl, x0[0]) and not lam.any()
 
 
-def test_set_state_resume(torch_cuda):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_set_state_resume(torch_cuda, kernel):
     """lopf_set_state / get_state: resuming from the oracle's iterate at K1 continues the oracle run."""
     f, p = _problem("13")
-    h = _solver(f)
+    h = _solver(f, kernel=kernel)
     mid = oracle.run_k(p, 400)
     h.set_state(mid.x_loc, mid.lam)
     h.run(100)
@@ -144,10 +153,11 @@ def test_set_state_resume(torch_cuda):
     _check_state(h, end)
 
 
-def test_trace_and_max_iter(torch_cuda):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_trace_and_max_iter(torch_cuda, kernel):
     f, p = _problem("13")
     from paper_2310_09410_b200 import Lopf, MAX_ITER
-    h = Lopf.setup(f, trace_every=10, max_iter=250).bind("cuda")
+    h = Lopf.setup(f, trace_every=10, max_iter=250, kernel=kernel).bind("cuda")
     r = h.solve()
     assert r.outcome == MAX_ITER and r.iters == 250
     tr = h.get_trace()
@@ -156,12 +166,23 @@ def test_trace_and_max_iter(torch_cuda):
     assert np.allclose(tr[:, 1:], o.trace, rtol=1e-7, atol=1e-12)
 
 
-def test_termination_fires_on_conjunction_only(torch_cuda):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_termination_fires_on_conjunction_only(torch_cuda, kernel):
     """Every traced sweep before K fails the test; sweep K passes both."""
     f, p = _problem("13")
     from paper_2310_09410_b200 import Lopf
-    h = Lopf.setup(f, trace_every=1, trace_cap=20000).bind("cuda")
+    h = Lopf.setup(f, trace_every=1, trace_cap=20000, kernel=kernel).bind("cuda")
     r = h.solve()
     tr = h.get_trace(cap=20000)
     ok = (tr[:, 1] <= tr[:, 3]) & (tr[:, 2] <= tr[:, 4])
     assert len(tr) == r.iters and ok[-1] and not ok[:-1].any()
+
+
+def test_resident_matches_streaming(torch_cuda):
+    """Both kernels iterate the same method: after 500 sweeps on the 8500 shape they agree to 1e-12."""
+    f, _ = _problem("8500")
+    a, b = _solver(f, kernel=1), _solver(f, kernel=2)
+    a.run(500)
+    b.run(500)
+    for u, v in zip(a.get_state(), b.get_state()):
+        assert _rel(u, v) <= 1e-12
