@@ -95,7 +95,8 @@ typedef struct {
     int32_t block_threads; /* 0 = default */
     int32_t max_ctas;      /* resident kernel: CTAs available (one per SM; 0 = 148, the B200 SM count) */
     int32_t grid_cap;      /* streaming kernel: cap on the persistent grid (0 = occupancy x SMs; test hook) */
-    int32_t reserved[3];
+    int32_t reserved[3];   /* [0] = 1: per-CTA phase cycle counters (lopf_get_profile); [1]: diagnostics phase-skip
+                              mask (bit 0 global update, bit 1 local/dual update) — results are then NOT the method */
 } lopf_options;
 
 typedef struct {
@@ -176,6 +177,10 @@ lopf_status lopf_set_state(lopf_handle *h, void *cuda_stream, const double *x_lo
 
 /* Trace rows {t, pres, dres, eps_prim, eps_dual} of the last solve: buf [cap*5]. */
 lopf_status lopf_get_trace(lopf_handle *h, void *cuda_stream, double *buf, int64_t cap, int64_t *n_rows);
+
+/* Diagnostics (resident kernel, options.reserved[0] = 1): per-CTA cycle counters of the last launch,
+ * rows {G-phase, L-phase, barrier wait, sweeps}: buf [cap*4]. */
+lopf_status lopf_get_profile(lopf_handle *h, void *cuda_stream, int64_t *buf, int64_t cap, int64_t *n_rows);
 
 void lopf_destroy(lopf_handle *h);
 

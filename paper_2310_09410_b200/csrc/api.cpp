@@ -167,6 +167,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         R.hdr = (const CtaHdr*)(b + L.off_hdr);
         R.blobs = b + L.off_blobs;
         R.xchg = (double*)(b + L.off_xchg);
+        R.flags = (unsigned long long*)(b + L.off_flags);
         R.partial = (double*)(b + L.off_partial);
         R.ctrl = (DevCtrl*)(b + L.off_ctrl);
         R.trace = (double*)(b + L.off_trace);
@@ -184,6 +185,8 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         R.rho = h->opt.rho;
         R.inv_rho = 1.0 / h->opt.rho;
         R.eps_rel = h->opt.eps_rel;
+        R.prof = h->opt.reserved[0] ? (long long*)(b + L.off_prof) : nullptr;   // diagnostics switch
+        R.skip = h->opt.reserved[1];
         h->dp = DevProblem{};
         h->dp.ctrl = R.ctrl;
         h->dp.x = R.x;
@@ -373,8 +376,8 @@ static lopf_status fetch_slots(lopf_handle* h, cudaStream_t s, std::vector<doubl
         for (int c = 0; c < L.G; ++c) {
             const CtaHdr& H = L.hdr[c];
             const uint8_t* blob = h->rp.blobs + H.blob_off;
-            CUDA_TRY(cudaMemcpyAsync(xl.data() + H.slot_base, blob + H.off_xl, 8 * (size_t)H.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
-            CUDA_TRY(cudaMemcpyAsync(lm.data() + H.slot_base, blob + H.off_lam, 8 * (size_t)H.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
+            CUDA_TRY(cudaMemcpyAsync(xl.data() + H.slot_base, blob + H.off_xl0, 8 * (size_t)H.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
+            CUDA_TRY(cudaMemcpyAsync(lm.data() + H.slot_base, blob + H.off_lam0, 8 * (size_t)H.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
         }
     }
     CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
@@ -423,8 +426,8 @@ lopf_status lopf_set_state(lopf_handle* h, void* stream, const double* x_loc, co
             const CtaHdr& H = L.hdr[c];
             uint8_t* blob = h->rp.blobs + H.blob_off;
             const size_t nb = 8 * (size_t)H.n_slots;
-            CUDA_TRY(cudaMemcpyAsync(blob + H.off_xl, xl.data() + H.slot_base, nb, cudaMemcpyHostToDevice, s), "state H2D");
-            CUDA_TRY(cudaMemcpyAsync(blob + H.off_lam, lm.data() + H.slot_base, nb, cudaMemcpyHostToDevice, s), "state H2D");
+            CUDA_TRY(cudaMemcpyAsync(blob + H.off_xl0, xl.data() + H.slot_base, nb, cudaMemcpyHostToDevice, s), "state H2D");
+            CUDA_TRY(cudaMemcpyAsync(blob + H.off_lam0, lm.data() + H.slot_base, nb, cudaMemcpyHostToDevice, s), "state H2D");
         }
     }
     CUDA_TRY(cudaMemsetAsync(&h->dp.ctrl->total, 0, sizeof(long long), s), "state memset");
@@ -444,6 +447,17 @@ lopf_status lopf_get_trace(lopf_handle* h, void* stream, double* buf, int64_t ca
         CUDA_TRY(cudaMemcpyAsync(buf, h->dp.trace, sizeof(double) * 5 * rows, cudaMemcpyDeviceToHost, s), "trace D2H");
         CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     }
+    if (n_rows) *n_rows = rows;
+    return LOPF_OK;
+}
+
+lopf_status lopf_get_profile(lopf_handle* h, void* stream, int64_t* buf, int64_t cap, int64_t* n_rows) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->bound || !h->resident() || !h->rp.prof) return fail(LOPF_E_STATE, "profiling needs the resident kernel with diagnostics enabled");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t rows = std::min<int64_t>(h->lay.G, cap);
+    CUDA_TRY(cudaMemcpyAsync(buf, h->rp.prof, sizeof(int64_t) * 4 * rows, cudaMemcpyDeviceToHost, s), "profile D2H");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     if (n_rows) *n_rows = rows;
     return LOPF_OK;
 }

@@ -108,29 +108,34 @@ struct DevProblem {                        // kernel argument (pointers into the
 // Every CTA owns a DFS-contiguous chunk of subsystems.  Its BLOB (global memory) is copied into
 // SMEM at kernel start; the iterate (x_s, lambda, u) lives in SMEM for the whole launch and is
 // written back at the end.  Offsets are bytes from the blob start.
-constexpr int kResBlock = 512;
-constexpr int kResSmemBudget = 222 * 1024;    // blob + scratch per CTA (227 KB usable on sm_100)
-// sinfo: base (bits 0-5, first slot of the subsystem in its task) | valid (bit 6) | n_s (bits 7-13) | gl (bits 14-31)
+constexpr int kResBlock = 1024;               // 31 worker warps + 1 reducer warp
+constexpr int kResSmemBudget = 222 * 1024;    // dynamic SMEM per CTA (227 KB usable on sm_100, minus static)
+// sinfo: base (bits 0-5, first slot of the subsystem in its task) | valid (bit 6) | first (bit 7: this slot
+// is the canonical first copy of a global whose x this CTA outputs) | n_s (bits 8-14) | gl (bits 15-31)
 constexpr int kResValid = 1 << 6;
-constexpr int kResNsShift = 7;
-constexpr int kResGlShift = 14;
+constexpr int kResFirst = 1 << 7;
+constexpr int kResNsShift = 8;
+constexpr int kResGlShift = 15;
 
 struct CtaHdr {                               // 128 B, one per CTA
-    int32_t n_tasks, n_slots, n_glob, n_seg, n_expl;
+    int32_t n_tasks, n_slots, n_glob, n_seg, n_nbr;
     int32_t blob_bytes, smem_bytes;
-    int32_t off_abar, off_bbar, off_xl, off_lam, off_gpar, off_tasks, off_sinfo, off_aoff, off_gsegoff, off_gseg,
-        off_gown, off_expl, off_xg;
+    // blob (global and SMEM): constant part then the state (x_s, lambda of sweep parity 0)
+    int32_t off_abar, off_bbar, off_gpar, off_tasks, off_sinfo, off_aoff, off_sexp, off_gsegoff, off_gseg, off_gown,
+        off_nbr, off_xl0, off_lam0;
+    // SMEM only (after the blob)
+    int32_t off_xl1, off_lam1, off_xout, off_dst;
     int32_t slot_base;
-    int32_t pad0;
     long long blob_off;
-    int32_t pad[4];
+    int32_t pad[2];
 };
 
 struct ResProblem {                           // resident kernel argument
     const CtaHdr* hdr;
     uint8_t* blobs;
-    double* xchg;                             // [2][n_exp] boundary u values (ping-pong)
-    double* partial;                          // [2][G][8]
+    double* xchg;                             // [2][n_exp] boundary u values (ping-pong by sweep parity)
+    double* partial;                          // [2][G][8] residual partials (ping-pong by sweep parity)
+    unsigned long long* flags;                // [G] sweeps published by each CTA (+1), zeroed per launch
     DevCtrl* ctrl;
     double* trace;
     double* x;                                // [n] solution
@@ -141,6 +146,9 @@ struct ResProblem {                           // resident kernel argument
     int32_t trace_cap, trace_every, total_slots, max_smem;
     double rho, inv_rho, eps_rel;
     long long max_iter;
+    long long* prof;                          // diagnostics: [G][4] cycles (work, publish+wait, -, sweeps) or NULL
+    int32_t skip;                             // diagnostics: bit 1 skips the update work (sync cost only)
+    int32_t pad1;
 };
 
 // Arena layout: byte offsets of every array (all 256-byte aligned).
@@ -156,7 +164,7 @@ struct Layout {
     std::vector<uint8_t> image;            // host image of the whole arena (initial state included)
     // resident kernel
     int32_t G = 0, n_exp = 0, max_smem = 0, total_slots = 0;
-    size_t off_hdr = 0, off_blobs = 0, off_xchg = 0, off_x0r = 0;
+    size_t off_hdr = 0, off_blobs = 0, off_xchg = 0, off_x0r = 0, off_prof = 0, off_flags = 0;
     std::vector<CtaHdr> hdr;               // host copy of the per-CTA headers
     std::vector<int32_t> slot_cta;         // [total slots] CTA of a global slot id
 };

@@ -117,10 +117,14 @@ int64_t chunk_bytes(const Canon& P, const std::vector<int64_t>& subs, std::vecto
     for (int64_t s : subs)
         for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) cnt[P.copy_global[k]] = 0;
     const int64_t NT = (int64_t)tasks.size();
+    bool r2 = false;
+    for (auto& t : tasks) r2 |= t.R > 1;
     int64_t b = 0;
-    for (int64_t sz : {8 * pool, 8 * NS, 8 * NS, 8 * NS, 32 * NG, 16 * NT, 4 * NS, 4 * NS, 4 * (NG + 1), 4 * NSEG, 4 * NG,
-                       8 * NX, 16 * NG})
+    for (int64_t sz : {8 * pool, 8 * NS, 32 * NG, 16 * NT, 4 * NS, 4 * NS, 4 * NS, 4 * (NG + 1), 4 * NSEG, 4 * NG,
+                       (int64_t)4 * 64, 8 * NS, 8 * NS, 8 * NS, 8 * NS, 16 * NG,
+                       (int64_t)8 * (r2 ? 64 : 32) * (kResBlock / 32)})
         b = a16(b + sz);
+    (void)NX;
     return b;
 }
 }  // namespace
@@ -236,33 +240,44 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
                 }
             }
         const int64_t NG = (int64_t)gl_list.size();
-        if (NG >= (1 << (32 - kResGlShift))) { err = "too many globals in one CTA chunk"; return LOPF_E_ARG; }
+        if (NG >= (1 << (31 - kResGlShift))) { err = "too many globals in one CTA chunk"; return LOPF_E_ARG; }
         int64_t NSEG = 0;
         for (int32_t g : gl_list) NSEG += P.seg_ptr[g + 1] - P.seg_ptr[g];
-        int64_t NX = 0;
-        for (auto& t : tasks)
-            for (int64_t s : t.subs)
-                for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) NX += xidx[k] >= 0;
         const int64_t NT = (int64_t)tasks.size();
+        bool r2 = false;
+        for (auto& t : tasks) r2 |= t.R > 1;
+        // neighbour CTAs: owners of the remote copies this chunk's segments read
+        std::vector<int32_t> nbrs;
+        for (int32_t g : gl_list)
+            for (int64_t p = P.seg_ptr[g]; p < P.seg_ptr[g + 1]; ++p) {
+                const int32_t oc = copy_chunk[P.seg_copy[p]];
+                if (oc != c && std::find(nbrs.begin(), nbrs.end(), oc) == nbrs.end()) nbrs.push_back(oc);
+            }
+        std::sort(nbrs.begin(), nbrs.end());
+        const int64_t NNB = (int64_t)nbrs.size();
         int32_t o = 0;
         h.off_abar = o;     o = a16(o + 8 * pool);
         h.off_bbar = o;     o = a16(o + 8 * NS);
-        h.off_xl = o;       o = a16(o + 8 * NS);
-        h.off_lam = o;      o = a16(o + 8 * NS);
         h.off_gpar = o;     o = a16(o + 32 * NG);
         h.off_tasks = o;    o = a16(o + 16 * NT);
         h.off_sinfo = o;    o = a16(o + 4 * NS);
         h.off_aoff = o;     o = a16(o + 4 * NS);
+        h.off_sexp = o;     o = a16(o + 4 * NS);
         h.off_gsegoff = o;  o = a16(o + 4 * (NG + 1));
         h.off_gseg = o;     o = a16(o + 4 * NSEG);
         h.off_gown = o;     o = a16(o + 4 * NG);
-        h.off_expl = o;     o = a16(o + 8 * NX);
+        h.off_nbr = o;      o = a16(o + 4 * std::max<int64_t>(NNB, 64));
+        h.off_xl0 = o;      o = a16(o + 8 * NS);
+        h.off_lam0 = o;     o = a16(o + 8 * NS);
         h.blob_bytes = o;
-        h.off_xg = o;       o = a16(o + 16 * NG);
+        h.off_xl1 = o;      o = a16(o + 8 * NS);
+        h.off_lam1 = o;     o = a16(o + 8 * NS);
+        h.off_xout = o;     o = a16(o + 16 * NG);
+        h.off_dst = o;      o = a16(o + 8 * (r2 ? 64 : 32) * (kResBlock / 32));
         h.smem_bytes = o;
         if (h.smem_bytes > kResSmemBudget) { err = "internal: chunk exceeds the SMEM budget"; return LOPF_E_ARG; }
         h.n_tasks = (int32_t)NT; h.n_slots = (int32_t)NS; h.n_glob = (int32_t)NG; h.n_seg = (int32_t)NSEG;
-        h.n_expl = (int32_t)NX;
+        h.n_nbr = (int32_t)NNB;
         h.slot_base = slot_base;
         max_smem = std::max(max_smem, h.smem_bytes);
         std::vector<uint8_t>& blob = B[c].blob;
@@ -270,13 +285,14 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         auto D = [&](int32_t off) { return (double*)(blob.data() + off); };
         auto I = [&](int32_t off) { return (int32_t*)(blob.data() + off); };
         std::memcpy(blob.data() + h.off_tasks, trec.data(), 16 * NT);
+        std::memcpy(blob.data() + h.off_nbr, nbrs.data(), 4 * NNB);
         double* abar = D(h.off_abar);
         int32_t* sinfo = I(h.off_sinfo);
         int32_t* aoff = I(h.off_aoff);
-        int2* expl = (int2*)(blob.data() + h.off_expl);
+        int32_t* sexp = I(h.off_sexp);
         B[c].x0.assign(NS, 0.0);
+        for (int64_t i = 0; i < NS; ++i) sexp[i] = -1;
         size_t si = 0;
-        int64_t nx = 0;
         for (size_t t = 0; t < tasks.size(); ++t) {
             int base = 0;
             for (int64_t s : tasks[t].subs) {
@@ -288,13 +304,15 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
                     const int64_t slot = trec[t].x + base + r;
                     const int64_t copy = P.sub_ptr[s] + r;
                     const int32_t g = P.copy_global[copy];
-                    sinfo[slot] = (base & 0x3F) | kResValid | (ns << kResNsShift) | (gl_of[g] << kResGlShift);
+                    const bool first = P.seg_copy[P.seg_ptr[g]] == copy;     // canonical first copy: writes x_g
+                    sinfo[slot] = (base & 0x3F) | kResValid | (first ? kResFirst : 0) | (ns << kResNsShift) |
+                                  (gl_of[g] << kResGlShift);
                     aoff[slot] = (int32_t)(ab + r);
+                    sexp[slot] = xidx[copy];
                     D(h.off_bbar)[slot] = P.bbar[copy];
-                    D(h.off_xl)[slot] = P.x0[copy];
+                    D(h.off_xl0)[slot] = P.x0[copy];
                     B[c].x0[slot] = P.x0[copy];
                     L.slot_of_copy[copy] = slot_base + (int32_t)slot;
-                    if (xidx[copy] >= 0) expl[nx++] = make_int2((int)slot, xidx[copy]);
                 }
                 base += ns;
             }
@@ -342,11 +360,13 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     for (auto& b : B) { b.h.blob_off = (long long)blobs_total; blobs_total = a256(blobs_total + b.blob.size()); }
     L.off_blobs = take(blobs_total);
     L.off_xchg = take(8 * 2 * (size_t)std::max(n_exp, 1));
+    L.off_flags = take(8 * (size_t)L.G);
     L.off_x0r = take(8 * (size_t)L.total_slots);
     L.off_x = take(8 * (size_t)P.n);
     L.off_partial = take(8 * 8 * 2 * (size_t)L.G);
     L.off_ctrl = take(sizeof(DevCtrl));
     L.off_trace = take(8 * 5 * (size_t)L.trace_cap);
+    L.off_prof = take(8 * 4 * (size_t)L.G);
     L.off_objidx = take(4 * obj_idx.size());
     L.off_objc = take(8 * obj_c.size());
     L.bytes = off;

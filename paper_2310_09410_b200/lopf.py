@@ -92,6 +92,7 @@ def load_library(path: str = LIB_PATH):
         "lopf_get_state": ([H, _vp, _vp, _vp, _vp], _i32),
         "lopf_set_state": ([H, _vp, _vp, _vp], _i32),
         "lopf_get_trace": ([H, _vp, _vp, _i64, _vp], _i32),
+        "lopf_get_profile": ([H, _vp, _vp, _i64, _vp], _i32),
         "lopf_destroy": ([H], None),
         "lopf_last_error": ([], C.c_char_p),
         "lopf_abi_version": ([], _i32),
@@ -162,13 +163,14 @@ class Lopf:
     @classmethod
     def setup(cls, feeder, rho: float = 100.0, eps_rel: float = 1e-3, max_iter: int = 1_000_000,
               trace_every: int = 0, trace_cap: int = 4096, single: bool = False, kernel: int = 0,
-              grid_cap: int = 0, max_ctas: int = 0) -> "Lopf":
+              grid_cap: int = 0, max_ctas: int = 0, diag_profile: bool = False, diag_skip: int = 0) -> "Lopf":
         lib = load_library()
         o = Options()
         _check(lib.lopf_options_default(C.byref(o)), "lopf_options_default")
         o.rho, o.eps_rel, o.max_iter = float(rho), float(eps_rel), int(max_iter)
         o.trace_every, o.trace_cap, o.single, o.kernel = int(trace_every), int(trace_cap), int(bool(single)), int(kernel)
         o.grid_cap, o.max_ctas = int(grid_cap), int(max_ctas)
+        o.reserved[0], o.reserved[1] = int(bool(diag_profile)), int(diag_skip)
         net, keep = _network(feeder)
         h = _vp()
         _check(lib.lopf_setup(C.byref(net), C.byref(o), C.byref(h)), "lopf_setup")
@@ -285,6 +287,15 @@ class Lopf:
         _check(load_library().lopf_get_trace(self._h, _vp(_stream_handle(stream)), _ptr(buf), cap, C.byref(n)),
                "lopf_get_trace")
         return buf[: n.value].copy()
+
+    def get_profile(self, stream=None) -> np.ndarray:
+        """Diagnostics: per-CTA cycles {G-phase, L-phase, barrier, sweeps} of the last resident launch."""
+        g = int(self.sizes.grid)
+        buf = np.zeros((g, 4), np.int64)
+        n = _i64(0)
+        _check(load_library().lopf_get_profile(self._h, _vp(_stream_handle(stream)), _ptr(buf), g, C.byref(n)),
+               "lopf_get_profile")
+        return buf[: n.value]
 
     def destroy(self):
         if self._h:
