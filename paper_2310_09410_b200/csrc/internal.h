@@ -121,10 +121,10 @@ struct CtaHdr {                               // 128 B, one per CTA
     int32_t n_tasks, n_slots, n_glob, n_seg, n_nbr;
     int32_t blob_bytes, smem_bytes;
     // blob (global and SMEM): constant part then the state (x_s, lambda of sweep parity 0)
-    int32_t off_abar, off_bbar, off_gpar, off_tasks, off_sinfo, off_aoff, off_sexp, off_gsegoff, off_gseg, off_gown,
+    int32_t off_abar, off_bbar, off_gpar, off_tasks, off_sinfo, off_sexp, off_gsegoff, off_gseg, off_gown,
         off_nbr, off_xl0, off_lam0;
     // SMEM only (after the blob)
-    int32_t off_xl1, off_lam1, off_xout, off_dst;
+    int32_t off_xl1, off_lam1, off_xout, off_dst, dst_stride;
     int32_t slot_base;
     long long blob_off;
     int32_t pad[2];

@@ -77,6 +77,7 @@ struct TaskR {
     std::vector<int64_t> subs;
 };
 
+// 64-row tasks (R = 2: lane l handles rows l and l + 32), subsystems first-fit-decreasing by n_s
 std::vector<TaskR> make_tasks(const Canon& P, const std::vector<int64_t>& subs) {
     std::vector<int64_t> v;
     for (int64_t s : subs)
@@ -86,11 +87,10 @@ std::vector<TaskR> make_tasks(const Canon& P, const std::vector<int64_t>& subs) 
     std::vector<int> room;
     for (int64_t s : v) {
         const int ns = P.n_s[s];
-        if (ns > 32) { tasks.push_back({2, ns, {s}}); room.push_back(0); continue; }
         size_t t = 0;
         for (; t < tasks.size(); ++t)
-            if (tasks[t].R == 1 && room[t] >= ns) break;
-        if (t == tasks.size()) { tasks.push_back({1, 0, {}}); room.push_back(32); }
+            if (room[t] >= ns) break;
+        if (t == tasks.size()) { tasks.push_back({2, 0, {}}); room.push_back(64); }
         tasks[t].subs.push_back(s);
         tasks[t].kmax = std::max(tasks[t].kmax, ns);
         room[t] -= ns;
@@ -101,30 +101,21 @@ std::vector<TaskR> make_tasks(const Canon& P, const std::vector<int64_t>& subs) 
 // exact SMEM bytes of a chunk (blob + xg scratch); mirrors the blob layout built below
 int64_t chunk_bytes(const Canon& P, const std::vector<int64_t>& subs, std::vector<int32_t>& cnt) {
     auto tasks = make_tasks(P, subs);
-    int64_t NS = 0, pool = 0, NG = 0, NSEG = 0, NX = 0;
-    for (auto& t : tasks) NS += 32 * t.R;
-    for (int64_t s : subs) pool += (int64_t)P.n_s[s] * P.n_s[s];
+    int64_t NS = 0, pool = 0, NG = 0, NSEG = 0;
+    int kpad = 0;
+    for (auto& t : tasks) { NS += 64; pool += (int64_t)t.kmax * 64; kpad = std::max(kpad, t.kmax); }
     for (int64_t s : subs)
         for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) {
             const int32_t g = P.copy_global[k];
             if (cnt[g]++ == 0) { ++NG; NSEG += P.seg_ptr[g + 1] - P.seg_ptr[g]; }
         }
-    for (int64_t s : subs)                       // exported copies: globals not entirely inside the chunk
-        for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) {
-            const int32_t g = P.copy_global[k];
-            NX += cnt[g] < P.seg_ptr[g + 1] - P.seg_ptr[g];
-        }
     for (int64_t s : subs)
         for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) cnt[P.copy_global[k]] = 0;
     const int64_t NT = (int64_t)tasks.size();
-    bool r2 = false;
-    for (auto& t : tasks) r2 |= t.R > 1;
     int64_t b = 0;
-    for (int64_t sz : {8 * pool, 8 * NS, 32 * NG, 16 * NT, 4 * NS, 4 * NS, 4 * NS, 4 * (NG + 1), 4 * NSEG, 4 * NG,
-                       (int64_t)4 * 64, 8 * NS, 8 * NS, 8 * NS, 8 * NS, 16 * NG,
-                       (int64_t)8 * (r2 ? 64 : 32) * (kResBlock / 32)})
+    for (int64_t sz : {8 * pool, 8 * NS, 32 * NG, 16 * NT, 4 * NS, 4 * NS, 4 * (NG + 1), 4 * NSEG, 4 * NG,
+                       (int64_t)4 * 64, 8 * NS, 8 * NS, 8 * NS, 8 * NS, 16 * NG, (int64_t)8 * (64 + kpad) * (kResBlock / 32)})
         b = a16(b + sz);
-    (void)NX;
     return b;
 }
 }  // namespace
@@ -224,16 +215,16 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         std::memset(&h, 0, sizeof(h));
         int64_t NS = 0, pool = 0;
         std::vector<int4> trec;
-        for (auto& t : tasks) {
-            trec.push_back(make_int4((int)NS, t.kmax, t.R, 0));
-            NS += 32 * t.R;
+        int kpad = 0;
+        for (auto& t : tasks) {                              // task tile: kmax columns x 64 rows, zero padded
+            trec.push_back(make_int4((int)NS, t.kmax, (int)pool, 0));
+            NS += 64;
+            pool += (int64_t)t.kmax * 64;
+            kpad = std::max(kpad, t.kmax);
         }
-        std::vector<int64_t> sub_abar;                          // compact operator offsets (doubles)
         std::vector<int32_t> gl_list;
         for (size_t t = 0; t < tasks.size(); ++t)
             for (int64_t s : tasks[t].subs) {
-                sub_abar.push_back(pool);
-                pool += (int64_t)P.n_s[s] * P.n_s[s];
                 for (int r = 0; r < P.n_s[s]; ++r) {
                     const int32_t g = P.copy_global[P.sub_ptr[s] + r];
                     if (gl_of[g] < 0) { gl_of[g] = (int32_t)gl_list.size(); gl_list.push_back(g); }
@@ -244,8 +235,6 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         int64_t NSEG = 0;
         for (int32_t g : gl_list) NSEG += P.seg_ptr[g + 1] - P.seg_ptr[g];
         const int64_t NT = (int64_t)tasks.size();
-        bool r2 = false;
-        for (auto& t : tasks) r2 |= t.R > 1;
         // neighbour CTAs: owners of the remote copies this chunk's segments read
         std::vector<int32_t> nbrs;
         for (int32_t g : gl_list)
@@ -261,7 +250,6 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         h.off_gpar = o;     o = a16(o + 32 * NG);
         h.off_tasks = o;    o = a16(o + 16 * NT);
         h.off_sinfo = o;    o = a16(o + 4 * NS);
-        h.off_aoff = o;     o = a16(o + 4 * NS);
         h.off_sexp = o;     o = a16(o + 4 * NS);
         h.off_gsegoff = o;  o = a16(o + 4 * (NG + 1));
         h.off_gseg = o;     o = a16(o + 4 * NSEG);
@@ -273,7 +261,8 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         h.off_xl1 = o;      o = a16(o + 8 * NS);
         h.off_lam1 = o;     o = a16(o + 8 * NS);
         h.off_xout = o;     o = a16(o + 16 * NG);
-        h.off_dst = o;      o = a16(o + 8 * (r2 ? 64 : 32) * (kResBlock / 32));
+        h.off_dst = o;      o = a16(o + 8 * (64 + kpad) * (kResBlock / 32));   // d staging; tail stays 0
+        h.dst_stride = 64 + kpad;
         h.smem_bytes = o;
         if (h.smem_bytes > kResSmemBudget) { err = "internal: chunk exceeds the SMEM budget"; return LOPF_E_ARG; }
         h.n_tasks = (int32_t)NT; h.n_slots = (int32_t)NS; h.n_glob = (int32_t)NG; h.n_seg = (int32_t)NSEG;
@@ -288,18 +277,16 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         std::memcpy(blob.data() + h.off_nbr, nbrs.data(), 4 * NNB);
         double* abar = D(h.off_abar);
         int32_t* sinfo = I(h.off_sinfo);
-        int32_t* aoff = I(h.off_aoff);
         int32_t* sexp = I(h.off_sexp);
         B[c].x0.assign(NS, 0.0);
         for (int64_t i = 0; i < NS; ++i) sexp[i] = -1;
-        size_t si = 0;
         for (size_t t = 0; t < tasks.size(); ++t) {
             int base = 0;
             for (int64_t s : tasks[t].subs) {
                 const int ns = P.n_s[s];
-                const int64_t ab = sub_abar[si++];
                 const double* Ab = &P.abar[P.abar_ptr[s]];
-                for (int64_t q = 0; q < (int64_t)ns * ns; ++q) abar[ab + q] = Ab[q];   // symmetric: col-major = row-major
+                for (int r = 0; r < ns; ++r)             // row base+r of the tile: tile[k][base + r] = Abar_s[r][k]
+                    for (int k = 0; k < ns; ++k) abar[(size_t)trec[t].z + (size_t)k * 64 + base + r] = Ab[(size_t)r * ns + k];
                 for (int r = 0; r < ns; ++r) {
                     const int64_t slot = trec[t].x + base + r;
                     const int64_t copy = P.sub_ptr[s] + r;
@@ -307,7 +294,6 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
                     const bool first = P.seg_copy[P.seg_ptr[g]] == copy;     // canonical first copy: writes x_g
                     sinfo[slot] = (base & 0x3F) | kResValid | (first ? kResFirst : 0) | (ns << kResNsShift) |
                                   (gl_of[g] << kResGlShift);
-                    aoff[slot] = (int32_t)(ab + r);
                     sexp[slot] = xidx[copy];
                     D(h.off_bbar)[slot] = P.bbar[copy];
                     D(h.off_xl0)[slot] = P.x0[copy];
@@ -342,7 +328,7 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     L.n_slots = slot_base;
     for (auto& b : B) L.n_tasks += b.h.n_tasks;
     int64_t pool_all = 0;
-    for (int64_t s = 0; s < P.S; ++s) pool_all += (int64_t)P.n_s[s] * P.n_s[s];
+    for (int c = 0; c < L.G; ++c) pool_all += (B[c].h.off_bbar - B[c].h.off_abar) / 8;
     L.abar_doubles = pool_all;
 
     // ---- objective, arena ---------------------------------------------------------------------------
@@ -360,10 +346,10 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     for (auto& b : B) { b.h.blob_off = (long long)blobs_total; blobs_total = a256(blobs_total + b.blob.size()); }
     L.off_blobs = take(blobs_total);
     L.off_xchg = take(8 * 2 * (size_t)std::max(n_exp, 1));
-    L.off_flags = take(8 * (size_t)L.G);
+    L.off_flags = take(8 * 32 * (size_t)(L.G + 1));   // one flag per 256-byte line + the published count
     L.off_x0r = take(8 * (size_t)L.total_slots);
     L.off_x = take(8 * (size_t)P.n);
-    L.off_partial = take(8 * 8 * 2 * (size_t)L.G);
+    L.off_partial = take(8 * 8 * 4 * (size_t)L.G);     // 4 sweep slots (lagged decision, see resident.cu)
     L.off_ctrl = take(sizeof(DevCtrl));
     L.off_trace = take(8 * 5 * (size_t)L.trace_cap);
     L.off_prof = take(8 * 4 * (size_t)L.G);

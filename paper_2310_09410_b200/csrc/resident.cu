@@ -10,11 +10,12 @@
 //     a5  d = -rho v - lambda, x_s = (1/rho) Abar_s d + bbar_s                  (closed_2)
 //     a6  lambda_s += rho (v - x_s)                                            (ADMM-3)
 //         boundary copies publish u to the exchange buffer; five residual sums per lane
-//   reducer (1 warp), concurrently: waits until every CTA has published sweep t, reduces the residual
-//     partials of sweep t in CTA order and takes the (termination) decision;
-//     identical in every CTA.  A stop at t discards the speculative sweep t+1 (state t is the other
-//     ping-pong buffer).
-//   publish: CTA partials, then flag[c] = t+2 (release); wait for the neighbour CTAs' flags only.
+//   reducer (1 warp), concurrently with the workers and the publish phase: waits until every CTA has
+//     published sweep t, reduces the residual partials of sweep t in CTA order and takes the
+//     (termination) decision; identical in every CTA.  A stop at t discards the
+//     speculative sweep t+1 (state t is the other ping-pong buffer).  Partials use 4 sweep slots: a CTA
+//     can run at most 3 sweeps ahead of the slowest reducer.
+//   publish: CTA partials, fence.acq_rel, flag[c] = t+2; wait for the neighbour CTAs' flags only.
 // No grid-wide barrier inside the loop; one at exit.  Diagnostics: optional per-CTA cycle counters.
 #include <cuda_runtime.h>
 
@@ -31,6 +32,7 @@ constexpr int RW = RB / 32;
 constexpr int NWORK = RW - 1;              // worker warps 0 .. RW-2
 constexpr int RED = RW - 1;                // reducer warp
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kPer = 5;                    // flags / partials per reducer lane per round (G <= 160 in one round)
 
 __device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p) {
     unsigned long long v;
@@ -45,6 +47,9 @@ __device__ __forceinline__ unsigned long long ld_rlx(const unsigned long long* p
 __device__ __forceinline__ void st_rel(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_rlx(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // consensus input u = x_s - lambda / rho, formed with the same rounding wherever it is needed
@@ -52,81 +57,84 @@ __device__ __forceinline__ double u_of(const double x, const double l, const dou
     return __fma_rn(-l, inv_rho, x);
 }
 
-struct Ctx {
-    const int32_t* sinfo;
-    const int32_t* saoff;
-    const int32_t* sexp;
-    const double* sabar;
-    const double* sbbar;
-    const int32_t* gsegoff;
-    const int32_t* gseg;
-    const double4* gpar;
-    const double* xl_c;
-    const double* lam_c;
-    double* xl_n;
-    double* lam_n;
-    double* xout_n;
+extern __shared__ __align__(16) uint8_t sm[];
+
+// SMEM accessors on 32-bit byte offsets (LDS/STS with 32-bit addresses, no 64-bit generic pointers)
+__device__ __forceinline__ double& Dd(int off, int i) { return reinterpret_cast<double*>(sm + off)[i]; }
+__device__ __forceinline__ int Ii(int off, int i) { return reinterpret_cast<const int*>(sm + off)[i]; }
+
+struct Ctx {                                       // byte offsets into SMEM + the two exchange slots
+    int sinfo, sexp, sabar, sbbar, gsegoff, gseg, gpar;
+    int xl_c, lam_c, xl_n, lam_n, xout_n, dst;
     const double* xch_c;
     double* xch_n;
     double rho, inv_rho;
 };
 
-template <int R>
-__device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double* __restrict__ dst, double (&acc)[5],
-                                           const int lane) {
-    double v[R], lam[R], xo[R];
-    int info[R];
+// value of one consensus-segment entry: u of an own copy (SMEM) or of a boundary copy (exchange buffer)
+__device__ __forceinline__ double seg_u(const Ctx& C, const int e) {
+    return e >= 0 ? u_of(Dd(C.xl_c, e), Dd(C.lam_c, e), C.inv_rho) : __ldcg(C.xch_c + (-e - 1));
+}
+
+// one 64-row task; lane l owns rows l and l + 32 (two independent dependency chains)
+__device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double (&acc)[5], const int lane) {
+    double v[2], lam[2], xo[2];
+    int info[2];
 #pragma unroll
-    for (int h = 0; h < R; ++h) {
+    for (int h = 0; h < 2; ++h) {
         const int slot = tr.x + h * 32 + lane;
-        info[h] = C.sinfo[slot];
+        info[h] = Ii(C.sinfo, slot);
         double d = 0.0;
         v[h] = lam[h] = xo[h] = 0.0;
         if (info[h] & kResValid) {
             const int gl = info[h] >> kResGlShift;
-            const int q0 = C.gsegoff[gl], q1 = C.gsegoff[gl + 1];
+            const int q0 = Ii(C.gsegoff, gl), nq = Ii(C.gsegoff, gl + 1) - q0;
+            int e[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) e[j] = j < nq ? Ii(C.gseg, q0 + j) : 0;
+            double u[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) u[j] = j < nq ? seg_u(C, e[j]) : 0.0;
             double sigma = 0.0;                                          // canonical copy order
-            for (int q = q0; q < q1; ++q) {
-                const int e = C.gseg[q];
-                sigma += e >= 0 ? u_of(C.xl_c[e], C.lam_c[e], C.inv_rho) : __ldcg(C.xch_c + (-e - 1));
-            }
-            const double4 gp = C.gpar[gl];
-            const double xg = fmin(fmax((sigma - gp.x) * gp.y, gp.z), gp.w);   // IEEE +-inf = no clamp
-            if (info[h] & kResFirst) C.xout_n[gl] = xg;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < nq) sigma += u[j];
+            for (int q = 4; q < nq; ++q) sigma += seg_u(C, Ii(C.gseg, q0 + q));
+            const double2 g0 = reinterpret_cast<const double2*>(sm + C.gpar)[2 * gl];       // {c/rho, 1/nu}
+            const double2 g1 = reinterpret_cast<const double2*>(sm + C.gpar)[2 * gl + 1];   // {lo, hi}
+            const double xg = fmin(fmax((sigma - g0.x) * g0.y, g1.x), g1.y);   // IEEE +-inf = no clamp
+            if (info[h] & kResFirst) Dd(C.xout_n, gl) = xg;
             v[h] = xg;
-            lam[h] = C.lam_c[slot];
-            xo[h] = C.xl_c[slot];
+            lam[h] = Dd(C.lam_c, slot);
+            xo[h] = Dd(C.xl_c, slot);
             d = -C.rho * xg - lam[h];
         }
-        dst[h * 32 + lane] = d;
+        Dd(C.dst, h * 32 + lane) = d;
     }
     __syncwarp();
-    double ax[R];
-    int ns[R], ao[R];
-#pragma unroll
-    for (int h = 0; h < R; ++h) {
-        ax[h] = 0.0;
-        ns[h] = (info[h] >> kResNsShift) & 0x7F;                        // 0 for unused lanes
-        ao[h] = C.saoff[tr.x + h * 32 + lane];
-    }
-    const double* __restrict__ db = dst + (R == 1 ? (info[0] & 0x3F) : 0);
+    // local update: x_s = (1/rho) Abar_s d + bbar_s.  The task tile is zero-padded (tile[k][row] = 0 for
+    // k >= n_s of the row's subsystem), so the loop has no masks: 2 tile loads + 2 staged-d loads + 2 DFMA
+    // per column; d indices beyond the subsystem land on finite d values or the zeroed staging tail.
     const int kmax = tr.y;
+    const int at = C.sabar + 8 * (tr.z + lane);                          // byte offset of tile[0][lane]
+    const int d0 = C.dst + 8 * (info[0] & 0x3F), d1 = C.dst + 8 * (info[1] & 0x3F);
+    double ax0 = 0.0, ax1 = 0.0;
 #pragma unroll 4
     for (int k = 0; k < kmax; ++k) {
-#pragma unroll
-        for (int h = 0; h < R; ++h)
-            if (k < ns[h]) ax[h] = fma(C.sabar[ao[h] + k * ns[h]], db[k], ax[h]);   // sum_k Abar_s[r][k] d_k
+        ax0 = fma(Dd(at, 64 * k), Dd(d0, k), ax0);
+        ax1 = fma(Dd(at, 64 * k + 32), Dd(d1, k), ax1);
     }
+    const double axr[2] = {ax0, ax1};
     __syncwarp();                                                        // dst is reused by the next task
 #pragma unroll
-    for (int h = 0; h < R; ++h) {
+    for (int h = 0; h < 2; ++h) {
         if (!(info[h] & kResValid)) continue;
         const int slot = tr.x + h * 32 + lane;
-        const double xn = fma(ax[h], C.inv_rho, C.sbbar[slot]);          // (1/rho) Abar d + bbar  (closed_2)
+        const double xn = fma(axr[h], C.inv_rho, Dd(C.sbbar, slot));         // (1/rho) Abar d + bbar
         const double ln = lam[h] + C.rho * (v[h] - xn);                  // ADMM-3
-        C.xl_n[slot] = xn;
-        C.lam_n[slot] = ln;
-        const int e = C.sexp[slot];
+        Dd(C.xl_n, slot) = xn;
+        Dd(C.lam_n, slot) = ln;
+        const int e = Ii(C.sexp, slot);
         if (e >= 0) __stcg(C.xch_n + e, u_of(xn, ln, C.inv_rho));        // boundary copy -> exchange
         const double r = v[h] - xn, dx = xn - xo[h];
         acc[0] += r * r;
@@ -137,8 +145,9 @@ __device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double* 
     }
 }
 
+constexpr int kFlagStride = 32;                    // one flag per 256-byte line (no L2 hot spot)
+
 __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
-    extern __shared__ __align__(16) uint8_t sm[];
     __shared__ CtaHdr H;
     __shared__ double red[RW][5];
     __shared__ double s_res[4];
@@ -157,64 +166,62 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     }
     __syncthreads();
     const int NS = H.n_slots, NG = H.n_glob, NT = H.n_tasks, NNB = H.n_nbr;
-    double* xl[2] = {(double*)(sm + H.off_xl0), (double*)(sm + H.off_xl1)};
-    double* lm[2] = {(double*)(sm + H.off_lam0), (double*)(sm + H.off_lam1)};
-    double* xout = (double*)(sm + H.off_xout);                   // [2][NG]
-    const int32_t* sexp = (const int32_t*)(sm + H.off_sexp);
-    const int32_t* gown = (const int32_t*)(sm + H.off_gown);
-    const int32_t* nbr = (const int32_t*)(sm + H.off_nbr);
-    const int4* stasks = (const int4*)(sm + H.off_tasks);
-    const int dst_stride = (H.smem_bytes - H.off_dst) / (8 * RW);      // 32 or 64 doubles per warp
-    double* dst = (double*)(sm + H.off_dst) + wid * dst_stride;
+    const int dst_stride = H.dst_stride;                              // 64 + largest task width, doubles
+    for (int i = tid; i < RW * dst_stride; i += RB) Dd(H.off_dst, i) = 0.0;   // zero tail of the d staging
     Ctx C;
-    C.sinfo = (const int32_t*)(sm + H.off_sinfo);
-    C.saoff = (const int32_t*)(sm + H.off_aoff);
-    C.sexp = sexp;
-    C.sabar = (const double*)(sm + H.off_abar);
-    C.sbbar = (const double*)(sm + H.off_bbar);
-    C.gsegoff = (const int32_t*)(sm + H.off_gsegoff);
-    C.gseg = (const int32_t*)(sm + H.off_gseg);
-    C.gpar = (const double4*)(sm + H.off_gpar);
+    C.sinfo = H.off_sinfo; C.sexp = H.off_sexp; C.sabar = H.off_abar; C.sbbar = H.off_bbar;
+    C.gsegoff = H.off_gsegoff; C.gseg = H.off_gseg; C.gpar = H.off_gpar;
+    C.dst = H.off_dst + 8 * wid * dst_stride;
     C.rho = P.rho;
     C.inv_rho = P.inv_rho;
+    unsigned long long* myflag = P.flags + (size_t)cta * kFlagStride;
+    unsigned long long* pub = P.flags + (size_t)G * kFlagStride;       // CTAs x sweeps published
     const long long total0 = *(volatile long long*)&P.ctrl->total;
     const bool prof = P.prof != nullptr;
     long long c_w = 0, c_p = 0, c0 = 0;
 
     // initial publication: boundary u of the state into exchange slot 0; flag = 1
     for (int i = tid; i < NS; i += RB) {
-        const int e = sexp[i];
-        if (e >= 0) __stcg(P.xchg + e, u_of(xl[0][i], lm[0][i], P.inv_rho));
+        const int e = Ii(H.off_sexp, i);
+        if (e >= 0) __stcg(P.xchg + e, u_of(Dd(H.off_xl0, i), Dd(H.off_lam0, i), P.inv_rho));
     }
     __syncthreads();
     if (tid == 0) {
         __threadfence();
-        st_rel(P.flags + cta, 1ULL);
-        for (int i = 0; i < NNB; ++i)
-            while (ld_acq(P.flags + nbr[i]) < 1ULL) {
+        st_rlx(myflag, 1ULL);
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pub) : "memory");
+    }
+    if (wid == 0) {
+        for (int i = lane; i < NNB; i += 32)
+            while (ld_rlx(P.flags + (size_t)Ii(H.off_nbr, i) * kFlagStride) < 1ULL) {
             }
+        fence_acq_rel();
     }
     __syncthreads();
 
     long long t = 0;                                   // sweeps completed; state t in buffer t & 1
     for (;;) {
-        const int cur = (int)(t & 1), nxt = cur ^ 1;
+        const int cur = (int)(t & 1);
         if (prof && tid == 0) c0 = clock64();
         if (wid == RED) {
-            if (t >= 1) {                              // decision for sweep t
-                const unsigned long long need = (unsigned long long)t + 1ULL;
-                for (;;) {
-                    bool ok = true;
-                    for (int b = lane; b < G; b += 32) ok &= ld_rlx(P.flags + b) >= need;
-                    if (__all_sync(kFull, ok)) break;
-                    __nanosleep(32);
-                }
+            if (t >= 1) {                              // decision for sweep t: every CTA has published it
+                const unsigned long long need = (unsigned long long)G * (unsigned long long)(t + 1);
+                while (ld_rlx(pub) < need) __nanosleep(20);
                 fence_acq_rel();
                 double ps[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-                const double* part = P.partial + (size_t)(t & 1) * G * 8;
-                for (int b = lane; b < G; b += 32) {
+                const double* part = P.partial + (size_t)(t & 3) * G * 8;
+                for (int b0 = 0; b0 < G; b0 += 32 * kPer) {
+                    double pv[kPer][5];
 #pragma unroll
-                    for (int k = 0; k < 5; ++k) ps[k] += __ldcg(part + (size_t)b * 8 + k);
+                    for (int j = 0; j < kPer; ++j) {
+                        const int b = b0 + j * 32 + lane;
+#pragma unroll
+                        for (int k = 0; k < 5; ++k) pv[j][k] = b < G ? __ldcg(part + (size_t)b * 8 + k) : 0.0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < kPer; ++j)
+#pragma unroll
+                        for (int k = 0; k < 5; ++k) ps[k] += pv[j][k];     // CTA order per lane: fixed
                 }
 #pragma unroll
                 for (int k = 0; k < 5; ++k) {
@@ -242,31 +249,34 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
             }
         } else {                                       // workers: sweep t+1 (speculative until decided)
             double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            if (t < P.max_iter && !(P.skip & 2)) {
-                C.xl_c = xl[cur]; C.lam_c = lm[cur]; C.xl_n = xl[nxt]; C.lam_n = lm[nxt];
-                C.xout_n = xout + nxt * NG;
+            const bool busy = t < P.max_iter && !(P.skip & 2) && wid < NT;
+            if (busy) {
+                C.xl_c = cur ? H.off_xl1 : H.off_xl0;
+                C.lam_c = cur ? H.off_lam1 : H.off_lam0;
+                C.xl_n = cur ? H.off_xl0 : H.off_xl1;
+                C.lam_n = cur ? H.off_lam0 : H.off_lam1;
+                C.xout_n = H.off_xout + (cur ? 0 : 8 * NG);
                 C.xch_c = P.xchg + (size_t)cur * P.n_exp;
-                C.xch_n = P.xchg + (size_t)nxt * P.n_exp;
+                C.xch_n = P.xchg + (size_t)(cur ^ 1) * P.n_exp;
                 for (int task = wid; task < NT; task += NWORK) {
-                    const int4 tr = stasks[task];
-                    if (tr.z == 1) task_sweep<1>(C, tr, dst, acc, lane);
-                    else task_sweep<2>(C, tr, dst, acc, lane);
+                    task_sweep(C, reinterpret_cast<const int4*>(sm + H.off_tasks)[task], acc, lane);
                 }
             }
+            if (busy) {                                // idle warps contribute exact zeros without shuffling
 #pragma unroll
-            for (int k = 0; k < 5; ++k) {
+                for (int k = 0; k < 5; ++k) {
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(kFull, acc[k], off);
+                    for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(kFull, acc[k], off);
+                }
             }
             if (lane == 0) {
 #pragma unroll
                 for (int k = 0; k < 5; ++k) red[wid][k] = acc[k];
             }
         }
-        __syncthreads();                               // [A]
+        __syncthreads();                               // [A]: sweep t+1 computed (if t < max_iter)
         if (prof && tid == 0) { const long long c1 = clock64(); c_w += c1 - c0; c0 = c1; }
-        if (s_stop) break;                             // state t (buffer cur); x^t in xout[cur]
-        if (wid == 0) {                                // publish sweep t+1, then wait for the neighbours
+        if (wid == 0 && t < P.max_iter) {              // publish sweep t+1, then wait for the neighbours
             double s[5];
 #pragma unroll
             for (int k = 0; k < 5; ++k) {
@@ -275,20 +285,22 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                 for (int off = 16; off > 0; off >>= 1) s[k] += __shfl_xor_sync(kFull, s[k], off);
             }
             if (lane == 0) {
-                double* part = P.partial + (size_t)((t + 1) & 1) * G * 8 + (size_t)cta * 8;
+                double* part = P.partial + (size_t)((t + 1) & 3) * G * 8 + (size_t)cta * 8;
 #pragma unroll
                 for (int k = 0; k < 5; ++k) __stcg(part + k, s[k]);
-                __threadfence();
-                st_rel(P.flags + cta, (unsigned long long)t + 2ULL);
+                fence_acq_rel();                       // release: exports + partials before the flag
+                st_rlx(myflag, (unsigned long long)t + 2ULL);
+                asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pub) : "memory");
             }
             const unsigned long long need = (unsigned long long)t + 2ULL;
             for (int i = lane; i < NNB; i += 32)
-                while (ld_acq(P.flags + nbr[i]) < need) {
+                while (ld_rlx(P.flags + (size_t)Ii(H.off_nbr, i) * kFlagStride) < need) {
                 }
-            __syncwarp();
+            fence_acq_rel();
         }
-        __syncthreads();                               // [B]
+        __syncthreads();                               // [B]: decision for sweep t known (reducer)
         if (prof && tid == 0) c_p += clock64() - c0;
+        if (s_stop) break;                             // state t (buffer t & 1); x^t in xout[t & 1]
         ++t;
     }
 
@@ -297,14 +309,15 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     {
         double* gx = (double*)(blob + H.off_xl0);
         double* gl = (double*)(blob + H.off_lam0);
+        const int oxl = fin ? H.off_xl1 : H.off_xl0, olm = fin ? H.off_lam1 : H.off_lam0;
         for (int i = tid; i < NS; i += RB) {
-            __stcg(gx + i, xl[fin][i]);
-            __stcg(gl + i, lm[fin][i]);
+            __stcg(gx + i, Dd(oxl, i));
+            __stcg(gl + i, Dd(olm, i));
         }
     }
     for (int j = tid; j < NG; j += RB) {
-        const int g = gown[j];
-        if (g >= 0) __stcg(P.x + g, xout[fin * NG + j]);
+        const int g = Ii(H.off_gown, j);
+        if (g >= 0) __stcg(P.x + g, Dd(H.off_xout, fin * NG + j));
     }
     if (prof && tid == 0) {
         long long* pr = P.prof + 4 * cta;
@@ -362,7 +375,7 @@ lopf_status launch_resident(const ResProblem& P, void* stream, std::string& err)
     cudaError_t e = cudaFuncSetAttribute(admm_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P.max_smem);
     if (e == cudaSuccess) e = cudaMemsetAsync(P.ctrl, 0, 2 * sizeof(unsigned long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(&P.ctrl->trace_rows, 0, sizeof(long long), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(P.flags, 0, sizeof(unsigned long long) * P.G, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P.flags, 0, sizeof(unsigned long long) * 32 * (P.G + 1), s);
     if (e == cudaSuccess && P.max_iter > 0) {
         ResProblem Q = P;
         void* args[] = {&Q};
