@@ -89,9 +89,10 @@ def cpu_oracle_rate(feeder, sweeps: int):
     """Oracle sweeps/s on this host (one thread), from the initial point; setup excluded."""
     import oracle
     p = oracle.build_problem(feeder)
-    oracle.run_k(p, 5)                                   # warm the C library
+    x0 = oracle.initial_state(p)
+    oracle.run_k(p, 5, state=x0)                         # warm the C library
     t = time.perf_counter()
-    oracle.run_k(p, sweeps)
+    oracle.run_k(p, sweeps, state=x0)
     dt = time.perf_counter() - t
     return sweeps / dt, dt
 
@@ -124,11 +125,12 @@ def main():
             return
         import oracle
         p = oracle.build_problem(feeder)
+        x0 = oracle.initial_state(p)                     # the oracle's own initial point
         for _ in range(args.warmup):
-            oracle.run_k(p, args.ref_sweeps)
+            oracle.run_k(p, args.ref_sweeps, state=x0)
         t = time.perf_counter()
         for _ in range(args.steps):
-            oracle.run_k(p, args.ref_sweeps)
+            oracle.run_k(p, args.ref_sweeps, state=x0)
         dt = time.perf_counter() - t
         v = args.steps * args.ref_sweeps / dt
         sample = f"{args.ref_sweeps} sweeps from the initial point per step (oracle O6 loop only; setup excluded)"
