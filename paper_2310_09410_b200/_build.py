@@ -19,11 +19,13 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile liblopf.so; `out` / `defines` build A/B variants (e.g. defines=["LOPF_BFIRST=1"])."""
+    so = out or SO
+    if not force and out is None and not _stale():
         return SO
-    tmp = SO + f".tmp{os.getpid()}"
-    cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-O3,-Wall",
+    tmp = so + f".tmp{os.getpid()}"
+    cmd = [NVCC, *[f"-D{d}" for d in defines], "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-O3,-Wall",
            "-shared", "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES, "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -31,10 +33,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building liblopf.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, SO)
-    with open(os.path.join(HERE, "ptxas_report.txt"), "w") as fh:
-        fh.write(res.stderr)
-    return SO
+    os.replace(tmp, so)
+    if out is None:
+        with open(os.path.join(HERE, "ptxas_report.txt"), "w") as fh:
+            fh.write(res.stderr)
+    return so
 
 
 if __name__ == "__main__":

@@ -132,6 +132,12 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
     }
     sz->alg_bytes = 8 * (psym + nbbar + 6 * P.nc + 4 * P.n + h->lay.n_obj) + 4 * (2 * P.nc + P.n + 1);
     sz->kernel = h->lay.kernel;
+    if (h->resident()) {                    // diagnostics: boundary tasks, largest SMEM footprint
+        int mt = 0;
+        for (const auto& c : h->lay.hdr) mt = std::max(mt, c.n_tasks);
+        sz->reserved[0] = mt;                 // largest task count of a CTA
+        sz->reserved[1] = h->lay.max_smem;
+    }
     sz->grid = h->resident() ? h->lay.G : h->grid;
     sz->block = h->resident() ? kResBlock : kStreamBlock;
     return LOPF_OK;

@@ -150,12 +150,15 @@ constexpr int kFlagStride = 32;                    // one flag per 256-byte line
 __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     __shared__ CtaHdr H;
     __shared__ double red[RW][5];
-    __shared__ double s_res[4];
-    __shared__ int s_stop, s_conv, s_num;
+    __shared__ double s_res[2][4];                 // decision records double-buffered by sweep parity: the
+    __shared__ int s_stop[2], s_conv[2], s_num[2]; // reducer writes t+1's while slow warps still read t's
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
     if (tid < (int)(sizeof(CtaHdr) / 4)) ((int*)&H)[tid] = ((const int*)(P.hdr + cta))[tid];
-    if (tid == 0) { s_stop = 0; s_conv = 0; s_num = 0; s_res[0] = s_res[1] = s_res[2] = s_res[3] = 0.0; }
+    if (tid < 2) {
+        s_stop[tid] = 0; s_conv[tid] = 0; s_num[tid] = 0;
+        s_res[tid][0] = s_res[tid][1] = s_res[tid][2] = s_res[tid][3] = 0.0;
+    }
     __syncthreads();
     uint8_t* blob = P.blobs + H.blob_off;
     {
@@ -195,6 +198,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
         for (int i = lane; i < NNB; i += 32)
             while (ld_rlx(P.flags + (size_t)Ii(H.off_nbr, i) * kFlagStride) < 1ULL) {
             }
+        __syncwarp();                              // all lanes past all polls before the fence
         fence_acq_rel();
     }
     __syncthreads();
@@ -234,9 +238,10 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                     const int num = !(isfinite(ps[0]) && isfinite(ps[1]) && isfinite(ps[2]) && isfinite(ps[3]) &&
                                       isfinite(ps[4]));
                     const int conv = P.test && pres <= ep && dres <= ed;
-                    s_res[0] = pres; s_res[1] = dres; s_res[2] = ep; s_res[3] = ed;
-                    s_conv = conv; s_num = num;
-                    s_stop = conv || num || t >= P.max_iter;
+                    const int q = (int)(t & 1);
+                    s_res[q][0] = pres; s_res[q][1] = dres; s_res[q][2] = ep; s_res[q][3] = ed;
+                    s_conv[q] = conv; s_num[q] = num;
+                    s_stop[q] = conv || num || t >= P.max_iter;
                     if (cta == 0 && P.trace_every > 0 && (t % P.trace_every) == 0) {
                         const long long row = t / P.trace_every - 1;
                         if (row < P.trace_cap) {
@@ -296,11 +301,12 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
             for (int i = lane; i < NNB; i += 32)
                 while (ld_rlx(P.flags + (size_t)Ii(H.off_nbr, i) * kFlagStride) < need) {
                 }
+            __syncwarp();                              // all lanes past all polls before the fence
             fence_acq_rel();
         }
         __syncthreads();                               // [B]: decision for sweep t known (reducer)
         if (prof && tid == 0) c_p += clock64() - c0;
-        if (s_stop) break;                             // state t (buffer t & 1); x^t in xout[t & 1]
+        if (s_stop[t & 1]) break;                             // state t (buffer t & 1); x^t in xout[t & 1]
         ++t;
     }
 
@@ -333,12 +339,13 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
             double obj = 0.0;
             for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * __ldcg(P.x + P.obj_idx[j]);
             DevCtrl* c = P.ctrl;
-            c->res[0] = s_res[0]; c->res[1] = s_res[1]; c->res[2] = s_res[2]; c->res[3] = s_res[3];
+            const int q = (int)(t & 1);
+            c->res[0] = s_res[q][0]; c->res[1] = s_res[q][1]; c->res[2] = s_res[q][2]; c->res[3] = s_res[q][3];
             c->objective = obj;
             c->iters = t;
             c->total = total0 + t;
-            c->outcome = s_conv ? LOPF_CONVERGED : LOPF_MAX_ITER;
-            c->numeric = s_num;
+            c->outcome = s_conv[q] ? LOPF_CONVERGED : LOPF_MAX_ITER;
+            c->numeric = s_num[q];
         }
     }
 }

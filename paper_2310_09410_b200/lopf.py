@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblopf.so")
+LIB_PATH = os.environ.get("LOPF_LIB", os.path.join(_HERE, "liblopf.so"))   # override: A/B of builds
 
 STATUS = {0: "LOPF_OK", 1: "LOPF_E_ARG", 2: "LOPF_E_NETWORK", 3: "LOPF_E_ORPHAN", 4: "LOPF_E_INFEASIBLE_SUB",
           5: "LOPF_E_RANK", 6: "LOPF_E_CUDA", 7: "LOPF_E_NCCL", 8: "LOPF_E_NUMERIC", 9: "LOPF_E_STATE"}
@@ -289,7 +289,8 @@ class Lopf:
         return buf[: n.value].copy()
 
     def get_profile(self, stream=None) -> np.ndarray:
-        """Diagnostics: per-CTA cycles {G-phase, L-phase, barrier, sweeps} of the last resident launch."""
+        """Diagnostics: per-CTA cycles {work, publish + neighbour wait, -, sweeps} of the last resident launch.
+        The counters perturb the kernel: use them for relative shares, not absolute times."""
         g = int(self.sizes.grid)
         buf = np.zeros((g, 4), np.int64)
         n = _i64(0)

@@ -186,3 +186,17 @@ def test_resident_matches_streaming(torch_cuda):
     b.run(500)
     for u, v in zip(a.get_state(), b.get_state()):
         assert _rel(u, v) <= 1e-12
+
+
+@pytest.mark.parametrize("shape,k", [("123", 600), ("8500", 200)])
+def test_resident_race_stress(torch_cuda, shape, k):
+    """Repeated multi-launch runs of the resident kernel (neighbour flags, lagged decision, ping-pong
+    state) must all land on the oracle's iterate: guards the inter-CTA protocol against rare races."""
+    f, p = _problem(shape)
+    ref = oracle.run_k(p, k)
+    h = _solver(f, kernel=2)
+    for _ in range(8):
+        h.reset()
+        for part in (1, k // 3, k - 1 - k // 3):
+            h.run(part)
+        _check_state(h, ref)

@@ -23,6 +23,6 @@ for skip, label in ((0, "full sweep"), (2, "sync only (no update work)")):
         r = h.run(a.iters)
     pr = h.get_profile()
     us = 1e3 * r.solve_ms / a.iters
-    cyc = pr[:, :3] / np.maximum(pr[:, 3:4], 1)
-    print(f"{label:26s} G={h.sizes.grid:3d} {us:7.3f} us/sweep | cycles/sweep mean [work+decision, publish+wait, -] = "
-          f"{cyc.mean(0).round(0)}  max = {cyc.max(0).round(0)}", flush=True)
+    cyc = pr[:, 0:2] / np.maximum(pr[:, 3:4], 1)
+    print(f"{label:26s} G={h.sizes.grid:3d} {us:7.3f} us/sweep (instrumented) | cycles/sweep [work, publish+wait] "
+          f"mean {cyc.mean(0).round(0)} max {cyc.max(0).round(0)}", flush=True)
