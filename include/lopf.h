@@ -107,7 +107,8 @@ typedef struct {
     int32_t grid;          /* CTAs of the persistent launch (known after bind) */
     int32_t block;         /* threads per CTA */
     int32_t max_ns, max_ms;
-    int32_t reserved[3];
+    int32_t n_scen;        /* scenarios of a batch handle (lopf_setup_batch), else 0 */
+    int32_t reserved[2];
 } lopf_sizes;
 
 typedef struct {
@@ -127,6 +128,28 @@ lopf_status lopf_options_default(lopf_options *o);
 lopf_status lopf_setup(const lopf_network *net, const lopf_options *opt, lopf_handle **out);
 
 lopf_status lopf_sizes_get(const lopf_handle *h, lopf_sizes *sz);
+
+/* Batch of n_scen load scenarios of one network (BASELINE.json configs[3]): scenario s scales every
+ * load's (a, b) by load_scale[s * n_load + l] (> 0).  Each scenario is an independent run of
+ * Algorithm 1 with its own (termination) test; only the operators of subsystems that hold a load
+ * differ between scenarios (VDLM-1/2).  lopf_solve / lopf_run / lopf_reset then act
+ * on every scenario; lopf_result reports iters = max over scenarios, outcome = CONVERGED iff every
+ * scenario converged, objective = sum of the scenarios' objectives.  Canonical getters describe the
+ * shared structure; per-scenario data comes from the *_scen getters below. */
+lopf_status lopf_setup_batch(const lopf_network *net, const lopf_options *opt, int32_t n_scen,
+                             const double *load_scale, lopf_handle **out);
+
+/* Per-scenario outcome of the last batch launch: iters [n_scen], outcome [n_scen] (0 converged,
+ * 2 max_iter, 8 numeric), res [n_scen*4] {pres, dres, eps_prim, eps_dual}, objective [n_scen]. */
+lopf_status lopf_get_batch_results(lopf_handle *h, void *cuda_stream, int64_t *iters, int32_t *outcome,
+                                   double *res, double *objective);
+
+/* Scenario scen's iterate (canonical order): x [n], x_loc, lam [n_copies]; any pointer may be NULL. */
+lopf_status lopf_get_state_scen(lopf_handle *h, void *cuda_stream, int32_t scen, double *x, double *x_loc,
+                                double *lam);
+
+/* Scenario scen's operator of subsystem s: abar [n_s*n_s], bbar [n_s]. */
+lopf_status lopf_get_operator_scen(const lopf_handle *h, int64_t s, int32_t scen, double *abar, double *bbar);
 
 /* Copy the packed problem into the caller's device arena (device pointer, >= device_bytes,
  * 256-byte aligned) on `stream`, and reset the iterate to the initial point of PAPER.md:495.

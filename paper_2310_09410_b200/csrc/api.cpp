@@ -24,7 +24,11 @@ struct lopf_handle {
     int grid = 0;
     DevProblem dp{};
     ResProblem rp{};
+    BatchProblem bp{};
+    BatchOps bo;
+    std::vector<ScenResult> scen_res;              // host copy of the last batch results
     bool resident() const { return lay.kernel == 2; }
+    bool batch() const { return lay.kernel == 3; }
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -103,6 +107,35 @@ lopf_status lopf_setup(const lopf_network* net, const lopf_options* opt, lopf_ha
     return LOPF_OK;
 }
 
+lopf_status lopf_setup_batch(const lopf_network* net, const lopf_options* opt, int32_t n_scen, const double* load_scale,
+                             lopf_handle** out) {
+    g_err.clear();
+    if (!out) return fail(LOPF_E_ARG, "out handle pointer is NULL");
+    *out = nullptr;
+    lopf_options o;
+    if (opt) o = *opt; else lopf_options_default(&o);
+    if (!(o.rho > 0) || !std::isfinite(o.rho)) return fail(LOPF_E_ARG, "rho must be > 0 (SPEC.md:186)");
+    if (!(o.eps_rel > 0) || !std::isfinite(o.eps_rel)) return fail(LOPF_E_ARG, "eps_rel must be > 0 (SPEC.md:186)");
+    if (o.max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
+    if (n_scen <= 0 || !load_scale) return fail(LOPF_E_ARG, "n_scen must be > 0 with a load_scale array");
+    lopf_handle* h = new (std::nothrow) lopf_handle();
+    if (!h) return fail(LOPF_E_ARG, "out of host memory");
+    h->opt = o;
+    std::string err;
+    try {
+        lopf_status st = copy_network(net, h->net, err);
+        if (st == LOPF_OK) st = build_canon(h->net, h->opt, h->cp, err);
+        if (st == LOPF_OK) st = build_batch_ops(h->net, h->cp, n_scen, load_scale, h->bo, err);
+        if (st == LOPF_OK) st = pack_batch(h->cp, h->bo, h->opt, h->lay, err);
+        if (st != LOPF_OK) { delete h; return fail(st, err); }
+    } catch (const std::bad_alloc&) {
+        delete h;
+        return fail(LOPF_E_ARG, "out of host memory during setup");
+    }
+    *out = h;
+    return LOPF_OK;
+}
+
 lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
     if (!h || !sz) return fail(LOPF_E_ARG, "NULL argument");
     std::memset(sz, 0, sizeof(*sz));
@@ -138,8 +171,9 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
         sz->reserved[0] = mt;                 // largest task count of a CTA
         sz->reserved[1] = h->lay.max_smem;
     }
-    sz->grid = h->resident() ? h->lay.G : h->grid;
-    sz->block = h->resident() ? kResBlock : kStreamBlock;
+    sz->grid = h->resident() ? h->lay.G : h->batch() ? h->lay.n_grp : h->grid;
+    sz->block = h->resident() ? kResBlock : h->batch() ? kBatchBlock : kStreamBlock;
+    sz->n_scen = h->batch() ? h->lay.n_scen : 0;
     return LOPF_OK;
 }
 
@@ -161,6 +195,38 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     CUDA_TRY(cudaMemcpyAsync(arena, h->lay.image.data(), h->lay.bytes, cudaMemcpyHostToDevice, s), "bind H2D");
     const Layout& L = h->lay;
     uint8_t* b = (uint8_t*)arena;
+    if (h->batch()) {
+        BatchProblem& B = h->bp;
+        B.n_scen = L.n_scen; B.n_grp = L.n_grp; B.S = (int32_t)h->cp.S; B.n = (int32_t)h->cp.n;
+        B.nc = (int32_t)h->cp.nc; B.VA = (int32_t)h->bo.VA; B.VB = (int32_t)h->bo.VB; B.n_obj = (int32_t)L.n_obj;
+        B.warp_sub = (const int32_t*)(b + L.off_bwarp);
+        B.sub_ptr = (const int32_t*)(b + L.off_bsubptr);
+        B.sub_ns = (const int32_t*)(b + L.off_bns);
+        B.sub_op = (const int32_t*)(b + L.off_bop);
+        B.vsub_a = (const int32_t*)(b + L.off_bva);
+        B.vsub_b = (const int32_t*)(b + L.off_bvb);
+        B.copy_info = (const int2*)(b + L.off_bcopy);
+        B.gpar = (const double4*)(b + L.off_gpar);
+        B.seg_ptr = (const int32_t*)(b + L.off_segptr);
+        B.seg_copy = (const int32_t*)(b + L.off_segslot);
+        B.shared_abar = (const double*)(b + L.off_bshared);
+        B.var_abar = (const double*)(b + L.off_bvabar);
+        B.var_bbar = (const double*)(b + L.off_bvbbar);
+        B.xl = (double*)(b + L.off_bxl);
+        B.lam = (double*)(b + L.off_blam);
+        B.xout = (double*)(b + L.off_bxout);
+        B.res = (ScenResult*)(b + L.off_bres);
+        B.obj_idx = (const int32_t*)(b + L.off_objidx);
+        B.obj_c = (const double*)(b + L.off_objc);
+        B.rho = h->opt.rho; B.inv_rho = 1.0 / h->opt.rho; B.eps_rel = h->opt.eps_rel;
+        B.ns_max = L.ns_max;
+        h->dp = DevProblem{};
+        h->dp.ctrl = (DevCtrl*)(b + L.off_ctrl);
+        h->arena = arena;
+        h->arena_bytes = bytes;
+        h->bound = true;
+        return LOPF_OK;
+    }
     if (h->resident()) {
         std::string err;
         int sms = 0, optin = 0;
@@ -251,7 +317,9 @@ lopf_status lopf_reset(lopf_handle* h, void* stream) {
     if (!h) return fail(LOPF_E_ARG, "NULL handle");
     if (!h->bound) return fail(LOPF_E_STATE, "lopf_reset before lopf_bind");
     std::string err;
-    lopf_status st = h->resident() ? launch_reset_resident(h->rp, stream, err) : launch_reset(h->dp, stream, err);
+    lopf_status st = h->resident() ? launch_reset_resident(h->rp, stream, err)
+                     : h->batch() ? launch_reset_batch(h->bp, (const double*)((uint8_t*)h->arena + h->lay.off_x0), stream, err)
+                                  : launch_reset(h->dp, stream, err);
     return st == LOPF_OK ? LOPF_OK : fail(st, err);
 }
 
@@ -268,6 +336,11 @@ lopf_status lopf_solve_async(lopf_handle* h, int64_t max_iter, int32_t test, voi
         R.max_iter = max_iter;
         R.test = test ? 1 : 0;
         st = launch_resident(R, stream, err);
+    } else if (h->batch()) {
+        BatchProblem B = h->bp;
+        B.max_iter = max_iter;
+        B.test = test ? 1 : 0;
+        st = launch_batch(B, stream, err);
     } else {
         DevProblem P = h->dp;
         P.max_iter = max_iter;
@@ -279,9 +352,40 @@ lopf_status lopf_solve_async(lopf_handle* h, int64_t max_iter, int32_t test, voi
     return LOPF_OK;
 }
 
+static lopf_status fetch_batch(lopf_handle* h, cudaStream_t s) {
+    h->scen_res.resize(h->lay.n_scen);
+    CUDA_TRY(cudaMemcpyAsync(h->scen_res.data(), h->bp.res, sizeof(ScenResult) * h->lay.n_scen, cudaMemcpyDeviceToHost, s),
+             "batch results D2H");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return LOPF_OK;
+}
+
 lopf_status lopf_result_get(lopf_handle* h, void* stream, lopf_result* res) {
     if (!h || !res) return fail(LOPF_E_ARG, "NULL argument");
     if (!h->bound) return fail(LOPF_E_STATE, "result before lopf_bind");
+    if (h->batch()) {
+        lopf_status st = fetch_batch(h, (cudaStream_t)stream);
+        if (st != LOPF_OK) return st;
+        std::memset(res, 0, sizeof(*res));
+        bool all = true, num = false;
+        int64_t worst = -1;
+        for (int32_t i = 0; i < h->lay.n_scen; ++i) {
+            const ScenResult& R = h->scen_res[i];
+            all &= R.status == 1;
+            num |= R.status == 3;
+            if (worst < 0 || R.iters > h->scen_res[worst].iters) worst = i;
+            res->objective += R.objective;
+        }
+        const ScenResult& W = h->scen_res[worst];
+        res->iters = W.iters;
+        res->pres = W.res[0]; res->dres = W.res[1]; res->eps_prim = W.res[2]; res->eps_dual = W.res[3];
+        res->outcome = all ? LOPF_CONVERGED : LOPF_MAX_ITER;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, h->ev0, h->ev1) == cudaSuccess) res->solve_ms = ms;
+        else cudaGetLastError();
+        if (num) return fail(LOPF_E_NUMERIC, "non-finite residual sum in a batch scenario");
+        return LOPF_OK;
+    }
     DevCtrl c;
     cudaStream_t s = (cudaStream_t)stream;
     CUDA_TRY(cudaMemcpyAsync(&c, h->dp.ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost, s), "result D2H");
@@ -454,6 +558,60 @@ lopf_status lopf_get_trace(lopf_handle* h, void* stream, double* buf, int64_t ca
         CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     }
     if (n_rows) *n_rows = rows;
+    return LOPF_OK;
+}
+
+lopf_status lopf_get_batch_results(lopf_handle* h, void* stream, int64_t* iters, int32_t* outcome, double* res,
+                                   double* objective) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->batch() || !h->bound) return fail(LOPF_E_STATE, "batch results need a bound batch handle");
+    lopf_status st = fetch_batch(h, (cudaStream_t)stream);
+    if (st != LOPF_OK) return st;
+    for (int32_t i = 0; i < h->lay.n_scen; ++i) {
+        const ScenResult& R = h->scen_res[i];
+        if (iters) iters[i] = R.iters;
+        if (outcome) outcome[i] = R.status == 1 ? LOPF_CONVERGED : R.status == 3 ? (int32_t)LOPF_E_NUMERIC : LOPF_MAX_ITER;
+        if (res) for (int q = 0; q < 4; ++q) res[4 * i + q] = R.res[q];
+        if (objective) objective[i] = R.objective;
+    }
+    return LOPF_OK;
+}
+
+lopf_status lopf_get_state_scen(lopf_handle* h, void* stream, int32_t scen, double* x, double* x_loc, double* lam) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->batch() || !h->bound) return fail(LOPF_E_STATE, "per-scenario state needs a bound batch handle");
+    if (scen < 0 || scen >= h->lay.n_scen) return fail(LOPF_E_ARG, "scenario index out of range");
+    cudaStream_t s = (cudaStream_t)stream;
+    ScenResult R;
+    CUDA_TRY(cudaMemcpyAsync(&R, h->bp.res + scen, sizeof(R), cudaMemcpyDeviceToHost, s), "state D2H");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    const int64_t g = scen / 32, ln = scen % 32, NC = h->cp.nc, N = h->cp.n, G = h->lay.n_grp;
+    const int cur = (int)(R.total & 1);
+    const size_t pitch = 32 * sizeof(double);
+    if (x_loc)
+        CUDA_TRY(cudaMemcpy2DAsync(x_loc, 8, h->bp.xl + (((size_t)cur * G + g) * NC) * 32 + ln, pitch, 8, NC,
+                                   cudaMemcpyDeviceToHost, s), "state D2H");
+    if (lam)
+        CUDA_TRY(cudaMemcpy2DAsync(lam, 8, h->bp.lam + (((size_t)cur * G + g) * NC) * 32 + ln, pitch, 8, NC,
+                                   cudaMemcpyDeviceToHost, s), "state D2H");
+    if (x)
+        CUDA_TRY(cudaMemcpy2DAsync(x, 8, h->bp.xout + ((size_t)g * N) * 32 + ln, pitch, 8, N, cudaMemcpyDeviceToHost, s),
+                 "state D2H");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return LOPF_OK;
+}
+
+lopf_status lopf_get_operator_scen(const lopf_handle* h, int64_t s, int32_t scen, double* abar, double* bbar) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    const Canon& P = h->cp;
+    if (s < 0 || s >= P.S) return fail(LOPF_E_ARG, "subsystem index out of range");
+    if (!h->batch()) return lopf_get_operator(h, s, abar, bbar);
+    if (scen < 0 || scen >= h->lay.n_scen) return fail(LOPF_E_ARG, "scenario index out of range");
+    const int32_t v = h->bo.vidx[s];
+    if (v < 0) return lopf_get_operator(h, s, abar, bbar);
+    const size_t a0 = (size_t)scen * h->bo.VA + h->bo.va_off[v], b0 = (size_t)scen * h->bo.VB + h->bo.vb_off[v];
+    if (abar) std::copy(h->bo.abar.begin() + a0, h->bo.abar.begin() + a0 + (size_t)P.n_s[s] * P.n_s[s], abar);
+    if (bbar) std::copy(h->bo.bbar.begin() + b0, h->bo.bbar.begin() + b0 + P.n_s[s], bbar);
     return LOPF_OK;
 }
 

@@ -151,6 +151,46 @@ struct ResProblem {                           // resident kernel argument
     int32_t pad1;
 };
 
+// ---- batch kernel (config 4: lane = scenario, 32 scenarios per CTA group) -----------------------
+constexpr int kBatchBlock = 512;               // 16 warps split the subsystems of one group
+constexpr int kBatchWarps = kBatchBlock / 32;
+
+struct ScenResult {                            // 64 B per scenario (device)
+    long long iters;                           // sweeps executed in the last launch
+    long long total;                           // sweeps since reset (state parity)
+    int status;                                // 0 running, 1 converged, 2 max_iter, 3 numeric
+    int pad;
+    double res[4];
+    double objective;
+};
+
+struct BatchProblem {
+    int32_t n_scen, n_grp, S, n;
+    int32_t nc, VA, VB, n_obj;
+    const int32_t* warp_sub;                   // [kBatchWarps + 1] subsystem ranges per warp
+    const int32_t* sub_ptr;                    // [S+1] copy offsets (canonical)
+    const int32_t* sub_ns;                     // [S]
+    const int32_t* sub_op;                     // [S] >= 0: shared pool offset; < 0: -(1 + varying index)
+    const int32_t* vsub_a;                     // [V] Abar offsets per scenario (doubles), [V] bbar offsets
+    const int32_t* vsub_b;
+    const int2* copy_info;                     // [nc] {global, first-copy flag}
+    const double4* gpar;                       // [n] {c/rho, 1/nu, lo, hi}
+    const int32_t* seg_ptr;                    // [n+1]
+    const int32_t* seg_copy;                   // [nc]
+    const double* shared_abar;                 // row-major n_s x n_s per shared subsystem
+    const double* var_abar;                    // [n_grp][VA][32]
+    const double* var_bbar;                    // [n_grp][VB][32]
+    double* xl;                                // [2][n_grp][nc][32]
+    double* lam;                               // [2][n_grp][nc][32]
+    double* xout;                              // [n_grp][n][32]
+    ScenResult* res;                           // [n_scen]
+    const int32_t* obj_idx;
+    const double* obj_c;
+    double rho, inv_rho, eps_rel;
+    long long max_iter;
+    int32_t test, ns_max;
+};
+
 // Arena layout: byte offsets of every array (all 256-byte aligned).
 struct Layout {
     int32_t kernel = 1;
@@ -167,16 +207,35 @@ struct Layout {
     size_t off_hdr = 0, off_blobs = 0, off_xchg = 0, off_x0r = 0, off_prof = 0, off_flags = 0;
     std::vector<CtaHdr> hdr;               // host copy of the per-CTA headers
     std::vector<int32_t> slot_cta;         // [total slots] CTA of a global slot id
+    // batch kernel
+    int32_t n_scen = 0, n_grp = 0, ns_max = 0;
+    size_t off_bwarp = 0, off_bsubptr = 0, off_bns = 0, off_bop = 0, off_bva = 0, off_bvb = 0, off_bcopy = 0,
+           off_bshared = 0, off_bvabar = 0, off_bvbbar = 0, off_bxl = 0, off_blam = 0, off_bxout = 0, off_bres = 0;
+};
+
+// Scenario batches (config 4): per-scenario operators of the subsystems that hold a load (their
+// A_s depends on the load level through VDLM-1/2); every other subsystem shares the base operator.
+struct BatchOps {
+    int32_t n_scen = 0;
+    std::vector<int64_t> vsub;                 // varying subsystems (canonical ids, ascending)
+    std::vector<int32_t> vidx;                 // [S] index into vsub or -1
+    std::vector<int64_t> va_off, vb_off;       // [V+1] offsets (doubles) of Abar (n_s^2) / bbar (n_s) per scenario
+    int64_t VA = 0, VB = 0;                    // doubles per scenario
+    std::vector<double> abar, bbar;            // [n_scen][VA], [n_scen][VB]
 };
 
 // setup.cpp
 lopf_status build_canon(const Net& net, const lopf_options& opt, Canon& out, std::string& err);
+lopf_status build_batch_ops(const Net& base, const Canon& cp, int32_t n_scen, const double* scale, BatchOps& out,
+                            std::string& err);
 lopf_status copy_network(const lopf_network* src, Net& dst, std::string& err);
 // pack.cpp
 lopf_status pack_streaming(const Canon& cp, const lopf_options& opt, int max_grid, Layout& lay, std::string& err);
 void init_state_image(const Canon& cp, Layout& lay);
 // pack_resident.cpp: returns LOPF_E_ARG (with err) when the problem does not fit max_ctas CTAs
 lopf_status pack_resident(const Net& net, const Canon& cp, const lopf_options& opt, Layout& lay, std::string& err);
+// pack_batch.cpp
+lopf_status pack_batch(const Canon& cp, const BatchOps& bo, const lopf_options& opt, Layout& lay, std::string& err);
 // kernels.cu
 constexpr int kStreamBlock = 512;
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
@@ -185,5 +244,8 @@ lopf_status query_grid(int* grid, std::string& err);
 lopf_status launch_resident(const ResProblem& P, void* stream, std::string& err);
 lopf_status launch_reset_resident(const ResProblem& P, void* stream, std::string& err);
 lopf_status resident_capacity(int* sms, int* smem_optin, std::string& err);
+// batch.cu
+lopf_status launch_batch(const BatchProblem& P, void* stream, std::string& err);
+lopf_status launch_reset_batch(const BatchProblem& P, const double* x0, void* stream, std::string& err);
 
 }  // namespace lopf

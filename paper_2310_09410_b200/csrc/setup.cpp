@@ -637,4 +637,100 @@ lopf_status build_canon(const Net& N, const lopf_options& opt, Canon& P, std::st
     return LOPF_OK;
 }
 
+// Per-scenario operators for config 4 (BASELINE.json configs[3]): scenario sigma scales every load's
+// (a, b) by scale[sigma * n_load + l] (> 0, so the structural column sets are unchanged).  Only the
+// subsystems holding a load see a different A_s / b_s; their Abar, bbar are recomputed per scenario.
+lopf_status build_batch_ops(const Net& base, const Canon& P, int32_t n_scen, const double* scale, BatchOps& out,
+                            std::string& err) {
+    out = BatchOps();
+    out.n_scen = n_scen;
+    if (n_scen <= 0 || !scale) { err = "batch: n_scen must be > 0 with a load_scale array"; return LOPF_E_ARG; }
+    for (int64_t q = 0; q < (int64_t)n_scen * base.n_load; ++q)
+        if (!(scale[q] > 0) || !std::isfinite(scale[q])) { err = "batch: load scales must be finite and > 0"; return LOPF_E_ARG; }
+    std::vector<char> has_load(base.n_bus, 0);
+    for (int l = 0; l < base.n_load; ++l) has_load[base.load_bus[l]] = 1;
+    out.vidx.assign(P.S, -1);
+    for (int64_t s = 0; s < P.S; ++s) {
+        bool v = false;
+        if (P.S == 1) v = base.n_load > 0;
+        else if (P.kind[s] == BUS) v = has_load[P.comp[s]];
+        else if (P.kind[s] == LEAF) v = has_load[P.leaf[s]];
+        if (v) { out.vidx[s] = (int32_t)out.vsub.size(); out.vsub.push_back(s); }
+    }
+    const int64_t V = (int64_t)out.vsub.size();
+    out.va_off.assign(V + 1, 0);
+    out.vb_off.assign(V + 1, 0);
+    for (int64_t v = 0; v < V; ++v) {
+        const int ns = P.n_s[out.vsub[v]];
+        out.va_off[v + 1] = out.va_off[v] + (int64_t)ns * ns;
+        out.vb_off[v + 1] = out.vb_off[v] + ns;
+    }
+    out.VA = out.va_off[V];
+    out.VB = out.vb_off[V];
+    out.abar.assign((size_t)n_scen * out.VA, 0.0);
+    out.bbar.assign((size_t)n_scen * out.VB, 0.0);
+    std::vector<int> status(n_scen, 0);
+    auto work = [&](int32_t s0, int32_t s1) {
+        Net N = base;                                  // this thread's scaled copy
+        Builder B(N);
+        for (int32_t sc = s0; sc < s1; ++sc) {
+            for (int l = 0; l < base.n_load; ++l)
+                for (int p = 0; p < 3; ++p) {
+                    const double k = scale[(int64_t)sc * base.n_load + l];
+                    N.load_a[3 * l + p] = base.load_a[3 * l + p] * k;
+                    N.load_b[3 * l + p] = base.load_b[3 * l + p] * k;
+                }
+            for (int64_t v = 0; v < V && !status[sc]; ++v) {
+                const int64_t s = out.vsub[v];
+                std::vector<RowB> rows;
+                if (P.S == 1) {
+                    for (int i = 0; i < N.n_bus; ++i) B.bus_rows(i, rows);
+                    for (int e = 0; e < N.n_line; ++e) B.line_rows(e, rows);
+                } else if (P.kind[s] == BUS) {
+                    B.bus_rows(P.comp[s], rows);
+                } else {
+                    B.line_rows(P.comp[s], rows);
+                    B.bus_rows(P.leaf[s], rows);
+                }
+                const int n = P.n_s[s], m = (int)rows.size();
+                const int32_t* cols = &P.copy_global[P.sub_ptr[s]];
+                std::vector<double> A((size_t)m * n, 0.0), b(m, 0.0);
+                for (int r = 0; r < m; ++r) {
+                    for (const Term& t : rows[r].t) {
+                        if (t.v == 0.0) continue;
+                        const int32_t* it = std::lower_bound(cols, cols + n, (int32_t)t.col);
+                        if (it == cols + n || *it != t.col) { status[sc] = -1; break; }
+                        A[(size_t)r * n + (it - cols)] += t.v;
+                    }
+                    b[r] = rows[r].rhs;
+                }
+                if (status[sc]) break;
+                SubOut o;
+                precompute_one(std::move(A), std::move(b), m, n, o);
+                if (o.status) { status[sc] = o.status; break; }
+                std::copy(o.abar.begin(), o.abar.end(), out.abar.begin() + (size_t)sc * out.VA + out.va_off[v]);
+                std::copy(o.bbar.begin(), o.bbar.end(), out.bbar.begin() + (size_t)sc * out.VB + out.vb_off[v]);
+            }
+        }
+    };
+    unsigned nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    nt = (unsigned)std::min<int64_t>(nt, n_scen);
+    std::vector<std::thread> th;
+    const int32_t chunk = (n_scen + (int32_t)nt - 1) / (int32_t)nt;
+    for (unsigned t = 0; t < nt; ++t) {
+        const int32_t s0 = (int32_t)t * chunk, s1 = std::min(n_scen, s0 + chunk);
+        if (s0 < s1) th.emplace_back(work, s0, s1);
+    }
+    for (auto& t : th) t.join();
+    for (int32_t sc = 0; sc < n_scen; ++sc)
+        if (status[sc]) {
+            err = "batch scenario " + std::to_string(sc) + ": " +
+                  (status[sc] == -1 ? std::string("row outside the structural column set")
+                                    : status[sc] == LOPF_E_RANK ? std::string("A_s A_s^T singular")
+                                                                : std::string("inconsistent equality rows"));
+            return status[sc] == -1 ? LOPF_E_NETWORK : (lopf_status)status[sc];
+        }
+    return LOPF_OK;
+}
+
 }  // namespace lopf

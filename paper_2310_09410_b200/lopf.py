@@ -50,7 +50,7 @@ class Options(C.Structure):
 class Sizes(C.Structure):
     _fields_ = [(k, _i64) for k in ("S", "n", "m", "n_copies", "p_sym", "n_tasks", "n_slots", "device_bytes",
                                     "abar_doubles", "alg_bytes")] + \
-               [(k, _i32) for k in ("kernel", "grid", "block", "max_ns", "max_ms")] + [("reserved", _i32 * 3)]
+               [(k, _i32) for k in ("kernel", "grid", "block", "max_ns", "max_ms", "n_scen")] + [("reserved", _i32 * 2)]
 
 
 class Result(C.Structure):
@@ -93,6 +93,10 @@ def load_library(path: str = LIB_PATH):
         "lopf_set_state": ([H, _vp, _vp, _vp], _i32),
         "lopf_get_trace": ([H, _vp, _vp, _i64, _vp], _i32),
         "lopf_get_profile": ([H, _vp, _vp, _i64, _vp], _i32),
+        "lopf_setup_batch": ([C.POINTER(Network), C.POINTER(Options), _i32, _vp, C.POINTER(H)], _i32),
+        "lopf_get_batch_results": ([H, _vp, _vp, _vp, _vp, _vp], _i32),
+        "lopf_get_state_scen": ([H, _vp, _i32, _vp, _vp, _vp], _i32),
+        "lopf_get_operator_scen": ([H, _i64, _i32, _vp, _vp], _i32),
         "lopf_destroy": ([H], None),
         "lopf_last_error": ([], C.c_char_p),
         "lopf_abi_version": ([], _i32),
@@ -176,6 +180,48 @@ class Lopf:
         _check(lib.lopf_setup(C.byref(net), C.byref(o), C.byref(h)), "lopf_setup")
         del keep
         return cls(h.value, o)
+
+    @classmethod
+    def setup_batch(cls, feeder, load_scale, rho: float = 100.0, eps_rel: float = 1e-3, max_iter: int = 1_000_000) -> "Lopf":
+        """lopf_setup_batch: load_scale [n_scen, n_load] (> 0) scales every load's (a, b) per scenario."""
+        lib = load_library()
+        o = Options()
+        _check(lib.lopf_options_default(C.byref(o)), "lopf_options_default")
+        o.rho, o.eps_rel, o.max_iter = float(rho), float(eps_rel), int(max_iter)
+        net, keep = _network(feeder)
+        sc = np.ascontiguousarray(load_scale, dtype=np.float64)
+        if sc.ndim != 2 or sc.shape[1] != feeder.n_load:
+            raise ValueError("load_scale must be [n_scen, n_load]")
+        h = _vp()
+        _check(lib.lopf_setup_batch(C.byref(net), C.byref(o), int(sc.shape[0]), _ptr(sc), C.byref(h)), "lopf_setup_batch")
+        del keep
+        return cls(h.value, o)
+
+    def get_batch_results(self, stream=None) -> dict:
+        ns = int(self.sizes.n_scen)
+        it = np.zeros(ns, np.int64)
+        oc = np.zeros(ns, np.int32)
+        rs = np.zeros((ns, 4))
+        ob = np.zeros(ns)
+        _check(load_library().lopf_get_batch_results(self._h, _vp(_stream_handle(stream)), _ptr(it), _ptr(oc), _ptr(rs),
+                                                     _ptr(ob)), "lopf_get_batch_results")
+        return dict(iters=it, outcome=oc, res=rs, objective=ob)
+
+    def get_state_scen(self, scen: int, stream=None):
+        s = self.sizes
+        x = np.zeros(int(s.n))
+        xl = np.zeros(int(s.n_copies))
+        lam = np.zeros(int(s.n_copies))
+        _check(load_library().lopf_get_state_scen(self._h, _vp(_stream_handle(stream)), int(scen), _ptr(x), _ptr(xl),
+                                                  _ptr(lam)), "lopf_get_state_scen")
+        return x, xl, lam
+
+    def get_operator_scen(self, s: int, scen: int, n_s: int):
+        ab = np.zeros(n_s * n_s)
+        bb = np.zeros(n_s)
+        _check(load_library().lopf_get_operator_scen(self._h, int(s), int(scen), _ptr(ab), _ptr(bb)),
+               "lopf_get_operator_scen")
+        return ab.reshape(n_s, n_s), bb
 
     def sizes_get(self) -> Sizes:
         s = Sizes()
