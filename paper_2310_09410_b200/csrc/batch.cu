@@ -1,7 +1,7 @@
 // Batch kernel for sm_100a (config 4): many load scenarios of one feeder, each an
 // independent run of Algorithm 1 with its own termination test.
 //
-// Lane = scenario: a CTA owns a group of 32 scenarios and its 16 warps split the subsystems.  All
+// Lane = scenario: a CTA owns a group of 32 scenarios and its 8 warps split the subsystems.  All
 // per-scenario arrays are scenario-fastest, so for every copy / operator entry a warp touches one
 // 256-byte line; operators of subsystems without a load are the same for every scenario (uniform
 // addresses: broadcast loads served by L1/L2).  Per sweep and subsystem:

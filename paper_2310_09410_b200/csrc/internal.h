@@ -152,7 +152,7 @@ struct ResProblem {                           // resident kernel argument
 };
 
 // ---- batch kernel (config 4: lane = scenario, 32 scenarios per CTA group) -----------------------
-constexpr int kBatchBlock = 512;               // 16 warps split the subsystems of one group
+constexpr int kBatchBlock = 256;               // 8 warps split the subsystems of one group (SMEM staging)
 constexpr int kBatchWarps = kBatchBlock / 32;
 
 struct ScenResult {                            // 64 B per scenario (device)
