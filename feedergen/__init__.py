@@ -443,3 +443,45 @@ def graph_stats(f: Feeder) -> dict:
     leaves = int(np.sum((deg == 1) & (np.arange(f.n_bus) != f.root_bus)))
     load_phases = int(sum(len(phase_list(m)) for m in f.load_phases))
     return dict(nodes=f.n_bus, lines=f.n_line, leaves=leaves, load_phases=load_phases)
+
+
+def make_stitched(n_sub: int = 64, shape: str = "8500", seed0: int | None = None, trunk_scale: float = 0.01) -> Feeder:
+    """Config 5 (BASELINE.json configs[4]): n_sub subfeeders of `shape` (seeds seed0 + f, their own
+    substation generators removed) each hung by a 3-phase line off bus f of an n_sub-bus 3-phase trunk
+    chain that starts at the substation; trunk r, x scaled by `trunk_scale`; the trunk, the tie lines and
+    the substation generator carry the whole load, so their bounds are widened to +-1000 p.u."""
+    seed0 = SEEDS[shape] if seed0 is None else seed0
+    rng = np.random.default_rng(seed0 + 10_000)
+    fb = FeederBuilder(f"stitched{n_sub}x{shape}")
+    root = fb.bus(ALL3, wmin=0.9025, wmax=1.1025)
+    fb.root = root
+    fb.gen(root, ALL3, -1000.0, 1000.0, -1000.0, 1000.0)
+    trunk, prev = [], root
+    for f in range(n_sub):
+        b = fb.bus(ALL3)
+        r = _sym3(rng, 0.0002 * trunk_scale, 0.0008 * trunk_scale, 0.25, 0.4)
+        x = _sym3(rng, 0.0004 * trunk_scale, 0.0024 * trunk_scale, 0.35, 0.5)
+        fb.line(prev, b, ALL3, r, x, fmin=-1000.0, fmax=1000.0)
+        trunk.append(b)
+        prev = b
+    subs = [make_radial(SHAPES[shape], seed0 + f, "sub") for f in range(n_sub)]
+    off = np.cumsum([1 + n_sub] + [s.n_bus for s in subs])[:-1]           # bus offset of each subfeeder
+    for f in range(n_sub):                                                  # tie lines trunk f -> sub root
+        r = _sym3(rng, 0.0002, 0.0008, 0.25, 0.4)
+        x = _sym3(rng, 0.0004, 0.0024, 0.35, 0.5)
+        fb.line(trunk[f], int(off[f] + subs[f].root_bus), ALL3, r, x, fmin=-1000.0, fmax=1000.0)
+    head = fb.build()
+    cat = lambda name, conv=None: np.concatenate([getattr(head, name)] + [  # noqa: E731
+        conv(getattr(s, name), f) if conv else getattr(s, name) for f, s in enumerate(subs)])
+    shift = lambda a, f: (a + off[f]).astype(np.int32)  # noqa: E731
+    kw = {}
+    for fld in dataclasses.fields(Feeder):
+        n = fld.name
+        if n in ("name", "root_bus", "meta") or n.startswith("gen_"):
+            continue
+        kw[n] = cat(n, shift if n in ("line_from", "line_to", "load_bus") else None)
+    for n in ("gen_bus", "gen_phases", "gen_pmin", "gen_pmax", "gen_qmin", "gen_qmax"):
+        kw[n] = getattr(head, n)                                            # only the substation generator
+    g = Feeder(name=head.name, root_bus=root, **kw)
+    g.meta = dict(shape=f"stitched{n_sub}x{shape}", seed0=seed0, n_sub=n_sub)
+    return g
