@@ -88,11 +88,11 @@ lopf_status lopf_setup(const lopf_network* net, const lopf_options* opt, lopf_ha
             if (h->opt.kernel == 2) {
                 st = pack_resident(h->net, h->cp, h->opt, h->lay, err);
             } else if (h->opt.kernel == 1) {
-                st = pack_streaming(h->cp, h->opt, kMaxGrid, h->lay, err);
+                st = pack_streaming(h->net, h->cp, h->opt, kMaxGrid, h->lay, err);
             } else {                                      // auto: operators on chip when they fit
                 std::string e2;
                 st = pack_resident(h->net, h->cp, h->opt, h->lay, e2);
-                if (st != LOPF_OK) st = pack_streaming(h->cp, h->opt, kMaxGrid, h->lay, err);
+                if (st != LOPF_OK) st = pack_streaming(h->net, h->cp, h->opt, kMaxGrid, h->lay, err);
             }
         }
         if (st != LOPF_OK) { delete h; return fail(st, err); }
@@ -271,6 +271,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     }
     DevProblem& P = h->dp;
     P.n_tasks = (int32_t)L.n_tasks;
+    P.rmax = L.rmax;
     P.n_slots = (int32_t)L.n_slots;
     P.n = h->cp.n;
     P.tasks = (const int4*)(b + L.off_tasks);
@@ -301,7 +302,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     P.eps_rel = h->opt.eps_rel;
     std::string err;
     int grid = 0;
-    lopf_status st = query_grid(&grid, err);
+    lopf_status st = query_grid(L.rmax, &grid, err);
     if (st != LOPF_OK) return fail(st, err);
     grid = std::min(grid, kMaxGrid);
     if (h->opt.grid_cap > 0) grid = std::min(grid, h->opt.grid_cap);   // test hook: cap the grid

@@ -62,6 +62,9 @@ constexpr int kInfoBaseMask = 0xFF;        // slot index of the subsystem's firs
 constexpr int kInfoValid = 1 << 8;
 constexpr int kInfoFirst = 1 << 9;         // first copy (canonical) of its global: writes x_g
 constexpr int kInfoInline = 1 << 10;       // segment slots stored inline (nu <= 4)
+constexpr int kInfoBbar = 1 << 11;         // the subsystem has a nonzero b-bar (load-bearing): read it
+constexpr int kWindow = 4096;              // streaming packer: DFS window (subsystems) grouped by n_s
+constexpr int kTaskHalves = 2;             // streaming packer: max 32-slot halves per small-n_s task
 constexpr int kInfoNuShift = 16;
 
 struct DevCtrl {                           // 256 B, device-resident control block
@@ -77,7 +80,7 @@ struct DevCtrl {                           // 256 B, device-resident control blo
 };
 
 struct DevProblem {                        // kernel argument (pointers into the arena)
-    int32_t n_tasks, n_slots, grid, pad0;
+    int32_t n_tasks, n_slots, grid, rmax;  // rmax: widest task (selects the kernel instantiation)
     int64_t n;
     const int4* tasks;                     // {slot_off, abar_off, kmax, R}
     const int32_t* s_info;
@@ -195,6 +198,7 @@ struct BatchProblem {
 struct Layout {
     int32_t kernel = 1;
     int64_t n_tasks = 0, n_slots = 0, abar_doubles = 0, n_obj = 0;
+    int32_t rmax = 1;                     // streaming: widest task (R)
     size_t off_tasks = 0, off_info = 0, off_g = 0, off_nbr = 0, off_bbar = 0, off_xl = 0, off_lam = 0,
            off_u0 = 0, off_u1 = 0, off_x0 = 0, off_gpar = 0, off_segptr = 0, off_segslot = 0, off_x = 0, off_abar = 0,
            off_partial = 0, off_ctrl = 0, off_trace = 0, off_objidx = 0, off_objc = 0;
@@ -230,7 +234,8 @@ lopf_status build_batch_ops(const Net& base, const Canon& cp, int32_t n_scen, co
                             std::string& err);
 lopf_status copy_network(const lopf_network* src, Net& dst, std::string& err);
 // pack.cpp
-lopf_status pack_streaming(const Canon& cp, const lopf_options& opt, int max_grid, Layout& lay, std::string& err);
+std::vector<int64_t> dfs_order(const Net& N, const Canon& P);
+lopf_status pack_streaming(const Net& N, const Canon& cp, const lopf_options& opt, int max_grid, Layout& lay, std::string& err);
 void init_state_image(const Canon& cp, Layout& lay);
 // pack_resident.cpp: returns LOPF_E_ARG (with err) when the problem does not fit max_ctas CTAs
 lopf_status pack_resident(const Net& net, const Canon& cp, const lopf_options& opt, Layout& lay, std::string& err);
@@ -238,9 +243,10 @@ lopf_status pack_resident(const Net& net, const Canon& cp, const lopf_options& o
 lopf_status pack_batch(const Canon& cp, const BatchOps& bo, const lopf_options& opt, Layout& lay, std::string& err);
 // kernels.cu
 constexpr int kStreamBlock = 512;
+constexpr int kStreamCtasPerSm = 2;          // 32 warps per SM (<= 64 registers per thread)
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
 lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err);
-lopf_status query_grid(int* grid, std::string& err);
+lopf_status query_grid(int rmax, int* grid, std::string& err);
 lopf_status launch_resident(const ResProblem& P, void* stream, std::string& err);
 lopf_status launch_reset_resident(const ResProblem& P, void* stream, std::string& err);
 lopf_status resident_capacity(int* sms, int* smem_optin, std::string& err);

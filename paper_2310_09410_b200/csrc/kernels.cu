@@ -48,9 +48,9 @@ __device__ __forceinline__ void task_sweep(const DevProblem& P, const int4 tr, c
         d[h] = 0.0; v[h] = 0.0; lam[h] = 0.0; xo[h] = 0.0; bb[h] = 0.0;
         if (info[h] & kInfoValid) {
             const int g = __ldg(P.s_g + slot);
-            lam[h] = P.lam[slot];
-            xo[h] = P.xl[slot];
-            bb[h] = __ldg(P.s_bbar + slot);
+            lam[h] = __ldcs(P.lam + slot);
+            xo[h] = __ldcs(P.xl + slot);
+            if (info[h] & kInfoBbar) bb[h] = __ldcs(P.s_bbar + slot);
             const double2 gp0 = __ldg(reinterpret_cast<const double2*>(P.gpar + g));       // {c/rho, 1/nu}
             const double2 gp1 = __ldg(reinterpret_cast<const double2*>(P.gpar + g) + 1);   // {lo, hi}
             double sigma;
@@ -84,32 +84,21 @@ __device__ __forceinline__ void task_sweep(const DevProblem& P, const int4 tr, c
     int base[R];
 #pragma unroll
     for (int h = 0; h < R; ++h) base[h] = info[h] & kInfoBaseMask;
-    if (R > 2) {                                   // large subsystems (n_s > 64): d staged in this warp's SMEM
-#pragma unroll
+    if (R > 1) {                                   // d staged in this warp's SMEM; row h*32+lane reads
+#pragma unroll                                     // d[base + k] of its own subsystem
         for (int h = 0; h < R; ++h) dsm[h * 32 + lane] = d[h];
         __syncwarp();
+#pragma unroll 2
         for (int k = 0; k < kmax; ++k) {
-            const double dk = dsm[k];             // one subsystem per R > 2 task: base = 0
 #pragma unroll
-            for (int h = 0; h < R; ++h) ax[h] = fma(__ldg(A + (size_t)k * (32 * R) + h * 32 + lane), dk, ax[h]);
+            for (int h = 0; h < R; ++h)
+                ax[h] = fma(__ldcs(A + (size_t)k * (32 * R) + h * 32 + lane), dsm[base[h] + k], ax[h]);
         }
         __syncwarp();
-    } else
+    } else {
 #pragma unroll 4
-    for (int k = 0; k < kmax; ++k) {
-#pragma unroll
-        for (int h = 0; h < R; ++h) {
-            const int src = base[h] + k;
-            double dk;
-            if (R == 1) {
-                dk = __shfl_sync(kFull, d[0], src);
-            } else {
-                const double e0 = __shfl_sync(kFull, d[0], src & 31);
-                const double e1 = __shfl_sync(kFull, d[R - 1], src & 31);
-                dk = (src >> 5) ? e1 : e0;
-            }
-            ax[h] = fma(__ldg(A + (size_t)k * (32 * R) + h * 32 + lane), dk, ax[h]);
-        }
+        for (int k = 0; k < kmax; ++k)
+            ax[0] = fma(__ldcs(A + (size_t)k * 32 + lane), __shfl_sync(kFull, d[0], base[0] + k), ax[0]);
     }
 #pragma unroll
     for (int h = 0; h < R; ++h) {
@@ -117,8 +106,8 @@ __device__ __forceinline__ void task_sweep(const DevProblem& P, const int4 tr, c
         const int slot = tr.x + h * 32 + lane;
         const double xn = fma(ax[h], P.inv_rho, bb[h]);                 // (1/rho) Abar d + bbar
         const double ln = lam[h] + P.rho * (v[h] - xn);                  // ADMM-3
-        P.xl[slot] = xn;
-        P.lam[slot] = ln;
+        __stcs(P.xl + slot, xn);
+        __stcs(P.lam + slot, ln);
         unext[slot] = xn - ln * P.inv_rho;                               // next consensus input
         const double r = v[h] - xn, dx = xn - xo[h];
         acc[0] += r * r;
@@ -129,7 +118,8 @@ __device__ __forceinline__ void task_sweep(const DevProblem& P, const int4 tr, c
     }
 }
 
-__global__ void __launch_bounds__(kBlock, 1) admm_stream_kernel(DevProblem P) {
+template <int RMAX>   // largest task width in the problem; RMAX <= 4 keeps 64 registers (2 CTAs / SM)
+__global__ void __launch_bounds__(kBlock, RMAX <= 4 ? kStreamCtasPerSm : 1) admm_stream_kernel(DevProblem P) {
     __shared__ double red[kWarps][5];
     __shared__ double dstage[kWarps][256];
     __shared__ int s_stop;
@@ -148,8 +138,8 @@ __global__ void __launch_bounds__(kBlock, 1) admm_stream_kernel(DevProblem P) {
             switch (tr.w) {
                 case 1: task_sweep<1>(P, tr, ucur, unext, acc, lane, dsm); break;
                 case 2: task_sweep<2>(P, tr, ucur, unext, acc, lane, dsm); break;
-                case 4: task_sweep<4>(P, tr, ucur, unext, acc, lane, dsm); break;
-                default: task_sweep<8>(P, tr, ucur, unext, acc, lane, dsm); break;
+                case 4: if constexpr (RMAX >= 4) task_sweep<4>(P, tr, ucur, unext, acc, lane, dsm); break;
+                default: if constexpr (RMAX >= 8) task_sweep<8>(P, tr, ucur, unext, acc, lane, dsm); break;
             }
         }
 #pragma unroll
@@ -245,11 +235,18 @@ __global__ void reset_kernel(DevProblem P) {
 
 }  // namespace
 
-lopf_status query_grid(int* grid, std::string& err) {
+static const void* stream_kernel_for(int rmax) {
+    return rmax <= 1 ? (const void*)admm_stream_kernel<1>
+         : rmax <= 2 ? (const void*)admm_stream_kernel<2>
+         : rmax <= 4 ? (const void*)admm_stream_kernel<4>
+                     : (const void*)admm_stream_kernel<8>;
+}
+
+lopf_status query_grid(int rmax, int* grid, std::string& err) {
     int dev = 0, sms = 0, per = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, admm_stream_kernel, kBlock, 0);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_kernel_for(rmax), kBlock, 0);
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     if (per < 1) { err = "streaming kernel cannot be resident (occupancy 0)"; return LOPF_E_CUDA; }
     *grid = sms * per;
@@ -263,7 +260,7 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
     if (e == cudaSuccess && P.max_iter > 0) {
         DevProblem Q = P;
         void* args[] = {&Q};
-        e = cudaLaunchCooperativeKernel((const void*)admm_stream_kernel, dim3(grid), dim3(kBlock), args, 0, s);
+        e = cudaLaunchCooperativeKernel(stream_kernel_for(P.rmax), dim3(grid), dim3(kBlock), args, 0, s);
     }
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;

@@ -1,12 +1,12 @@
 // Device layout of the streaming kernel.
 //
 // Subsystems are packed into warp TASKS: a task owns 32*R row SLOTS (lane l handles slots
-// l, l+32, ...).  Subsystems with n_s <= 32 are packed floor(32/n_s) to a task, all of one
-// n_s (so a task's column loop has no padding); 32 < n_s <= 64 gives one subsystem per
-// R = 2 task.  The operator pool stores, per task, Abar columns k = 0..kmax-1 as 32*R
-// consecutive doubles (slot-major inside a column), so every column read of a warp is one
-// coalesced 256-byte (R = 1) request.  Per-slot metadata, b-bar and the iterate (x_s, lambda,
-// u ping-pong) are slot-indexed arrays; globals keep {c/rho, 1/nu, lo, hi} as one 32-byte record.
+// l, l+32, ...).  Tasks follow the depth-first order of the feeder (gather locality, see
+// pack_streaming) and are homogeneous in n_s, so a task's column loop has no padding.  The operator
+// pool stores, per task, Abar columns k = 0..kmax-1 as 32*R consecutive doubles (slot-major inside
+// a column), so every column read of a warp is one coalesced 256-byte request per half.  Per-slot
+// metadata, b-bar and the iterate (x_s, lambda, u ping-pong) are slot-indexed arrays; globals keep
+// {c/rho, 1/nu, lo, hi} as one 32-byte record.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -20,41 +20,60 @@ namespace lopf {
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-lopf_status pack_streaming(const Canon& P, const lopf_options& opt, int max_grid, Layout& L, std::string& err) {
+lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt, int max_grid, Layout& L,
+                           std::string& err) {
     L = Layout();
     L.kernel = 1;
     // ---- tasks ---------------------------------------------------------------------------------
-    std::map<int, std::vector<int64_t>> by_ns;       // n_s -> subsystems (canonical order)
-    for (int64_t s = 0; s < P.S; ++s) {
+    // Locality first: walk the subsystems in depth-first order (neighbouring subsystems share
+    // globals, so the u values a task gathers were fetched into L2 by a task that ran moments
+    // earlier) and cut that order into windows of kWindow subsystems; inside a window the
+    // subsystems are grouped by n_s so every task is homogeneous (its column loop has no padding).
+    // A task of n_s <= 32 holds up to kTaskHalves halves of floor(32 / n_s) subsystems each (a
+    // subsystem never straddles a half); n_s > 32 gives one subsystem per R = 2, 4 or 8 task.
+    struct T { int R, kmax; size_t pos; std::vector<int64_t> subs; std::vector<int> base; };
+    std::vector<T> tasks;
+    for (int64_t s = 0; s < P.S; ++s)
         if (P.n_s[s] > 256) {
             err = "subsystem " + std::to_string(s) + " has n_s = " + std::to_string(P.n_s[s]) +
                   " > 256 (unsupported by the warp-task layout; the S = 1 path is for small feeders)";
             return LOPF_E_ARG;
         }
-        if (P.n_s[s] > 0) by_ns[P.n_s[s]].push_back(s);
-    }
-    struct T { int R, kmax; std::vector<int64_t> subs; };
-    std::vector<T> tasks;
-    for (auto it = by_ns.rbegin(); it != by_ns.rend(); ++it) {   // heavy tasks first
-        const int ns = it->first;
-        const auto& v = it->second;
-        if (ns > 32) {                                            // one subsystem per task, R = 2, 4 or 8
-            const int R = ns <= 64 ? 2 : ns <= 128 ? 4 : 8;
-            for (int64_t s : v) tasks.push_back({R, ns, {s}});
-        } else {
-            const int per = 32 / ns;
-            for (size_t i = 0; i < v.size(); i += per) {
-                T t{1, ns, {}};
-                for (size_t j = i; j < std::min(v.size(), i + (size_t)per); ++j) t.subs.push_back(v[j]);
-                tasks.push_back(std::move(t));
+    const std::vector<int64_t> order = dfs_order(N, P);
+    for (size_t w0 = 0; w0 < order.size(); w0 += kWindow) {
+        const size_t w1 = std::min(order.size(), w0 + kWindow);
+        std::map<int, std::vector<std::pair<size_t, int64_t>>> by_ns;   // n_s -> (position, subsystem)
+        for (size_t i = w0; i < w1; ++i)
+            if (P.n_s[order[i]] > 0) by_ns[P.n_s[order[i]]].push_back({i, order[i]});
+        std::vector<T> wt;
+        for (const auto& [ns, v] : by_ns) {
+            if (ns > 32) {
+                const int R = ns <= 64 ? 2 : ns <= 128 ? 4 : 8;
+                for (const auto& [pos, s] : v) wt.push_back({R, ns, pos, {s}, {0}});
+                continue;
+            }
+            const size_t per = 32 / ns, cap = per * kTaskHalves;
+            for (size_t i = 0; i < v.size(); i += cap) {
+                const size_t cnt = std::min(cap, v.size() - i);
+                int R = 1;
+                while ((size_t)R * per < cnt) R *= 2;
+                T t{R, ns, v[i].first, {}, {}};
+                for (size_t j = 0; j < cnt; ++j) {
+                    t.subs.push_back(v[i + j].second);
+                    t.base.push_back((int)((j / per) * 32 + (j % per) * ns));
+                }
+                wt.push_back(std::move(t));
             }
         }
+        std::stable_sort(wt.begin(), wt.end(), [](const T& a, const T& b) { return a.pos < b.pos; });
+        for (auto& t : wt) tasks.push_back(std::move(t));
     }
     L.n_tasks = (int64_t)tasks.size();
     std::vector<int4> trec(L.n_tasks);
     int64_t slots = 0, pool = 0;
     for (int64_t t = 0; t < L.n_tasks; ++t) {
         trec[t] = make_int4((int)slots, (int)pool, tasks[t].kmax, tasks[t].R);
+        L.rmax = std::max(L.rmax, tasks[t].R);
         slots += 32 * tasks[t].R;
         pool += (int64_t)tasks[t].kmax * 32 * tasks[t].R;
     }
@@ -110,24 +129,27 @@ lopf_status pack_streaming(const Canon& P, const lopf_options& opt, int max_grid
 
     L.slot_of_copy.assign(NC, -1);
     for (int64_t t = 0; t < L.n_tasks; ++t) {
-        const int R = tasks[t].R, P32 = 32 * R, kmax = tasks[t].kmax;
-        int base = 0;
-        for (int64_t s : tasks[t].subs) {
-            const int ns = P.n_s[s];
+        const int P32 = 32 * tasks[t].R;
+        for (size_t j = 0; j < tasks[t].subs.size(); ++j) {
+            const int64_t s = tasks[t].subs[j];
+            const int ns = P.n_s[s], base = tasks[t].base[j];
+            const bool has_b = [&] {
+                for (int r = 0; r < ns; ++r)
+                    if (P.bbar[P.sub_ptr[s] + r] != 0.0) return true;
+                return false;
+            }();
             for (int r = 0; r < ns; ++r) {
                 const int64_t slot = trec[t].x + base + r;
                 const int64_t copy = P.sub_ptr[s] + r;
                 L.slot_of_copy[copy] = (int32_t)slot;
-                info[slot] = (base & kInfoBaseMask) | kInfoValid;
+                info[slot] = (base & kInfoBaseMask) | kInfoValid | (has_b ? kInfoBbar : 0);
                 gs[slot] = P.copy_global[copy];
                 bbar[slot] = P.bbar[copy];
                 const double* Ab = &P.abar[P.abar_ptr[s]];
                 for (int k = 0; k < ns; ++k)      // lane (slot) r computes row r: sum_k Abar[r][k] d[k]
                     abar[(size_t)trec[t].y + (size_t)k * P32 + base + r] = Ab[(size_t)r * ns + k];
             }
-            base += ns;
         }
-        (void)kmax;
     }
     // segments: inline neighbour slots (nu <= 4) + CSR fallback; first-copy flag
     int32_t* segptr = (int32_t*)at(L.off_segptr);

@@ -26,7 +26,7 @@ static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 static int32_t a16(int64_t x) { return (int32_t)((x + 15) & ~(int64_t)15); }
 
 // depth-first order of the subsystems from the root bus
-static std::vector<int64_t> dfs_order(const Net& N, const Canon& P) {
+std::vector<int64_t> dfs_order(const Net& N, const Canon& P) {
     std::vector<int64_t> order;
     order.reserve(P.S);
     if (P.S == 1) { order.push_back(0); return order; }

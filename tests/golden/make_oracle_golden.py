@@ -1,5 +1,6 @@
 """Write tests/golden/oracle_golden.json: the ORACLE's iteration count to (termination),
-objective and final residuals for configs 1-3 at the paper's defaults.
+objective and final residuals for configs 1-3 at the paper's defaults, plus two small
+instances of the config-5 stitched family (feedergen.make_stitched: 4 x 13-shaped, 2 x 8500-shaped).
 Calls only oracle/ and feedergen (no CUDA path); re-run after any change to either.
 Usage: python tests/golden/make_oracle_golden.py"""
 import json
@@ -13,8 +14,11 @@ import feedergen as fg  # noqa: E402
 import oracle  # noqa: E402
 
 out = {"_note": "written by tests/golden/make_oracle_golden.py from oracle/ only", "configs": {}}
-for shape in ("13", "123", "8500"):
-    f = fg.make_feeder(shape)
+CASES = {"13": lambda: fg.make_feeder("13"), "123": lambda: fg.make_feeder("123"),
+         "8500": lambda: fg.make_feeder("8500"), "s4x13": lambda: fg.make_stitched(4, "13"),
+         "s2x8500": lambda: fg.make_stitched(2, "8500")}
+for shape, make in CASES.items():
+    f = make()
     t = time.time()
     p = oracle.build_problem(f, rho=100.0, eps_rel=1e-3)
     r = oracle.solve(p, max_iter=1_000_000)
