@@ -58,14 +58,20 @@ struct Canon {
 
 // ---- device layout shared by pack.cpp and kernels.cu ---------------------------------------
 // Slot info bit fields (streaming kernel).
-constexpr int kInfoBaseMask = 0xFF;        // slot index of the subsystem's first row in its task (R <= 2)
+constexpr int kInfoBaseMask = 0xFF;        // slot index (in its task) of the subsystem's first row
 constexpr int kInfoValid = 1 << 8;
 constexpr int kInfoFirst = 1 << 9;         // first copy (canonical) of its global: writes x_g
 constexpr int kInfoInline = 1 << 10;       // segment slots stored inline (nu <= 4)
 constexpr int kInfoBbar = 1 << 11;         // the subsystem has a nonzero b-bar (load-bearing): read it
-constexpr int kWindow = 4096;              // streaming packer: DFS window (subsystems) grouped by n_s
-constexpr int kTaskHalves = 2;             // streaming packer: max 32-slot halves per small-n_s task
-constexpr int kInfoNuShift = 16;
+constexpr int kInfoNuShift = 12;           // nu (4 bits, capped at 15; used when inline)
+constexpr int kInfoNsShift = 16;           // n_s (6 bits; packed tasks)
+constexpr int kInfoPoffShift = 22;         // offset (doubles) of the subsystem's packed Abar in its task
+// Task record {slot_off, abar_off, kmax | plen, R | flags}
+constexpr int kTaskPacked = 1 << 4;        // packed task: .z = block doubles, kmax in bits 8..15 of .w
+constexpr int kTaskDirect = 1 << 5;        // packed task whose block exceeds the stage: read from HBM
+constexpr int kTaskKmaxShift = 8;
+constexpr int kTaskHalves = 2;             // streaming packer: max 32-slot halves per packed task
+constexpr int kPackBudget = 224;           // doubles of operator block per staged task (per-warp SMEM stage)
 
 struct DevCtrl {                           // 256 B, device-resident control block
     unsigned long long arrive;             // barrier arrivals of this launch
@@ -242,8 +248,9 @@ lopf_status pack_resident(const Net& net, const Canon& cp, const lopf_options& o
 // pack_batch.cpp
 lopf_status pack_batch(const Canon& cp, const BatchOps& bo, const lopf_options& opt, Layout& lay, std::string& err);
 // kernels.cu
-constexpr int kStreamBlock = 512;
-constexpr int kStreamCtasPerSm = 2;          // 32 warps per SM (<= 64 registers per thread)
+constexpr int kStreamWarps = 24;             // streaming CTA (one per SM): 24 warps x 2 SMEM stages
+constexpr int kStreamWarpsWide = 16;         // ... when tasks of R > 2 exist (n_s > 64)
+int stream_block(int rmax);
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
 lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err);
 lopf_status query_grid(int rmax, int* grid, std::string& err);

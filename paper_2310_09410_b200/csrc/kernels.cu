@@ -22,8 +22,6 @@ namespace lopf {
 
 namespace {
 
-constexpr int kBlock = kStreamBlock;
-constexpr int kWarps = kBlock / 32;
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -35,98 +33,232 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// ---- bulk-copy (TMA) staging ---------------------------------------------------------------------
+// A packed task's inputs are contiguous byte ranges: its operator block (upper-triangular Abar of
+// each subsystem, then b-bar if nonzero) in the pool, and 32*R entries of each per-slot array.  One
+// elected lane copies them into one of the warp's two SMEM stages with cp.async.bulk, completing
+// on that stage's mbarrier, one task ahead of the compute.
+constexpr int kOffInfo = 8 * kPackBudget;
+constexpr int kOffG = kOffInfo + 4 * 64;
+constexpr int kOffNbr = kOffG + 4 * 64;
+constexpr int kOffLam = kOffNbr + 16 * 64;
+constexpr int kOffXl = kOffLam + 8 * 64;
+constexpr int kStageBytes = kOffXl + 8 * 64;
+static_assert(kStageBytes % 16 == 0, "bulk copies need 16-byte alignment");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* m) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+    asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}"
+                 ::"r"(smem_u32(m)), "r"(parity) : "memory");
+}
+
+struct Stage {                   // per-warp pipeline: the j-th staged task of this warp uses stage j & 1
+    char* buf;                   // [2][kStageBytes]
+    uint64_t* bar;               // [2]
+    uint32_t issued, consumed;
+};
+
+__device__ __forceinline__ void issue_task(const DevProblem& P, Stage& st, const int task, const int lane) {
+    if (task >= P.n_tasks) return;
+    const int4 tr = __ldg(P.tasks + task);
+    if (!(tr.w & kTaskPacked)) return;                          // full tasks read HBM directly
+    const int b = st.issued & 1;
+    ++st.issued;
+    if (lane == 0) {
+        char* sb = st.buf + b * kStageBytes;
+        const uint32_t n = 32u * (uint32_t)(tr.w & 0xF);
+        const bool ablk = !(tr.w & kTaskDirect);
+        const uint32_t bytes = 40u * n + (ablk ? 8u * (uint32_t)tr.z : 0u);
+        uint64_t* m = st.bar + b;
+        // order this warp's earlier generic accesses (SMEM reads of the stage, global stores of lambda
+        // and x_s) before the async-proxy copies
+        asm volatile("fence.proxy.async;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+        if (ablk) bulk_g2s(sb, P.abar + tr.y, 8u * (uint32_t)tr.z, m);
+        bulk_g2s(sb + kOffInfo, P.s_info + tr.x, 4u * n, m);
+        bulk_g2s(sb + kOffG, P.s_g + tr.x, 4u * n, m);
+        bulk_g2s(sb + kOffNbr, P.s_nbr + tr.x, 16u * n, m);
+        bulk_g2s(sb + kOffLam, P.lam + tr.x, 8u * n, m);
+        bulk_g2s(sb + kOffXl, P.xl + tr.x, 8u * n, m);
+    }
+}
+
+// a4 for one slot: the global's consensus value from the ping-pong copies (closed_1, rho restored)
+__device__ __forceinline__ double consensus(const DevProblem& P, const int inf, const int g, const int4 nb,
+                                            const double* __restrict__ ucur) {
+    const double2 gp0 = __ldg(reinterpret_cast<const double2*>(P.gpar + g));       // {c/rho, 1/nu}
+    const double2 gp1 = __ldg(reinterpret_cast<const double2*>(P.gpar + g) + 1);   // {lo, hi}
+    double sigma;
+    if (inf & kInfoInline) {                               // nu <= 4: neighbour slots inline
+        const int nu = (inf >> kInfoNuShift) & 0xF;
+        const double a0 = __ldcg(ucur + nb.x);
+        const double a1 = nu > 1 ? __ldcg(ucur + nb.y) : 0.0;
+        const double a2 = nu > 2 ? __ldcg(ucur + nb.z) : 0.0;
+        const double a3 = nu > 3 ? __ldcg(ucur + nb.w) : 0.0;
+        sigma = a0;                                        // ascending canonical copy order
+        if (nu > 1) sigma += a1;
+        if (nu > 2) sigma += a2;
+        if (nu > 3) sigma += a3;
+    } else {
+        const int q0 = __ldg(P.seg_ptr + g), q1 = __ldg(P.seg_ptr + g + 1);
+        sigma = 0.0;
+        for (int q = q0; q < q1; ++q) sigma += __ldcg(ucur + __ldg(P.seg_slot + q));
+    }
+    const double xg = fmin(fmax((sigma - gp0.x) * gp0.y, gp1.x), gp1.y);   // IEEE +-inf = no clamp
+    if (inf & kInfoFirst) P.x[g] = xg;
+    return xg;
+}
+
+// a6 + a7 for one slot
+__device__ __forceinline__ void finish_slot(const DevProblem& P, const int slot, const double ax, const double bb,
+                                            const double v, const double lam, const double xo,
+                                            double* __restrict__ unext, double (&acc)[5]) {
+    const double xn = fma(ax, P.inv_rho, bb);                          // (1/rho) Abar d + bbar
+    const double ln = lam + P.rho * (v - xn);                          // ADMM-3
+    __stcs(P.xl + slot, xn);
+    __stcs(P.lam + slot, ln);
+    unext[slot] = xn - ln * P.inv_rho;                                 // next consensus input
+    const double rr = v - xn, dx = xn - xo;
+    acc[0] += rr * rr;
+    acc[1] += dx * dx;
+    acc[2] += v * v;
+    acc[3] += xn * xn;
+    acc[4] += ln * ln;
+}
+
+// Packed task (R <= 2 halves): inputs from the SMEM stage; operator block from the stage or, for a
+// lone large subsystem (kTaskDirect), straight from the pool.
 template <int R>
-__device__ __forceinline__ void task_sweep(const DevProblem& P, const int4 tr, const double* __restrict__ ucur,
-                                           double* __restrict__ unext, double (&acc)[5], const int lane,
-                                           double* __restrict__ dsm) {
-    double d[R], v[R], lam[R], xo[R], bb[R];
+__device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, const double* __restrict__ ucur,
+                                            double* __restrict__ unext, double (&acc)[5], const int lane,
+                                            double* __restrict__ dsm, Stage& st) {
+    const int b = st.consumed & 1;
+    mbar_wait(st.bar + b, (st.consumed >> 1) & 1);
+    ++st.consumed;
+    const char* sb = st.buf + b * kStageBytes;
+    const int* s_info = reinterpret_cast<const int*>(sb + kOffInfo);
+    const int* s_g = reinterpret_cast<const int*>(sb + kOffG);
+    const int4* s_nbr = reinterpret_cast<const int4*>(sb + kOffNbr);
+    const double* s_lam = reinterpret_cast<const double*>(sb + kOffLam);
+    const double* s_xl = reinterpret_cast<const double*>(sb + kOffXl);
+    const double* S = (tr.w & kTaskDirect) ? P.abar + tr.y : reinterpret_cast<const double*>(sb);
+    double v[R], ax[R];
+    int info[R];
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        const int j = h * 32 + lane;
+        info[h] = s_info[j];
+        v[h] = 0.0;
+        double d = 0.0;
+        if (info[h] & kInfoValid) {
+            v[h] = consensus(P, info[h], s_g[j], s_nbr[j], ucur);
+            d = -P.rho * v[h] - s_lam[j];
+        }
+        dsm[j] = d;
+        ax[h] = 0.0;
+    }
+    __syncwarp();
+    // Row r of subsystem s: sum_k Abar[r][k] d[k], k ascending, from the upper-triangular block
+    // (row-major, (i, j >= i) at i*n - i(i-1)/2 + j - i): entry (min(r,k), max(r,k)); the walk p(k)
+    // steps by n - k - 1 while k < r (down column r) and by 1 after (along row r).
+    int ns[R], r[R], p[R], base[R];
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        base[h] = info[h] & kInfoBaseMask;
+        ns[h] = (info[h] & kInfoValid) ? (info[h] >> kInfoNsShift) & 0x3F : 0;
+        r[h] = h * 32 + lane - base[h];
+        p[h] = ((unsigned)info[h] >> kInfoPoffShift) + r[h];
+    }
+    const int kmax = (tr.w >> kTaskKmaxShift) & 0xFF;
+    for (int k = 0; k < kmax; ++k) {
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+            if (k < ns[h]) {
+                ax[h] = fma(S[p[h]], dsm[base[h] + k], ax[h]);
+                p[h] += k < r[h] ? ns[h] - k - 1 : 1;
+            }
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        if (!(info[h] & kInfoValid)) continue;
+        const int j = h * 32 + lane;
+        // b-bar follows the subsystem's triangle in the block when nonzero
+        const double bb = (info[h] & kInfoBbar)
+                              ? S[((unsigned)info[h] >> kInfoPoffShift) + ns[h] * (ns[h] + 1) / 2 + r[h]] : 0.0;
+        finish_slot(P, tr.x + j, ax[h], bb, v[h], s_lam[j], s_xl[j], unext, acc);
+    }
+    __syncwarp();
+}
+
+// Full task (one subsystem of n_s > 63, R = 2, 4 or 8): Abar as kmax columns of 32*R doubles and the
+// per-slot inputs read straight from HBM.
+template <int R>
+__device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, const double* __restrict__ ucur,
+                                          double* __restrict__ unext, double (&acc)[5], const int lane,
+                                          double* __restrict__ dsm) {
+    double v[R], ax[R];
     int info[R];
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         const int slot = tr.x + h * 32 + lane;
         info[h] = __ldg(P.s_info + slot);
-        d[h] = 0.0; v[h] = 0.0; lam[h] = 0.0; xo[h] = 0.0; bb[h] = 0.0;
+        v[h] = 0.0;
+        double d = 0.0;
         if (info[h] & kInfoValid) {
-            const int g = __ldg(P.s_g + slot);
-            lam[h] = __ldcs(P.lam + slot);
-            xo[h] = __ldcs(P.xl + slot);
-            if (info[h] & kInfoBbar) bb[h] = __ldcs(P.s_bbar + slot);
-            const double2 gp0 = __ldg(reinterpret_cast<const double2*>(P.gpar + g));       // {c/rho, 1/nu}
-            const double2 gp1 = __ldg(reinterpret_cast<const double2*>(P.gpar + g) + 1);   // {lo, hi}
-            double sigma;
-            if (info[h] & kInfoInline) {                       // nu <= 4: neighbour slots inline
-                const int4 nb = __ldg(P.s_nbr + slot);
-                const int nu = (info[h] >> kInfoNuShift) & 0xFF;
-                const double a0 = __ldcg(ucur + nb.x);
-                const double a1 = nu > 1 ? __ldcg(ucur + nb.y) : 0.0;
-                const double a2 = nu > 2 ? __ldcg(ucur + nb.z) : 0.0;
-                const double a3 = nu > 3 ? __ldcg(ucur + nb.w) : 0.0;
-                sigma = a0;                                    // ascending canonical copy order
-                if (nu > 1) sigma += a1;
-                if (nu > 2) sigma += a2;
-                if (nu > 3) sigma += a3;
-            } else {
-                const int q0 = __ldg(P.seg_ptr + g), q1 = __ldg(P.seg_ptr + g + 1);
-                sigma = 0.0;
-                for (int q = q0; q < q1; ++q) sigma += __ldcg(ucur + __ldg(P.seg_slot + q));
-            }
-            const double xg = fmin(fmax((sigma - gp0.x) * gp0.y, gp1.x), gp1.y);   // IEEE +-inf = no clamp
-            if (info[h] & kInfoFirst) P.x[g] = xg;
-            v[h] = xg;
-            d[h] = -P.rho * xg - lam[h];
+            v[h] = consensus(P, info[h], __ldg(P.s_g + slot), __ldg(P.s_nbr + slot), ucur);
+            d = -P.rho * v[h] - P.lam[slot];
         }
+        dsm[h * 32 + lane] = d;
+        ax[h] = 0.0;
     }
-    double ax[R];
-#pragma unroll
-    for (int h = 0; h < R; ++h) ax[h] = 0.0;
+    __syncwarp();
     const double* __restrict__ A = P.abar + tr.y;
-    const int kmax = tr.z;
-    int base[R];
+    for (int k = 0; k < tr.z; ++k) {
+        const double dk = dsm[k];                              // one subsystem per full task: base 0
 #pragma unroll
-    for (int h = 0; h < R; ++h) base[h] = info[h] & kInfoBaseMask;
-    if (R > 1) {                                   // d staged in this warp's SMEM; row h*32+lane reads
-#pragma unroll                                     // d[base + k] of its own subsystem
-        for (int h = 0; h < R; ++h) dsm[h * 32 + lane] = d[h];
-        __syncwarp();
-#pragma unroll 2
-        for (int k = 0; k < kmax; ++k) {
-#pragma unroll
-            for (int h = 0; h < R; ++h)
-                ax[h] = fma(__ldcs(A + (size_t)k * (32 * R) + h * 32 + lane), dsm[base[h] + k], ax[h]);
-        }
-        __syncwarp();
-    } else {
-#pragma unroll 4
-        for (int k = 0; k < kmax; ++k)
-            ax[0] = fma(__ldcs(A + (size_t)k * 32 + lane), __shfl_sync(kFull, d[0], base[0] + k), ax[0]);
+        for (int h = 0; h < R; ++h) ax[h] = fma(__ldcs(A + (size_t)k * (32 * R) + h * 32 + lane), dk, ax[h]);
     }
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         if (!(info[h] & kInfoValid)) continue;
         const int slot = tr.x + h * 32 + lane;
-        const double xn = fma(ax[h], P.inv_rho, bb[h]);                 // (1/rho) Abar d + bbar
-        const double ln = lam[h] + P.rho * (v[h] - xn);                  // ADMM-3
-        __stcs(P.xl + slot, xn);
-        __stcs(P.lam + slot, ln);
-        unext[slot] = xn - ln * P.inv_rho;                               // next consensus input
-        const double r = v[h] - xn, dx = xn - xo[h];
-        acc[0] += r * r;
-        acc[1] += dx * dx;
-        acc[2] += v[h] * v[h];
-        acc[3] += xn * xn;
-        acc[4] += ln * ln;
+        const double bb = (info[h] & kInfoBbar) ? __ldg(P.s_bbar + slot) : 0.0;
+        finish_slot(P, slot, ax[h], bb, v[h], P.lam[slot], P.xl[slot], unext, acc);
     }
+    __syncwarp();
 }
 
-template <int RMAX>   // largest task width in the problem; RMAX <= 4 keeps 64 registers (2 CTAs / SM)
-__global__ void __launch_bounds__(kBlock, RMAX <= 4 ? kStreamCtasPerSm : 1) admm_stream_kernel(DevProblem P) {
+template <int RMAX>
+struct StreamWarps { static constexpr int value = RMAX <= 2 ? kStreamWarps : kStreamWarpsWide; };
+
+template <int RMAX>   // largest task width in the problem (RMAX > 2 only with n_s > 64: the S = 1 path)
+__global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_stream_kernel(DevProblem P) {
+    constexpr int kWarps = StreamWarps<RMAX>::value;
+    extern __shared__ __align__(128) char sdyn[];      // [kWarps][2][kStageBytes] stages, [kWarps][32*RMAX] d
     __shared__ double red[kWarps][5];
-    __shared__ double dstage[kWarps][256];
+    __shared__ uint64_t sbar[kWarps][2];
     __shared__ int s_stop;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
+    Stage st{sdyn + (size_t)wid * 2 * kStageBytes, sbar[wid], 0u, 0u};
+    double* dsm = reinterpret_cast<double*>(sdyn + (size_t)kWarps * 2 * kStageBytes) + (size_t)wid * 32 * RMAX;
+    if (lane == 0) {
+        mbar_init(st.bar);
+        mbar_init(st.bar + 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
     const long long total0 = *(volatile long long*)&P.ctrl->total;
     long long it = 0;
+    if (P.max_iter > 0) issue_task(P, st, gw, lane);
     while (it < P.max_iter) {
         const long long t = total0 + it;
         const double* ucur = (t & 1) ? P.u1 : P.u0;
@@ -134,14 +266,21 @@ __global__ void __launch_bounds__(kBlock, RMAX <= 4 ? kStreamCtasPerSm : 1) admm
         double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         for (int task = gw; task < P.n_tasks; task += nw) {
             const int4 tr = __ldg(P.tasks + task);
-            double* dsm = dstage[wid];
-            switch (tr.w) {
-                case 1: task_sweep<1>(P, tr, ucur, unext, acc, lane, dsm); break;
-                case 2: task_sweep<2>(P, tr, ucur, unext, acc, lane, dsm); break;
-                case 4: if constexpr (RMAX >= 4) task_sweep<4>(P, tr, ucur, unext, acc, lane, dsm); break;
-                default: if constexpr (RMAX >= 8) task_sweep<8>(P, tr, ucur, unext, acc, lane, dsm); break;
+            if (task + nw < P.n_tasks) issue_task(P, st, task + nw, lane);     // one task ahead
+            if (tr.w & kTaskPacked) {
+                if ((tr.w & 0xF) == 1) task_packed<1>(P, tr, ucur, unext, acc, lane, dsm, st);
+                else if constexpr (RMAX >= 2) task_packed<2>(P, tr, ucur, unext, acc, lane, dsm, st);
+            } else {
+                switch (tr.w & 0xF) {
+                    case 2: if constexpr (RMAX >= 2) task_full<2>(P, tr, ucur, unext, acc, lane, dsm); break;
+                    case 4: if constexpr (RMAX >= 4) task_full<4>(P, tr, ucur, unext, acc, lane, dsm); break;
+                    default: if constexpr (RMAX >= 8) task_full<8>(P, tr, ucur, unext, acc, lane, dsm); break;
+                }
             }
         }
+        // this warp's first task of the next sweep, staged across the grid barrier: its operators are
+        // constant and its lambda / x_s were written by this warp only (all lanes, before __syncwarp)
+        if (it + 1 < P.max_iter) issue_task(P, st, gw, lane);
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
 #pragma unroll
@@ -216,6 +355,10 @@ __global__ void __launch_bounds__(kBlock, RMAX <= 4 ? kStreamCtasPerSm : 1) admm
         __syncthreads();
         if (s_stop) break;
     }
+    while (st.consumed < st.issued) {                          // drain the prefetch of a sweep not run
+        mbar_wait(st.bar + (st.consumed & 1), (st.consumed >> 1) & 1);
+        ++st.consumed;
+    }
 }
 
 // a3: reset the iterate to the initial point: x_s = x0, lambda = 0, u = x0.
@@ -242,11 +385,21 @@ static const void* stream_kernel_for(int rmax) {
                      : (const void*)admm_stream_kernel<8>;
 }
 
+static int stream_smem(int rmax) {
+    const int r = rmax <= 1 ? 1 : rmax <= 2 ? 2 : rmax <= 4 ? 4 : 8;
+    return (rmax <= 2 ? kStreamWarps : kStreamWarpsWide) * (2 * kStageBytes + 8 * 32 * r);
+}
+
+int stream_block(int rmax) { return 32 * (rmax <= 2 ? kStreamWarps : kStreamWarpsWide); }
+
 lopf_status query_grid(int rmax, int* grid, std::string& err) {
     int dev = 0, sms = 0, per = 0;
+    const void* k = stream_kernel_for(rmax);
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_kernel_for(rmax), kBlock, 0);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem(rmax));
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, stream_block(rmax), stream_smem(rmax));
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     if (per < 1) { err = "streaming kernel cannot be resident (occupancy 0)"; return LOPF_E_CUDA; }
     *grid = sms * per;
@@ -260,7 +413,8 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
     if (e == cudaSuccess && P.max_iter > 0) {
         DevProblem Q = P;
         void* args[] = {&Q};
-        e = cudaLaunchCooperativeKernel(stream_kernel_for(P.rmax), dim3(grid), dim3(kBlock), args, 0, s);
+        e = cudaLaunchCooperativeKernel(stream_kernel_for(P.rmax), dim3(grid), dim3(stream_block(P.rmax)), args,
+                                        stream_smem(P.rmax), s);
     }
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;

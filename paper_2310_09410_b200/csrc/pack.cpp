@@ -25,13 +25,14 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     L = Layout();
     L.kernel = 1;
     // ---- tasks ---------------------------------------------------------------------------------
-    // Locality first: walk the subsystems in depth-first order (neighbouring subsystems share
+    // Subsystems are taken in depth-first order of the feeder (neighbouring subsystems share
     // globals, so the u values a task gathers were fetched into L2 by a task that ran moments
-    // earlier) and cut that order into windows of kWindow subsystems; inside a window the
-    // subsystems are grouped by n_s so every task is homogeneous (its column loop has no padding).
-    // A task of n_s <= 32 holds up to kTaskHalves halves of floor(32 / n_s) subsystems each (a
-    // subsystem never straddles a half); n_s > 32 gives one subsystem per R = 2, 4 or 8 task.
-    struct T { int R, kmax; size_t pos; std::vector<int64_t> subs; std::vector<int> base; };
+    // earlier) and packed greedily into PACKED tasks of up to kTaskHalves 32-slot halves (a
+    // subsystem never straddles a half) whose upper-triangular Abar blocks, concatenated, fit the
+    // per-warp SMEM stage (kPackBudget doubles): the kernel bulk-copies (TMA) that block into SMEM
+    // one task ahead.  A subsystem whose packed block alone exceeds the stage (n_s >= 27) gets a
+    // FULL task of its own: Abar as kmax columns of 32*R doubles read straight from HBM.
+    struct T { int R, kmax, plen; bool packed, direct; std::vector<int64_t> subs; std::vector<int> base, poff; };
     std::vector<T> tasks;
     for (int64_t s = 0; s < P.S; ++s)
         if (P.n_s[s] > 256) {
@@ -39,43 +40,61 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
                   " > 256 (unsupported by the warp-task layout; the S = 1 path is for small feeders)";
             return LOPF_E_ARG;
         }
-    const std::vector<int64_t> order = dfs_order(N, P);
-    for (size_t w0 = 0; w0 < order.size(); w0 += kWindow) {
-        const size_t w1 = std::min(order.size(), w0 + kWindow);
-        std::map<int, std::vector<std::pair<size_t, int64_t>>> by_ns;   // n_s -> (position, subsystem)
-        for (size_t i = w0; i < w1; ++i)
-            if (P.n_s[order[i]] > 0) by_ns[P.n_s[order[i]]].push_back({i, order[i]});
-        std::vector<T> wt;
-        for (const auto& [ns, v] : by_ns) {
-            if (ns > 32) {
+    auto has_bbar = [&](int64_t s) {
+        for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k)
+            if (P.bbar[k] != 0.0) return true;
+        return false;
+    };
+    {
+        T cur{1, 0, 0, true, false, {}, {}, {}};
+        int half = 0, fill = 0;
+        auto close = [&] {
+            if (!cur.subs.empty()) {
+                cur.R = half + (fill > 0 ? 1 : 0);
+                cur.plen = (cur.plen + 1) & ~1;                  // 16-byte multiple for the bulk copy
+                tasks.push_back(std::move(cur));
+            }
+            cur = T{1, 0, 0, true, false, {}, {}, {}};
+            half = 0;
+            fill = 0;
+        };
+        for (int64_t s : dfs_order(N, P)) {
+            const int ns = P.n_s[s];
+            if (ns == 0) continue;
+            const int ps = ns * (ns + 1) / 2 + (has_bbar(s) ? ns : 0);   // triangle (+ b-bar)
+            if (ns > 63) {                                       // full task (S = 1 path)
+                close();
                 const int R = ns <= 64 ? 2 : ns <= 128 ? 4 : 8;
-                for (const auto& [pos, s] : v) wt.push_back({R, ns, pos, {s}, {0}});
+                tasks.push_back(T{R, ns, 0, false, false, {s}, {0}, {0}});
                 continue;
             }
-            const size_t per = 32 / ns, cap = per * kTaskHalves;
-            for (size_t i = 0; i < v.size(); i += cap) {
-                const size_t cnt = std::min(cap, v.size() - i);
-                int R = 1;
-                while ((size_t)R * per < cnt) R *= 2;
-                T t{R, ns, v[i].first, {}, {}};
-                for (size_t j = 0; j < cnt; ++j) {
-                    t.subs.push_back(v[i + j].second);
-                    t.base.push_back((int)((j / per) * 32 + (j % per) * ns));
-                }
-                wt.push_back(std::move(t));
+            if (ps > kPackBudget) {                              // block read from HBM, task of its own
+                close();
+                tasks.push_back(T{ns <= 32 ? 1 : 2, ns, (ps + 1) & ~1, true, true, {s}, {0}, {0}});
+                continue;
             }
+            if (fill + ns > 32) { ++half; fill = 0; }
+            if (half == kTaskHalves || cur.plen + ps > kPackBudget) close();
+            cur.subs.push_back(s);
+            cur.base.push_back(half * 32 + fill);
+            cur.poff.push_back(cur.plen);
+            cur.kmax = std::max(cur.kmax, ns);
+            cur.plen += ps;
+            fill += ns;
         }
-        std::stable_sort(wt.begin(), wt.end(), [](const T& a, const T& b) { return a.pos < b.pos; });
-        for (auto& t : wt) tasks.push_back(std::move(t));
+        close();
     }
     L.n_tasks = (int64_t)tasks.size();
     std::vector<int4> trec(L.n_tasks);
     int64_t slots = 0, pool = 0;
     for (int64_t t = 0; t < L.n_tasks; ++t) {
-        trec[t] = make_int4((int)slots, (int)pool, tasks[t].kmax, tasks[t].R);
-        L.rmax = std::max(L.rmax, tasks[t].R);
-        slots += 32 * tasks[t].R;
-        pool += (int64_t)tasks[t].kmax * 32 * tasks[t].R;
+        const T& k = tasks[t];
+        trec[t] = k.packed ? make_int4((int)slots, (int)pool, k.plen,
+                                       k.R | kTaskPacked | (k.direct ? kTaskDirect : 0) | (k.kmax << kTaskKmaxShift))
+                           : make_int4((int)slots, (int)pool, k.kmax, k.R);
+        L.rmax = std::max(L.rmax, k.R);
+        slots += 32 * k.R;
+        pool += k.packed ? (int64_t)k.plen : (int64_t)k.kmax * 32 * k.R;
     }
     if (slots > INT32_MAX || pool > INT32_MAX) { err = "problem too large for 32-bit slot / pool offsets"; return LOPF_E_ARG; }
     L.n_slots = slots;
@@ -129,25 +148,29 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
 
     L.slot_of_copy.assign(NC, -1);
     for (int64_t t = 0; t < L.n_tasks; ++t) {
-        const int P32 = 32 * tasks[t].R;
-        for (size_t j = 0; j < tasks[t].subs.size(); ++j) {
-            const int64_t s = tasks[t].subs[j];
-            const int ns = P.n_s[s], base = tasks[t].base[j];
-            const bool has_b = [&] {
-                for (int r = 0; r < ns; ++r)
-                    if (P.bbar[P.sub_ptr[s] + r] != 0.0) return true;
-                return false;
-            }();
+        const T& tk = tasks[t];
+        const int P32 = 32 * tk.R;
+        for (size_t j = 0; j < tk.subs.size(); ++j) {
+            const int64_t s = tk.subs[j];
+            const int ns = P.n_s[s], base = tk.base[j];
+            const double* Ab = &P.abar[P.abar_ptr[s]];
+            const bool has_b = has_bbar(s);
             for (int r = 0; r < ns; ++r) {
                 const int64_t slot = trec[t].x + base + r;
                 const int64_t copy = P.sub_ptr[s] + r;
                 L.slot_of_copy[copy] = (int32_t)slot;
-                info[slot] = (base & kInfoBaseMask) | kInfoValid | (has_b ? kInfoBbar : 0);
+                info[slot] = base | kInfoValid | (has_b ? kInfoBbar : 0) | (ns << kInfoNsShift) |
+                             (tk.packed ? tk.poff[j] << kInfoPoffShift : 0);
                 gs[slot] = P.copy_global[copy];
                 bbar[slot] = P.bbar[copy];
-                const double* Ab = &P.abar[P.abar_ptr[s]];
-                for (int k = 0; k < ns; ++k)      // lane (slot) r computes row r: sum_k Abar[r][k] d[k]
-                    abar[(size_t)trec[t].y + (size_t)k * P32 + base + r] = Ab[(size_t)r * ns + k];
+                if (tk.packed) {                  // upper triangle, row-major: (r, k >= r); then b-bar
+                    double* dst = abar + trec[t].y + tk.poff[j];
+                    for (int k = r; k < ns; ++k) dst[r * ns - r * (r - 1) / 2 + (k - r)] = Ab[(size_t)r * ns + k];
+                    if (has_b) dst[ns * (ns + 1) / 2 + r] = P.bbar[copy];
+                } else {                          // lane (slot) r computes row r: sum_k Abar[r][k] d[k]
+                    for (int k = 0; k < ns; ++k)
+                        abar[(size_t)trec[t].y + (size_t)k * P32 + base + r] = Ab[(size_t)r * ns + k];
+                }
             }
         }
     }
@@ -160,7 +183,7 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
         const int32_t slot = L.slot_of_copy[k];
         const int32_t g = P.copy_global[k];
         const int64_t s0 = P.seg_ptr[g], nu = P.seg_ptr[g + 1] - s0;
-        info[slot] |= (int)(std::min<int64_t>(nu, 255) << kInfoNuShift);
+        info[slot] |= (int)(std::min<int64_t>(nu, 15) << kInfoNuShift);
         if (P.seg_copy[s0] == k) info[slot] |= kInfoFirst;
         if (nu <= 4) {
             info[slot] |= kInfoInline;
