@@ -284,7 +284,8 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     P.u0 = (double*)(b + L.off_u0);
     P.u1 = (double*)(b + L.off_u1);
     P.x0 = (const double*)(b + L.off_x0);
-    P.gpar = (const double4*)(b + L.off_gpar);
+    P.gbnd = (const double2*)(b + L.off_gpar);
+    P.gcost = (const double*)(b + L.off_gcost);
     P.seg_ptr = (const int32_t*)(b + L.off_segptr);
     P.seg_slot = (const int32_t*)(b + L.off_segslot);
     P.x = (double*)(b + L.off_x);

@@ -58,7 +58,8 @@ struct Canon {
 
 // ---- device layout shared by pack.cpp and kernels.cu ---------------------------------------
 // Slot info bit fields (streaming kernel).
-constexpr int kInfoBaseMask = 0xFF;        // slot index (in its task) of the subsystem's first row
+constexpr int kInfoBaseMask = 0x3F;        // slot index (in its task) of the subsystem's first row
+constexpr int kInfoCost = 1 << 6;          // the global has c != 0 (a p^g column): read c/rho
 constexpr int kInfoValid = 1 << 8;
 constexpr int kInfoFirst = 1 << 9;         // first copy (canonical) of its global: writes x_g
 constexpr int kInfoInline = 1 << 10;       // segment slots stored inline (nu <= 4)
@@ -70,6 +71,7 @@ constexpr int kInfoPoffShift = 22;         // offset (doubles) of the subsystem'
 constexpr int kTaskPacked = 1 << 4;        // packed task: .z = block doubles, kmax in bits 8..15 of .w
 constexpr int kTaskDirect = 1 << 5;        // packed task whose block exceeds the stage: read from HBM
 constexpr int kTaskKmaxShift = 8;
+constexpr int kTaskUsedShift = 16;         // packed task: slots in use (rounded up to 4), bits 16..23 of .w
 constexpr int kTaskHalves = 2;             // streaming packer: max 32-slot halves per packed task
 constexpr int kPackBudget = 224;           // doubles of operator block per staged task (per-warp SMEM stage)
 
@@ -98,7 +100,8 @@ struct DevProblem {                        // kernel argument (pointers into the
     double* u0;
     double* u1;
     const double* x0;                      // initial x_s per slot
-    const double4* gpar;                   // {c/rho, 1/nu, lo, hi} per global
+    const double2* gbnd;                   // {lo, hi} per global
+    const double* gcost;                   // c/rho per global (read for kInfoCost slots only)
     const int32_t* seg_ptr;                // [n+1] into seg_slot
     const int32_t* seg_slot;               // [nc] slots in canonical copy order
     double* x;                             // [n]
@@ -206,7 +209,7 @@ struct Layout {
     int64_t n_tasks = 0, n_slots = 0, abar_doubles = 0, n_obj = 0;
     int32_t rmax = 1;                     // streaming: widest task (R)
     size_t off_tasks = 0, off_info = 0, off_g = 0, off_nbr = 0, off_bbar = 0, off_xl = 0, off_lam = 0,
-           off_u0 = 0, off_u1 = 0, off_x0 = 0, off_gpar = 0, off_segptr = 0, off_segslot = 0, off_x = 0, off_abar = 0,
+           off_u0 = 0, off_u1 = 0, off_x0 = 0, off_gpar = 0, off_gcost = 0, off_segptr = 0, off_segslot = 0, off_x = 0, off_abar = 0,
            off_partial = 0, off_ctrl = 0, off_trace = 0, off_objidx = 0, off_objc = 0;
     size_t bytes = 0;
     int32_t max_grid = 0, trace_cap = 0;

@@ -33,6 +33,8 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+constexpr int kInvNu = 64;                 // SMEM table of 1 / nu (the host's 1.0 / nu, bit for bit)
+
 // ---- bulk-copy (TMA) staging ---------------------------------------------------------------------
 // A packed task's inputs are contiguous byte ranges: its operator block (upper-triangular Abar of
 // each subsystem, then b-bar if nonzero) in the pool, and 32*R entries of each per-slot array.  One
@@ -65,21 +67,21 @@ struct Stage {                   // per-warp pipeline: the j-th staged task of t
     uint32_t issued, consumed;
 };
 
-__device__ __forceinline__ void issue_task(const DevProblem& P, Stage& st, const int task, const int lane) {
-    if (task >= P.n_tasks) return;
-    const int4 tr = __ldg(P.tasks + task);
+// `full_fence`: the copies read lambda / x_s this warp stored in the same sweep (the next-sweep
+// prefetch); otherwise only the stage's SMEM (read by this warp's previous task) needs ordering.
+__device__ __forceinline__ void issue_task(const DevProblem& P, Stage& st, const int4 tr, const int lane,
+                                           const bool full_fence) {
     if (!(tr.w & kTaskPacked)) return;                          // full tasks read HBM directly
     const int b = st.issued & 1;
     ++st.issued;
     if (lane == 0) {
         char* sb = st.buf + b * kStageBytes;
-        const uint32_t n = 32u * (uint32_t)(tr.w & 0xF);
+        const uint32_t n = (uint32_t)(tr.w >> kTaskUsedShift) & 0xFFu;
         const bool ablk = !(tr.w & kTaskDirect);
         const uint32_t bytes = 40u * n + (ablk ? 8u * (uint32_t)tr.z : 0u);
         uint64_t* m = st.bar + b;
-        // order this warp's earlier generic accesses (SMEM reads of the stage, global stores of lambda
-        // and x_s) before the async-proxy copies
-        asm volatile("fence.proxy.async;" ::: "memory");
+        if (full_fence) asm volatile("fence.proxy.async;" ::: "memory");
+        else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
         if (ablk) bulk_g2s(sb, P.abar + tr.y, 8u * (uint32_t)tr.z, m);
         bulk_g2s(sb + kOffInfo, P.s_info + tr.x, 4u * n, m);
@@ -92,10 +94,10 @@ __device__ __forceinline__ void issue_task(const DevProblem& P, Stage& st, const
 
 // a4 for one slot: the global's consensus value from the ping-pong copies (closed_1, rho restored)
 __device__ __forceinline__ double consensus(const DevProblem& P, const int inf, const int g, const int4 nb,
-                                            const double* __restrict__ ucur) {
-    const double2 gp0 = __ldg(reinterpret_cast<const double2*>(P.gpar + g));       // {c/rho, 1/nu}
-    const double2 gp1 = __ldg(reinterpret_cast<const double2*>(P.gpar + g) + 1);   // {lo, hi}
-    double sigma;
+                                            const double* __restrict__ ucur, const double* __restrict__ inv_nu) {
+    const double2 bd = __ldg(P.gbnd + g);                               // {lo, hi}
+    const double cr = (inf & kInfoCost) ? __ldg(P.gcost + g) : 0.0;     // c / rho
+    double sigma, inv;
     if (inf & kInfoInline) {                               // nu <= 4: neighbour slots inline
         const int nu = (inf >> kInfoNuShift) & 0xF;
         const double a0 = __ldcg(ucur + nb.x);
@@ -106,12 +108,14 @@ __device__ __forceinline__ double consensus(const DevProblem& P, const int inf, 
         if (nu > 1) sigma += a1;
         if (nu > 2) sigma += a2;
         if (nu > 3) sigma += a3;
+        inv = inv_nu[nu];
     } else {
         const int q0 = __ldg(P.seg_ptr + g), q1 = __ldg(P.seg_ptr + g + 1);
         sigma = 0.0;
         for (int q = q0; q < q1; ++q) sigma += __ldcg(ucur + __ldg(P.seg_slot + q));
+        inv = q1 - q0 < kInvNu ? inv_nu[q1 - q0] : 1.0 / (double)(q1 - q0);
     }
-    const double xg = fmin(fmax((sigma - gp0.x) * gp0.y, gp1.x), gp1.y);   // IEEE +-inf = no clamp
+    const double xg = fmin(fmax((sigma - cr) * inv, bd.x), bd.y);      // IEEE +-inf = no clamp
     if (inf & kInfoFirst) P.x[g] = xg;
     return xg;
 }
@@ -138,7 +142,7 @@ __device__ __forceinline__ void finish_slot(const DevProblem& P, const int slot,
 template <int R>
 __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, const double* __restrict__ ucur,
                                             double* __restrict__ unext, double (&acc)[5], const int lane,
-                                            double* __restrict__ dsm, Stage& st) {
+                                            double* __restrict__ dsm, Stage& st, const double* __restrict__ inv_nu) {
     const int b = st.consumed & 1;
     mbar_wait(st.bar + b, (st.consumed >> 1) & 1);
     ++st.consumed;
@@ -149,16 +153,17 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
     const double* s_lam = reinterpret_cast<const double*>(sb + kOffLam);
     const double* s_xl = reinterpret_cast<const double*>(sb + kOffXl);
     const double* S = (tr.w & kTaskDirect) ? P.abar + tr.y : reinterpret_cast<const double*>(sb);
+    const int used = (tr.w >> kTaskUsedShift) & 0xFF;       // stage entries past `used` are stale
     double v[R], ax[R];
     int info[R];
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         const int j = h * 32 + lane;
-        info[h] = s_info[j];
+        info[h] = j < used ? s_info[j] : 0;
         v[h] = 0.0;
         double d = 0.0;
         if (info[h] & kInfoValid) {
-            v[h] = consensus(P, info[h], s_g[j], s_nbr[j], ucur);
+            v[h] = consensus(P, info[h], s_g[j], s_nbr[j], ucur, inv_nu);
             d = -P.rho * v[h] - s_lam[j];
         }
         dsm[j] = d;
@@ -203,7 +208,7 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
 template <int R>
 __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, const double* __restrict__ ucur,
                                           double* __restrict__ unext, double (&acc)[5], const int lane,
-                                          double* __restrict__ dsm) {
+                                          double* __restrict__ dsm, const double* __restrict__ inv_nu) {
     double v[R], ax[R];
     int info[R];
 #pragma unroll
@@ -213,7 +218,7 @@ __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, co
         v[h] = 0.0;
         double d = 0.0;
         if (info[h] & kInfoValid) {
-            v[h] = consensus(P, info[h], __ldg(P.s_g + slot), __ldg(P.s_nbr + slot), ucur);
+            v[h] = consensus(P, info[h], __ldg(P.s_g + slot), __ldg(P.s_nbr + slot), ucur, inv_nu);
             d = -P.rho * v[h] - P.lam[slot];
         }
         dsm[h * 32 + lane] = d;
@@ -245,42 +250,49 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_stream_
     extern __shared__ __align__(128) char sdyn[];      // [kWarps][2][kStageBytes] stages, [kWarps][32*RMAX] d
     __shared__ double red[kWarps][5];
     __shared__ uint64_t sbar[kWarps][2];
+    __shared__ double inv_nu[kInvNu];
     __shared__ int s_stop;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
     Stage st{sdyn + (size_t)wid * 2 * kStageBytes, sbar[wid], 0u, 0u};
     double* dsm = reinterpret_cast<double*>(sdyn + (size_t)kWarps * 2 * kStageBytes) + (size_t)wid * 32 * RMAX;
+    for (int i = threadIdx.x; i < kInvNu; i += blockDim.x) inv_nu[i] = i > 0 ? 1.0 / (double)i : 0.0;
     if (lane == 0) {
         mbar_init(st.bar);
         mbar_init(st.bar + 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncwarp();
+    __syncthreads();
     const long long total0 = *(volatile long long*)&P.ctrl->total;
+    const int4 tr0 = gw < P.n_tasks ? __ldg(P.tasks + gw) : make_int4(0, 0, 0, 0);
     long long it = 0;
-    if (P.max_iter > 0) issue_task(P, st, gw, lane);
+    if (P.max_iter > 0) issue_task(P, st, tr0, lane, false);
     while (it < P.max_iter) {
         const long long t = total0 + it;
         const double* ucur = (t & 1) ? P.u1 : P.u0;
         double* unext = (t & 1) ? P.u0 : P.u1;
         double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        int4 tr = tr0;
+        int4 tr1 = gw + nw < P.n_tasks ? __ldg(P.tasks + gw + nw) : make_int4(0, 0, 0, 0);
         for (int task = gw; task < P.n_tasks; task += nw) {
-            const int4 tr = __ldg(P.tasks + task);
-            if (task + nw < P.n_tasks) issue_task(P, st, task + nw, lane);     // one task ahead
+            const int4 tr2 = task + 2 * nw < P.n_tasks ? __ldg(P.tasks + task + 2 * nw) : make_int4(0, 0, 0, 0);
+            if (task + nw < P.n_tasks) issue_task(P, st, tr1, lane, false);   // one task ahead
             if (tr.w & kTaskPacked) {
-                if ((tr.w & 0xF) == 1) task_packed<1>(P, tr, ucur, unext, acc, lane, dsm, st);
-                else if constexpr (RMAX >= 2) task_packed<2>(P, tr, ucur, unext, acc, lane, dsm, st);
+                if ((tr.w & 0xF) == 1) task_packed<1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
+                else if constexpr (RMAX >= 2) task_packed<2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
             } else {
                 switch (tr.w & 0xF) {
-                    case 2: if constexpr (RMAX >= 2) task_full<2>(P, tr, ucur, unext, acc, lane, dsm); break;
-                    case 4: if constexpr (RMAX >= 4) task_full<4>(P, tr, ucur, unext, acc, lane, dsm); break;
-                    default: if constexpr (RMAX >= 8) task_full<8>(P, tr, ucur, unext, acc, lane, dsm); break;
+                    case 2: if constexpr (RMAX >= 2) task_full<2>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
+                    case 4: if constexpr (RMAX >= 4) task_full<4>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
+                    default: if constexpr (RMAX >= 8) task_full<8>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
                 }
             }
+            tr = tr1;
+            tr1 = tr2;
         }
         // this warp's first task of the next sweep, staged across the grid barrier: its operators are
         // constant and its lambda / x_s were written by this warp only (all lanes, before __syncwarp)
-        if (it + 1 < P.max_iter) issue_task(P, st, gw, lane);
+        if (it + 1 < P.max_iter && gw < P.n_tasks) issue_task(P, st, tr0, lane, true);
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
 #pragma unroll

@@ -27,12 +27,13 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     // ---- tasks ---------------------------------------------------------------------------------
     // Subsystems are taken in depth-first order of the feeder (neighbouring subsystems share
     // globals, so the u values a task gathers were fetched into L2 by a task that ran moments
-    // earlier) and packed greedily into PACKED tasks of up to kTaskHalves 32-slot halves (a
-    // subsystem never straddles a half) whose upper-triangular Abar blocks, concatenated, fit the
-    // per-warp SMEM stage (kPackBudget doubles): the kernel bulk-copies (TMA) that block into SMEM
-    // one task ahead.  A subsystem whose packed block alone exceeds the stage (n_s >= 27) gets a
-    // FULL task of its own: Abar as kmax columns of 32*R doubles read straight from HBM.
-    struct T { int R, kmax, plen; bool packed, direct; std::vector<int64_t> subs; std::vector<int> base, poff; };
+    // earlier) and packed greedily into PACKED tasks of up to 32 * kTaskHalves slots whose operator
+    // blocks (upper-triangular Abar of each subsystem, then its b-bar if nonzero), concatenated, fit
+    // the per-warp SMEM stage (kPackBudget doubles): the kernel bulk-copies (TMA) the block and the
+    // task's per-slot inputs into SMEM one task ahead.  A subsystem whose block alone exceeds the
+    // stage is a DIRECT packed task of its own (block read from HBM); n_s > 63 (the S = 1 path) gets
+    // a FULL task: Abar as kmax columns of 32*R doubles.
+    struct T { int R, kmax, plen, used; bool packed, direct; std::vector<int64_t> subs; std::vector<int> base, poff; };
     std::vector<T> tasks;
     for (int64_t s = 0; s < P.S; ++s)
         if (P.n_s[s] > 256) {
@@ -46,16 +47,16 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
         return false;
     };
     {
-        T cur{1, 0, 0, true, false, {}, {}, {}};
-        int half = 0, fill = 0;
+        T cur{1, 0, 0, 0, true, false, {}, {}, {}};
+        int fill = 0;
         auto close = [&] {
             if (!cur.subs.empty()) {
-                cur.R = half + (fill > 0 ? 1 : 0);
-                cur.plen = (cur.plen + 1) & ~1;                  // 16-byte multiple for the bulk copy
+                cur.R = fill > 32 ? 2 : 1;
+                cur.used = (fill + 3) & ~3;                      // slots the bulk copies move (16-byte multiples)
+                cur.plen = (cur.plen + 1) & ~1;
                 tasks.push_back(std::move(cur));
             }
-            cur = T{1, 0, 0, true, false, {}, {}, {}};
-            half = 0;
+            cur = T{1, 0, 0, 0, true, false, {}, {}, {}};
             fill = 0;
         };
         for (int64_t s : dfs_order(N, P)) {
@@ -65,18 +66,17 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
             if (ns > 63) {                                       // full task (S = 1 path)
                 close();
                 const int R = ns <= 64 ? 2 : ns <= 128 ? 4 : 8;
-                tasks.push_back(T{R, ns, 0, false, false, {s}, {0}, {0}});
+                tasks.push_back(T{R, ns, 0, 32 * R, false, false, {s}, {0}, {0}});
                 continue;
             }
             if (ps > kPackBudget) {                              // block read from HBM, task of its own
                 close();
-                tasks.push_back(T{ns <= 32 ? 1 : 2, ns, (ps + 1) & ~1, true, true, {s}, {0}, {0}});
+                tasks.push_back(T{ns <= 32 ? 1 : 2, ns, (ps + 1) & ~1, (ns + 3) & ~3, true, true, {s}, {0}, {0}});
                 continue;
             }
-            if (fill + ns > 32) { ++half; fill = 0; }
-            if (half == kTaskHalves || cur.plen + ps > kPackBudget) close();
+            if (fill + ns > 32 * kTaskHalves || cur.plen + ps > kPackBudget) close();
             cur.subs.push_back(s);
-            cur.base.push_back(half * 32 + fill);
+            cur.base.push_back(fill);                            // rows may straddle the two halves
             cur.poff.push_back(cur.plen);
             cur.kmax = std::max(cur.kmax, ns);
             cur.plen += ps;
@@ -90,7 +90,8 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     for (int64_t t = 0; t < L.n_tasks; ++t) {
         const T& k = tasks[t];
         trec[t] = k.packed ? make_int4((int)slots, (int)pool, k.plen,
-                                       k.R | kTaskPacked | (k.direct ? kTaskDirect : 0) | (k.kmax << kTaskKmaxShift))
+                                       k.R | kTaskPacked | (k.direct ? kTaskDirect : 0) | (k.kmax << kTaskKmaxShift) |
+                                           (k.used << kTaskUsedShift))
                            : make_int4((int)slots, (int)pool, k.kmax, k.R);
         L.rmax = std::max(L.rmax, k.R);
         slots += 32 * k.R;
@@ -123,7 +124,8 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     L.off_u0 = take(8 * NS);
     L.off_u1 = take(8 * NS);
     L.off_x0 = take(8 * NS);
-    L.off_gpar = take(32 * NG);
+    L.off_gpar = take(16 * NG);
+    L.off_gcost = take(8 * NG);
     L.off_segptr = take(4 * (NG + 1));
     L.off_segslot = take(4 * NC);
     L.off_x = take(8 * NG);
@@ -185,6 +187,7 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
         const int64_t s0 = P.seg_ptr[g], nu = P.seg_ptr[g + 1] - s0;
         info[slot] |= (int)(std::min<int64_t>(nu, 15) << kInfoNuShift);
         if (P.seg_copy[s0] == k) info[slot] |= kInfoFirst;
+        if (P.c[g] != 0.0) info[slot] |= kInfoCost;
         if (nu <= 4) {
             info[slot] |= kInfoInline;
             int v[4] = {0, 0, 0, 0};
@@ -192,10 +195,11 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
             nbr[slot] = make_int4(v[0], v[1], v[2], v[3]);
         }
     }
-    double4* gpar = (double4*)at(L.off_gpar);
+    double2* gbnd = (double2*)at(L.off_gpar);
+    double* gcost = (double*)at(L.off_gcost);
     for (int64_t i = 0; i < P.n; ++i) {
-        const double nu = (double)(P.seg_ptr[i + 1] - P.seg_ptr[i]);
-        gpar[i] = make_double4(P.c[i] / opt.rho, 1.0 / nu, P.lo[i], P.hi[i]);
+        gbnd[i] = make_double2(P.lo[i], P.hi[i]);
+        gcost[i] = P.c[i] / opt.rho;
     }
     std::memcpy(at(L.off_objidx), obj_idx.data(), 4 * obj_idx.size());
     std::memcpy(at(L.off_objc), obj_c.data(), 8 * obj_c.size());
