@@ -73,7 +73,10 @@ constexpr int kTaskDirect = 1 << 5;        // packed task whose block exceeds th
 constexpr int kTaskKmaxShift = 8;
 constexpr int kTaskUsedShift = 16;         // packed task: slots in use (rounded up to 4), bits 16..23 of .w
 constexpr int kTaskHalves = 2;             // streaming packer: max 32-slot halves per packed task
-constexpr int kPackBudget = 224;           // doubles of operator block per staged task (per-warp SMEM stage)
+#ifndef LOPF_PACK_BUDGET
+#define LOPF_PACK_BUDGET 224
+#endif
+constexpr int kPackBudget = LOPF_PACK_BUDGET;  // doubles of operator block per staged task (per-warp SMEM stage)
 
 struct DevCtrl {                           // 256 B, device-resident control block
     unsigned long long arrive;             // barrier arrivals of this launch
@@ -251,7 +254,10 @@ lopf_status pack_resident(const Net& net, const Canon& cp, const lopf_options& o
 // pack_batch.cpp
 lopf_status pack_batch(const Canon& cp, const BatchOps& bo, const lopf_options& opt, Layout& lay, std::string& err);
 // kernels.cu
-constexpr int kStreamWarps = 24;             // streaming CTA (one per SM): 24 warps x 2 SMEM stages
+#ifndef LOPF_STREAM_WARPS
+#define LOPF_STREAM_WARPS 24
+#endif
+constexpr int kStreamWarps = LOPF_STREAM_WARPS;  // streaming CTA (one per SM): 24 warps x 2 SMEM stages
 constexpr int kStreamWarpsWide = 16;         // ... when tasks of R > 2 exist (n_s > 64)
 int stream_block(int rmax);
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);

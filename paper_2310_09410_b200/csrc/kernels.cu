@@ -156,14 +156,48 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
     const int used = (tr.w >> kTaskUsedShift) & 0xFF;       // stage entries past `used` are stale
     double v[R], ax[R];
     int info[R];
+    // a4, split so that every gather of both halves is in flight before the first is consumed
+    double ua[R][4], lo[R], hi[R], cr[R];
+    int g[R];
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         const int j = h * 32 + lane;
         info[h] = j < used ? s_info[j] : 0;
+        const bool val = info[h] & kInfoValid, inl = val && (info[h] & kInfoInline);
+        const int nu = (info[h] >> kInfoNuShift) & 0xF;
+        g[h] = s_g[j];
+        const int4 nb = s_nbr[j];
+        ua[h][0] = inl ? __ldcg(ucur + nb.x) : 0.0;
+        ua[h][1] = inl && nu > 1 ? __ldcg(ucur + nb.y) : 0.0;
+        ua[h][2] = inl && nu > 2 ? __ldcg(ucur + nb.z) : 0.0;
+        ua[h][3] = inl && nu > 3 ? __ldcg(ucur + nb.w) : 0.0;
+        const double2 bd = val ? __ldg(P.gbnd + g[h]) : make_double2(0.0, 0.0);
+        lo[h] = bd.x;
+        hi[h] = bd.y;
+        cr[h] = val && (info[h] & kInfoCost) ? __ldg(P.gcost + g[h]) : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        const int j = h * 32 + lane;
         v[h] = 0.0;
         double d = 0.0;
         if (info[h] & kInfoValid) {
-            v[h] = consensus(P, info[h], s_g[j], s_nbr[j], ucur, inv_nu);
+            double sigma, inv;
+            if (info[h] & kInfoInline) {
+                const int nu = (info[h] >> kInfoNuShift) & 0xF;
+                sigma = ua[h][0];                                  // ascending canonical copy order
+                if (nu > 1) sigma += ua[h][1];
+                if (nu > 2) sigma += ua[h][2];
+                if (nu > 3) sigma += ua[h][3];
+                inv = inv_nu[nu];
+            } else {
+                const int q0 = __ldg(P.seg_ptr + g[h]), q1 = __ldg(P.seg_ptr + g[h] + 1);
+                sigma = 0.0;
+                for (int q = q0; q < q1; ++q) sigma += __ldcg(ucur + __ldg(P.seg_slot + q));
+                inv = q1 - q0 < kInvNu ? inv_nu[q1 - q0] : 1.0 / (double)(q1 - q0);
+            }
+            v[h] = fmin(fmax((sigma - cr[h]) * inv, lo[h]), hi[h]);   // closed_1; IEEE +-inf = no clamp
+            if (info[h] & kInfoFirst) P.x[g[h]] = v[h];
             d = -P.rho * v[h] - s_lam[j];
         }
         dsm[j] = d;
