@@ -123,7 +123,10 @@ struct DevProblem {                        // kernel argument (pointers into the
 // Every CTA owns a DFS-contiguous chunk of subsystems.  Its BLOB (global memory) is copied into
 // SMEM at kernel start; the iterate (x_s, lambda, u) lives in SMEM for the whole launch and is
 // written back at the end.  Offsets are bytes from the blob start.
-constexpr int kResBlock = 1024;               // 31 worker warps + 1 reducer warp
+#ifndef LOPF_RES_BLOCK
+#define LOPF_RES_BLOCK 768
+#endif
+constexpr int kResBlock = LOPF_RES_BLOCK;     // worker warps + 1 reducer warp (768: 80 registers, no spills)
 constexpr int kResSmemBudget = 222 * 1024;    // dynamic SMEM per CTA (227 KB usable on sm_100, minus static)
 // sinfo: base (bits 0-5, first slot of the subsystem in its task) | valid (bit 6) | first (bit 7: this slot
 // is the canonical first copy of a global whose x this CTA outputs) | n_s (bits 8-14) | gl (bits 15-31)

@@ -181,7 +181,8 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     unsigned long long* pub = P.flags + (size_t)G * kFlagStride;       // CTAs x sweeps published
     const long long total0 = *(volatile long long*)&P.ctrl->total;
     const bool prof = P.prof != nullptr;
-    long long c_w = 0, c_p = 0, c0 = 0;
+    __shared__ long long s_prof[3];
+    if (tid == 0) s_prof[0] = s_prof[1] = s_prof[2] = 0;
 
     // initial publication: boundary u of the state into exchange slot 0; flag = 1
     for (int i = tid; i < NS; i += RB) {
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     long long t = 0;                                   // sweeps completed; state t in buffer t & 1
     for (;;) {
         const int cur = (int)(t & 1);
-        if (prof && tid == 0) c0 = clock64();
+        if (prof && tid == 0) s_prof[2] = clock64();
         if (wid == RED) {
             if (t >= 1) {                              // decision for sweep t: every CTA has published it
                 const unsigned long long need = (unsigned long long)G * (unsigned long long)(t + 1);
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
             }
         }
         __syncthreads();                               // [A]: sweep t+1 computed (if t < max_iter)
-        if (prof && tid == 0) { const long long c1 = clock64(); c_w += c1 - c0; c0 = c1; }
+        if (prof && tid == 0) { const long long c1 = clock64(); s_prof[0] += c1 - s_prof[2]; s_prof[2] = c1; }
         if (wid == 0 && t < P.max_iter) {              // publish sweep t+1, then wait for the neighbours
             double s[5];
 #pragma unroll
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
             fence_acq_rel();
         }
         __syncthreads();                               // [B]: decision for sweep t known (reducer)
-        if (prof && tid == 0) c_p += clock64() - c0;
+        if (prof && tid == 0) s_prof[1] += clock64() - s_prof[2];
         if (s_stop[t & 1]) break;                             // state t (buffer t & 1); x^t in xout[t & 1]
         ++t;
     }
@@ -327,7 +328,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     }
     if (prof && tid == 0) {
         long long* pr = P.prof + 4 * cta;
-        pr[0] = c_w; pr[1] = c_p; pr[2] = 0; pr[3] = t;
+        pr[0] = s_prof[0]; pr[1] = s_prof[1]; pr[2] = 0; pr[3] = t;
     }
     __syncthreads();
     if (tid == 0) {
