@@ -483,5 +483,18 @@ def make_stitched(n_sub: int = 64, shape: str = "8500", seed0: int | None = None
     for n in ("gen_bus", "gen_phases", "gen_pmin", "gen_pmax", "gen_qmin", "gen_qmax"):
         kw[n] = getattr(head, n)                                            # only the substation generator
     g = Feeder(name=head.name, root_bus=root, **kw)
-    g.meta = dict(shape=f"stitched{n_sub}x{shape}", seed0=seed0, n_sub=n_sub)
+    g.meta = dict(shape=f"stitched{n_sub}x{shape}", seed0=seed0, n_sub=n_sub,
+                  sub_bus_off=[int(v) for v in off] + [int(off[-1] + subs[-1].n_bus)])
     return g
+
+
+def stitched_bus_owner(f: Feeder, world: int) -> np.ndarray:
+    """The natural partition of a stitched feeder over `world` ranks: rank
+    r = floor(f * world / n_sub) owns subfeeder f and trunk bus f; the substation bus goes to rank 0."""
+    n_sub, off = f.meta["n_sub"], f.meta["sub_bus_off"]
+    own = np.zeros(f.n_bus, np.int32)
+    for k in range(n_sub):
+        r = k * world // n_sub
+        own[1 + k] = r                                   # trunk bus k
+        own[off[k]:off[k + 1]] = r
+    return own

@@ -151,6 +151,35 @@ lopf_status lopf_get_state_scen(lopf_handle *h, void *cuda_stream, int32_t scen,
 /* Scenario scen's operator of subsystem s: abar [n_s*n_s], bbar [n_s]. */
 lopf_status lopf_get_operator_scen(const lopf_handle *h, int64_t s, int32_t scen, double *abar, double *bbar);
 
+/* ---- partitioned mode (config 5: one feeder over `world` GPUs) ----
+ * Every rank calls lopf_setup_part with the SAME network and options.  The buses are split into
+ * `world` contiguous depth-first intervals balanced by work (bus_owner == NULL) or as given by
+ * bus_owner [n_bus] (values in [0, world)); subsystems follow their anchor bus (BUS: the bus,
+ * LINE: the end away from the substation, LEAF: the leaf bus).  A rank keeps only its subsystems;
+ * the copies its globals share with other ranks (boundary copies) travel through an exchange
+ * buffer of n_bnd + 8*world doubles inside the arena: per sweep
+ *     lopf_part_sweep(h, s)      one sweep (a4-a7) of this rank's subsystems; writes its boundary
+ *                                copies' u and its five residual sums into its own exchange slots
+ *     <sum-allreduce of the exchange buffer over the ranks>     (NCCL, caller-side)
+ *     lopf_part_import(h, s)     the other ranks' u into this rank's ghost slots; the termination
+ *                                test on the rank-ordered residual sums; clears
+ *                                the exchange buffer for the next sweep.
+ * Each slot is written by exactly one rank, so the sum is an exact gather, and the consensus of a
+ * boundary global adds its copies in canonical order on every rank: iterates are bit-identical to
+ * the single-GPU streaming kernel.  After termination both calls are no-ops.  lopf_result_get
+ * reports K (iters), the residuals and this rank's share of the objective (sum over ranks = c^T x);
+ * lopf_get_state returns this rank's copies and the globals whose first copy is here, NaN elsewhere.
+ * lopf_solve / lopf_run / lopf_set_state return LOPF_E_STATE on a partitioned handle. */
+lopf_status lopf_setup_part(const lopf_network *net, const lopf_options *opt, int32_t rank, int32_t world,
+                            const int32_t *bus_owner, lopf_handle **out);
+/* Exchange buffer location: byte offset in the arena, length in doubles; boundary slots; ghost slots. */
+lopf_status lopf_part_info(const lopf_handle *h, int64_t *xbuf_offset, int64_t *xbuf_doubles, int32_t *n_bnd,
+                           int32_t *n_imp);
+/* The partition: bus_owner [n_bus], copy_owner [n_copies], exchange slot of every copy or -1 [n_copies]. */
+lopf_status lopf_part_owner(const lopf_handle *h, int32_t *bus_owner, int32_t *copy_owner, int32_t *bidx);
+lopf_status lopf_part_sweep(lopf_handle *h, void *cuda_stream);
+lopf_status lopf_part_import(lopf_handle *h, void *cuda_stream);
+
 /* Copy the packed problem into the caller's device arena (device pointer, >= device_bytes,
  * 256-byte aligned) on `stream`, and reset the iterate to the initial point of PAPER.md:495.
  * May be called again (e.g. to re-upload for an end-to-end timing). */

@@ -27,7 +27,9 @@ struct lopf_handle {
     BatchProblem bp{};
     BatchOps bo;
     std::vector<ScenResult> scen_res;              // host copy of the last batch results
+    PartSpec part;                                 // partitioned mode (lay.part != 0)
     bool resident() const { return lay.kernel == 2; }
+    bool parted() const { return lay.part != 0; }
     bool batch() const { return lay.kernel == 3; }
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
@@ -133,6 +135,82 @@ lopf_status lopf_setup_batch(const lopf_network* net, const lopf_options* opt, i
         return fail(LOPF_E_ARG, "out of host memory during setup");
     }
     *out = h;
+    return LOPF_OK;
+}
+
+lopf_status lopf_setup_part(const lopf_network* net, const lopf_options* opt, int32_t rank, int32_t world,
+                            const int32_t* bus_owner, lopf_handle** out) {
+    g_err.clear();
+    if (!out) return fail(LOPF_E_ARG, "out handle pointer is NULL");
+    *out = nullptr;
+    lopf_options o;
+    if (opt) o = *opt; else lopf_options_default(&o);
+    if (!(o.rho > 0) || !std::isfinite(o.rho)) return fail(LOPF_E_ARG, "rho must be > 0 (SPEC.md:186)");
+    if (!(o.eps_rel > 0) || !std::isfinite(o.eps_rel)) return fail(LOPF_E_ARG, "eps_rel must be > 0 (SPEC.md:186)");
+    if (o.max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
+    if (world < 1 || rank < 0 || rank >= world) return fail(LOPF_E_ARG, "need 0 <= rank < world");
+    lopf_handle* h = new (std::nothrow) lopf_handle();
+    if (!h) return fail(LOPF_E_ARG, "out of host memory");
+    h->opt = o;
+    h->opt.trace_every = 0;
+    std::string err;
+    try {
+        lopf_status st = copy_network(net, h->net, err);
+        if (st == LOPF_OK) st = build_canon(h->net, h->opt, h->cp, err);
+        if (st == LOPF_OK) st = build_partition(h->net, h->cp, world, bus_owner, h->part, err);
+        if (st == LOPF_OK) st = pack_streaming(h->net, h->cp, h->opt, kMaxGrid, h->lay, err, &h->part, rank);
+        if (st != LOPF_OK) { delete h; return fail(st, err); }
+    } catch (const std::bad_alloc&) {
+        delete h;
+        return fail(LOPF_E_ARG, "out of host memory during setup");
+    }
+    *out = h;
+    return LOPF_OK;
+}
+
+lopf_status lopf_part_info(const lopf_handle* h, int64_t* xbuf_offset, int64_t* xbuf_doubles, int32_t* n_bnd,
+                           int32_t* n_imp) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->parted()) return fail(LOPF_E_STATE, "not a partitioned handle (lopf_setup_part)");
+    if (xbuf_offset) *xbuf_offset = (int64_t)h->lay.off_xbuf;
+    if (xbuf_doubles) *xbuf_doubles = (int64_t)h->lay.n_bnd + 8LL * h->lay.world;
+    if (n_bnd) *n_bnd = h->lay.n_bnd;
+    if (n_imp) *n_imp = h->lay.n_imp;
+    return LOPF_OK;
+}
+
+lopf_status lopf_part_owner(const lopf_handle* h, int32_t* bus_owner, int32_t* copy_owner, int32_t* bidx) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->parted()) return fail(LOPF_E_STATE, "not a partitioned handle (lopf_setup_part)");
+    if (bus_owner) std::copy(h->part.bus_owner.begin(), h->part.bus_owner.end(), bus_owner);
+    if (copy_owner) std::copy(h->part.copy_owner.begin(), h->part.copy_owner.end(), copy_owner);
+    if (bidx) std::copy(h->part.bidx.begin(), h->part.bidx.end(), bidx);
+    return LOPF_OK;
+}
+
+lopf_status lopf_part_sweep(lopf_handle* h, void* stream) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->parted()) return fail(LOPF_E_STATE, "not a partitioned handle (lopf_setup_part)");
+    if (!h->bound) return fail(LOPF_E_STATE, "lopf_part_sweep before lopf_bind");
+    DevProblem P = h->dp;
+    P.max_iter = 1;
+    P.test = 0;
+    std::string err;
+    lopf_status st = launch_solve(P, h->grid, stream, err);
+    return st == LOPF_OK ? LOPF_OK : fail(st, err);
+}
+
+lopf_status lopf_part_import(lopf_handle* h, void* stream) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->parted()) return fail(LOPF_E_STATE, "not a partitioned handle (lopf_setup_part)");
+    if (!h->bound) return fail(LOPF_E_STATE, "lopf_part_import before lopf_bind");
+    DevProblem P = h->dp;
+    P.test = 1;
+    std::string err;
+    lopf_status st = launch_part_import(P, stream, err);
+    if (st != LOPF_OK) return fail(st, err);
+    CUDA_TRY(cudaMemsetAsync(h->dp.xbuf, 0, sizeof(double) * ((size_t)h->lay.n_bnd + 8 * (size_t)h->lay.world),
+                             (cudaStream_t)stream), "exchange clear");
     return LOPF_OK;
 }
 
@@ -301,6 +379,11 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     P.rho = h->opt.rho;
     P.inv_rho = 1.0 / h->opt.rho;
     P.eps_rel = h->opt.eps_rel;
+    P.part = L.part; P.rank = L.rank; P.world = L.world; P.n_bnd = L.n_bnd;
+    P.n_imp = L.n_imp; P.ghost0 = L.ghost0;
+    P.xbuf = L.part ? (double*)(b + L.off_xbuf) : nullptr;
+    P.s_exp = L.part ? (const int32_t*)(b + L.off_sexp) : nullptr;
+    P.imp = L.part ? (const int32_t*)(b + L.off_imp) : nullptr;
     std::string err;
     int grid = 0;
     lopf_status st = query_grid(L.rmax, &grid, err);
@@ -322,12 +405,16 @@ lopf_status lopf_reset(lopf_handle* h, void* stream) {
     lopf_status st = h->resident() ? launch_reset_resident(h->rp, stream, err)
                      : h->batch() ? launch_reset_batch(h->bp, (const double*)((uint8_t*)h->arena + h->lay.off_x0), stream, err)
                                   : launch_reset(h->dp, stream, err);
+    if (st == LOPF_OK && h->parted())
+        CUDA_TRY(cudaMemsetAsync(h->dp.xbuf, 0, sizeof(double) * ((size_t)h->lay.n_bnd + 8 * (size_t)h->lay.world),
+                                 (cudaStream_t)stream), "exchange clear");
     return st == LOPF_OK ? LOPF_OK : fail(st, err);
 }
 
 lopf_status lopf_solve_async(lopf_handle* h, int64_t max_iter, int32_t test, void* stream) {
     if (!h) return fail(LOPF_E_ARG, "NULL handle");
     if (!h->bound) return fail(LOPF_E_STATE, "solve before lopf_bind");
+    if (h->parted()) return fail(LOPF_E_STATE, "partitioned handle: drive it with lopf_part_sweep / lopf_part_import");
     if (max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
     cudaStream_t s = (cudaStream_t)stream;
     CUDA_TRY(cudaEventRecord(h->ev0, s), "cudaEventRecord");
@@ -507,17 +594,22 @@ lopf_status lopf_get_state(lopf_handle* h, void* stream, double* x, double* x_lo
         lopf_status st = fetch_slots(h, s, xl, lm);
         if (st != LOPF_OK) return st;
         for (int64_t k = 0; k < h->cp.nc; ++k) {
-            if (x_loc) x_loc[k] = xl[L.slot_of_copy[k]];
-            if (lam) lam[k] = lm[L.slot_of_copy[k]];
+            const bool here = !h->parted() || h->part.copy_owner[k] == h->lay.rank;   // partitioned: own copies
+            if (x_loc) x_loc[k] = here ? xl[L.slot_of_copy[k]] : NAN;
+            if (lam) lam[k] = here ? lm[L.slot_of_copy[k]] : NAN;
         }
     } else {
         CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     }
+    if (x && h->parted())                          // x_g is this rank's where its first copy is
+        for (int64_t g = 0; g < h->cp.n; ++g)
+            if (h->part.copy_owner[h->cp.seg_copy[h->cp.seg_ptr[g]]] != h->lay.rank) x[g] = NAN;
     return LOPF_OK;
 }
 
 lopf_status lopf_set_state(lopf_handle* h, void* stream, const double* x_loc, const double* lam) {
     if (!h || !x_loc || !lam) return fail(LOPF_E_ARG, "NULL argument");
+    if (h->parted()) return fail(LOPF_E_STATE, "lopf_set_state is not supported on a partitioned handle");
     if (!h->bound) return fail(LOPF_E_STATE, "set_state before lopf_bind");
     cudaStream_t s = (cudaStream_t)stream;
     const Layout& L = h->lay;

@@ -60,6 +60,7 @@ struct Canon {
 // Slot info bit fields (streaming kernel).
 constexpr int kInfoBaseMask = 0x3F;        // slot index (in its task) of the subsystem's first row
 constexpr int kInfoCost = 1 << 6;          // the global has c != 0 (a p^g column): read c/rho
+constexpr int kInfoExport = 1 << 7;        // partitioned mode: boundary copy, its u goes to the exchange buffer
 constexpr int kInfoValid = 1 << 8;
 constexpr int kInfoFirst = 1 << 9;         // first copy (canonical) of its global: writes x_g
 constexpr int kInfoInline = 1 << 10;       // segment slots stored inline (nu <= 4)
@@ -87,7 +88,8 @@ struct DevCtrl {                           // 256 B, device-resident control blo
     double res[4];                         // pres, dres, eps_prim, eps_dual of the last sweep
     double objective;
     long long trace_rows;
-    double pad[19];
+    long long stopped;                     // partitioned mode: the termination test has fired
+    double pad[18];
 };
 
 struct DevProblem {                        // kernel argument (pointers into the arena)
@@ -117,6 +119,12 @@ struct DevProblem {                        // kernel argument (pointers into the
     int32_t n_obj, trace_cap, trace_every, test;
     double rho, inv_rho, eps_rel;
     long long max_iter;
+    // partitioned mode (config 5): one sweep per launch, exchange through `xbuf`
+    int32_t part, rank, world, n_bnd;      // n_bnd boundary-copy slots, then world x 8 residual slots
+    double* xbuf;
+    const int32_t* s_exp;                  // [n_slots] exchange slot of an exported copy (kInfoExport)
+    const int32_t* imp;                    // [n_imp] exchange slot feeding each ghost slot
+    int32_t n_imp, ghost0;                 // ghost slots ghost0 .. ghost0 + n_imp - 1 (after the task slots)
 };
 
 // ---- resident kernel (operators + iterate in shared memory) -----------------------------------
@@ -214,6 +222,9 @@ struct Layout {
     int32_t kernel = 1;
     int64_t n_tasks = 0, n_slots = 0, abar_doubles = 0, n_obj = 0;
     int32_t rmax = 1;                     // streaming: widest task (R)
+    // partitioned mode
+    int32_t part = 0, rank = 0, world = 1, n_bnd = 0, n_imp = 0, ghost0 = 0;
+    size_t off_sexp = 0, off_imp = 0, off_xbuf = 0;
     size_t off_tasks = 0, off_info = 0, off_g = 0, off_nbr = 0, off_bbar = 0, off_xl = 0, off_lam = 0,
            off_u0 = 0, off_u1 = 0, off_x0 = 0, off_gpar = 0, off_gcost = 0, off_segptr = 0, off_segslot = 0, off_x = 0, off_abar = 0,
            off_partial = 0, off_ctrl = 0, off_trace = 0, off_objidx = 0, off_objc = 0;
@@ -250,7 +261,19 @@ lopf_status build_batch_ops(const Net& base, const Canon& cp, int32_t n_scen, co
 lopf_status copy_network(const lopf_network* src, Net& dst, std::string& err);
 // pack.cpp
 std::vector<int64_t> dfs_order(const Net& N, const Canon& P);
-lopf_status pack_streaming(const Net& N, const Canon& cp, const lopf_options& opt, int max_grid, Layout& lay, std::string& err);
+
+// Feeder partition over `world` ranks (partition.cpp).
+struct PartSpec {
+    int32_t world = 1, n_bnd = 0;
+    std::vector<int32_t> bus_owner;        // [n_bus]
+    std::vector<int32_t> sub_owner;        // [S]
+    std::vector<int32_t> copy_owner;       // [nc]
+    std::vector<int32_t> bidx;             // [nc] exchange slot of a boundary copy, else -1
+};
+lopf_status build_partition(const Net& N, const Canon& P, int32_t world, const int32_t* bus_owner, PartSpec& out,
+                            std::string& err);
+lopf_status pack_streaming(const Net& N, const Canon& cp, const lopf_options& opt, int max_grid, Layout& lay, std::string& err,
+                           const PartSpec* part = nullptr, int32_t rank = 0);
 void init_state_image(const Canon& cp, Layout& lay);
 // pack_resident.cpp: returns LOPF_E_ARG (with err) when the problem does not fit max_ctas CTAs
 lopf_status pack_resident(const Net& net, const Canon& cp, const lopf_options& opt, Layout& lay, std::string& err);
@@ -265,6 +288,7 @@ constexpr int kStreamWarpsWide = 16;         // ... when tasks of R > 2 exist (n
 int stream_block(int rmax);
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
 lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err);
+lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err);
 lopf_status query_grid(int rmax, int* grid, std::string& err);
 lopf_status launch_resident(const ResProblem& P, void* stream, std::string& err);
 lopf_status launch_reset_resident(const ResProblem& P, void* stream, std::string& err);

@@ -121,14 +121,16 @@ __device__ __forceinline__ double consensus(const DevProblem& P, const int inf, 
 }
 
 // a6 + a7 for one slot
-__device__ __forceinline__ void finish_slot(const DevProblem& P, const int slot, const double ax, const double bb,
+__device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, const int slot, const double ax, const double bb,
                                             const double v, const double lam, const double xo,
                                             double* __restrict__ unext, double (&acc)[5]) {
     const double xn = fma(ax, P.inv_rho, bb);                          // (1/rho) Abar d + bbar
     const double ln = lam + P.rho * (v - xn);                          // ADMM-3
     __stcs(P.xl + slot, xn);
     __stcs(P.lam + slot, ln);
-    unext[slot] = xn - ln * P.inv_rho;                                 // next consensus input
+    const double un = xn - ln * P.inv_rho;                             // next consensus input
+    unext[slot] = un;
+    if (inf & kInfoExport) __stcg(P.xbuf + __ldg(P.s_exp + slot), un);   // partitioned: to the other ranks
     const double rr = v - xn, dx = xn - xo;
     acc[0] += rr * rr;
     acc[1] += dx * dx;
@@ -232,7 +234,7 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
         // b-bar follows the subsystem's triangle in the block when nonzero
         const double bb = (info[h] & kInfoBbar)
                               ? S[((unsigned)info[h] >> kInfoPoffShift) + ns[h] * (ns[h] + 1) / 2 + r[h]] : 0.0;
-        finish_slot(P, tr.x + j, ax[h], bb, v[h], s_lam[j], s_xl[j], unext, acc);
+        finish_slot(P, info[h], tr.x + j, ax[h], bb, v[h], s_lam[j], s_xl[j], unext, acc);
     }
     __syncwarp();
 }
@@ -270,7 +272,7 @@ __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, co
         if (!(info[h] & kInfoValid)) continue;
         const int slot = tr.x + h * 32 + lane;
         const double bb = (info[h] & kInfoBbar) ? __ldg(P.s_bbar + slot) : 0.0;
-        finish_slot(P, slot, ax[h], bb, v[h], P.lam[slot], P.xl[slot], unext, acc);
+        finish_slot(P, info[h], slot, ax[h], bb, v[h], P.lam[slot], P.xl[slot], unext, acc);
     }
     __syncwarp();
 }
@@ -297,6 +299,7 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_stream_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (P.part && *(volatile long long*)&P.ctrl->stopped) return;      // partitioned: decided, no more sweeps
     const long long total0 = *(volatile long long*)&P.ctrl->total;
     const int4 tr0 = gw < P.n_tasks ? __ldg(P.tasks + gw) : make_int4(0, 0, 0, 0);
     long long it = 0;
@@ -361,7 +364,13 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_stream_
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) s[k] += __shfl_xor_sync(kFull, s[k], off);
                 }
-                if (lane == 0) {
+                if (lane == 0 && P.part) {             // partitioned: this rank's sums go to the exchange;
+                    double* rs = P.xbuf + P.n_bnd + (size_t)P.rank * 8;   // the import kernel decides
+                    for (int k = 0; k < 5; ++k) rs[k] = s[k];
+                    __threadfence();
+                    st_release_u64(&P.ctrl->flag, ((unsigned long long)it << 2));
+                    s_stop = 0;
+                } else if (lane == 0) {
                     const double pres = sqrt(s[0]), dres = P.rho * sqrt(s[1]);
                     const double ep = P.eps_rel * fmax(sqrt(s[2]), sqrt(s[3])), ed = P.eps_rel * sqrt(s[4]);
                     const int numeric = !(isfinite(s[0]) && isfinite(s[1]) && isfinite(s[2]) && isfinite(s[3]) && isfinite(s[4]));
@@ -407,6 +416,36 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_stream_
     }
 }
 
+// Partitioned mode, after the exchange-buffer allreduce of sweep t: the other ranks' boundary u into
+// this rank's ghost slots of the buffer sweep t+1 reads, then the termination test of sweep t on the
+// residual sums added in rank order (identical on every rank).  One launch of one CTA per 256 ghosts.
+__global__ void part_import_kernel(DevProblem P) {
+    DevCtrl* c = P.ctrl;
+    if (*(volatile long long*)&c->stopped) return;
+    const long long t = *(volatile long long*)&c->total;
+    double* dst = (t & 1) ? P.u0 : P.u1;                               // = unext of sweep t
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_imp; i += gridDim.x * blockDim.x)
+        dst[P.ghost0 + i] = __ldcg(P.xbuf + P.imp[i]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int r = 0; r < P.world; ++r)
+            for (int k = 0; k < 5; ++k) s[k] += __ldcg(P.xbuf + P.n_bnd + (size_t)r * 8 + k);
+        const double pres = sqrt(s[0]), dres = P.rho * sqrt(s[1]);
+        const double ep = P.eps_rel * fmax(sqrt(s[2]), sqrt(s[3])), ed = P.eps_rel * sqrt(s[4]);
+        const int numeric = !(isfinite(s[0]) && isfinite(s[1]) && isfinite(s[2]) && isfinite(s[3]) && isfinite(s[4]));
+        const int conv = P.test && (pres <= ep) && (dres <= ed);
+        double obj = 0.0;                                              // this rank's share of c^T x
+        for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * __ldcg(P.x + P.obj_idx[j]);
+        c->res[0] = pres; c->res[1] = dres; c->res[2] = ep; c->res[3] = ed;
+        c->objective = obj;
+        c->iters = c->iters + 1;
+        c->total = t + 1;
+        c->outcome = conv ? LOPF_CONVERGED : LOPF_MAX_ITER;
+        c->numeric = numeric;
+        if (conv || numeric) c->stopped = 1;
+    }
+}
+
 // a3: reset the iterate to the initial point: x_s = x0, lambda = 0, u = x0.
 __global__ void reset_kernel(DevProblem P) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -419,6 +458,7 @@ __global__ void reset_kernel(DevProblem P) {
     }
     if (i == 0) {
         P.ctrl->arrive = 0; P.ctrl->flag = 0; P.ctrl->total = 0; P.ctrl->iters = 0; P.ctrl->trace_rows = 0;
+        P.ctrl->stopped = 0;
     }
 }
 
@@ -462,6 +502,14 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
         e = cudaLaunchCooperativeKernel(stream_kernel_for(P.rmax), dim3(grid), dim3(stream_block(P.rmax)), args,
                                         stream_smem(P.rmax), s);
     }
+    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
+    return LOPF_OK;
+}
+
+lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err) {
+    const int nb = P.n_imp > 0 ? (P.n_imp + 255) / 256 : 1;
+    part_import_kernel<<<nb < 148 ? nb : 148, 256, 0, (cudaStream_t)stream>>>(P);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;
 }

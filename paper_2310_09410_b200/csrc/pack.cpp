@@ -21,9 +21,11 @@ namespace lopf {
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt, int max_grid, Layout& L,
-                           std::string& err) {
+                           std::string& err, const PartSpec* part, int32_t rank) {
     L = Layout();
     L.kernel = 1;
+    // partitioned mode: only this rank's subsystems; remote copies its globals read become ghost slots
+    auto local_sub = [&](int64_t s) { return !part || part->sub_owner[s] == rank; };
     // ---- tasks ---------------------------------------------------------------------------------
     // Subsystems are taken in depth-first order of the feeder (neighbouring subsystems share
     // globals, so the u values a task gathers were fetched into L2 by a task that ran moments
@@ -61,7 +63,7 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
         };
         for (int64_t s : dfs_order(N, P)) {
             const int ns = P.n_s[s];
-            if (ns == 0) continue;
+            if (ns == 0 || !local_sub(s)) continue;
             const int ps = ns * (ns + 1) / 2 + (has_bbar(s) ? ns : 0);   // triangle (+ b-bar)
             if (ns > 63) {                                       // full task (S = 1 path)
                 close();
@@ -97,6 +99,28 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
         slots += 32 * k.R;
         pool += k.packed ? (int64_t)k.plen : (int64_t)k.kmax * 32 * k.R;
     }
+    // ghost slots (partitioned mode): remote copies of the globals this rank's copies belong to, in
+    // canonical (global, copy) order; their u arrives through the exchange buffer every sweep
+    std::vector<int64_t> ghosts;
+    if (part) {
+        std::vector<char> seen(P.n, 0);
+        std::vector<int32_t> gl;
+        for (int64_t s = 0; s < P.S; ++s)
+            if (local_sub(s))
+                for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k)
+                    if (!seen[P.copy_global[k]]) { seen[P.copy_global[k]] = 1; gl.push_back(P.copy_global[k]); }
+        std::sort(gl.begin(), gl.end());
+        for (int32_t g : gl)
+            for (int64_t q = P.seg_ptr[g]; q < P.seg_ptr[g + 1]; ++q)
+                if (part->copy_owner[P.seg_copy[q]] != rank) ghosts.push_back(P.seg_copy[q]);
+        L.part = 1;
+        L.rank = rank;
+        L.world = part->world;
+        L.n_bnd = part->n_bnd;
+        L.n_imp = (int32_t)ghosts.size();
+        L.ghost0 = (int32_t)slots;
+        slots += (int64_t)ghosts.size();
+    }
     if (slots > INT32_MAX || pool > INT32_MAX) { err = "problem too large for 32-bit slot / pool offsets"; return LOPF_E_ARG; }
     L.n_slots = slots;
     L.abar_doubles = pool;
@@ -106,8 +130,11 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     // ---- objective terms (c != 0) -----------------------------------------------------------------
     std::vector<int32_t> obj_idx;
     std::vector<double> obj_c;
-    for (int64_t i = 0; i < P.n; ++i)
-        if (P.c[i] != 0.0) { obj_idx.push_back((int32_t)i); obj_c.push_back(P.c[i]); }
+    for (int64_t i = 0; i < P.n; ++i)          // partitioned: the globals whose first copy is local
+        if (P.c[i] != 0.0 && (!part || part->copy_owner[P.seg_copy[P.seg_ptr[i]]] == rank)) {
+            obj_idx.push_back((int32_t)i);
+            obj_c.push_back(P.c[i]);
+        }
     L.n_obj = (int64_t)obj_idx.size();
 
     // ---- arena offsets --------------------------------------------------------------------------------
@@ -135,6 +162,11 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     L.off_trace = take(8 * 5 * (size_t)L.trace_cap);
     L.off_objidx = take(4 * obj_idx.size());
     L.off_objc = take(8 * obj_c.size());
+    if (part) {
+        L.off_sexp = take(4 * NS);
+        L.off_imp = take(4 * ghosts.size());
+        L.off_xbuf = take(8 * ((size_t)part->n_bnd + 8 * (size_t)part->world));
+    }
     L.bytes = o;
     L.image.assign(L.bytes, 0);
     uint8_t* img = L.image.data();
@@ -176,6 +208,18 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
             }
         }
     }
+    for (size_t i = 0; i < ghosts.size(); ++i) L.slot_of_copy[ghosts[i]] = L.ghost0 + (int32_t)i;
+    if (part) {
+        int32_t* sexp = (int32_t*)at(L.off_sexp);
+        int32_t* imp = (int32_t*)at(L.off_imp);
+        for (size_t i = 0; i < NS; ++i) sexp[i] = -1;
+        for (size_t i = 0; i < ghosts.size(); ++i) imp[i] = part->bidx[ghosts[i]];
+        for (int64_t k = 0; k < P.nc; ++k)
+            if (part->copy_owner[k] == rank && part->bidx[k] >= 0) {
+                info[L.slot_of_copy[k]] |= kInfoExport;
+                sexp[L.slot_of_copy[k]] = part->bidx[k];
+            }
+    }
     // segments: inline neighbour slots (nu <= 4) + CSR fallback; first-copy flag
     int32_t* segptr = (int32_t*)at(L.off_segptr);
     int32_t* segslot = (int32_t*)at(L.off_segslot);
@@ -183,6 +227,7 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     for (int64_t q = 0; q < P.nc; ++q) segslot[q] = L.slot_of_copy[P.seg_copy[q]];
     for (int64_t k = 0; k < P.nc; ++k) {
         const int32_t slot = L.slot_of_copy[k];
+        if (slot < 0 || (part && part->copy_owner[k] != rank)) continue;   // not computed here
         const int32_t g = P.copy_global[k];
         const int64_t s0 = P.seg_ptr[g], nu = P.seg_ptr[g + 1] - s0;
         info[slot] |= (int)(std::min<int64_t>(nu, 15) << kInfoNuShift);
@@ -218,7 +263,7 @@ void init_state_image(const Canon& P, Layout& L) {
     for (int64_t i = 0; i < L.n_slots; ++i) xl[i] = lam[i] = u0[i] = u1[i] = x0[i] = 0.0;
     for (int64_t k = 0; k < P.nc; ++k) {
         const int32_t s = L.slot_of_copy[k];
-        xl[s] = u0[s] = x0[s] = P.x0[k];
+        if (s >= 0) xl[s] = u0[s] = x0[s] = P.x0[k];          // (partitioned: own copies and ghosts)
     }
     std::memset(img + L.off_ctrl, 0, sizeof(DevCtrl));
 }

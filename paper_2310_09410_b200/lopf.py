@@ -97,6 +97,11 @@ def load_library(path: str = LIB_PATH):
         "lopf_get_batch_results": ([H, _vp, _vp, _vp, _vp, _vp], _i32),
         "lopf_get_state_scen": ([H, _vp, _i32, _vp, _vp, _vp], _i32),
         "lopf_get_operator_scen": ([H, _i64, _i32, _vp, _vp], _i32),
+        "lopf_setup_part": ([C.POINTER(Network), C.POINTER(Options), _i32, _i32, _vp, C.POINTER(H)], _i32),
+        "lopf_part_info": ([H, _vp, _vp, _vp, _vp], _i32),
+        "lopf_part_owner": ([H, _vp, _vp, _vp], _i32),
+        "lopf_part_sweep": ([H, _vp], _i32),
+        "lopf_part_import": ([H, _vp], _i32),
         "lopf_destroy": ([H], None),
         "lopf_last_error": ([], C.c_char_p),
         "lopf_abi_version": ([], _i32),
@@ -196,6 +201,49 @@ class Lopf:
         _check(lib.lopf_setup_batch(C.byref(net), C.byref(o), int(sc.shape[0]), _ptr(sc), C.byref(h)), "lopf_setup_batch")
         del keep
         return cls(h.value, o)
+
+    @classmethod
+    def setup_part(cls, feeder, rank: int, world: int, bus_owner=None, rho: float = 100.0, eps_rel: float = 1e-3,
+                   max_iter: int = 1_000_000) -> "Lopf":
+        """lopf_setup_part: this rank's share of a feeder partitioned over `world` ranks (config 5)."""
+        lib = load_library()
+        o = Options()
+        _check(lib.lopf_options_default(C.byref(o)), "lopf_options_default")
+        o.rho, o.eps_rel, o.max_iter, o.kernel = float(rho), float(eps_rel), int(max_iter), 1
+        net, keep = _network(feeder)
+        own = None if bus_owner is None else np.ascontiguousarray(bus_owner, dtype=np.int32)
+        h = _vp()
+        _check(lib.lopf_setup_part(C.byref(net), C.byref(o), int(rank), int(world),
+                                   None if own is None else _ptr(own), C.byref(h)), "lopf_setup_part")
+        del keep
+        return cls(h.value, o)
+
+    def part_info(self) -> dict:
+        off, nd = _i64(0), _i64(0)
+        nb, ni = _i32(0), _i32(0)
+        _check(load_library().lopf_part_info(self._h, C.byref(off), C.byref(nd), C.byref(nb), C.byref(ni)),
+               "lopf_part_info")
+        return dict(offset=off.value, doubles=nd.value, n_bnd=nb.value, n_imp=ni.value)
+
+    def part_owner(self, n_bus: int):
+        nc = int(self.sizes.n_copies)
+        bo = np.zeros(n_bus, np.int32)
+        co = np.zeros(nc, np.int32)
+        bi = np.zeros(nc, np.int32)
+        _check(load_library().lopf_part_owner(self._h, _ptr(bo), _ptr(co), _ptr(bi)), "lopf_part_owner")
+        return bo, co, bi
+
+    def exchange(self):
+        """The exchange buffer as a float64 torch view of the arena (for the allreduce)."""
+        import torch
+        inf = self.part_info()
+        return self.arena[inf["offset"]: inf["offset"] + 8 * inf["doubles"]].view(torch.float64)
+
+    def part_sweep(self, stream=None):
+        _check(load_library().lopf_part_sweep(self._h, _vp(_stream_handle(stream))), "lopf_part_sweep")
+
+    def part_import(self, stream=None):
+        _check(load_library().lopf_part_import(self._h, _vp(_stream_handle(stream))), "lopf_part_import")
 
     def get_batch_results(self, stream=None) -> dict:
         ns = int(self.sizes.n_scen)

@@ -1,0 +1,112 @@
+"""Partitioned mode (BASELINE.json configs[4]): one feeder split over the
+ranks of a torch.distributed group, one GPU per rank.
+
+Every sweep of Algorithm 1 runs in liblopf on each rank's own subsystems
+(`lopf_part_sweep`); the only data that crosses ranks is the exchange buffer: the u values of the
+boundary copies (copies of globals shared by two ranks) plus five residual sums per rank.  Each slot
+is written by exactly one rank and the buffer is zero elsewhere, so one sum-allreduce (NCCL over
+NVLink on GPUs) is an exact gather; `lopf_part_import` then fills the ghost slots, takes the
+termination decision on the rank-ordered sums (identical everywhere) and clears the buffer.  The
+paper's own multi-GPU runs stage the same exchange through the host with MPI.
+
+PyTorch here is plumbing only (the arena tensor, the stream, the process group and its allreduce).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .lopf import CONVERGED, Lopf
+
+
+class PartitionedSolver:
+    """This rank's share of a partitioned feeder.  All ranks construct it with the same feeder and
+    options; `solve` / `run` are collective calls."""
+
+    def __init__(self, feeder, group=None, device=None, bus_owner=None, rank=None, world=None, **opts):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        if rank is None:
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank, self.world = int(rank), int(world)
+        self.feeder = feeder
+        self.h = Lopf.setup_part(feeder, self.rank, self.world, bus_owner=bus_owner, **opts)
+        self.h.bind(device or (torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cuda"))
+        self.xbuf = self.h.exchange()
+
+    def _allreduce(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.xbuf, group=self.group)
+
+    def sweep(self, stream=None):
+        """One sweep on every rank (collective)."""
+        self.h.part_sweep(stream)
+        self._allreduce()
+        self.h.part_import(stream)
+
+    def reset(self, stream=None):
+        self.h.reset(stream)
+
+    def run(self, k: int, check_every: int = 64, stream=None):
+        """Up to k sweeps, stopping early at (termination); polls the device result every
+        `check_every` sweeps (the kernels become no-ops once the test has fired)."""
+        done = 0
+        r = None
+        while done < k:
+            n = min(check_every, k - done)
+            for _ in range(n):
+                self.sweep(stream)
+            done += n
+            r = self.h.result_get(stream)
+            if r.outcome == CONVERGED:
+                break
+        return r if r is not None else self.h.result_get(stream)
+
+    def gather_x(self) -> np.ndarray:
+        """The full solution x (each global from the rank holding its first copy)."""
+        x = self.h.get_x()
+        if self.world > 1:
+            import torch.distributed as dist
+            parts = [None] * self.world
+            dist.all_gather_object(parts, x, group=self.group)
+            return merge_owned(parts)
+        return x
+
+    def objective(self) -> float:
+        """c^T x summed over the ranks' shares."""
+        share = float(self.h.result_get().objective)
+        if self.world > 1:
+            import torch.distributed as dist
+            parts = [None] * self.world
+            dist.all_gather_object(parts, share, group=self.group)
+            return float(sum(parts))
+        return share
+
+
+def merge_owned(parts) -> np.ndarray:
+    """Combine per-rank arrays that are NaN where another rank owns the entry."""
+    out = np.array(parts[0], copy=True)
+    for p in parts[1:]:
+        m = ~np.isnan(p)
+        out[m] = p[m]
+    return out
+
+
+def emulate_sweeps(handles, k: int, xbufs=None):
+    """Test helper: k sweeps of several partitioned handles of ONE process (one device), the
+    allreduce replaced by a device-side sum of their exchange buffers.  Every launch is stream-ordered
+    after the previous one, so no kernel waits on another rank's kernel."""
+    xbufs = xbufs or [h.exchange() for h in handles]
+    for _ in range(k):
+        for h in handles:
+            h.part_sweep()
+        total = xbufs[0].clone()
+        for xb in xbufs[1:]:
+            total += xb
+        for xb in xbufs:
+            xb.copy_(total)
+        for h in handles:
+            h.part_import()
+    return xbufs
