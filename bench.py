@@ -108,7 +108,17 @@ def main():
     ap.add_argument("--cpu-sweeps", type=int, default=2000, help="oracle sweeps timed for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sweeps", type=int, default=100, help="oracle sweeps per step for --impl reference")
+    ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5],
+                    help="3: 8500-shaped single solve (default, the headline); 4: 4096 scenarios of the "
+                         "123 shape, sharded; 5: 64 x 8500 stitched feeder, partitioned over the ranks")
+    ap.add_argument("--sweeps", type=int, default=500, help="config 5: sweeps per step (fixed K, test off)")
+    ap.add_argument("--n-sub", type=int, default=64, help="config 5: stitched subfeeders")
+    ap.add_argument("--n-scen", type=int, default=4096, help="config 4: scenarios")
     args = ap.parse_args()
+    if args.config == 5:
+        return bench_stitched(args)
+    if args.config == 4:
+        return bench_batch(args)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -252,6 +262,292 @@ def main():
         }
         print(json.dumps(out))
     if world > 1:
+        dist.destroy_process_group()
+
+
+def _dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def _max_over_ranks(world, dev, *vals):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    if world > 1:
+        allv = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allv, t)
+        return torch.stack(allv).cpu().numpy()
+    return t.cpu().numpy()[None, :]
+
+
+def bench_stitched(args):
+    """Config 5 (BASELINE.json configs[4]): the 64 x 8500-shaped stitched feeder (~0.84M buses).
+    N = 1: the streaming kernel, one persistent launch of --sweeps sweeps per step.  N > 1: the feeder
+    partitioned over the ranks (subfeeders to ranks, feedergen.stitched_bus_owner), one NCCL
+    sum-allreduce of the exchange buffer per sweep (paper_2310_09410_b200.partition): strong scaling.
+    A step is --sweeps sweeps from the initial point with the test off (fixed K for
+    iterations/s); time-to-tolerance is measured once after the timed region."""
+    import feedergen as fg
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        import oracle
+        sub = fg.make_stitched(2, "8500")                 # bounded sample: 2 of the 64 subfeeders
+        p = oracle.build_problem(sub)
+        x0 = oracle.initial_state(p)
+        k = max(1, args.ref_sweeps // 10)
+        oracle.run_k(p, 2, state=x0)
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            oracle.run_k(p, k, state=x0)
+        dt = time.perf_counter() - t
+        v = args.steps * k / dt * (p.dec.n_copies / (args.n_sub / 2 * p.dec.n_copies))   # scaled to 64 subfeeders
+        sample = (f"{k} oracle sweeps per step on the 2 x 8500 stitched feeder ({p.dec.n_copies} copies), the rate "
+                  f"scaled by copies to the {args.n_sub} x 8500 instance (linear in size; extrapolated)")
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": "iterations/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"stitched {args.n_sub} x 8500-shaped feeder (config 5)"},
+            "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2310_09410_b200 import CONVERGED, Lopf
+    from paper_2310_09410_b200.partition import PartitionedSolver
+
+    world, rank, local = _dist_setup()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    t0 = time.perf_counter()
+    feeder = fg.make_stitched(args.n_sub, "8500")
+    gen_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    if world == 1:
+        h = Lopf.setup(feeder, kernel=1, max_iter=100_000).bind(dev)
+        solver = None
+    else:
+        solver = PartitionedSolver(feeder, device=dev, bus_owner=fg.stitched_bus_owner(feeder, world), max_iter=100_000)
+        h = solver.h
+    setup_s = time.perf_counter() - t0
+    sz = h.sizes
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def step(k):
+        h.reset()
+        if solver is None:
+            h.solve_async(k, False)
+        else:
+            for _ in range(k):
+                solver.sweep()
+
+    for _ in range(args.warmup):
+        step(args.sweeps)
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step(args.sweeps)
+            ev[i][1].record(stream)
+        barrier()
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    # time to tolerance (one solve, after the timed region)
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h.reset()
+    a.record(stream)
+    if solver is None:
+        r = h.solve()
+    else:
+        r = solver.run(100_000, check_every=200)
+    b.record(stream)
+    barrier()
+    ttt_ms = a.elapsed_time(b)
+    k_tol = int(r.iters)
+    conv = int(r.outcome) == CONVERGED
+    # end to end: upload the packed problem from pinned host memory, --sweeps sweeps, x back
+    e2e_steps = 3
+    barrier()
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        h.bind(dev)
+        if solver is None:
+            h.run(args.sweeps)
+        else:
+            for _ in range(args.sweeps):
+                solver.sweep()
+        x = h.get_x()
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t
+    allv = _max_over_ranks(world, dev, dev_ms, e2e_s, ttt_ms)
+    max_ms, e2e_max, ttt_max = float(allv[:, 0].max()), float(allv[:, 1].max()), float(allv[:, 2].max())
+    value = args.steps * args.sweeps / (max_ms / 1e3)
+    if rank == 0:
+        peak, peak_src = _peaks()
+        us = 1e3 * max_ms / (args.steps * args.sweeps)
+        achieved = sz.alg_bytes / (us * 1e-6) / 1e9 / world            # per GPU (alg bytes of the whole feeder)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            import oracle
+            sub = fg.make_stitched(2, "8500")
+            p = oracle.build_problem(sub)
+            x0 = oracle.initial_state(p)
+            tt = time.perf_counter()
+            oracle.run_k(p, 20, state=x0)
+            dt = time.perf_counter() - tt
+            rate = 20 / dt * (2.0 / args.n_sub)
+            cpu = {"value": rate, "unit": "iterations/s", "cores": 1, "kind": "oracle",
+                   "sample": f"20 oracle sweeps of the 2 x 8500 stitched feeder ({dt:.1f} s), rate scaled by 2/{args.n_sub} "
+                             f"to the full instance (extrapolated, linear in size)"}
+        dram = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_summary_config5.json")) as fh:
+                dram = json.load(fh).get("dram_bytes_per_sweep")
+        except Exception:
+            pass
+        out = {
+            "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"stitched {args.n_sub} x 8500-shaped feeder (BASELINE configs[4]): "
+                                   f"{feeder.n_bus} buses, one scenario, {args.sweeps} sweeps per step (test off)",
+                       "S": int(sz.S), "n": int(sz.n), "n_copies": int(sz.n_copies),
+                       "mode": "streaming kernel" if world == 1 else f"partitioned over {world} ranks (NCCL allreduce)",
+                       "iters_to_tolerance": k_tol, "converged": conv, "time_to_tolerance_ms": ttt_max,
+                       "l2": "working set >> L2; flushed between steps anyway", "gen_s": round(gen_s, 1),
+                       "setup_s": round(setup_s, 1)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": dram, "peak_source": peak_src, "kernel": "admm_stream_kernel",
+                         "alg_bytes_per_sweep": int(sz.alg_bytes), "us_per_sweep": us},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_steps * args.sweeps / e2e_max, "unit": "iterations/s",
+                    "h2d_bytes_per_step": int(sz.device_bytes), "d2h_bytes_per_step": int(8 * sz.n), "steps": e2e_steps},
+            "clocks": clk.summary(),
+            "gpu_launches": args.steps * (1 if world == 1 else 2 * args.sweeps),
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_batch(args):
+    """Config 4 (BASELINE.json configs[3]): --n-scen load scenarios of the 123-shaped feeder (kappa ~ U[0.5, 1.5]
+    per load, seed 4096), sharded over the ranks with no collective (paper_2310_09410_b200.dist.shard_range);
+    each rank solves its shard with the batch kernel (lane = scenario, per-scenario termination).  A step =
+    reset + solve of the shard; value = scenario-sweeps / s summed over ranks (strong scaling: the total
+    number of scenarios is fixed)."""
+    import numpy as np
+    import feedergen as fg
+    from paper_2310_09410_b200.dist import shard_range
+    f = fg.make_feeder("123")
+    scales = fg.scenario_scales(f, args.n_scen, seed=4096)
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        import oracle
+        t = time.perf_counter()
+        sw = 0
+        for i in range(args.steps):
+            p = oracle.build_problem(fg.scale_loads(f, scales[i % args.n_scen]))
+            x0 = oracle.initial_state(p)
+            oracle.run_k(p, args.ref_sweeps * 10, state=x0)
+            sw += args.ref_sweeps * 10
+        dt = time.perf_counter() - t
+        v = sw / dt
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": "scenario-iterations/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.n_scen} load scenarios of the 123-shaped feeder (config 4)"},
+            "cpu_baseline": {"value": v, "unit": "scenario-iterations/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.ref_sweeps * 10} oracle sweeps of one scenario per step (setup included)"},
+            "e2e": {"value": v, "unit": "scenario-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+    import torch
+    from paper_2310_09410_b200 import Lopf
+    world, rank, local = _dist_setup()
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    lo, hi = shard_range(args.n_scen, rank, world)
+    t0 = time.perf_counter()
+    h = Lopf.setup_batch(f, scales[lo:hi]).bind(dev)
+    setup_s = time.perf_counter() - t0
+    sz = h.sizes
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        h.reset()
+        h.solve()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sweeps = 0
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            h.reset()
+            h.solve_async(int(h.opts.max_iter), True)
+            ev[i][1].record(stream)
+            h.result_get()
+            sweeps += int(h.get_batch_results()["iters"].sum())
+        torch.cuda.synchronize(dev)
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    res = h.get_batch_results()
+    e2e_steps = 2
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        h.bind(dev)
+        h.solve()
+        h.get_batch_results()
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t
+    allv = _max_over_ranks(world, dev, dev_ms, float(sweeps), e2e_s, float(res["iters"].sum()), float(res["iters"].max()))
+    max_ms = float(allv[:, 0].max())
+    value = float(allv[:, 1].sum()) / (max_ms / 1e3)
+    if rank == 0:
+        peak, peak_src = _peaks()
+        batch_sweeps = float(allv[:, 4].max())                 # launch length = slowest scenario
+        us_per_batch_sweep = 1e3 * (max_ms / args.steps) / batch_sweeps
+        achieved = sz.alg_bytes / (us_per_batch_sweep * 1e-6) / 1e9
+        out = {
+            "metric": METRIC, "value": value, "unit": "scenario-iterations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.n_scen} load scenarios of the 123-shaped feeder (BASELINE configs[3]), "
+                                   f"kappa ~ U[0.5,1.5] per load (seed 4096), each solved to the stopping criterion",
+                       "scenarios_per_rank": hi - lo, "max_iters": int(allv[:, 4].max()),
+                       "mean_iters": float(allv[:, 3].sum()) / args.n_scen, "time_to_tolerance_ms": max_ms / args.steps,
+                       "l2": "flushed between steps (512 MiB write)", "setup_s": round(setup_s, 1)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "peak_source": peak_src, "kernel": "admm_batch_kernel",
+                         "alg_bytes_per_batch_sweep": int(sz.alg_bytes), "us_per_batch_sweep": us_per_batch_sweep},
+            "cpu_baseline": None,
+            "e2e": {"value": float(allv[:, 3].sum()) * e2e_steps / float(allv[:, 2].max()), "unit": "scenario-iterations/s",
+                    "h2d_bytes_per_step": int(sz.device_bytes), "d2h_bytes_per_step": 64 * (hi - lo), "steps": e2e_steps},
+            "clocks": clk.summary(),
+            "gpu_launches": 2 * args.steps,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
         dist.destroy_process_group()
 
 

@@ -235,13 +235,21 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
     // algorithmic bytes per sweep: packed symmetric Abar + bbar of load-bearing
     // subsystems + 6 per-copy streams (lambda, x_s rd+wr; u wr+rd) + 4 per-global (x wr+rd, lo, hi)
     // + c nonzeros, in fp64; plus the int32 copy->global map and CSR.
-    int64_t nbbar = 0;
+    int64_t nbbar = 0, psym_var = 0;
     for (int64_t s = 0; s < P.S; ++s) {
         bool any = false;
         for (int64_t r = P.b_ptr[s]; r < P.b_ptr[s + 1]; ++r) any |= P.b[r] != 0.0;
-        if (any) nbbar += P.n_s[s];
+        if (any) {
+            nbbar += P.n_s[s];
+            psym_var += (int64_t)P.n_s[s] * (P.n_s[s] + 1) / 2;
+        }
     }
     sz->alg_bytes = 8 * (psym + nbbar + 6 * P.nc + 4 * P.n + h->lay.n_obj) + 4 * (2 * P.nc + P.n + 1);
+    if (h->batch()) {                       // per batch sweep: shared operators once, the rest per scenario
+        const int64_t ns = h->lay.n_scen;
+        sz->alg_bytes = 8 * ((psym - psym_var) + ns * (psym_var + nbbar + 6 * P.nc + 4 * P.n + h->lay.n_obj)) +
+                        4 * (2 * P.nc + P.n + 1);
+    }
     sz->kernel = h->lay.kernel;
     if (h->resident()) {                    // diagnostics: boundary tasks, largest SMEM footprint
         int mt = 0;
