@@ -128,7 +128,7 @@ lopf_status lopf_setup_batch(const lopf_network* net, const lopf_options* opt, i
         lopf_status st = copy_network(net, h->net, err);
         if (st == LOPF_OK) st = build_canon(h->net, h->opt, h->cp, err);
         if (st == LOPF_OK) st = build_batch_ops(h->net, h->cp, n_scen, load_scale, h->bo, err);
-        if (st == LOPF_OK) st = pack_batch(h->cp, h->bo, h->opt, h->lay, err);
+        if (st == LOPF_OK) st = pack_batch(h->net, h->cp, h->bo, h->opt, h->lay, err);
         if (st != LOPF_OK) { delete h; return fail(st, err); }
     } catch (const std::bad_alloc&) {
         delete h;
@@ -257,8 +257,8 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
         sz->reserved[0] = mt;                 // largest task count of a CTA
         sz->reserved[1] = h->lay.max_smem;
     }
-    sz->grid = h->resident() ? h->lay.G : h->batch() ? h->lay.n_grp : h->grid;
-    sz->block = h->resident() ? kResBlock : h->batch() ? kBatchBlock : stream_block(h->lay.rmax);
+    sz->grid = h->resident() ? h->lay.G : h->grid;
+    sz->block = h->resident() ? kResBlock : stream_block(h->lay.rmax);
     sz->n_scen = h->batch() ? h->lay.n_scen : 0;
     return LOPF_OK;
 }
@@ -281,33 +281,56 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     CUDA_TRY(cudaMemcpyAsync(arena, h->lay.image.data(), h->lay.bytes, cudaMemcpyHostToDevice, s), "bind H2D");
     const Layout& L = h->lay;
     uint8_t* b = (uint8_t*)arena;
-    if (h->batch()) {
+    if (h->batch()) {                              // streaming template + per-scenario arrays
+        DevProblem& P = h->dp;
+        P = DevProblem{};
+        P.n_tasks = (int32_t)L.n_tasks;
+        P.n_slots = (int32_t)L.n_slots;
+        P.rmax = L.rmax;
+        P.n = h->cp.n;
+        P.tasks = (const int4*)(b + L.off_tasks);
+        P.s_info = (const int32_t*)(b + L.off_info);
+        P.s_g = (const int32_t*)(b + L.off_g);
+        P.s_nbr = (const int4*)(b + L.off_nbr);
+        P.s_bbar = (const double*)(b + L.off_bbar);
+        P.xl = (double*)(b + L.off_xl);
+        P.lam = (double*)(b + L.off_lam);
+        P.u0 = (double*)(b + L.off_u0);
+        P.u1 = (double*)(b + L.off_u1);
+        P.x0 = (const double*)(b + L.off_x0);
+        P.gbnd = (const double2*)(b + L.off_gpar);
+        P.gcost = (const double*)(b + L.off_gcost);
+        P.seg_ptr = (const int32_t*)(b + L.off_segptr);
+        P.seg_slot = (const int32_t*)(b + L.off_segslot);
+        P.x = (double*)(b + L.off_x);
+        P.abar = (const double*)(b + L.off_abar);
+        P.partial = (double*)(b + L.off_partial);
+        P.ctrl = (DevCtrl*)(b + L.off_ctrl);
+        P.trace = (double*)(b + L.off_trace);
+        P.obj_idx = (const int32_t*)(b + L.off_objidx);
+        P.obj_c = (const double*)(b + L.off_objc);
+        P.n_obj = (int32_t)L.n_obj;
+        P.rho = h->opt.rho;
+        P.inv_rho = 1.0 / h->opt.rho;
+        P.eps_rel = h->opt.eps_rel;
         BatchProblem& B = h->bp;
-        B.n_scen = L.n_scen; B.n_grp = L.n_grp; B.S = (int32_t)h->cp.S; B.n = (int32_t)h->cp.n;
-        B.nc = (int32_t)h->cp.nc; B.VA = (int32_t)h->bo.VA; B.VB = (int32_t)h->bo.VB; B.n_obj = (int32_t)L.n_obj;
-        B.warp_sub = (const int32_t*)(b + L.off_bwarp);
-        B.sub_ptr = (const int32_t*)(b + L.off_bsubptr);
-        B.sub_ns = (const int32_t*)(b + L.off_bns);
-        B.sub_op = (const int32_t*)(b + L.off_bop);
-        B.vsub_a = (const int32_t*)(b + L.off_bva);
-        B.vsub_b = (const int32_t*)(b + L.off_bvb);
-        B.copy_info = (const int2*)(b + L.off_bcopy);
-        B.gpar = (const double4*)(b + L.off_gpar);
-        B.seg_ptr = (const int32_t*)(b + L.off_segptr);
-        B.seg_copy = (const int32_t*)(b + L.off_segslot);
-        B.shared_abar = (const double*)(b + L.off_bshared);
-        B.var_abar = (const double*)(b + L.off_bvabar);
-        B.var_bbar = (const double*)(b + L.off_bvbbar);
-        B.xl = (double*)(b + L.off_bxl);
-        B.lam = (double*)(b + L.off_blam);
-        B.xout = (double*)(b + L.off_bxout);
+        B.n_scen = L.n_scen;
+        B.n_tasks = (int32_t)L.n_tasks;
+        B.ns_stride = (int32_t)L.n_slots;
+        B.n_stride = (int32_t)h->cp.n;
+        B.vp_stride = L.VP;
+        B.var_pool = (const double*)(b + L.off_bvar);
         B.res = (ScenResult*)(b + L.off_bres);
-        B.obj_idx = (const int32_t*)(b + L.off_objidx);
-        B.obj_c = (const double*)(b + L.off_objc);
-        B.rho = h->opt.rho; B.inv_rho = 1.0 / h->opt.rho; B.eps_rel = h->opt.eps_rel;
-        B.ns_max = L.ns_max;
-        h->dp = DevProblem{};
-        h->dp.ctrl = (DevCtrl*)(b + L.off_ctrl);
+        B.stopped = (int32_t*)(b + L.off_bstop);
+        B.partial = (double*)(b + L.off_bpart);
+        B.cnt = (unsigned long long*)(b + L.off_bcnt);
+        std::string err;
+        int grid = 0;
+        lopf_status st = query_grid(L.rmax, &grid, err);
+        if (st != LOPF_OK) return fail(st, err);
+        h->grid = grid;
+        st = launch_reset_batch(P, B, stream, err);
+        if (st != LOPF_OK) return fail(st, err);
         h->arena = arena;
         h->arena_bytes = bytes;
         h->bound = true;
@@ -411,7 +434,7 @@ lopf_status lopf_reset(lopf_handle* h, void* stream) {
     if (!h->bound) return fail(LOPF_E_STATE, "lopf_reset before lopf_bind");
     std::string err;
     lopf_status st = h->resident() ? launch_reset_resident(h->rp, stream, err)
-                     : h->batch() ? launch_reset_batch(h->bp, (const double*)((uint8_t*)h->arena + h->lay.off_x0), stream, err)
+                     : h->batch() ? launch_reset_batch(h->dp, h->bp, stream, err)
                                   : launch_reset(h->dp, stream, err);
     if (st == LOPF_OK && h->parted())
         CUDA_TRY(cudaMemsetAsync(h->dp.xbuf, 0, sizeof(double) * ((size_t)h->lay.n_bnd + 8 * (size_t)h->lay.world),
@@ -434,10 +457,10 @@ lopf_status lopf_solve_async(lopf_handle* h, int64_t max_iter, int32_t test, voi
         R.test = test ? 1 : 0;
         st = launch_resident(R, stream, err);
     } else if (h->batch()) {
-        BatchProblem B = h->bp;
-        B.max_iter = max_iter;
-        B.test = test ? 1 : 0;
-        st = launch_batch(B, stream, err);
+        DevProblem P = h->dp;
+        P.max_iter = max_iter;
+        P.test = test ? 1 : 0;
+        st = launch_batch(P, h->bp, h->grid, stream, err);
     } else {
         DevProblem P = h->dp;
         P.max_iter = max_iter;
@@ -684,22 +707,17 @@ lopf_status lopf_get_state_scen(lopf_handle* h, void* stream, int32_t scen, doub
     if (!h->batch() || !h->bound) return fail(LOPF_E_STATE, "per-scenario state needs a bound batch handle");
     if (scen < 0 || scen >= h->lay.n_scen) return fail(LOPF_E_ARG, "scenario index out of range");
     cudaStream_t s = (cudaStream_t)stream;
-    ScenResult R;
-    CUDA_TRY(cudaMemcpyAsync(&R, h->bp.res + scen, sizeof(R), cudaMemcpyDeviceToHost, s), "state D2H");
+    const Layout& L = h->lay;
+    const size_t NS = (size_t)L.n_slots, N = (size_t)h->cp.n;
+    std::vector<double> xl(NS), lm(NS);
+    CUDA_TRY(cudaMemcpyAsync(xl.data(), h->dp.xl + (size_t)scen * NS, 8 * NS, cudaMemcpyDeviceToHost, s), "state D2H");
+    CUDA_TRY(cudaMemcpyAsync(lm.data(), h->dp.lam + (size_t)scen * NS, 8 * NS, cudaMemcpyDeviceToHost, s), "state D2H");
+    if (x) CUDA_TRY(cudaMemcpyAsync(x, h->dp.x + (size_t)scen * N, 8 * N, cudaMemcpyDeviceToHost, s), "state D2H");
     CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-    const int64_t g = scen / 32, ln = scen % 32, NC = h->cp.nc, N = h->cp.n, G = h->lay.n_grp;
-    const int cur = (int)(R.total & 1);
-    const size_t pitch = 32 * sizeof(double);
-    if (x_loc)
-        CUDA_TRY(cudaMemcpy2DAsync(x_loc, 8, h->bp.xl + (((size_t)cur * G + g) * NC) * 32 + ln, pitch, 8, NC,
-                                   cudaMemcpyDeviceToHost, s), "state D2H");
-    if (lam)
-        CUDA_TRY(cudaMemcpy2DAsync(lam, 8, h->bp.lam + (((size_t)cur * G + g) * NC) * 32 + ln, pitch, 8, NC,
-                                   cudaMemcpyDeviceToHost, s), "state D2H");
-    if (x)
-        CUDA_TRY(cudaMemcpy2DAsync(x, 8, h->bp.xout + ((size_t)g * N) * 32 + ln, pitch, 8, N, cudaMemcpyDeviceToHost, s),
-                 "state D2H");
-    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    for (int64_t k = 0; k < h->cp.nc; ++k) {
+        if (x_loc) x_loc[k] = xl[L.slot_of_copy[k]];
+        if (lam) lam[k] = lm[L.slot_of_copy[k]];
+    }
     return LOPF_OK;
 }
 

@@ -72,6 +72,7 @@ constexpr int kInfoPoffShift = 22;         // offset (doubles) of the subsystem'
 constexpr int kTaskPacked = 1 << 4;        // packed task: .z = block doubles, kmax in bits 8..15 of .w
 constexpr int kTaskDirect = 1 << 5;        // packed task whose block exceeds the stage: read from HBM
 constexpr int kTaskKmaxShift = 8;
+constexpr int kTaskVar = 1 << 6;           // batch: the task's operator block is per scenario (holds a load)
 constexpr int kTaskUsedShift = 16;         // packed task: slots in use (rounded up to 4), bits 16..23 of .w
 constexpr int kTaskHalves = 2;             // streaming packer: max 32-slot halves per packed task
 #ifndef LOPF_PACK_BUDGET
@@ -178,8 +179,7 @@ struct ResProblem {                           // resident kernel argument
 };
 
 // ---- batch kernel (config 4: lane = scenario, 32 scenarios per CTA group) -----------------------
-constexpr int kBatchBlock = 256;               // 8 warps split the subsystems of one group (SMEM staging)
-constexpr int kBatchWarps = kBatchBlock / 32;
+
 
 struct ScenResult {                            // 64 B per scenario (device)
     long long iters;                           // sweeps executed in the last launch
@@ -190,31 +190,14 @@ struct ScenResult {                            // 64 B per scenario (device)
     double objective;
 };
 
-struct BatchProblem {
-    int32_t n_scen, n_grp, S, n;
-    int32_t nc, VA, VB, n_obj;
-    const int32_t* warp_sub;                   // [kBatchWarps + 1] subsystem ranges per warp
-    const int32_t* sub_ptr;                    // [S+1] copy offsets (canonical)
-    const int32_t* sub_ns;                     // [S]
-    const int32_t* sub_op;                     // [S] >= 0: shared pool offset; < 0: -(1 + varying index)
-    const int32_t* vsub_a;                     // [V] Abar offsets per scenario (doubles), [V] bbar offsets
-    const int32_t* vsub_b;
-    const int2* copy_info;                     // [nc] {global, first-copy flag}
-    const double4* gpar;                       // [n] {c/rho, 1/nu, lo, hi}
-    const int32_t* seg_ptr;                    // [n+1]
-    const int32_t* seg_copy;                   // [nc]
-    const double* shared_abar;                 // row-major n_s x n_s per shared subsystem
-    const double* var_abar;                    // [n_grp][VA][32]
-    const double* var_bbar;                    // [n_grp][VB][32]
-    double* xl;                                // [2][n_grp][nc][32]
-    double* lam;                               // [2][n_grp][nc][32]
-    double* xout;                              // [n_grp][n][32]
+struct BatchProblem {                          // config 4: streaming kernel over (scenario, task) items
+    int32_t n_scen, n_tasks, ns_stride, n_stride;  // scenarios; tasks per scenario; slot / global strides
+    int64_t vp_stride;                         // doubles of per-scenario operator blocks
+    const double* var_pool;                    // [n_scen][vp_stride] blocks of tasks flagged kTaskVar
     ScenResult* res;                           // [n_scen]
-    const int32_t* obj_idx;
-    const double* obj_c;
-    double rho, inv_rho, eps_rel;
-    long long max_iter;
-    int32_t test, ns_max;
+    int32_t* stopped;                          // [n_scen] converged / non-finite: no more sweeps
+    double* partial;                           // [n_scen][n_tasks][8] residual sums per item
+    unsigned long long* cnt;                   // [2]: barrier arrivals, cumulative active count
 };
 
 // Arena layout: byte offsets of every array (all 256-byte aligned).
@@ -237,10 +220,13 @@ struct Layout {
     size_t off_hdr = 0, off_blobs = 0, off_xchg = 0, off_x0r = 0, off_prof = 0, off_flags = 0;
     std::vector<CtaHdr> hdr;               // host copy of the per-CTA headers
     std::vector<int32_t> slot_cta;         // [total slots] CTA of a global slot id
-    // batch kernel
+    // streaming task composition (kept for the batch packer): subsystems and block offsets per task
+    std::vector<int4> trec;
+    std::vector<int32_t> tsub_ptr, tsub_s, tsub_poff;
+    // batch kernel (config 4): the streaming layout of one scenario, replicated over the scenarios
     int32_t n_scen = 0, n_grp = 0, ns_max = 0;
-    size_t off_bwarp = 0, off_bsubptr = 0, off_bns = 0, off_bop = 0, off_bva = 0, off_bvb = 0, off_bcopy = 0,
-           off_bshared = 0, off_bvabar = 0, off_bvbbar = 0, off_bxl = 0, off_blam = 0, off_bxout = 0, off_bres = 0;
+    int64_t VP = 0;                        // doubles of per-scenario operator blocks (tasks holding a load)
+    size_t off_bvar = 0, off_bres = 0, off_bstop = 0, off_bpart = 0, off_bcnt = 0;
 };
 
 // Scenario batches (config 4): per-scenario operators of the subsystems that hold a load (their
@@ -278,7 +264,8 @@ void init_state_image(const Canon& cp, Layout& lay);
 // pack_resident.cpp: returns LOPF_E_ARG (with err) when the problem does not fit max_ctas CTAs
 lopf_status pack_resident(const Net& net, const Canon& cp, const lopf_options& opt, Layout& lay, std::string& err);
 // pack_batch.cpp
-lopf_status pack_batch(const Canon& cp, const BatchOps& bo, const lopf_options& opt, Layout& lay, std::string& err);
+lopf_status pack_batch(const Net& N, const Canon& cp, const BatchOps& bo, const lopf_options& opt, Layout& lay,
+                       std::string& err);
 // kernels.cu
 #ifndef LOPF_STREAM_WARPS
 #define LOPF_STREAM_WARPS 24
@@ -294,7 +281,7 @@ lopf_status launch_resident(const ResProblem& P, void* stream, std::string& err)
 lopf_status launch_reset_resident(const ResProblem& P, void* stream, std::string& err);
 lopf_status resident_capacity(int* sms, int* smem_optin, std::string& err);
 // batch.cu
-lopf_status launch_batch(const BatchProblem& P, void* stream, std::string& err);
-lopf_status launch_reset_batch(const BatchProblem& P, const double* x0, void* stream, std::string& err);
+lopf_status launch_batch(const DevProblem& P, const BatchProblem& B, int grid, void* stream, std::string& err);
+lopf_status launch_reset_batch(const DevProblem& P, const BatchProblem& B, void* stream, std::string& err);
 
 }  // namespace lopf

@@ -446,6 +446,174 @@ __global__ void part_import_kernel(DevProblem P) {
     }
 }
 
+// ---- batch mode (config 4): (scenario, task) items over the one-scenario streaming layout ---------
+// Item i = scenario * n_tasks + task.  Per sweep every warp walks its items (skipping scenarios that
+// have stopped) with the same TMA pipeline and task code as the streaming kernel, on a view whose
+// iterate / solution / varying-operator pointers are offset to the item's scenario; the item's five
+// residual sums go to partial[scenario][task].  Grid barrier; then warp w decides scenarios w, w + nw,
+// ... (their partials summed in task order: deterministic), freezing converged ones; grid barrier.
+__device__ __forceinline__ void grid_sync(unsigned long long* cnt, const unsigned long long target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(cnt, 1ULL);
+        while (ld_acquire_u64(cnt) < target) {
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ DevProblem batch_view(const DevProblem& P, const BatchProblem& B, const long long sc,
+                                                 const int4 tr) {
+    DevProblem Q = P;
+    const size_t so = (size_t)sc * B.ns_stride;
+    Q.xl = P.xl + so;
+    Q.lam = P.lam + so;
+    Q.u0 = P.u0 + so;
+    Q.u1 = P.u1 + so;
+    Q.x = P.x + (size_t)sc * B.n_stride;
+    if (tr.w & kTaskVar) Q.abar = B.var_pool + (size_t)sc * B.vp_stride;
+    return Q;
+}
+
+template <int RMAX>
+__global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_batch_kernel(DevProblem P, BatchProblem B) {
+    constexpr int kWarps = StreamWarps<RMAX>::value;
+    extern __shared__ __align__(128) char sdyn[];
+    __shared__ uint64_t sbar[kWarps][2];
+    __shared__ double inv_nu[kInvNu];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const long long gw = (long long)blockIdx.x * kWarps + wid, nw = (long long)gridDim.x * kWarps;
+    Stage st{sdyn + (size_t)wid * 2 * kStageBytes, sbar[wid], 0u, 0u};
+    double* dsm = reinterpret_cast<double*>(sdyn + (size_t)kWarps * 2 * kStageBytes) + (size_t)wid * 32 * RMAX;
+    for (int i = threadIdx.x; i < kInvNu; i += blockDim.x) inv_nu[i] = i > 0 ? 1.0 / (double)i : 0.0;
+    if (lane == 0) {
+        mbar_init(st.bar);
+        mbar_init(st.bar + 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const long long total0 = *(volatile long long*)&P.ctrl->total;
+    const int NT = B.n_tasks;
+    const long long NI = (long long)B.n_scen * NT;
+    const volatile int32_t* stopped = B.stopped;
+    unsigned long long bars = 0, seen = 0;
+    long long it = 0;
+    while (it < P.max_iter) {
+        const long long t = total0 + it;
+        const double* ucur = (t & 1) ? P.u1 : P.u0;
+        double* unext = (t & 1) ? P.u0 : P.u1;
+        long long item = gw;
+        while (item < NI && stopped[item / NT]) item += nw;
+        int4 tr = make_int4(0, 0, 0, 0);
+        if (item < NI) {
+            tr = __ldg(P.tasks + item % NT);
+            issue_task(batch_view(P, B, item / NT, tr), st, tr, lane, true);
+        }
+        while (item < NI) {
+            long long nxt = item + nw;
+            while (nxt < NI && stopped[nxt / NT]) nxt += nw;
+            int4 tr1 = make_int4(0, 0, 0, 0);
+            if (nxt < NI) {
+                tr1 = __ldg(P.tasks + nxt % NT);
+                issue_task(batch_view(P, B, nxt / NT, tr1), st, tr1, lane, false);
+            }
+            const long long sc = item / NT;
+            const size_t so = (size_t)sc * B.ns_stride;
+            const DevProblem Q = batch_view(P, B, sc, tr);
+            double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+            if ((tr.w & 0xF) == 1) task_packed<1>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+            else if constexpr (RMAX >= 2) task_packed<2>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(kFull, acc[k], off);
+            }
+            if (lane < 5) {
+                double a = acc[0];
+#pragma unroll
+                for (int k = 1; k < 5; ++k) a = lane == k ? acc[k] : a;
+                B.partial[(size_t)item * 8 + lane] = a;
+            }
+            item = nxt;
+            tr = tr1;
+        }
+        grid_sync(B.cnt, (++bars) * gridDim.x);
+        // per-scenario (termination)
+        unsigned long long active = 0;
+        for (long long sc = gw; sc < B.n_scen; sc += nw) {
+            if (stopped[sc]) continue;
+            double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+            for (int k2 = lane; k2 < NT; k2 += 32) {
+                const double* pp = B.partial + ((size_t)sc * NT + k2) * 8;
+#pragma unroll
+                for (int k = 0; k < 5; ++k) s5[k] += __ldcg(pp + k);
+            }
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) s5[k] += __shfl_xor_sync(kFull, s5[k], off);
+            }
+            const double pres = sqrt(s5[0]), dres = P.rho * sqrt(s5[1]);
+            const double ep = P.eps_rel * fmax(sqrt(s5[2]), sqrt(s5[3])), ed = P.eps_rel * sqrt(s5[4]);
+            const int num = !(isfinite(s5[0]) && isfinite(s5[1]) && isfinite(s5[2]) && isfinite(s5[3]) && isfinite(s5[4]));
+            const int conv = P.test && pres <= ep && dres <= ed;
+            const bool fin = conv || num || it + 1 == P.max_iter;
+            if (lane == 0) {
+                ScenResult& R = B.res[sc];
+                R.iters = it + 1;
+                R.total = t + 1;
+                R.res[0] = pres; R.res[1] = dres; R.res[2] = ep; R.res[3] = ed;
+                R.status = conv ? 1 : num ? 3 : (fin ? 2 : 0);
+                if (fin) {
+                    double obj = 0.0;
+                    const double* xs = P.x + (size_t)sc * B.n_stride;
+                    for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * __ldcg(xs + P.obj_idx[j]);
+                    R.objective = obj;
+                }
+                if (conv || num) B.stopped[sc] = 1;
+            }
+            active += (conv || num) ? 0ULL : 1ULL;
+        }
+        if (lane == 0 && active) atomicAdd(B.cnt + 1, active);
+        grid_sync(B.cnt, (++bars) * gridDim.x);
+        const unsigned long long cum = *(volatile unsigned long long*)(B.cnt + 1);
+        const unsigned long long act = cum - seen;
+        seen = cum;
+        ++it;
+        if (act == 0) break;
+    }
+    while (st.consumed < st.issued) {
+        mbar_wait(st.bar + (st.consumed & 1), (st.consumed >> 1) & 1);
+        ++st.consumed;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        P.ctrl->total = total0 + it;
+        P.ctrl->iters = it;
+    }
+}
+
+// a3 for every scenario: x_s = x0 (template slots), lambda = 0, u = x0; decisions cleared.
+__global__ void reset_batch_kernel(DevProblem P, BatchProblem B) {
+    const size_t n = (size_t)B.n_scen * B.ns_stride;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const double x0 = P.x0[i % B.ns_stride];
+        P.xl[i] = x0;
+        P.lam[i] = 0.0;
+        P.u0[i] = x0;
+        P.u1[i] = 0.0;
+    }
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < (size_t)B.n_scen; i += (size_t)gridDim.x * blockDim.x) {
+        ScenResult& R = B.res[i];
+        R.iters = 0; R.total = 0; R.status = 0; R.objective = 0.0;
+        R.res[0] = R.res[1] = R.res[2] = R.res[3] = 0.0;
+        B.stopped[i] = 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        P.ctrl->total = 0; P.ctrl->iters = 0;
+    }
+}
+
 // a3: reset the iterate to the initial point: x_s = x0, lambda = 0, u = x0.
 __global__ void reset_kernel(DevProblem P) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -502,6 +670,33 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
         e = cudaLaunchCooperativeKernel(stream_kernel_for(P.rmax), dim3(grid), dim3(stream_block(P.rmax)), args,
                                         stream_smem(P.rmax), s);
     }
+    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
+    return LOPF_OK;
+}
+
+static const void* batch_kernel_for(int rmax) {
+    return rmax <= 1 ? (const void*)admm_batch_kernel<1> : (const void*)admm_batch_kernel<2>;
+}
+
+lopf_status launch_batch(const DevProblem& P, const BatchProblem& B, int grid, void* stream, std::string& err) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const void* k = batch_kernel_for(P.rmax);
+    const int smem = stream_smem(P.rmax);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaMemsetAsync(B.cnt, 0, 2 * sizeof(unsigned long long), s);
+    if (e == cudaSuccess && P.max_iter > 0) {
+        DevProblem Q = P;
+        BatchProblem C = B;
+        void* args[] = {&Q, &C};
+        e = cudaLaunchCooperativeKernel(k, dim3(grid), dim3(stream_block(P.rmax)), args, smem, s);
+    }
+    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
+    return LOPF_OK;
+}
+
+lopf_status launch_reset_batch(const DevProblem& P, const BatchProblem& B, void* stream, std::string& err) {
+    reset_batch_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(P, B);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;
 }

@@ -181,6 +181,15 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     for (size_t i = 0; i < NS; ++i) { gs[i] = -1; nbr[i] = make_int4(0, 0, 0, 0); }
 
     L.slot_of_copy.assign(NC, -1);
+    L.trec = trec;
+    L.tsub_ptr.assign(1, 0);
+    for (int64_t t = 0; t < L.n_tasks; ++t) {
+        for (size_t j = 0; j < tasks[t].subs.size(); ++j) {
+            L.tsub_s.push_back((int32_t)tasks[t].subs[j]);
+            L.tsub_poff.push_back(tasks[t].poff[j]);
+        }
+        L.tsub_ptr.push_back((int32_t)L.tsub_s.size());
+    }
     for (int64_t t = 0; t < L.n_tasks; ++t) {
         const T& tk = tasks[t];
         const int P32 = 32 * tk.R;
