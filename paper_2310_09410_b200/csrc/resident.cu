@@ -118,6 +118,23 @@ __device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double (
     const int kmax = tr.y;
     const int at = C.sabar + 8 * (tr.z + lane);                          // byte offset of tile[0][lane]
     const int d0 = C.dst + 8 * (info[0] & 0x3F), d1 = C.dst + 8 * (info[1] & 0x3F);
+#if LOPF_RES_SPLIT
+    // even and odd columns in separate chains (half the dependent-FMA latency), added at the end
+    double ax0 = 0.0, ax1 = 0.0, bx0 = 0.0, bx1 = 0.0;
+    int k = 0;
+#pragma unroll 2
+    for (; k + 1 < kmax; k += 2) {
+        ax0 = fma(Dd(at, 64 * k), Dd(d0, k), ax0);
+        ax1 = fma(Dd(at, 64 * k + 32), Dd(d1, k), ax1);
+        bx0 = fma(Dd(at, 64 * k + 64), Dd(d0, k + 1), bx0);
+        bx1 = fma(Dd(at, 64 * k + 96), Dd(d1, k + 1), bx1);
+    }
+    if (k < kmax) {
+        ax0 = fma(Dd(at, 64 * k), Dd(d0, k), ax0);
+        ax1 = fma(Dd(at, 64 * k + 32), Dd(d1, k), ax1);
+    }
+    const double axr[2] = {ax0 + bx0, ax1 + bx1};
+#else
     double ax0 = 0.0, ax1 = 0.0;
 #pragma unroll 4
     for (int k = 0; k < kmax; ++k) {
@@ -125,6 +142,7 @@ __device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double (
         ax1 = fma(Dd(at, 64 * k + 32), Dd(d1, k), ax1);
     }
     const double axr[2] = {ax0, ax1};
+#endif
     __syncwarp();                                                        // dst is reused by the next task
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -146,6 +164,13 @@ __device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double (
 }
 
 constexpr int kFlagStride = 32;                    // one flag per 256-byte line (no L2 hot spot)
+
+#if LOPF_RES_TIMELINE   // diagnostics build: per-warp clock64 events of CTA G/2, sweeps 500..502, into P.prof
+#define TL(e) do { if (P.prof && cta == G / 2 && t >= 500 && t < 503 && lane == 0) \
+    P.prof[((t - 500) * RW + wid) * 8 + (e)] = clock64(); } while (0)
+#else
+#define TL(e) do { } while (0)
+#endif
 
 __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     __shared__ CtaHdr H;
@@ -208,6 +233,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     for (;;) {
         const int cur = (int)(t & 1);
         if (prof && tid == 0) s_prof[2] = clock64();
+        TL(0);
         if (wid == RED) {
             if (t >= 1) {                              // decision for sweep t: every CTA has published it
                 const unsigned long long need = (unsigned long long)G * (unsigned long long)(t + 1);
@@ -253,6 +279,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                     }
                 }
             }
+            TL(1);
         } else {                                       // workers: sweep t+1 (speculative until decided)
             double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
             const bool busy = t < P.max_iter && !(P.skip & 2) && wid < NT;
@@ -268,6 +295,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                     task_sweep(C, reinterpret_cast<const int4*>(sm + H.off_tasks)[task], acc, lane);
                 }
             }
+            TL(1);
             if (busy) {                                // idle warps contribute exact zeros without shuffling
 #pragma unroll
                 for (int k = 0; k < 5; ++k) {
@@ -279,10 +307,26 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
 #pragma unroll
                 for (int k = 0; k < 5; ++k) red[wid][k] = acc[k];
             }
+            TL(2);
         }
         __syncthreads();                               // [A]: sweep t+1 computed (if t < max_iter)
+        TL(3);
         if (prof && tid == 0) { const long long c1 = clock64(); s_prof[0] += c1 - s_prof[2]; s_prof[2] = c1; }
         if (wid == 0 && t < P.max_iter) {              // publish sweep t+1, then wait for the neighbours
+            if (lane == 0) {                           // neighbour-critical first: exports -> flag
+                fence_acq_rel();                       // release: this CTA's exports before the flag
+                st_rlx(myflag, (unsigned long long)t + 2ULL);
+            }
+            TL(4);
+            const unsigned long long need = (unsigned long long)t + 2ULL;
+            for (int i = lane; i < NNB; i += 32)
+                while (ld_rlx(P.flags + (size_t)Ii(H.off_nbr, i) * kFlagStride) < need) {
+                }
+            __syncwarp();                              // all lanes past all polls before the fence
+            TL(5);
+            fence_acq_rel();
+            TL(6);
+        } else if (wid == RED && t < P.max_iter) {     // residual partials of sweep t+1 (used one sweep later)
             double s[5];
 #pragma unroll
             for (int k = 0; k < 5; ++k) {
@@ -294,18 +338,12 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                 double* part = P.partial + (size_t)((t + 1) & 3) * G * 8 + (size_t)cta * 8;
 #pragma unroll
                 for (int k = 0; k < 5; ++k) __stcg(part + k, s[k]);
-                fence_acq_rel();                       // release: exports + partials before the flag
-                st_rlx(myflag, (unsigned long long)t + 2ULL);
+                fence_acq_rel();                       // release: partials before the published count
                 asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pub) : "memory");
             }
-            const unsigned long long need = (unsigned long long)t + 2ULL;
-            for (int i = lane; i < NNB; i += 32)
-                while (ld_rlx(P.flags + (size_t)Ii(H.off_nbr, i) * kFlagStride) < need) {
-                }
-            __syncwarp();                              // all lanes past all polls before the fence
-            fence_acq_rel();
         }
         __syncthreads();                               // [B]: decision for sweep t known (reducer)
+        TL(7);
         if (prof && tid == 0) s_prof[1] += clock64() - s_prof[2];
         if (s_stop[t & 1]) break;                             // state t (buffer t & 1); x^t in xout[t & 1]
         ++t;
@@ -326,10 +364,12 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
         const int g = Ii(H.off_gown, j);
         if (g >= 0) __stcg(P.x + g, Dd(H.off_xout, fin * NG + j));
     }
+#if !LOPF_RES_TIMELINE
     if (prof && tid == 0) {
         long long* pr = P.prof + 4 * cta;
         pr[0] = s_prof[0]; pr[1] = s_prof[1]; pr[2] = 0; pr[3] = t;
     }
+#endif
     __syncthreads();
     if (tid == 0) {
         __threadfence();
