@@ -28,6 +28,7 @@ struct lopf_handle {
     BatchOps bo;
     std::vector<ScenResult> scen_res;              // host copy of the last batch results
     PartSpec part;                                 // partitioned mode (lay.part != 0)
+    uint32_t epoch = 0;                            // resident launches so far (exchange tag epoch)
     bool resident() const { return lay.kernel == 2; }
     bool parted() const { return lay.part != 0; }
     bool batch() const { return lay.kernel == 3; }
@@ -455,6 +456,7 @@ lopf_status lopf_solve_async(lopf_handle* h, int64_t max_iter, int32_t test, voi
         ResProblem R = h->rp;
         R.max_iter = max_iter;
         R.test = test ? 1 : 0;
+        R.epoch = ++h->epoch;
         st = launch_resident(R, stream, err);
     } else if (h->batch()) {
         DevProblem P = h->dp;

@@ -160,7 +160,7 @@ struct CtaHdr {                               // 128 B, one per CTA
 struct ResProblem {                           // resident kernel argument
     const CtaHdr* hdr;
     uint8_t* blobs;
-    double* xchg;                             // [2][n_exp] boundary u values (ping-pong by sweep parity)
+    double* xchg;                             // [2][n_exp] {u, tag} 16-byte boundary entries (by sweep parity)
     double* partial;                          // [2][G][8] residual partials (ping-pong by sweep parity)
     unsigned long long* flags;                // [G] sweeps published by each CTA (+1), zeroed per launch
     DevCtrl* ctrl;
@@ -175,7 +175,7 @@ struct ResProblem {                           // resident kernel argument
     long long max_iter;
     long long* prof;                          // diagnostics: [G][4] cycles (work, publish+wait, -, sweeps) or NULL
     int32_t skip;                             // diagnostics: bit 1 skips the update work (sync cost only)
-    int32_t pad1;
+    uint32_t epoch;                           // launch number (> 0): high half of the exchange tags
 };
 
 // ---- batch kernel (config 4: lane = scenario, 32 scenarios per CTA group) -----------------------

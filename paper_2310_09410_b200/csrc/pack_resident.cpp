@@ -345,7 +345,7 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     size_t blobs_total = 0;
     for (auto& b : B) { b.h.blob_off = (long long)blobs_total; blobs_total = a256(blobs_total + b.blob.size()); }
     L.off_blobs = take(blobs_total);
-    L.off_xchg = take(8 * 2 * (size_t)std::max(n_exp, 1));
+    L.off_xchg = take(16 * 2 * (size_t)std::max(n_exp, 1));   // {u, tag} per boundary copy and parity
     L.off_flags = take(8 * 32 * (size_t)(L.G + 1));   // one flag per 256-byte line + the published count
     L.off_x0r = take(8 * (size_t)L.total_slots);
     L.off_x = take(8 * (size_t)P.n);

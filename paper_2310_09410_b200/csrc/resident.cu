@@ -2,21 +2,25 @@
 // with every CTA owning a connected, DFS-contiguous chunk of the feeder.
 //
 // At launch each CTA copies its blob (operators Abar_s / bbar_s, maps, iterate) into shared memory;
-// the iterate then stays on chip for the whole solve, ping-ponged by sweep parity.  Per sweep t+1:
-//   workers (31 warps), one lane per row slot of a packed task:
+// the iterate then stays on chip for the whole solve, ping-ponged by sweep parity.  Iteration t
+// (state t known) computes sweep t+1:
+//   workers (all warps but one), one lane per row slot of a packed task:
 //     a4  x_g = clamp((sum_{k in seg(g)} u_k - c_g/rho) / nu_g, lo_g, hi_g)   (closed_1, rho restored;
 //         PAPER.md:305-310, reading C1) in canonical copy order; u_k = x_k - lambda_k/rho is formed from
-//         SMEM for this CTA's copies and read from the L2 exchange buffer for boundary copies
+//         SMEM for this CTA's copies; a boundary copy (owned by another CTA) is read from the exchange
+//         buffer as a 16-byte {u, tag} entry, spinning until its tag says "state t"
 //     a5  d = -rho v - lambda, x_s = (1/rho) Abar_s d + bbar_s                  (closed_2)
 //     a6  lambda_s += rho (v - x_s)                                            (ADMM-3)
-//         boundary copies publish u to the exchange buffer; five residual sums per lane
-//   reducer (1 warp), concurrently with the workers and the publish phase: waits until every CTA has
-//     published sweep t, reduces the residual partials of sweep t in CTA order and takes the
-//     (termination) decision; identical in every CTA.  A stop at t discards the
-//     speculative sweep t+1 (state t is the other ping-pong buffer).  Partials use 4 sweep slots: a CTA
-//     can run at most 3 sweeps ahead of the slowest reducer.
-//   publish: CTA partials, fence.acq_rel, flag[c] = t+2; wait for the neighbour CTAs' flags only.
-// No grid-wide barrier inside the loop; one at exit.  Diagnostics: optional per-CTA cycle counters.
+//         each exported copy's u goes out at once as {u, tag of state t+1}; five residual sums per lane
+//   reducer (1 warp), concurrently: publishes this CTA's residual partials of sweep t (summed by the
+//     workers in iteration t-1), waits until every CTA has, reduces them in CTA order and takes the
+//     (termination) decision for sweep t, identical in every CTA.
+//   one CTA barrier; a stop at t discards the speculative sweep t+1 (state t is the other buffer).
+// No flags, fences or grid barrier inside the loop: a CTA waits only for the boundary values it reads,
+// each entry written by one 128-bit store (value and tag travel together).  Two parity slots suffice:
+// the copy of a shared global that a CTA writes for state t+2 depends on every copy of that global at
+// state t+1, and those are written only after their owners have read the state-t entries.  Tags
+// carry the launch number, so entries from earlier launches never match.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -44,12 +48,6 @@ __device__ __forceinline__ unsigned long long ld_rlx(const unsigned long long* p
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_rel(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_rlx(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // consensus input u = x_s - lambda / rho, formed with the same rounding wherever it is needed
@@ -66,14 +64,28 @@ __device__ __forceinline__ int Ii(int off, int i) { return reinterpret_cast<cons
 struct Ctx {                                       // byte offsets into SMEM + the two exchange slots
     int sinfo, sexp, sabar, sbbar, gsegoff, gseg, gpar;
     int xl_c, lam_c, xl_n, lam_n, xout_n, dst;
-    const double* xch_c;
-    double* xch_n;
+    const double2* xch_c;                          // {u, tag} entries of state t / t+1
+    double2* xch_n;
+    unsigned long long tag_c, tag_n;
     double rho, inv_rho;
 };
 
+__device__ __forceinline__ void st_entry(double2* p, const double u, const unsigned long long tag) {
+    asm volatile("{\n .reg .b128 v;\n mov.b128 v, {%1, %2};\n st.relaxed.gpu.global.b128 [%0], v;\n}"
+                 ::"l"(p), "l"(__double_as_longlong(u)), "l"(tag) : "memory");
+}
+__device__ __forceinline__ double ld_entry(const double2* p, const unsigned long long tag) {
+    unsigned long long lo, hi;
+    do {
+        asm volatile("{\n .reg .b128 v;\n ld.relaxed.gpu.global.b128 v, [%2];\n mov.b128 {%0, %1}, v;\n}"
+                     : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
+    } while (hi != tag);
+    return __longlong_as_double(lo);
+}
+
 // value of one consensus-segment entry: u of an own copy (SMEM) or of a boundary copy (exchange buffer)
 __device__ __forceinline__ double seg_u(const Ctx& C, const int e) {
-    return e >= 0 ? u_of(Dd(C.xl_c, e), Dd(C.lam_c, e), C.inv_rho) : __ldcg(C.xch_c + (-e - 1));
+    return e >= 0 ? u_of(Dd(C.xl_c, e), Dd(C.lam_c, e), C.inv_rho) : ld_entry(C.xch_c + (-e - 1), C.tag_c);
 }
 
 // one 64-row task; lane l owns rows l and l + 32 (two independent dependency chains)
@@ -153,7 +165,7 @@ __device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double (
         Dd(C.xl_n, slot) = xn;
         Dd(C.lam_n, slot) = ln;
         const int e = Ii(C.sexp, slot);
-        if (e >= 0) __stcg(C.xch_n + e, u_of(xn, ln, C.inv_rho));        // boundary copy -> exchange
+        if (e >= 0) st_entry(C.xch_n + e, u_of(xn, ln, C.inv_rho), C.tag_n);   // boundary copy -> exchange
         const double r = v[h] - xn, dx = xn - xo[h];
         acc[0] += r * r;
         acc[1] += dx * dx;
@@ -174,7 +186,7 @@ constexpr int kFlagStride = 32;                    // one flag per 256-byte line
 
 __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     __shared__ CtaHdr H;
-    __shared__ double red[RW][5];
+    __shared__ double red[2][RW][5];               // worker sums by sweep parity (reducer reads the older)
     __shared__ double s_res[2][4];                 // decision records double-buffered by sweep parity: the
     __shared__ int s_stop[2], s_conv[2], s_num[2]; // reducer writes t+1's while slow warps still read t's
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -193,7 +205,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
         for (int i = tid; i < n16; i += RB) d16[i] = __ldcg(src + i);
     }
     __syncthreads();
-    const int NS = H.n_slots, NG = H.n_glob, NT = H.n_tasks, NNB = H.n_nbr;
+    const int NS = H.n_slots, NG = H.n_glob, NT = H.n_tasks;
     const int dst_stride = H.dst_stride;                              // 64 + largest task width, doubles
     for (int i = tid; i < RW * dst_stride; i += RB) Dd(H.off_dst, i) = 0.0;   // zero tail of the d staging
     Ctx C;
@@ -202,30 +214,19 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     C.dst = H.off_dst + 8 * wid * dst_stride;
     C.rho = P.rho;
     C.inv_rho = P.inv_rho;
-    unsigned long long* myflag = P.flags + (size_t)cta * kFlagStride;
     unsigned long long* pub = P.flags + (size_t)G * kFlagStride;       // CTAs x sweeps published
     const long long total0 = *(volatile long long*)&P.ctrl->total;
     const bool prof = P.prof != nullptr;
     __shared__ long long s_prof[3];
     if (tid == 0) s_prof[0] = s_prof[1] = s_prof[2] = 0;
 
-    // initial publication: boundary u of the state into exchange slot 0; flag = 1
+    double2* xchg = reinterpret_cast<double2*>(P.xchg);
+    // tag of state t in this launch (0 = never written; the epoch keeps earlier launches' entries out)
+    auto tag_of = [&](long long tt) { return ((unsigned long long)P.epoch << 32) | (unsigned long long)(tt + 1); };
+    // state 0: boundary u into exchange slot 0
     for (int i = tid; i < NS; i += RB) {
         const int e = Ii(H.off_sexp, i);
-        if (e >= 0) __stcg(P.xchg + e, u_of(Dd(H.off_xl0, i), Dd(H.off_lam0, i), P.inv_rho));
-    }
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        st_rlx(myflag, 1ULL);
-        asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pub) : "memory");
-    }
-    if (wid == 0) {
-        for (int i = lane; i < NNB; i += 32)
-            while (ld_rlx(P.flags + (size_t)Ii(H.off_nbr, i) * kFlagStride) < 1ULL) {
-            }
-        __syncwarp();                              // all lanes past all polls before the fence
-        fence_acq_rel();
+        if (e >= 0) st_entry(xchg + e, u_of(Dd(H.off_xl0, i), Dd(H.off_lam0, i), P.inv_rho), tag_of(0));
     }
     __syncthreads();
 
@@ -235,9 +236,22 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
         if (prof && tid == 0) s_prof[2] = clock64();
         TL(0);
         if (wid == RED) {
-            if (t >= 1) {                              // decision for sweep t: every CTA has published it
-                const unsigned long long need = (unsigned long long)G * (unsigned long long)(t + 1);
+            if (t >= 1) {
+                // this CTA's residual partials of sweep t (the workers' sums of iteration t-1), then the
+                // decision for sweep t once every CTA has published its own
+                if (lane < 5) {
+                    double sk = 0.0;
+                    for (int w = 0; w < NWORK; ++w) sk += red[cur][w][lane];
+                    __stcg(P.partial + (size_t)(t & 3) * G * 8 + (size_t)cta * 8 + lane, sk);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    fence_acq_rel();                   // release: partials before the published count
+                    asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pub) : "memory");
+                }
+                const unsigned long long need = (unsigned long long)G * (unsigned long long)t;
                 while (ld_rlx(pub) < need) __nanosleep(20);
+                __syncwarp();
                 fence_acq_rel();
                 double ps[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
                 const double* part = P.partial + (size_t)(t & 3) * G * 8;
@@ -289,8 +303,10 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                 C.xl_n = cur ? H.off_xl0 : H.off_xl1;
                 C.lam_n = cur ? H.off_lam0 : H.off_lam1;
                 C.xout_n = H.off_xout + (cur ? 0 : 8 * NG);
-                C.xch_c = P.xchg + (size_t)cur * P.n_exp;
-                C.xch_n = P.xchg + (size_t)(cur ^ 1) * P.n_exp;
+                C.xch_c = xchg + (size_t)cur * P.n_exp;
+                C.xch_n = xchg + (size_t)(cur ^ 1) * P.n_exp;
+                C.tag_c = tag_of(t);
+                C.tag_n = tag_of(t + 1);
                 for (int task = wid; task < NT; task += NWORK) {
                     task_sweep(C, reinterpret_cast<const int4*>(sm + H.off_tasks)[task], acc, lane);
                 }
@@ -305,47 +321,14 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
             }
             if (lane == 0) {
 #pragma unroll
-                for (int k = 0; k < 5; ++k) red[wid][k] = acc[k];
+                for (int k = 0; k < 5; ++k) red[cur ^ 1][wid][k] = acc[k];   // sums of sweep t+1
             }
             TL(2);
         }
-        __syncthreads();                               // [A]: sweep t+1 computed (if t < max_iter)
-        TL(3);
+        __syncthreads();                               // sweep t+1 computed; decision for sweep t known
         if (prof && tid == 0) { const long long c1 = clock64(); s_prof[0] += c1 - s_prof[2]; s_prof[2] = c1; }
-        if (wid == 0 && t < P.max_iter) {              // publish sweep t+1, then wait for the neighbours
-            if (lane == 0) {                           // neighbour-critical first: exports -> flag
-                fence_acq_rel();                       // release: this CTA's exports before the flag
-                st_rlx(myflag, (unsigned long long)t + 2ULL);
-            }
-            TL(4);
-            const unsigned long long need = (unsigned long long)t + 2ULL;
-            for (int i = lane; i < NNB; i += 32)
-                while (ld_rlx(P.flags + (size_t)Ii(H.off_nbr, i) * kFlagStride) < need) {
-                }
-            __syncwarp();                              // all lanes past all polls before the fence
-            TL(5);
-            fence_acq_rel();
-            TL(6);
-        } else if (wid == RED && t < P.max_iter) {     // residual partials of sweep t+1 (used one sweep later)
-            double s[5];
-#pragma unroll
-            for (int k = 0; k < 5; ++k) {
-                s[k] = lane < NWORK ? red[lane][k] : 0.0;
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) s[k] += __shfl_xor_sync(kFull, s[k], off);
-            }
-            if (lane == 0) {
-                double* part = P.partial + (size_t)((t + 1) & 3) * G * 8 + (size_t)cta * 8;
-#pragma unroll
-                for (int k = 0; k < 5; ++k) __stcg(part + k, s[k]);
-                fence_acq_rel();                       // release: partials before the published count
-                asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pub) : "memory");
-            }
-        }
-        __syncthreads();                               // [B]: decision for sweep t known (reducer)
         TL(7);
-        if (prof && tid == 0) s_prof[1] += clock64() - s_prof[2];
-        if (s_stop[t & 1]) break;                             // state t (buffer t & 1); x^t in xout[t & 1]
+        if (s_stop[t & 1]) break;                      // state t (buffer t & 1); x^t in xout[t & 1]
         ++t;
     }
 
