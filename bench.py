@@ -105,6 +105,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--shape", default="8500", choices=["13", "123", "8500"])
     ap.add_argument("--kernel", type=int, default=0)
+    ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
+                    help="32: the fp32 variant (the paper's GPU precision, PAPER.md:414; streaming/batch kernels)")
     ap.add_argument("--cpu-sweeps", type=int, default=2000, help="oracle sweeps timed for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sweeps", type=int, default=100, help="oracle sweeps per step for --impl reference")
@@ -166,7 +168,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     t0 = time.perf_counter()
-    h = Lopf.setup(feeder, kernel=args.kernel)
+    h = Lopf.setup(feeder, kernel=args.kernel, precision=args.precision)
     setup_s = time.perf_counter() - t0
     h.bind(dev)
     sz = h.sizes
@@ -242,7 +244,7 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
             "config": {"workload": workload, "shape": args.shape, "S": int(sz.S), "n": int(sz.n),
                        "n_copies": int(sz.n_copies), "iters_to_tolerance": iters[0],
                        "time_to_tolerance_ms": statistics.median(step_ms), "l2": "flushed between steps (512 MiB write)",
@@ -333,10 +335,11 @@ def bench_stitched(args):
     gen_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     if world == 1:
-        h = Lopf.setup(feeder, kernel=1, max_iter=100_000).bind(dev)
+        h = Lopf.setup(feeder, kernel=1, max_iter=100_000, precision=args.precision).bind(dev)
         solver = None
     else:
-        solver = PartitionedSolver(feeder, device=dev, bus_owner=fg.stitched_bus_owner(feeder, world), max_iter=100_000)
+        solver = PartitionedSolver(feeder, device=dev, bus_owner=fg.stitched_bus_owner(feeder, world), max_iter=100_000,
+                                   precision=args.precision)
         h = solver.h
     setup_s = time.perf_counter() - t0
     sz = h.sizes
@@ -424,7 +427,7 @@ def bench_stitched(args):
         out = {
             "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
             "config": {"workload": f"stitched {args.n_sub} x 8500-shaped feeder (BASELINE configs[4]): "
                                    f"{feeder.n_bus} buses, one scenario, {args.sweeps} sweeps per step (test off)",
                        "S": int(sz.S), "n": int(sz.n), "n_copies": int(sz.n_copies),
@@ -486,7 +489,7 @@ def bench_batch(args):
     stream = torch.cuda.current_stream(dev)
     lo, hi = shard_range(args.n_scen, rank, world)
     t0 = time.perf_counter()
-    h = Lopf.setup_batch(f, scales[lo:hi]).bind(dev)
+    h = Lopf.setup_batch(f, scales[lo:hi], precision=args.precision).bind(dev)
     setup_s = time.perf_counter() - t0
     sz = h.sizes
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
@@ -530,7 +533,7 @@ def bench_batch(args):
         out = {
             "metric": METRIC, "value": value, "unit": "scenario-iterations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
             "config": {"workload": f"{args.n_scen} load scenarios of the 123-shaped feeder (BASELINE configs[3]), "
                                    f"kappa ~ U[0.5,1.5] per load (seed 4096), each solved to the stopping criterion",
                        "scenarios_per_rank": hi - lo, "max_iters": int(allv[:, 4].max()),

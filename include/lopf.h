@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define LOPF_ABI_VERSION 1
+#define LOPF_ABI_VERSION 2
 
 typedef struct lopf_handle lopf_handle;
 
@@ -95,13 +95,17 @@ typedef struct {
     int32_t block_threads; /* 0 = default */
     int32_t max_ctas;      /* resident kernel: CTAs available (one per SM; 0 = 148, the B200 SM count) */
     int32_t grid_cap;      /* streaming kernel: cap on the persistent grid (0 = occupancy x SMs; test hook) */
-    int32_t reserved[3];   /* [0] = 1: per-CTA phase cycle counters (lopf_get_profile); [1]: diagnostics phase-skip
+    int32_t reserved[2];   /* [0] = 1: per-CTA phase cycle counters (lopf_get_profile); [1]: diagnostics phase-skip
                               mask (bit 0 global update, bit 1 local/dual update) — results are then NOT the method */
+    int32_t precision;     /* 0 or 64: fp64 (the parity path); 32: fp32 operators, iterate and arithmetic — the
+                              paper's GPU precision (reading F1).  Residual sums,
+                              the termination test and the objective stay fp64.  Streaming and batch kernels only
+                              (kernel = 2 with precision 32 is LOPF_E_ARG; auto selects streaming). */
 } lopf_options;
 
 typedef struct {
     int64_t S, n, m, n_copies, p_sym, n_tasks, n_slots, device_bytes;
-    int64_t abar_doubles;  /* doubles of the packed operator pool streamed per iteration */
+    int64_t abar_doubles;  /* entries (fp64 or fp32, see precision) of the packed operator pool */
     int64_t alg_bytes;     /* algorithmic bytes per iteration (DESIGN.md §5 byte model) */
     int32_t kernel;        /* kernel actually selected (1 streaming, 2 resident) */
     int32_t grid;          /* CTAs of the persistent launch (known after bind) */

@@ -43,6 +43,14 @@ class _Problem(C.Structure):
                 ("rho", C.c_double), ("eps_rel", C.c_double)]
 
 
+class _ProblemF32(C.Structure):
+    _fields_ = [("n", C.c_int64), ("S", C.c_int64), ("nc", C.c_int64),
+                ("c", C.c_void_p), ("lo", C.c_void_p), ("hi", C.c_void_p),
+                ("seg_ptr", C.c_void_p), ("seg_copy", C.c_void_p), ("copy_global", C.c_void_p),
+                ("sub_ptr", C.c_void_p), ("abar_ptr", C.c_void_p), ("abar", C.c_void_p), ("bbar", C.c_void_p),
+                ("rho", C.c_float), ("rho64", C.c_double), ("eps_rel", C.c_double)]
+
+
 _lib = None
 
 
@@ -58,6 +66,8 @@ def lib():
         _lib.oracle_residuals.argtypes = [P, vp, vp, vp, vp, vp]
         _lib.oracle_run.argtypes = [P, vp, vp, vp, C.c_int64, C.c_int32, vp, vp, vp, C.c_int64, C.c_int32, vp]
         _lib.oracle_run.restype = C.c_int64
+        _lib.oracle_run_f32.argtypes = [C.POINTER(_ProblemF32), vp, vp, vp, C.c_int64, C.c_int32, vp, vp]
+        _lib.oracle_run_f32.restype = C.c_int64
     return _lib
 
 
@@ -220,3 +230,47 @@ def run_k(prob: OracleProblem, k: int, state=None) -> OracleResult:
     """Exactly k sweeps with the test disabled (fixed-K parity)."""
     xl, lam = state if state is not None else initial_state(prob)
     return _run(prob, xl, lam, k, False)
+
+
+# ---- fp32 variant (PAPER.md:414, 499-501; DESIGN.md reading F1) ---------------------------------------
+def _f32_struct(prob: OracleProblem):
+    """The binary32 copy of the problem: every fp64 datum rounded once to nearest (+-inf preserved)."""
+    if getattr(prob, "_st32", None) is None:
+        d = prob.dec
+        keep = [np.ascontiguousarray(a, dtype=np.float32) for a in (prob.lp.c, prob.lp.lo, prob.lp.hi,
+                                                                    prob.abar_flat, prob.bbar_flat)]
+        c, lo, hi, ab, bb = keep
+        idx = prob._keep
+        prob._keep32 = keep
+        prob._st32 = _ProblemF32(prob.lp.n, d.S, d.n_copies, _p(c).value, _p(lo).value, _p(hi).value,
+                                 _p(idx[3]).value, _p(idx[4]).value, _p(idx[5]).value, _p(idx[6]).value,
+                                 _p(prob.abar_ptr).value, _p(ab).value, _p(bb).value,
+                                 float(np.float32(prob.rho)), float(prob.rho), float(prob.eps_rel))
+    return prob._st32
+
+
+def _run_f32(prob: OracleProblem, xl, lam, max_iter: int, test: bool) -> OracleResult:
+    st = _f32_struct(prob)
+    x = np.zeros(prob.n, np.float32)
+    xl = np.array(xl, dtype=np.float32, copy=True)
+    lam = np.array(lam, dtype=np.float32, copy=True)
+    res = np.zeros(4)
+    conv = C.c_int32(0)
+    k = lib().oracle_run_f32(C.byref(st), _p(x), _p(xl), _p(lam), int(max_iter), int(bool(test)), _p(res),
+                             C.byref(conv))
+    x64 = x.astype(np.float64)
+    return OracleResult(converged=bool(conv.value), iters=int(k), x=x64, x_loc=xl.astype(np.float64),
+                        lam=lam.astype(np.float64), pres=res[0], dres=res[1], eps_prim=res[2], eps_dual=res[3],
+                        objective=float(prob.lp.c @ x64), trace=np.zeros((0, 4)))
+
+
+def solve_f32(prob: OracleProblem, max_iter: int = 1_000_000, state=None) -> OracleResult:
+    """Algorithm 1 in binary32 (the paper's GPU precision) until (termination) or max_iter."""
+    xl, lam = state if state is not None else initial_state(prob)
+    return _run_f32(prob, xl, lam, max_iter, True)
+
+
+def run_k_f32(prob: OracleProblem, k: int, state=None) -> OracleResult:
+    """Exactly k binary32 sweeps with the test disabled (fixed-K parity of the fp32 variant)."""
+    xl, lam = state if state is not None else initial_state(prob)
+    return _run_f32(prob, xl, lam, k, False)

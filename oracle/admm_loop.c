@@ -134,3 +134,81 @@ int64_t oracle_run(const oracle_problem *p, double *x, double *xl, double *lam, 
     free(xl_old);
     return t;
 }
+
+/* ---- fp32 variant (the paper's GPU precision; reading F1) --------
+ * The same Algorithm 1 with every datum of the iteration in binary32: Abar_s, bbar_s, c, lo, hi, rho
+ * and the initial point are the fp64 values rounded once to nearest (IEEE +-inf stays +-inf), and every
+ * operation of closed_1, closed_2 and ADMM-3 is a binary32 operation in the order written above.  The
+ * five residual terms are formed in binary32 and summed in binary64 (sequentially, ascending copy), and
+ * the test of (termination) is evaluated in binary64 from those sums — the paper does not say how its
+ * fp32 norms are reduced; an fp64 sum keeps the decision independent of the summation order. */
+typedef struct {
+    int64_t n, S, nc;
+    const float *c, *lo, *hi;
+    const int64_t *seg_ptr;
+    const int32_t *seg_copy;
+    const int32_t *copy_global;
+    const int64_t *sub_ptr;
+    const int64_t *abar_ptr;
+    const float *abar, *bbar;
+    float rho;
+    double rho64, eps_rel;
+} oracle_problem_f32;
+
+int64_t oracle_run_f32(const oracle_problem_f32 *p, float *x, float *xl, float *lam, int64_t max_iter,
+                       int32_t test, double *res, int32_t *converged)
+{
+    float *xl_old = (float *)malloc(sizeof(float) * (size_t)(p->nc > 0 ? p->nc : 1));
+    float *d = NULL;
+    int64_t dcap = 0, t = 0;
+    *converged = 0;
+    res[0] = res[1] = res[2] = res[3] = 0.0;
+    while (t < max_iter) {
+        memcpy(xl_old, xl, sizeof(float) * (size_t)p->nc);
+        /* line 5: closed_1 with rho restored (C1) */
+        for (int64_t i = 0; i < p->n; ++i) {
+            float sigma = 0.0f;
+            int64_t nu = p->seg_ptr[i + 1] - p->seg_ptr[i];
+            for (int64_t q = p->seg_ptr[i]; q < p->seg_ptr[i + 1]; ++q) {
+                int32_t k = p->seg_copy[q];
+                sigma += xl[k] - lam[k] / p->rho;
+            }
+            float xhat = (sigma - p->c[i] / p->rho) / (float)nu;
+            x[i] = fminf(fmaxf(xhat, p->lo[i]), p->hi[i]);
+        }
+        /* line 7: closed_2 */
+        for (int64_t s = 0; s < p->S; ++s) {
+            int64_t o = p->sub_ptr[s], ns = p->sub_ptr[s + 1] - o;
+            if (ns > dcap) { free(d); dcap = ns; d = (float *)malloc(sizeof(float) * (size_t)dcap); }
+            for (int64_t k = 0; k < ns; ++k) d[k] = -p->rho * x[p->copy_global[o + k]] - lam[o + k];
+            const float *Ab = p->abar + p->abar_ptr[s];
+            for (int64_t r = 0; r < ns; ++r) {
+                float acc = 0.0f;
+                for (int64_t k = 0; k < ns; ++k) acc += Ab[r * ns + k] * d[k];
+                xl[o + r] = acc / p->rho + p->bbar[o + r];
+            }
+        }
+        /* line 8: ADMM-3 */
+        for (int64_t k = 0; k < p->nc; ++k) lam[k] = lam[k] + p->rho * (x[p->copy_global[k]] - xl[k]);
+        ++t;
+        /* (termination): binary32 terms, binary64 sums */
+        double sp = 0.0, sd = 0.0, sv = 0.0, sx = 0.0, sl = 0.0;
+        for (int64_t k = 0; k < p->nc; ++k) {
+            float v = x[p->copy_global[k]];
+            float r = v - xl[k], dx = xl[k] - xl_old[k];
+            sp += (double)(r * r);
+            sd += (double)(dx * dx);
+            sv += (double)(v * v);
+            sx += (double)(xl[k] * xl[k]);
+            sl += (double)(lam[k] * lam[k]);
+        }
+        res[0] = sqrt(sp);
+        res[1] = p->rho64 * sqrt(sd);
+        res[2] = p->eps_rel * fmax(sqrt(sv), sqrt(sx));
+        res[3] = p->eps_rel * sqrt(sl);
+        if (test && res[0] <= res[2] && res[1] <= res[3]) { *converged = 1; break; }
+    }
+    free(d);
+    free(xl_old);
+    return t;
+}

@@ -53,6 +53,31 @@ static lopf_status cuda_fail(cudaError_t e, const char* where) {
 
 static constexpr int kMaxGrid = 4096;
 
+// (T) device arrays (reading F1) <-> host fp64: n elements of esz bytes at `dev`.
+static cudaError_t d2h_elems(double* out, const void* dev, size_t n, int esz, cudaStream_t s) {
+    if (esz == 8) return cudaMemcpyAsync(out, dev, 8 * n, cudaMemcpyDeviceToHost, s);
+    std::vector<float> tmp(n);
+    cudaError_t e = cudaMemcpyAsync(tmp.data(), dev, 4 * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    for (size_t i = 0; e == cudaSuccess && i < n; ++i) out[i] = (double)tmp[i];
+    return e;
+}
+static cudaError_t h2d_elems(void* dev, const double* in, size_t n, int esz, cudaStream_t s) {
+    if (esz == 8) {
+        cudaError_t e = cudaMemcpyAsync(dev, in, 8 * n, cudaMemcpyHostToDevice, s);
+        return e == cudaSuccess ? cudaStreamSynchronize(s) : e;    // `in` may be a temporary
+    }
+    std::vector<float> tmp(n);
+    for (size_t i = 0; i < n; ++i) tmp[i] = (float)in[i];
+    cudaError_t e = cudaMemcpyAsync(dev, tmp.data(), 4 * n, cudaMemcpyHostToDevice, s);
+    return e == cudaSuccess ? cudaStreamSynchronize(s) : e;
+}
+static lopf_status check_precision(const lopf_options& o) {
+    if (o.precision != 0 && o.precision != 32 && o.precision != 64)
+        return fail(LOPF_E_ARG, "precision must be 0 / 64 (fp64) or 32 (fp32)");
+    return LOPF_OK;
+}
+
 extern "C" {
 
 int32_t lopf_abi_version(void) { return LOPF_ABI_VERSION; }
@@ -80,6 +105,9 @@ lopf_status lopf_setup(const lopf_network* net, const lopf_options* opt, lopf_ha
     if (o.max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
     if (o.trace_every < 0) return fail(LOPF_E_ARG, "trace_every must be >= 0");
     if (o.kernel < 0 || o.kernel > 2) return fail(LOPF_E_ARG, "kernel must be 0 (auto), 1 or 2");
+    if (check_precision(o) != LOPF_OK) return LOPF_E_ARG;
+    if (o.precision == 32 && o.kernel == 2)
+        return fail(LOPF_E_ARG, "the resident kernel is fp64 only: use kernel 0 / 1 with precision 32");
     lopf_handle* h = new (std::nothrow) lopf_handle();
     if (!h) return fail(LOPF_E_ARG, "out of host memory");
     h->opt = o;
@@ -92,9 +120,9 @@ lopf_status lopf_setup(const lopf_network* net, const lopf_options* opt, lopf_ha
                 st = pack_resident(h->net, h->cp, h->opt, h->lay, err);
             } else if (h->opt.kernel == 1) {
                 st = pack_streaming(h->net, h->cp, h->opt, kMaxGrid, h->lay, err);
-            } else {                                      // auto: operators on chip when they fit
+            } else {                                      // auto: operators on chip when they fit (fp64)
                 std::string e2;
-                st = pack_resident(h->net, h->cp, h->opt, h->lay, e2);
+                st = h->opt.precision == 32 ? LOPF_E_ARG : pack_resident(h->net, h->cp, h->opt, h->lay, e2);
                 if (st != LOPF_OK) st = pack_streaming(h->net, h->cp, h->opt, kMaxGrid, h->lay, err);
             }
         }
@@ -121,6 +149,9 @@ lopf_status lopf_setup_batch(const lopf_network* net, const lopf_options* opt, i
     if (!(o.eps_rel > 0) || !std::isfinite(o.eps_rel)) return fail(LOPF_E_ARG, "eps_rel must be > 0 (SPEC.md:186)");
     if (o.max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
     if (n_scen <= 0 || !load_scale) return fail(LOPF_E_ARG, "n_scen must be > 0 with a load_scale array");
+    if (n_scen > kBatchMaxScen)
+        return fail(LOPF_E_ARG, "n_scen > " + std::to_string(kBatchMaxScen) + " per handle: shard the scenarios");
+    if (check_precision(o) != LOPF_OK) return LOPF_E_ARG;
     lopf_handle* h = new (std::nothrow) lopf_handle();
     if (!h) return fail(LOPF_E_ARG, "out of host memory");
     h->opt = o;
@@ -150,6 +181,7 @@ lopf_status lopf_setup_part(const lopf_network* net, const lopf_options* opt, in
     if (!(o.eps_rel > 0) || !std::isfinite(o.eps_rel)) return fail(LOPF_E_ARG, "eps_rel must be > 0 (SPEC.md:186)");
     if (o.max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
     if (world < 1 || rank < 0 || rank >= world) return fail(LOPF_E_ARG, "need 0 <= rank < world");
+    if (check_precision(o) != LOPF_OK) return LOPF_E_ARG;
     lopf_handle* h = new (std::nothrow) lopf_handle();
     if (!h) return fail(LOPF_E_ARG, "out of host memory");
     h->opt = o;
@@ -245,10 +277,11 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
             psym_var += (int64_t)P.n_s[s] * (P.n_s[s] + 1) / 2;
         }
     }
-    sz->alg_bytes = 8 * (psym + nbbar + 6 * P.nc + 4 * P.n + h->lay.n_obj) + 4 * (2 * P.nc + P.n + 1);
+    const int64_t E = h->lay.esz;           // 8 (fp64) or 4 (fp32 variant): the (T) arrays
+    sz->alg_bytes = E * (psym + nbbar + 6 * P.nc + 4 * P.n + h->lay.n_obj) + 4 * (2 * P.nc + P.n + 1);
     if (h->batch()) {                       // per batch sweep: shared operators once, the rest per scenario
         const int64_t ns = h->lay.n_scen;
-        sz->alg_bytes = 8 * ((psym - psym_var) + ns * (psym_var + nbbar + 6 * P.nc + 4 * P.n + h->lay.n_obj)) +
+        sz->alg_bytes = E * ((psym - psym_var) + ns * (psym_var + nbbar + 6 * P.nc + 4 * P.n + h->lay.n_obj)) +
                         4 * (2 * P.nc + P.n + 1);
     }
     sz->kernel = h->lay.kernel;
@@ -288,6 +321,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         P.n_tasks = (int32_t)L.n_tasks;
         P.n_slots = (int32_t)L.n_slots;
         P.rmax = L.rmax;
+        P.esz = L.esz;
         P.n = h->cp.n;
         P.tasks = (const int4*)(b + L.off_tasks);
         P.s_info = (const int32_t*)(b + L.off_info);
@@ -325,9 +359,10 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         B.stopped = (int32_t*)(b + L.off_bstop);
         B.partial = (double*)(b + L.off_bpart);
         B.cnt = (unsigned long long*)(b + L.off_bcnt);
+        B.amask = (uint32_t*)(b + L.off_bmask);
         std::string err;
         int grid = 0;
-        lopf_status st = query_grid(L.rmax, &grid, err);
+        lopf_status st = query_grid(L.rmax, L.esz, &grid, err);
         if (st != LOPF_OK) return fail(st, err);
         h->grid = grid;
         st = launch_reset_batch(P, B, stream, err);
@@ -382,6 +417,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     DevProblem& P = h->dp;
     P.n_tasks = (int32_t)L.n_tasks;
     P.rmax = L.rmax;
+    P.esz = L.esz;
     P.n_slots = (int32_t)L.n_slots;
     P.n = h->cp.n;
     P.tasks = (const int4*)(b + L.off_tasks);
@@ -418,7 +454,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     P.imp = L.part ? (const int32_t*)(b + L.off_imp) : nullptr;
     std::string err;
     int grid = 0;
-    lopf_status st = query_grid(L.rmax, &grid, err);
+    lopf_status st = query_grid(L.rmax, L.esz, &grid, err);
     if (st != LOPF_OK) return fail(st, err);
     grid = std::min(grid, kMaxGrid);
     if (h->opt.grid_cap > 0) grid = std::min(grid, h->opt.grid_cap);   // test hook: cap the grid
@@ -602,8 +638,8 @@ static lopf_status fetch_slots(lopf_handle* h, cudaStream_t s, std::vector<doubl
     xl.assign(L.n_slots, 0.0);
     lm.assign(L.n_slots, 0.0);
     if (!h->resident()) {
-        CUDA_TRY(cudaMemcpyAsync(xl.data(), h->dp.xl, 8 * L.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
-        CUDA_TRY(cudaMemcpyAsync(lm.data(), h->dp.lam, 8 * L.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
+        CUDA_TRY(d2h_elems(xl.data(), h->dp.xl, L.n_slots, L.esz, s), "state D2H");
+        CUDA_TRY(d2h_elems(lm.data(), h->dp.lam, L.n_slots, L.esz, s), "state D2H");
     } else {
         for (int c = 0; c < L.G; ++c) {
             const CtaHdr& H = L.hdr[c];
@@ -621,7 +657,7 @@ lopf_status lopf_get_state(lopf_handle* h, void* stream, double* x, double* x_lo
     if (!h->bound) return fail(LOPF_E_STATE, "get_state before lopf_bind");
     cudaStream_t s = (cudaStream_t)stream;
     const Layout& L = h->lay;
-    if (x) CUDA_TRY(cudaMemcpyAsync(x, h->dp.x, sizeof(double) * h->cp.n, cudaMemcpyDeviceToHost, s), "state D2H");
+    if (x) CUDA_TRY(d2h_elems(x, h->dp.x, h->cp.n, L.esz, s), "state D2H");
     if (x_loc || lam) {
         std::vector<double> xl, lm;
         lopf_status st = fetch_slots(h, s, xl, lm);
@@ -655,9 +691,9 @@ lopf_status lopf_set_state(lopf_handle* h, void* stream, const double* x_loc, co
         u[sl] = x_loc[k] - lam[k] * inv_rho;
     }
     if (!h->resident()) {
-        CUDA_TRY(cudaMemcpyAsync(h->dp.xl, xl.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
-        CUDA_TRY(cudaMemcpyAsync(h->dp.lam, lm.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
-        CUDA_TRY(cudaMemcpyAsync(h->dp.u0, u.data(), 8 * L.n_slots, cudaMemcpyHostToDevice, s), "state H2D");
+        CUDA_TRY(h2d_elems(h->dp.xl, xl.data(), L.n_slots, L.esz, s), "state H2D");
+        CUDA_TRY(h2d_elems(h->dp.lam, lm.data(), L.n_slots, L.esz, s), "state H2D");
+        CUDA_TRY(h2d_elems(h->dp.u0, u.data(), L.n_slots, L.esz, s), "state H2D");
     } else {
         for (int c = 0; c < L.G; ++c) {
             const CtaHdr& H = L.hdr[c];
@@ -712,9 +748,10 @@ lopf_status lopf_get_state_scen(lopf_handle* h, void* stream, int32_t scen, doub
     const Layout& L = h->lay;
     const size_t NS = (size_t)L.n_slots, N = (size_t)h->cp.n;
     std::vector<double> xl(NS), lm(NS);
-    CUDA_TRY(cudaMemcpyAsync(xl.data(), h->dp.xl + (size_t)scen * NS, 8 * NS, cudaMemcpyDeviceToHost, s), "state D2H");
-    CUDA_TRY(cudaMemcpyAsync(lm.data(), h->dp.lam + (size_t)scen * NS, 8 * NS, cudaMemcpyDeviceToHost, s), "state D2H");
-    if (x) CUDA_TRY(cudaMemcpyAsync(x, h->dp.x + (size_t)scen * N, 8 * N, cudaMemcpyDeviceToHost, s), "state D2H");
+    const size_t E = (size_t)L.esz;
+    CUDA_TRY(d2h_elems(xl.data(), (const uint8_t*)h->dp.xl + E * scen * NS, NS, L.esz, s), "state D2H");
+    CUDA_TRY(d2h_elems(lm.data(), (const uint8_t*)h->dp.lam + E * scen * NS, NS, L.esz, s), "state D2H");
+    if (x) CUDA_TRY(d2h_elems(x, (const uint8_t*)h->dp.x + E * scen * N, N, L.esz, s), "state D2H");
     CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     for (int64_t k = 0; k < h->cp.nc; ++k) {
         if (x_loc) x_loc[k] = xl[L.slot_of_copy[k]];

@@ -93,25 +93,29 @@ struct DevCtrl {                           // 256 B, device-resident control blo
     double pad[18];
 };
 
+// Arrays marked (T) hold doubles when esz == 8 and floats when esz == 4 (the fp32 variant, reading F1:
+// the paper's GPU precision); the kernels cast them to the element type they were
+// instantiated for.  Residual sums, partials, trace, objective coefficients and the exchange are fp64.
 struct DevProblem {                        // kernel argument (pointers into the arena)
     int32_t n_tasks, n_slots, grid, rmax;  // rmax: widest task (selects the kernel instantiation)
+    int32_t esz;                           // element size of operators / iterate / globals: 8 (fp64) or 4 (fp32)
     int64_t n;
     const int4* tasks;                     // {slot_off, abar_off, kmax, R}
     const int32_t* s_info;
     const int32_t* s_g;
     const int4* s_nbr;
-    const double* s_bbar;
-    double* xl;
-    double* lam;
-    double* u0;
-    double* u1;
-    const double* x0;                      // initial x_s per slot
-    const double2* gbnd;                   // {lo, hi} per global
-    const double* gcost;                   // c/rho per global (read for kInfoCost slots only)
+    const void* s_bbar;                    // (T)
+    void* xl;                              // (T)
+    void* lam;                             // (T)
+    void* u0;                              // (T)
+    void* u1;                              // (T)
+    const void* x0;                        // (T) initial x_s per slot
+    const void* gbnd;                      // (T) {lo, hi} per global
+    const void* gcost;                     // (T) c/rho per global (read for kInfoCost slots only)
     const int32_t* seg_ptr;                // [n+1] into seg_slot
     const int32_t* seg_slot;               // [nc] slots in canonical copy order
-    double* x;                             // [n]
-    const double* abar;                    // packed operator pool
+    void* x;                               // (T) [n]
+    const void* abar;                      // (T) packed operator pool
     double* partial;                       // [grid * 8]
     DevCtrl* ctrl;
     double* trace;                         // [trace_cap * 5]
@@ -193,18 +197,21 @@ struct ScenResult {                            // 64 B per scenario (device)
 struct BatchProblem {                          // config 4: streaming kernel over (scenario, task) items
     int32_t n_scen, n_tasks, ns_stride, n_stride;  // scenarios; tasks per scenario; slot / global strides
     int64_t vp_stride;                         // doubles of per-scenario operator blocks
-    const double* var_pool;                    // [n_scen][vp_stride] blocks of tasks flagged kTaskVar
+    const void* var_pool;                      // (T) [n_scen][vp_stride] blocks of tasks flagged kTaskVar
     ScenResult* res;                           // [n_scen]
     int32_t* stopped;                          // [n_scen] converged / non-finite: no more sweeps
     double* partial;                           // [n_scen][n_tasks][8] residual sums per item
     unsigned long long* cnt;                   // [2]: barrier arrivals, cumulative active count
+    uint32_t* amask;                           // [2][ceil(n_scen/32)] active-scenario bits by sweep parity
 };
+constexpr int kBatchMaxScen = 8192;            // scenarios per batch handle (SMEM active-set tables)
 
 // Arena layout: byte offsets of every array (all 256-byte aligned).
 struct Layout {
     int32_t kernel = 1;
     int64_t n_tasks = 0, n_slots = 0, abar_doubles = 0, n_obj = 0;
     int32_t rmax = 1;                     // streaming: widest task (R)
+    int32_t esz = 8;                      // streaming / batch: element size of the (T) arrays (8 fp64, 4 fp32)
     // partitioned mode
     int32_t part = 0, rank = 0, world = 1, n_bnd = 0, n_imp = 0, ghost0 = 0;
     size_t off_sexp = 0, off_imp = 0, off_xbuf = 0;
@@ -226,7 +233,7 @@ struct Layout {
     // batch kernel (config 4): the streaming layout of one scenario, replicated over the scenarios
     int32_t n_scen = 0, n_grp = 0, ns_max = 0;
     int64_t VP = 0;                        // doubles of per-scenario operator blocks (tasks holding a load)
-    size_t off_bvar = 0, off_bres = 0, off_bstop = 0, off_bpart = 0, off_bcnt = 0;
+    size_t off_bvar = 0, off_bres = 0, off_bstop = 0, off_bpart = 0, off_bcnt = 0, off_bmask = 0;
 };
 
 // Scenario batches (config 4): per-scenario operators of the subsystems that hold a load (their
@@ -276,7 +283,7 @@ int stream_block(int rmax);
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
 lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err);
 lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err);
-lopf_status query_grid(int rmax, int* grid, std::string& err);
+lopf_status query_grid(int rmax, int esz, int* grid, std::string& err);
 lopf_status launch_resident(const ResProblem& P, void* stream, std::string& err);
 lopf_status launch_reset_resident(const ResProblem& P, void* stream, std::string& err);
 lopf_status resident_capacity(int* sms, int* smem_optin, std::string& err);

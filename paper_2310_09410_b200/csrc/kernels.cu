@@ -40,13 +40,21 @@ constexpr int kInvNu = 64;                 // SMEM table of 1 / nu (the host's 1
 // each subsystem, then b-bar if nonzero) in the pool, and 32*R entries of each per-slot array.  One
 // elected lane copies them into one of the warp's two SMEM stages with cp.async.bulk, completing
 // on that stage's mbarrier, one task ahead of the compute.
+// T = double (the parity path) or float (the paper's GPU precision; reading F1): the
+// operator block budget is the same 8 * kPackBudget bytes, per-slot iterate entries are sizeof(T).
 constexpr int kOffInfo = 8 * kPackBudget;
 constexpr int kOffG = kOffInfo + 4 * 64;
 constexpr int kOffNbr = kOffG + 4 * 64;
 constexpr int kOffLam = kOffNbr + 16 * 64;
-constexpr int kOffXl = kOffLam + 8 * 64;
-constexpr int kStageBytes = kOffXl + 8 * 64;
-static_assert(kStageBytes % 16 == 0, "bulk copies need 16-byte alignment");
+template <class T> struct Stg {
+    static constexpr int kOffXl = kOffLam + (int)sizeof(T) * 64;
+    static constexpr int kBytes = kOffXl + (int)sizeof(T) * 64;
+    static_assert(kBytes % 16 == 0, "bulk copies need 16-byte alignment");
+};
+template <class T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
+template <class T> using vec2_t = typename Vec2<T>::type;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* m) {
@@ -69,8 +77,10 @@ struct Stage {                   // per-warp pipeline: the j-th staged task of t
 
 // `full_fence`: the copies read lambda / x_s this warp stored in the same sweep (the next-sweep
 // prefetch); otherwise only the stage's SMEM (read by this warp's previous task) needs ordering.
+template <class T>
 __device__ __forceinline__ void issue_task(const DevProblem& P, Stage& st, const int4 tr, const int lane,
                                            const bool full_fence) {
+    constexpr int kStageBytes = Stg<T>::kBytes;
     if (!(tr.w & kTaskPacked)) return;                          // full tasks read HBM directly
     const int b = st.issued & 1;
     ++st.issued;
@@ -78,32 +88,34 @@ __device__ __forceinline__ void issue_task(const DevProblem& P, Stage& st, const
         char* sb = st.buf + b * kStageBytes;
         const uint32_t n = (uint32_t)(tr.w >> kTaskUsedShift) & 0xFFu;
         const bool ablk = !(tr.w & kTaskDirect);
-        const uint32_t bytes = 40u * n + (ablk ? 8u * (uint32_t)tr.z : 0u);
+        constexpr uint32_t E = sizeof(T);
+        const uint32_t bytes = (24u + 2u * E) * n + (ablk ? E * (uint32_t)tr.z : 0u);
         uint64_t* m = st.bar + b;
         if (full_fence) asm volatile("fence.proxy.async;" ::: "memory");
         else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
-        if (ablk) bulk_g2s(sb, P.abar + tr.y, 8u * (uint32_t)tr.z, m);
+        if (ablk) bulk_g2s(sb, reinterpret_cast<const T*>(P.abar) + tr.y, E * (uint32_t)tr.z, m);
         bulk_g2s(sb + kOffInfo, P.s_info + tr.x, 4u * n, m);
         bulk_g2s(sb + kOffG, P.s_g + tr.x, 4u * n, m);
         bulk_g2s(sb + kOffNbr, P.s_nbr + tr.x, 16u * n, m);
-        bulk_g2s(sb + kOffLam, P.lam + tr.x, 8u * n, m);
-        bulk_g2s(sb + kOffXl, P.xl + tr.x, 8u * n, m);
+        bulk_g2s(sb + kOffLam, reinterpret_cast<const T*>(P.lam) + tr.x, E * n, m);
+        bulk_g2s(sb + Stg<T>::kOffXl, reinterpret_cast<const T*>(P.xl) + tr.x, E * n, m);
     }
 }
 
 // a4 for one slot: the global's consensus value from the ping-pong copies (closed_1, rho restored)
-__device__ __forceinline__ double consensus(const DevProblem& P, const int inf, const int g, const int4 nb,
-                                            const double* __restrict__ ucur, const double* __restrict__ inv_nu) {
-    const double2 bd = __ldg(P.gbnd + g);                               // {lo, hi}
-    const double cr = (inf & kInfoCost) ? __ldg(P.gcost + g) : 0.0;     // c / rho
-    double sigma, inv;
+template <class T>
+__device__ __forceinline__ T consensus(const DevProblem& P, const int inf, const int g, const int4 nb,
+                                       const T* __restrict__ ucur, const T* __restrict__ inv_nu) {
+    const vec2_t<T> bd = __ldg(reinterpret_cast<const vec2_t<T>*>(P.gbnd) + g);        // {lo, hi}
+    const T cr = (inf & kInfoCost) ? __ldg(reinterpret_cast<const T*>(P.gcost) + g) : T(0);   // c / rho
+    T sigma, inv;
     if (inf & kInfoInline) {                               // nu <= 4: neighbour slots inline
         const int nu = (inf >> kInfoNuShift) & 0xF;
-        const double a0 = __ldcg(ucur + nb.x);
-        const double a1 = nu > 1 ? __ldcg(ucur + nb.y) : 0.0;
-        const double a2 = nu > 2 ? __ldcg(ucur + nb.z) : 0.0;
-        const double a3 = nu > 3 ? __ldcg(ucur + nb.w) : 0.0;
+        const T a0 = __ldcg(ucur + nb.x);
+        const T a1 = nu > 1 ? __ldcg(ucur + nb.y) : T(0);
+        const T a2 = nu > 2 ? __ldcg(ucur + nb.z) : T(0);
+        const T a3 = nu > 3 ? __ldcg(ucur + nb.w) : T(0);
         sigma = a0;                                        // ascending canonical copy order
         if (nu > 1) sigma += a1;
         if (nu > 2) sigma += a2;
@@ -111,40 +123,43 @@ __device__ __forceinline__ double consensus(const DevProblem& P, const int inf, 
         inv = inv_nu[nu];
     } else {
         const int q0 = __ldg(P.seg_ptr + g), q1 = __ldg(P.seg_ptr + g + 1);
-        sigma = 0.0;
+        sigma = T(0);
         for (int q = q0; q < q1; ++q) sigma += __ldcg(ucur + __ldg(P.seg_slot + q));
-        inv = q1 - q0 < kInvNu ? inv_nu[q1 - q0] : 1.0 / (double)(q1 - q0);
+        inv = q1 - q0 < kInvNu ? inv_nu[q1 - q0] : T(1) / (T)(q1 - q0);
     }
-    const double xg = fmin(fmax((sigma - cr) * inv, bd.x), bd.y);      // IEEE +-inf = no clamp
-    if (inf & kInfoFirst) P.x[g] = xg;
+    const T xg = fmin(fmax((sigma - cr) * inv, bd.x), bd.y);            // IEEE +-inf = no clamp
+    if (inf & kInfoFirst) reinterpret_cast<T*>(P.x)[g] = xg;
     return xg;
 }
 
-// a6 + a7 for one slot
-__device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, const int slot, const double ax, const double bb,
-                                            const double v, const double lam, const double xo,
-                                            double* __restrict__ unext, double (&acc)[5]) {
-    const double xn = fma(ax, P.inv_rho, bb);                          // (1/rho) Abar d + bbar
-    const double ln = lam + P.rho * (v - xn);                          // ADMM-3
-    __stcs(P.xl + slot, xn);
-    __stcs(P.lam + slot, ln);
-    const double un = xn - ln * P.inv_rho;                             // next consensus input
+// a6 + a7 for one slot.  The five residual terms are formed in T and summed in fp64 (reading F1).
+template <class T>
+__device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, const int slot, const T ax, const T bb,
+                                            const T v, const T lam, const T xo, T* __restrict__ unext,
+                                            double (&acc)[5]) {
+    const T rho = (T)P.rho, inv_rho = (T)P.inv_rho;
+    const T xn = fma(ax, inv_rho, bb);                                 // (1/rho) Abar d + bbar
+    const T ln = lam + rho * (v - xn);                                 // ADMM-3
+    __stcs(reinterpret_cast<T*>(P.xl) + slot, xn);
+    __stcs(reinterpret_cast<T*>(P.lam) + slot, ln);
+    const T un = xn - ln * inv_rho;                                    // next consensus input
     unext[slot] = un;
-    if (inf & kInfoExport) __stcg(P.xbuf + __ldg(P.s_exp + slot), un);   // partitioned: to the other ranks
-    const double rr = v - xn, dx = xn - xo;
-    acc[0] += rr * rr;
-    acc[1] += dx * dx;
-    acc[2] += v * v;
-    acc[3] += xn * xn;
-    acc[4] += ln * ln;
+    if (inf & kInfoExport) __stcg(P.xbuf + __ldg(P.s_exp + slot), (double)un);   // partitioned: to the other ranks
+    const T rr = v - xn, dx = xn - xo;
+    acc[0] += (double)(rr * rr);
+    acc[1] += (double)(dx * dx);
+    acc[2] += (double)(v * v);
+    acc[3] += (double)(xn * xn);
+    acc[4] += (double)(ln * ln);
 }
 
 // Packed task (R <= 2 halves): inputs from the SMEM stage; operator block from the stage or, for a
 // lone large subsystem (kTaskDirect), straight from the pool.
-template <int R>
-__device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, const double* __restrict__ ucur,
-                                            double* __restrict__ unext, double (&acc)[5], const int lane,
-                                            double* __restrict__ dsm, Stage& st, const double* __restrict__ inv_nu) {
+template <int R, class T>
+__device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, const T* __restrict__ ucur,
+                                            T* __restrict__ unext, double (&acc)[5], const int lane,
+                                            T* __restrict__ dsm, Stage& st, const T* __restrict__ inv_nu) {
+    constexpr int kStageBytes = Stg<T>::kBytes;
     const int b = st.consumed & 1;
     mbar_wait(st.bar + b, (st.consumed >> 1) & 1);
     ++st.consumed;
@@ -152,14 +167,15 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
     const int* s_info = reinterpret_cast<const int*>(sb + kOffInfo);
     const int* s_g = reinterpret_cast<const int*>(sb + kOffG);
     const int4* s_nbr = reinterpret_cast<const int4*>(sb + kOffNbr);
-    const double* s_lam = reinterpret_cast<const double*>(sb + kOffLam);
-    const double* s_xl = reinterpret_cast<const double*>(sb + kOffXl);
-    const double* S = (tr.w & kTaskDirect) ? P.abar + tr.y : reinterpret_cast<const double*>(sb);
+    const T* s_lam = reinterpret_cast<const T*>(sb + kOffLam);
+    const T* s_xl = reinterpret_cast<const T*>(sb + Stg<T>::kOffXl);
+    const T* S = (tr.w & kTaskDirect) ? reinterpret_cast<const T*>(P.abar) + tr.y : reinterpret_cast<const T*>(sb);
     const int used = (tr.w >> kTaskUsedShift) & 0xFF;       // stage entries past `used` are stale
-    double v[R], ax[R];
+    const T rho = (T)P.rho;
+    T v[R], ax[R];
     int info[R];
     // a4, split so that every gather of both halves is in flight before the first is consumed
-    double ua[R][4], lo[R], hi[R], cr[R];
+    T ua[R][4], lo[R], hi[R], cr[R];
     int g[R];
 #pragma unroll
     for (int h = 0; h < R; ++h) {
@@ -169,22 +185,24 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
         const int nu = (info[h] >> kInfoNuShift) & 0xF;
         g[h] = s_g[j];
         const int4 nb = s_nbr[j];
-        ua[h][0] = inl ? __ldcg(ucur + nb.x) : 0.0;
-        ua[h][1] = inl && nu > 1 ? __ldcg(ucur + nb.y) : 0.0;
-        ua[h][2] = inl && nu > 2 ? __ldcg(ucur + nb.z) : 0.0;
-        ua[h][3] = inl && nu > 3 ? __ldcg(ucur + nb.w) : 0.0;
-        const double2 bd = val ? __ldg(P.gbnd + g[h]) : make_double2(0.0, 0.0);
+        ua[h][0] = inl ? __ldcg(ucur + nb.x) : T(0);
+        ua[h][1] = inl && nu > 1 ? __ldcg(ucur + nb.y) : T(0);
+        ua[h][2] = inl && nu > 2 ? __ldcg(ucur + nb.z) : T(0);
+        ua[h][3] = inl && nu > 3 ? __ldcg(ucur + nb.w) : T(0);
+        vec2_t<T> bd;
+        bd.x = T(0), bd.y = T(0);
+        if (val) bd = __ldg(reinterpret_cast<const vec2_t<T>*>(P.gbnd) + g[h]);
         lo[h] = bd.x;
         hi[h] = bd.y;
-        cr[h] = val && (info[h] & kInfoCost) ? __ldg(P.gcost + g[h]) : 0.0;
+        cr[h] = val && (info[h] & kInfoCost) ? __ldg(reinterpret_cast<const T*>(P.gcost) + g[h]) : T(0);
     }
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         const int j = h * 32 + lane;
-        v[h] = 0.0;
-        double d = 0.0;
+        v[h] = T(0);
+        T d = T(0);
         if (info[h] & kInfoValid) {
-            double sigma, inv;
+            T sigma, inv;
             if (info[h] & kInfoInline) {
                 const int nu = (info[h] >> kInfoNuShift) & 0xF;
                 sigma = ua[h][0];                                  // ascending canonical copy order
@@ -194,16 +212,16 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
                 inv = inv_nu[nu];
             } else {
                 const int q0 = __ldg(P.seg_ptr + g[h]), q1 = __ldg(P.seg_ptr + g[h] + 1);
-                sigma = 0.0;
+                sigma = T(0);
                 for (int q = q0; q < q1; ++q) sigma += __ldcg(ucur + __ldg(P.seg_slot + q));
-                inv = q1 - q0 < kInvNu ? inv_nu[q1 - q0] : 1.0 / (double)(q1 - q0);
+                inv = q1 - q0 < kInvNu ? inv_nu[q1 - q0] : T(1) / (T)(q1 - q0);
             }
             v[h] = fmin(fmax((sigma - cr[h]) * inv, lo[h]), hi[h]);   // closed_1; IEEE +-inf = no clamp
-            if (info[h] & kInfoFirst) P.x[g[h]] = v[h];
-            d = -P.rho * v[h] - s_lam[j];
+            if (info[h] & kInfoFirst) reinterpret_cast<T*>(P.x)[g[h]] = v[h];
+            d = -rho * v[h] - s_lam[j];
         }
         dsm[j] = d;
-        ax[h] = 0.0;
+        ax[h] = T(0);
     }
     __syncwarp();
     // Row r of subsystem s: sum_k Abar[r][k] d[k], k ascending, from the upper-triangular block
@@ -232,38 +250,40 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
         if (!(info[h] & kInfoValid)) continue;
         const int j = h * 32 + lane;
         // b-bar follows the subsystem's triangle in the block when nonzero
-        const double bb = (info[h] & kInfoBbar)
-                              ? S[((unsigned)info[h] >> kInfoPoffShift) + ns[h] * (ns[h] + 1) / 2 + r[h]] : 0.0;
-        finish_slot(P, info[h], tr.x + j, ax[h], bb, v[h], s_lam[j], s_xl[j], unext, acc);
+        const T bb = (info[h] & kInfoBbar)
+                         ? S[((unsigned)info[h] >> kInfoPoffShift) + ns[h] * (ns[h] + 1) / 2 + r[h]] : T(0);
+        finish_slot<T>(P, info[h], tr.x + j, ax[h], bb, v[h], s_lam[j], s_xl[j], unext, acc);
     }
     __syncwarp();
 }
 
-// Full task (one subsystem of n_s > 63, R = 2, 4 or 8): Abar as kmax columns of 32*R doubles and the
+// Full task (one subsystem of n_s > 63, R = 2, 4 or 8): Abar as kmax columns of 32*R entries and the
 // per-slot inputs read straight from HBM.
-template <int R>
-__device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, const double* __restrict__ ucur,
-                                          double* __restrict__ unext, double (&acc)[5], const int lane,
-                                          double* __restrict__ dsm, const double* __restrict__ inv_nu) {
-    double v[R], ax[R];
+template <int R, class T>
+__device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, const T* __restrict__ ucur,
+                                          T* __restrict__ unext, double (&acc)[5], const int lane,
+                                          T* __restrict__ dsm, const T* __restrict__ inv_nu) {
+    const T* lamp = reinterpret_cast<const T*>(P.lam);
+    const T rho = (T)P.rho;
+    T v[R], ax[R];
     int info[R];
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         const int slot = tr.x + h * 32 + lane;
         info[h] = __ldg(P.s_info + slot);
-        v[h] = 0.0;
-        double d = 0.0;
+        v[h] = T(0);
+        T d = T(0);
         if (info[h] & kInfoValid) {
-            v[h] = consensus(P, info[h], __ldg(P.s_g + slot), __ldg(P.s_nbr + slot), ucur, inv_nu);
-            d = -P.rho * v[h] - P.lam[slot];
+            v[h] = consensus<T>(P, info[h], __ldg(P.s_g + slot), __ldg(P.s_nbr + slot), ucur, inv_nu);
+            d = -rho * v[h] - lamp[slot];
         }
         dsm[h * 32 + lane] = d;
-        ax[h] = 0.0;
+        ax[h] = T(0);
     }
     __syncwarp();
-    const double* __restrict__ A = P.abar + tr.y;
+    const T* __restrict__ A = reinterpret_cast<const T*>(P.abar) + tr.y;
     for (int k = 0; k < tr.z; ++k) {
-        const double dk = dsm[k];                              // one subsystem per full task: base 0
+        const T dk = dsm[k];                                   // one subsystem per full task: base 0
 #pragma unroll
         for (int h = 0; h < R; ++h) ax[h] = fma(__ldcs(A + (size_t)k * (32 * R) + h * 32 + lane), dk, ax[h]);
     }
@@ -271,8 +291,8 @@ __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, co
     for (int h = 0; h < R; ++h) {
         if (!(info[h] & kInfoValid)) continue;
         const int slot = tr.x + h * 32 + lane;
-        const double bb = (info[h] & kInfoBbar) ? __ldg(P.s_bbar + slot) : 0.0;
-        finish_slot(P, info[h], slot, ax[h], bb, v[h], P.lam[slot], P.xl[slot], unext, acc);
+        const T bb = (info[h] & kInfoBbar) ? __ldg(reinterpret_cast<const T*>(P.s_bbar) + slot) : T(0);
+        finish_slot<T>(P, info[h], slot, ax[h], bb, v[h], lamp[slot], reinterpret_cast<const T*>(P.xl)[slot], unext, acc);
     }
     __syncwarp();
 }
@@ -280,19 +300,20 @@ __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, co
 template <int RMAX>
 struct StreamWarps { static constexpr int value = RMAX <= 2 ? kStreamWarps : kStreamWarpsWide; };
 
-template <int RMAX>   // largest task width in the problem (RMAX > 2 only with n_s > 64: the S = 1 path)
+template <int RMAX, class T>   // largest task width in the problem (RMAX > 2 only with n_s > 64: the S = 1 path)
 __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_stream_kernel(DevProblem P) {
     constexpr int kWarps = StreamWarps<RMAX>::value;
+    constexpr int kStageBytes = Stg<T>::kBytes;
     extern __shared__ __align__(128) char sdyn[];      // [kWarps][2][kStageBytes] stages, [kWarps][32*RMAX] d
     __shared__ double red[kWarps][5];
     __shared__ uint64_t sbar[kWarps][2];
-    __shared__ double inv_nu[kInvNu];
+    __shared__ T inv_nu[kInvNu];
     __shared__ int s_stop;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
     Stage st{sdyn + (size_t)wid * 2 * kStageBytes, sbar[wid], 0u, 0u};
-    double* dsm = reinterpret_cast<double*>(sdyn + (size_t)kWarps * 2 * kStageBytes) + (size_t)wid * 32 * RMAX;
-    for (int i = threadIdx.x; i < kInvNu; i += blockDim.x) inv_nu[i] = i > 0 ? 1.0 / (double)i : 0.0;
+    T* dsm = reinterpret_cast<T*>(sdyn + (size_t)kWarps * 2 * kStageBytes) + (size_t)wid * 32 * RMAX;
+    for (int i = threadIdx.x; i < kInvNu; i += blockDim.x) inv_nu[i] = i > 0 ? T(1) / (T)i : T(0);
     if (lane == 0) {
         mbar_init(st.bar);
         mbar_init(st.bar + 1);
@@ -303,25 +324,25 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_stream_
     const long long total0 = *(volatile long long*)&P.ctrl->total;
     const int4 tr0 = gw < P.n_tasks ? __ldg(P.tasks + gw) : make_int4(0, 0, 0, 0);
     long long it = 0;
-    if (P.max_iter > 0) issue_task(P, st, tr0, lane, false);
+    if (P.max_iter > 0) issue_task<T>(P, st, tr0, lane, false);
     while (it < P.max_iter) {
         const long long t = total0 + it;
-        const double* ucur = (t & 1) ? P.u1 : P.u0;
-        double* unext = (t & 1) ? P.u0 : P.u1;
+        const T* ucur = reinterpret_cast<const T*>((t & 1) ? P.u1 : P.u0);
+        T* unext = reinterpret_cast<T*>((t & 1) ? P.u0 : P.u1);
         double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         int4 tr = tr0;
         int4 tr1 = gw + nw < P.n_tasks ? __ldg(P.tasks + gw + nw) : make_int4(0, 0, 0, 0);
         for (int task = gw; task < P.n_tasks; task += nw) {
             const int4 tr2 = task + 2 * nw < P.n_tasks ? __ldg(P.tasks + task + 2 * nw) : make_int4(0, 0, 0, 0);
-            if (task + nw < P.n_tasks) issue_task(P, st, tr1, lane, false);   // one task ahead
+            if (task + nw < P.n_tasks) issue_task<T>(P, st, tr1, lane, false);   // one task ahead
             if (tr.w & kTaskPacked) {
-                if ((tr.w & 0xF) == 1) task_packed<1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
-                else if constexpr (RMAX >= 2) task_packed<2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
+                if ((tr.w & 0xF) == 1) task_packed<1, T>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
+                else if constexpr (RMAX >= 2) task_packed<2, T>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
             } else {
                 switch (tr.w & 0xF) {
-                    case 2: if constexpr (RMAX >= 2) task_full<2>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
-                    case 4: if constexpr (RMAX >= 4) task_full<4>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
-                    default: if constexpr (RMAX >= 8) task_full<8>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
+                    case 2: if constexpr (RMAX >= 2) task_full<2, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
+                    case 4: if constexpr (RMAX >= 4) task_full<4, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
+                    default: if constexpr (RMAX >= 8) task_full<8, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
                 }
             }
             tr = tr1;
@@ -329,7 +350,7 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_stream_
         }
         // this warp's first task of the next sweep, staged across the grid barrier: its operators are
         // constant and its lambda / x_s were written by this warp only (all lanes, before __syncwarp)
-        if (it + 1 < P.max_iter && gw < P.n_tasks) issue_task(P, st, tr0, lane, true);
+        if (it + 1 < P.max_iter && gw < P.n_tasks) issue_task<T>(P, st, tr0, lane, true);
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
 #pragma unroll
@@ -387,7 +408,8 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_stream_
                     }
                     if (stop || it == P.max_iter) {                // final sweep of this launch
                         double obj = 0.0;
-                        for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * __ldcg(P.x + P.obj_idx[j]);
+                        const T* xg = reinterpret_cast<const T*>(P.x);
+                        for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * (double)__ldcg(xg + P.obj_idx[j]);
                         c->res[0] = pres; c->res[1] = dres; c->res[2] = ep; c->res[3] = ed;
                         c->objective = obj;
                         c->iters = it;
@@ -419,13 +441,14 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_stream_
 // Partitioned mode, after the exchange-buffer allreduce of sweep t: the other ranks' boundary u into
 // this rank's ghost slots of the buffer sweep t+1 reads, then the termination test of sweep t on the
 // residual sums added in rank order (identical on every rank).  One launch of one CTA per 256 ghosts.
+template <class T>
 __global__ void part_import_kernel(DevProblem P) {
     DevCtrl* c = P.ctrl;
     if (*(volatile long long*)&c->stopped) return;
     const long long t = *(volatile long long*)&c->total;
-    double* dst = (t & 1) ? P.u0 : P.u1;                               // = unext of sweep t
+    T* dst = reinterpret_cast<T*>((t & 1) ? P.u0 : P.u1);               // = unext of sweep t
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_imp; i += gridDim.x * blockDim.x)
-        dst[P.ghost0 + i] = __ldcg(P.xbuf + P.imp[i]);
+        dst[P.ghost0 + i] = (T)__ldcg(P.xbuf + P.imp[i]);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         for (int r = 0; r < P.world; ++r)
@@ -435,7 +458,8 @@ __global__ void part_import_kernel(DevProblem P) {
         const int numeric = !(isfinite(s[0]) && isfinite(s[1]) && isfinite(s[2]) && isfinite(s[3]) && isfinite(s[4]));
         const int conv = P.test && (pres <= ep) && (dres <= ed);
         double obj = 0.0;                                              // this rank's share of c^T x
-        for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * __ldcg(P.x + P.obj_idx[j]);
+        const T* xg = reinterpret_cast<const T*>(P.x);
+        for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * (double)__ldcg(xg + P.obj_idx[j]);
         c->res[0] = pres; c->res[1] = dres; c->res[2] = ep; c->res[3] = ed;
         c->objective = obj;
         c->iters = c->iters + 1;
@@ -447,11 +471,15 @@ __global__ void part_import_kernel(DevProblem P) {
 }
 
 // ---- batch mode (config 4): (scenario, task) items over the one-scenario streaming layout ---------
-// Item i = scenario * n_tasks + task.  Per sweep every warp walks its items (skipping scenarios that
-// have stopped) with the same TMA pipeline and task code as the streaming kernel, on a view whose
-// iterate / solution / varying-operator pointers are offset to the item's scenario; the item's five
-// residual sums go to partial[scenario][task].  Grid barrier; then warp w decides scenarios w, w + nw,
-// ... (their partials summed in task order: deterministic), freezing converged ones; grid barrier.
+// The ACTIVE items of a sweep (tasks of scenarios not yet stopped, scenario-major, tasks in DFS order)
+// are cut into nw contiguous chunks, one per warp: a warp walks consecutive tasks of one scenario
+// (neighbouring subsystems: its u gathers hit lines the previous task fetched), with the same TMA
+// pipeline and task code as the streaming kernel on a view whose iterate / solution / varying-operator
+// pointers are offset to the scenario.  Residual sums accumulate in registers over a warp's RUN of
+// one scenario; the run's last item gets the warp-reduced sums in partial[scenario][task], its other
+// items exact zeros.  Grid barrier; then warp w decides scenarios w, w + nw, ... (partials summed in
+// task order: deterministic), freezing converged ones and setting the next sweep's active bits; grid
+// barrier.  As scenarios converge the chunks shrink, so the active work stays spread over every warp.
 __device__ __forceinline__ void grid_sync(unsigned long long* cnt, const unsigned long long target) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -463,30 +491,48 @@ __device__ __forceinline__ void grid_sync(unsigned long long* cnt, const unsigne
     __syncthreads();
 }
 
-__device__ __forceinline__ DevProblem batch_view(const DevProblem& P, const BatchProblem& B, const long long sc,
+template <class T>
+__device__ __forceinline__ DevProblem batch_view(const DevProblem& P, const BatchProblem& B, const int sc,
                                                  const int4 tr) {
     DevProblem Q = P;
     const size_t so = (size_t)sc * B.ns_stride;
-    Q.xl = P.xl + so;
-    Q.lam = P.lam + so;
-    Q.u0 = P.u0 + so;
-    Q.u1 = P.u1 + so;
-    Q.x = P.x + (size_t)sc * B.n_stride;
-    if (tr.w & kTaskVar) Q.abar = B.var_pool + (size_t)sc * B.vp_stride;
+    Q.xl = reinterpret_cast<T*>(P.xl) + so;
+    Q.lam = reinterpret_cast<T*>(P.lam) + so;
+    Q.u0 = reinterpret_cast<T*>(P.u0) + so;
+    Q.u1 = reinterpret_cast<T*>(P.u1) + so;
+    Q.x = reinterpret_cast<T*>(P.x) + (size_t)sc * B.n_stride;
+    if (tr.w & kTaskVar) Q.abar = reinterpret_cast<const T*>(B.var_pool) + (size_t)sc * B.vp_stride;
     return Q;
 }
 
-template <int RMAX>
+// next active scenario after sc (its bit set in the SMEM copy of the active mask), or -1
+__device__ __forceinline__ int next_active(const uint32_t* m, const int W, const int sc) {
+    int w = (sc + 1) >> 5;
+    if (w >= W) return -1;
+    uint32_t bits = m[w] & (0xffffffffu << ((sc + 1) & 31));
+    while (bits == 0) {
+        if (++w >= W) return -1;
+        bits = m[w];
+    }
+    return (w << 5) + __ffs(bits) - 1;
+}
+
+constexpr int kBatchMaskWords = kBatchMaxScen / 32;
+
+template <int RMAX, class T>
 __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_batch_kernel(DevProblem P, BatchProblem B) {
     constexpr int kWarps = StreamWarps<RMAX>::value;
+    constexpr int kStageBytes = Stg<T>::kBytes;
     extern __shared__ __align__(128) char sdyn[];
     __shared__ uint64_t sbar[kWarps][2];
-    __shared__ double inv_nu[kInvNu];
+    __shared__ T inv_nu[kInvNu];
+    __shared__ uint32_t s_mask[kBatchMaskWords];           // active scenarios of this sweep
+    __shared__ uint16_t s_wpre[kBatchMaskWords + 1];       // active scenarios before word w
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const long long gw = (long long)blockIdx.x * kWarps + wid, nw = (long long)gridDim.x * kWarps;
+    const int gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
     Stage st{sdyn + (size_t)wid * 2 * kStageBytes, sbar[wid], 0u, 0u};
-    double* dsm = reinterpret_cast<double*>(sdyn + (size_t)kWarps * 2 * kStageBytes) + (size_t)wid * 32 * RMAX;
-    for (int i = threadIdx.x; i < kInvNu; i += blockDim.x) inv_nu[i] = i > 0 ? 1.0 / (double)i : 0.0;
+    T* dsm = reinterpret_cast<T*>(sdyn + (size_t)kWarps * 2 * kStageBytes) + (size_t)wid * 32 * RMAX;
+    for (int i = threadIdx.x; i < kInvNu; i += blockDim.x) inv_nu[i] = i > 0 ? T(1) / (T)i : T(0);
     if (lane == 0) {
         mbar_init(st.bar);
         mbar_init(st.bar + 1);
@@ -494,54 +540,94 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_batch_k
     }
     __syncthreads();
     const long long total0 = *(volatile long long*)&P.ctrl->total;
-    const int NT = B.n_tasks;
-    const long long NI = (long long)B.n_scen * NT;
+    const int NT = B.n_tasks, W = (B.n_scen + 31) >> 5;
     const volatile int32_t* stopped = B.stopped;
     unsigned long long bars = 0, seen = 0;
     long long it = 0;
     while (it < P.max_iter) {
         const long long t = total0 + it;
-        const double* ucur = (t & 1) ? P.u1 : P.u0;
-        double* unext = (t & 1) ? P.u0 : P.u1;
-        long long item = gw;
-        while (item < NI && stopped[item / NT]) item += nw;
-        int4 tr = make_int4(0, 0, 0, 0);
-        if (item < NI) {
-            tr = __ldg(P.tasks + item % NT);
-            issue_task(batch_view(P, B, item / NT, tr), st, tr, lane, true);
+        const T* ucur = reinterpret_cast<const T*>((t & 1) ? P.u1 : P.u0);
+        T* unext = reinterpret_cast<T*>((t & 1) ? P.u0 : P.u1);
+        const uint32_t* mcur = B.amask + (size_t)(it & 1) * W;
+        // the active set of this sweep into SMEM (warp 0), and the next sweep's mask cleared (CTA 0)
+        if (wid == 0) {
+            int run = 0;
+            for (int w0 = 0; w0 < W; w0 += 32) {
+                const int w = w0 + lane;
+                const uint32_t m = w < W ? __ldcg(mcur + w) : 0u;
+                int c = __popc(m), inc = c;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int y = __shfl_up_sync(kFull, inc, off);
+                    if (lane >= off) inc += y;
+                }
+                if (w < W) { s_mask[w] = m; s_wpre[w] = (uint16_t)(run + inc - c); }
+                run += __shfl_sync(kFull, inc, 31);
+            }
+            if (lane == 0) s_wpre[W] = (uint16_t)run;
         }
-        while (item < NI) {
-            long long nxt = item + nw;
-            while (nxt < NI && stopped[nxt / NT]) nxt += nw;
-            int4 tr1 = make_int4(0, 0, 0, 0);
-            if (nxt < NI) {
-                tr1 = __ldg(P.tasks + nxt % NT);
-                issue_task(batch_view(P, B, nxt / NT, tr1), st, tr1, lane, false);
+        if (blockIdx.x == 0)
+            for (int w = threadIdx.x; w < W; w += blockDim.x) B.amask[(size_t)((it + 1) & 1) * W + w] = 0u;
+        __syncthreads();
+        const int NA = s_wpre[W];
+        const long long items = (long long)NA * NT;
+        const long long C = (items + nw - 1) / nw;
+        long long a0 = (long long)gw * C, a1 = a0 + C < items ? a0 + C : items;
+        if (a0 < a1) {
+            // scenario of active rank a0 / NT: its mask word by binary search on the prefix, then the bit
+            const int ar = (int)(a0 / NT);
+            int tk = (int)(a0 - (long long)ar * NT);
+            int lo = 0, hi = W - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_wpre[mid] <= ar) lo = mid; else hi = mid - 1;
             }
-            const long long sc = item / NT;
-            const size_t so = (size_t)sc * B.ns_stride;
-            const DevProblem Q = batch_view(P, B, sc, tr);
+            int sc = (lo << 5) + (int)__fns(s_mask[lo], 0, ar - s_wpre[lo] + 1);
+            int4 tr = __ldg(P.tasks + tk);
+            issue_task<T>(batch_view<T>(P, B, sc, tr), st, tr, lane, true);
             double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            if ((tr.w & 0xF) == 1) task_packed<1>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
-            else if constexpr (RMAX >= 2) task_packed<2>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+            for (long long a = a0; a < a1; ++a) {
+                // the next item: the next task of this scenario or task 0 of the next active one
+                int sc1 = sc, tk1 = tk + 1;
+                if (tk1 == NT) { tk1 = 0; sc1 = next_active(s_mask, W, sc); }
+                const bool more = a + 1 < a1;
+                int4 tr1 = make_int4(0, 0, 0, 0);
+                if (more) {
+                    tr1 = __ldg(P.tasks + tk1);
+                    issue_task<T>(batch_view<T>(P, B, sc1, tr1), st, tr1, lane, false);
+                }
+                const size_t so = (size_t)sc * B.ns_stride;
+                const DevProblem Q = batch_view<T>(P, B, sc, tr);
+                if ((tr.w & 0xF) == 1) task_packed<1, T>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+                else if constexpr (RMAX >= 2) task_packed<2, T>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+                double* pp = B.partial + ((size_t)sc * NT + tk) * 8;
+                if (more && sc1 == sc) {                       // the run goes on: this item's slot holds 0
+                    if (lane < 5) pp[lane] = 0.0;
+                } else {                                       // end of the run: its sums
 #pragma unroll
-            for (int k = 0; k < 5; ++k) {
+                    for (int k = 0; k < 5; ++k) {
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(kFull, acc[k], off);
+                        for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(kFull, acc[k], off);
+                    }
+                    if (lane < 5) {
+                        double v = acc[0];
+#pragma unroll
+                        for (int k = 1; k < 5; ++k) v = lane == k ? acc[k] : v;
+                        pp[lane] = v;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) acc[k] = 0.0;
+                }
+                sc = sc1;
+                tk = tk1;
+                tr = tr1;
             }
-            if (lane < 5) {
-                double a = acc[0];
-#pragma unroll
-                for (int k = 1; k < 5; ++k) a = lane == k ? acc[k] : a;
-                B.partial[(size_t)item * 8 + lane] = a;
-            }
-            item = nxt;
-            tr = tr1;
         }
         grid_sync(B.cnt, (++bars) * gridDim.x);
         // per-scenario (termination)
+        uint32_t* mnext = B.amask + (size_t)((it + 1) & 1) * W;
         unsigned long long active = 0;
-        for (long long sc = gw; sc < B.n_scen; sc += nw) {
+        for (int sc = gw; sc < B.n_scen; sc += nw) {
             if (stopped[sc]) continue;
             double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
             for (int k2 = lane; k2 < NT; k2 += 32) {
@@ -567,11 +653,12 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_batch_k
                 R.status = conv ? 1 : num ? 3 : (fin ? 2 : 0);
                 if (fin) {
                     double obj = 0.0;
-                    const double* xs = P.x + (size_t)sc * B.n_stride;
-                    for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * __ldcg(xs + P.obj_idx[j]);
+                    const T* xs = reinterpret_cast<const T*>(P.x) + (size_t)sc * B.n_stride;
+                    for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * (double)__ldcg(xs + P.obj_idx[j]);
                     R.objective = obj;
                 }
                 if (conv || num) B.stopped[sc] = 1;
+                else atomicOr(mnext + (sc >> 5), 1u << (sc & 31));
             }
             active += (conv || num) ? 0ULL : 1ULL;
         }
@@ -593,15 +680,36 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_batch_k
     }
 }
 
+// Before each batch launch: the active mask of its first sweep from the stopped flags (scenarios that
+// converged in an earlier launch stay frozen); the other parity cleared.
+__global__ void batch_mask_kernel(BatchProblem B) {
+    const int W = (B.n_scen + 31) >> 5;
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) {
+        uint32_t m = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int sc = (w << 5) + b;
+            if (sc < B.n_scen && !B.stopped[sc]) m |= 1u << b;
+        }
+        B.amask[w] = m;
+        B.amask[W + w] = 0u;
+    }
+}
+
 // a3 for every scenario: x_s = x0 (template slots), lambda = 0, u = x0; decisions cleared.
+template <class T>
 __global__ void reset_batch_kernel(DevProblem P, BatchProblem B) {
     const size_t n = (size_t)B.n_scen * B.ns_stride;
+    const T* x0p = reinterpret_cast<const T*>(P.x0);
+    T* xl = reinterpret_cast<T*>(P.xl);
+    T* lam = reinterpret_cast<T*>(P.lam);
+    T* u0 = reinterpret_cast<T*>(P.u0);
+    T* u1 = reinterpret_cast<T*>(P.u1);
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const double x0 = P.x0[i % B.ns_stride];
-        P.xl[i] = x0;
-        P.lam[i] = 0.0;
-        P.u0[i] = x0;
-        P.u1[i] = 0.0;
+        const T x0 = x0p[i % B.ns_stride];
+        xl[i] = x0;
+        lam[i] = T(0);
+        u0[i] = x0;
+        u1[i] = T(0);
     }
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < (size_t)B.n_scen; i += (size_t)gridDim.x * blockDim.x) {
         ScenResult& R = B.res[i];
@@ -615,14 +723,15 @@ __global__ void reset_batch_kernel(DevProblem P, BatchProblem B) {
 }
 
 // a3: reset the iterate to the initial point: x_s = x0, lambda = 0, u = x0.
+template <class T>
 __global__ void reset_kernel(DevProblem P) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < P.n_slots) {
-        const double x0 = P.x0[i];
-        P.xl[i] = x0;
-        P.lam[i] = 0.0;
-        P.u0[i] = x0;
-        P.u1[i] = 0.0;
+        const T x0 = reinterpret_cast<const T*>(P.x0)[i];
+        reinterpret_cast<T*>(P.xl)[i] = x0;
+        reinterpret_cast<T*>(P.lam)[i] = T(0);
+        reinterpret_cast<T*>(P.u0)[i] = x0;
+        reinterpret_cast<T*>(P.u1)[i] = T(0);
     }
     if (i == 0) {
         P.ctrl->arrive = 0; P.ctrl->flag = 0; P.ctrl->total = 0; P.ctrl->iters = 0; P.ctrl->trace_rows = 0;
@@ -632,28 +741,33 @@ __global__ void reset_kernel(DevProblem P) {
 
 }  // namespace
 
-static const void* stream_kernel_for(int rmax) {
-    return rmax <= 1 ? (const void*)admm_stream_kernel<1>
-         : rmax <= 2 ? (const void*)admm_stream_kernel<2>
-         : rmax <= 4 ? (const void*)admm_stream_kernel<4>
-                     : (const void*)admm_stream_kernel<8>;
+template <class T>
+static const void* stream_kernel_t(int rmax) {
+    return rmax <= 1 ? (const void*)admm_stream_kernel<1, T>
+         : rmax <= 2 ? (const void*)admm_stream_kernel<2, T>
+         : rmax <= 4 ? (const void*)admm_stream_kernel<4, T>
+                     : (const void*)admm_stream_kernel<8, T>;
+}
+static const void* stream_kernel_for(int rmax, int esz) {
+    return esz == 4 ? stream_kernel_t<float>(rmax) : stream_kernel_t<double>(rmax);
 }
 
-static int stream_smem(int rmax) {
+static int stream_smem(int rmax, int esz) {
     const int r = rmax <= 1 ? 1 : rmax <= 2 ? 2 : rmax <= 4 ? 4 : 8;
-    return (rmax <= 2 ? kStreamWarps : kStreamWarpsWide) * (2 * kStageBytes + 8 * 32 * r);
+    const int stage = esz == 4 ? Stg<float>::kBytes : Stg<double>::kBytes;
+    return (rmax <= 2 ? kStreamWarps : kStreamWarpsWide) * (2 * stage + esz * 32 * r);
 }
 
 int stream_block(int rmax) { return 32 * (rmax <= 2 ? kStreamWarps : kStreamWarpsWide); }
 
-lopf_status query_grid(int rmax, int* grid, std::string& err) {
+lopf_status query_grid(int rmax, int esz, int* grid, std::string& err) {
     int dev = 0, sms = 0, per = 0;
-    const void* k = stream_kernel_for(rmax);
+    const void* k = stream_kernel_for(rmax, esz);
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem(rmax));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem(rmax, esz));
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, stream_block(rmax), stream_smem(rmax));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, stream_block(rmax), stream_smem(rmax, esz));
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     if (per < 1) { err = "streaming kernel cannot be resident (occupancy 0)"; return LOPF_E_CUDA; }
     *grid = sms * per;
@@ -667,23 +781,28 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
     if (e == cudaSuccess && P.max_iter > 0) {
         DevProblem Q = P;
         void* args[] = {&Q};
-        e = cudaLaunchCooperativeKernel(stream_kernel_for(P.rmax), dim3(grid), dim3(stream_block(P.rmax)), args,
-                                        stream_smem(P.rmax), s);
+        e = cudaLaunchCooperativeKernel(stream_kernel_for(P.rmax, P.esz), dim3(grid), dim3(stream_block(P.rmax)), args,
+                                        stream_smem(P.rmax, P.esz), s);
     }
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;
 }
 
-static const void* batch_kernel_for(int rmax) {
-    return rmax <= 1 ? (const void*)admm_batch_kernel<1> : (const void*)admm_batch_kernel<2>;
+static const void* batch_kernel_for(int rmax, int esz) {
+    if (esz == 4) return rmax <= 1 ? (const void*)admm_batch_kernel<1, float> : (const void*)admm_batch_kernel<2, float>;
+    return rmax <= 1 ? (const void*)admm_batch_kernel<1, double> : (const void*)admm_batch_kernel<2, double>;
 }
 
 lopf_status launch_batch(const DevProblem& P, const BatchProblem& B, int grid, void* stream, std::string& err) {
     cudaStream_t s = (cudaStream_t)stream;
-    const void* k = batch_kernel_for(P.rmax);
-    const int smem = stream_smem(P.rmax);
+    const void* k = batch_kernel_for(P.rmax, P.esz);
+    const int smem = stream_smem(P.rmax, P.esz);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) e = cudaMemsetAsync(B.cnt, 0, 2 * sizeof(unsigned long long), s);
+    if (e == cudaSuccess) {
+        batch_mask_kernel<<<((B.n_scen + 31) / 32 + 255) / 256, 256, 0, s>>>(B);
+        e = cudaGetLastError();
+    }
     if (e == cudaSuccess && P.max_iter > 0) {
         DevProblem Q = P;
         BatchProblem C = B;
@@ -695,7 +814,8 @@ lopf_status launch_batch(const DevProblem& P, const BatchProblem& B, int grid, v
 }
 
 lopf_status launch_reset_batch(const DevProblem& P, const BatchProblem& B, void* stream, std::string& err) {
-    reset_batch_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(P, B);
+    if (P.esz == 4) reset_batch_kernel<float><<<1184, 256, 0, (cudaStream_t)stream>>>(P, B);
+    else reset_batch_kernel<double><<<1184, 256, 0, (cudaStream_t)stream>>>(P, B);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;
@@ -703,7 +823,8 @@ lopf_status launch_reset_batch(const DevProblem& P, const BatchProblem& B, void*
 
 lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err) {
     const int nb = P.n_imp > 0 ? (P.n_imp + 255) / 256 : 1;
-    part_import_kernel<<<nb < 148 ? nb : 148, 256, 0, (cudaStream_t)stream>>>(P);
+    if (P.esz == 4) part_import_kernel<float><<<nb < 148 ? nb : 148, 256, 0, (cudaStream_t)stream>>>(P);
+    else part_import_kernel<double><<<nb < 148 ? nb : 148, 256, 0, (cudaStream_t)stream>>>(P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;
@@ -712,7 +833,8 @@ lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& e
 lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err) {
     cudaStream_t s = (cudaStream_t)stream;
     const int nb = (P.n_slots + 255) / 256;
-    reset_kernel<<<nb > 0 ? nb : 1, 256, 0, s>>>(P);
+    if (P.esz == 4) reset_kernel<float><<<nb > 0 ? nb : 1, 256, 0, s>>>(P);
+    else reset_kernel<double><<<nb > 0 ? nb : 1, 256, 0, s>>>(P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;

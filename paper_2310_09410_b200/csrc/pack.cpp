@@ -24,6 +24,11 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
                            std::string& err, const PartSpec* part, int32_t rank) {
     L = Layout();
     L.kernel = 1;
+    // element size of operators / iterate / globals (fp32 variant: reading F1); the SMEM stage keeps its
+    // byte budget, so an fp32 task packs twice the operator entries; bulk copies stay 16-byte aligned
+    const int esz = opt.precision == 32 ? 4 : 8;
+    const int budget = kPackBudget * 8 / esz, al = 16 / esz;
+    L.esz = esz;
     // partitioned mode: only this rank's subsystems; remote copies its globals read become ghost slots
     auto local_sub = [&](int64_t s) { return !part || part->sub_owner[s] == rank; };
     // ---- tasks ---------------------------------------------------------------------------------
@@ -55,7 +60,7 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
             if (!cur.subs.empty()) {
                 cur.R = fill > 32 ? 2 : 1;
                 cur.used = (fill + 3) & ~3;                      // slots the bulk copies move (16-byte multiples)
-                cur.plen = (cur.plen + 1) & ~1;
+                cur.plen = (cur.plen + al - 1) & ~(al - 1);
                 tasks.push_back(std::move(cur));
             }
             cur = T{1, 0, 0, 0, true, false, {}, {}, {}};
@@ -71,12 +76,12 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
                 tasks.push_back(T{R, ns, 0, 32 * R, false, false, {s}, {0}, {0}});
                 continue;
             }
-            if (ps > kPackBudget) {                              // block read from HBM, task of its own
+            if (ps > budget) {                                   // block read from HBM, task of its own
                 close();
-                tasks.push_back(T{ns <= 32 ? 1 : 2, ns, (ps + 1) & ~1, (ns + 3) & ~3, true, true, {s}, {0}, {0}});
+                tasks.push_back(T{ns <= 32 ? 1 : 2, ns, (ps + al - 1) & ~(al - 1), (ns + 3) & ~3, true, true, {s}, {0}, {0}});
                 continue;
             }
-            if (fill + ns > 32 * kTaskHalves || cur.plen + ps > kPackBudget) close();
+            if (fill + ns > 32 * kTaskHalves || cur.plen + ps > budget) close();
             cur.subs.push_back(s);
             cur.base.push_back(fill);                            // rows may straddle the two halves
             cur.poff.push_back(cur.plen);
@@ -145,18 +150,18 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     L.off_info = take(4 * NS);
     L.off_g = take(4 * NS);
     L.off_nbr = take(16 * NS);
-    L.off_bbar = take(8 * NS);
-    L.off_xl = take(8 * NS);
-    L.off_lam = take(8 * NS);
-    L.off_u0 = take(8 * NS);
-    L.off_u1 = take(8 * NS);
-    L.off_x0 = take(8 * NS);
-    L.off_gpar = take(16 * NG);
-    L.off_gcost = take(8 * NG);
+    L.off_bbar = take(esz * NS);
+    L.off_xl = take(esz * NS);
+    L.off_lam = take(esz * NS);
+    L.off_u0 = take(esz * NS);
+    L.off_u1 = take(esz * NS);
+    L.off_x0 = take(esz * NS);
+    L.off_gpar = take(2 * esz * NG);
+    L.off_gcost = take(esz * NG);
     L.off_segptr = take(4 * (NG + 1));
     L.off_segslot = take(4 * NC);
-    L.off_x = take(8 * NG);
-    L.off_abar = take(8 * (size_t)pool);
+    L.off_x = take(esz * NG);
+    L.off_abar = take(esz * (size_t)pool);
     L.off_partial = take(8 * 8 * (size_t)max_grid);
     L.off_ctrl = take(sizeof(DevCtrl));
     L.off_trace = take(8 * 5 * (size_t)L.trace_cap);
@@ -176,8 +181,13 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     int32_t* info = (int32_t*)at(L.off_info);
     int32_t* gs = (int32_t*)at(L.off_g);
     int4* nbr = (int4*)at(L.off_nbr);
-    double* bbar = (double*)at(L.off_bbar);
-    double* abar = (double*)at(L.off_abar);
+    // (T) arrays: values computed in fp64, stored as T (fp32: each rounded once to nearest)
+    auto put = [esz](uint8_t* base, size_t i, double v) {
+        if (esz == 8) reinterpret_cast<double*>(base)[i] = v;
+        else reinterpret_cast<float*>(base)[i] = (float)v;
+    };
+    uint8_t* bbar = at(L.off_bbar);
+    uint8_t* abar = at(L.off_abar);
     for (size_t i = 0; i < NS; ++i) { gs[i] = -1; nbr[i] = make_int4(0, 0, 0, 0); }
 
     L.slot_of_copy.assign(NC, -1);
@@ -205,14 +215,14 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
                 info[slot] = base | kInfoValid | (has_b ? kInfoBbar : 0) | (ns << kInfoNsShift) |
                              (tk.packed ? tk.poff[j] << kInfoPoffShift : 0);
                 gs[slot] = P.copy_global[copy];
-                bbar[slot] = P.bbar[copy];
+                put(bbar, slot, P.bbar[copy]);
                 if (tk.packed) {                  // upper triangle, row-major: (r, k >= r); then b-bar
-                    double* dst = abar + trec[t].y + tk.poff[j];
-                    for (int k = r; k < ns; ++k) dst[r * ns - r * (r - 1) / 2 + (k - r)] = Ab[(size_t)r * ns + k];
-                    if (has_b) dst[ns * (ns + 1) / 2 + r] = P.bbar[copy];
+                    const size_t dst = (size_t)trec[t].y + tk.poff[j];
+                    for (int k = r; k < ns; ++k) put(abar, dst + r * ns - r * (r - 1) / 2 + (k - r), Ab[(size_t)r * ns + k]);
+                    if (has_b) put(abar, dst + ns * (ns + 1) / 2 + r, P.bbar[copy]);
                 } else {                          // lane (slot) r computes row r: sum_k Abar[r][k] d[k]
                     for (int k = 0; k < ns; ++k)
-                        abar[(size_t)trec[t].y + (size_t)k * P32 + base + r] = Ab[(size_t)r * ns + k];
+                        put(abar, (size_t)trec[t].y + (size_t)k * P32 + base + r, Ab[(size_t)r * ns + k]);
                 }
             }
         }
@@ -249,11 +259,12 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
             nbr[slot] = make_int4(v[0], v[1], v[2], v[3]);
         }
     }
-    double2* gbnd = (double2*)at(L.off_gpar);
-    double* gcost = (double*)at(L.off_gcost);
+    uint8_t* gbnd = at(L.off_gpar);                   // {lo, hi} pairs (IEEE +-inf kept in fp32 too)
+    uint8_t* gcost = at(L.off_gcost);
     for (int64_t i = 0; i < P.n; ++i) {
-        gbnd[i] = make_double2(P.lo[i], P.hi[i]);
-        gcost[i] = P.c[i] / opt.rho;
+        put(gbnd, 2 * i, P.lo[i]);
+        put(gbnd, 2 * i + 1, P.hi[i]);
+        put(gcost, i, P.c[i] / opt.rho);
     }
     std::memcpy(at(L.off_objidx), obj_idx.data(), 4 * obj_idx.size());
     std::memcpy(at(L.off_objc), obj_c.data(), 8 * obj_c.size());
@@ -264,15 +275,15 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
 // Initial iterate (Algorithm 1 line 1): x_s = x0, lambda = 0, u = x_s - lambda/rho = x0.
 void init_state_image(const Canon& P, Layout& L) {
     uint8_t* img = L.image.data();
-    double* xl = (double*)(img + L.off_xl);
-    double* lam = (double*)(img + L.off_lam);
-    double* u0 = (double*)(img + L.off_u0);
-    double* u1 = (double*)(img + L.off_u1);
-    double* x0 = (double*)(img + L.off_x0);
-    for (int64_t i = 0; i < L.n_slots; ++i) xl[i] = lam[i] = u0[i] = u1[i] = x0[i] = 0.0;
+    const size_t e = (size_t)L.esz;
+    for (size_t off : {L.off_xl, L.off_lam, L.off_u0, L.off_u1, L.off_x0}) std::memset(img + off, 0, e * L.n_slots);
     for (int64_t k = 0; k < P.nc; ++k) {
         const int32_t s = L.slot_of_copy[k];
-        if (s >= 0) xl[s] = u0[s] = x0[s] = P.x0[k];          // (partitioned: own copies and ghosts)
+        if (s < 0) continue;                                   // (partitioned: own copies and ghosts)
+        for (size_t off : {L.off_xl, L.off_u0, L.off_x0}) {
+            if (e == 8) reinterpret_cast<double*>(img + off)[s] = P.x0[k];
+            else reinterpret_cast<float*>(img + off)[s] = (float)P.x0[k];
+        }
     }
     std::memset(img + L.off_ctrl, 0, sizeof(DevCtrl));
 }

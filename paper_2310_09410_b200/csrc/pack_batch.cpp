@@ -34,12 +34,14 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
         var_off[t] = VP;
         trec[t].y = (int)VP;
         trec[t].w |= kTaskVar;
-        VP += trec[t].z;                                     // block length (doubles, even)
+        VP += trec[t].z;                                     // block length (entries, 16-byte multiple)
     }
     if (VP * NSC > ((int64_t)1 << 40)) { err = "batch: per-scenario operators too large"; return LOPF_E_ARG; }
 
     L = Layout();
     L.kernel = 3;
+    const size_t e = (size_t)T.esz;                          // (T) element size (fp32 variant: reading F1)
+    L.esz = T.esz;
     L.n_scen = (int32_t)NSC;
     L.n_tasks = NT;
     L.n_slots = NS;
@@ -55,25 +57,26 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     L.off_info = take(4 * NS);
     L.off_g = take(4 * NS);
     L.off_nbr = take(16 * NS);
-    L.off_bbar = take(8 * NS);
-    L.off_x0 = take(8 * NS);
-    L.off_gpar = take(16 * NG);
-    L.off_gcost = take(8 * NG);
+    L.off_bbar = take(e * NS);
+    L.off_x0 = take(e * NS);
+    L.off_gpar = take(2 * e * NG);
+    L.off_gcost = take(e * NG);
     L.off_segptr = take(4 * (NG + 1));
     L.off_segslot = take(4 * P.nc);
-    L.off_abar = take(8 * (size_t)T.abar_doubles);
+    L.off_abar = take(e * (size_t)T.abar_doubles);
     L.off_objidx = take(4 * (size_t)T.n_obj);
     L.off_objc = take(8 * (size_t)T.n_obj);
-    L.off_bvar = take(8 * (size_t)VP * NSC);
-    L.off_xl = take(8 * (size_t)NS * NSC);
-    L.off_lam = take(8 * (size_t)NS * NSC);
-    L.off_u0 = take(8 * (size_t)NS * NSC);
-    L.off_u1 = take(8 * (size_t)NS * NSC);
-    L.off_x = take(8 * (size_t)NG * NSC);
+    L.off_bvar = take(e * (size_t)VP * NSC);
+    L.off_xl = take(e * (size_t)NS * NSC);
+    L.off_lam = take(e * (size_t)NS * NSC);
+    L.off_u0 = take(e * (size_t)NS * NSC);
+    L.off_u1 = take(e * (size_t)NS * NSC);
+    L.off_x = take(e * (size_t)NG * NSC);
     L.off_bres = take(sizeof(ScenResult) * (size_t)NSC);
     L.off_bstop = take(4 * (size_t)NSC);
     L.off_bpart = take(8 * 8 * (size_t)NT * NSC);
     L.off_bcnt = take(8 * 4);
+    L.off_bmask = take(4 * 2 * (((size_t)NSC + 31) / 32));
     L.off_partial = take(8 * 8 * 4096);
     L.off_ctrl = take(sizeof(DevCtrl));
     L.off_trace = take(8 * 5);
@@ -85,25 +88,29 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     std::memcpy(img + L.off_info, ti + T.off_info, 4 * NS);
     std::memcpy(img + L.off_g, ti + T.off_g, 4 * NS);
     std::memcpy(img + L.off_nbr, ti + T.off_nbr, 16 * NS);
-    std::memcpy(img + L.off_bbar, ti + T.off_bbar, 8 * NS);
-    std::memcpy(img + L.off_x0, ti + T.off_x0, 8 * NS);
-    std::memcpy(img + L.off_gpar, ti + T.off_gpar, 16 * NG);
-    std::memcpy(img + L.off_gcost, ti + T.off_gcost, 8 * NG);
+    std::memcpy(img + L.off_bbar, ti + T.off_bbar, e * NS);
+    std::memcpy(img + L.off_x0, ti + T.off_x0, e * NS);
+    std::memcpy(img + L.off_gpar, ti + T.off_gpar, 2 * e * NG);
+    std::memcpy(img + L.off_gcost, ti + T.off_gcost, e * NG);
     std::memcpy(img + L.off_segptr, ti + T.off_segptr, 4 * (NG + 1));
     std::memcpy(img + L.off_segslot, ti + T.off_segslot, 4 * P.nc);
-    std::memcpy(img + L.off_abar, ti + T.off_abar, 8 * (size_t)T.abar_doubles);
+    std::memcpy(img + L.off_abar, ti + T.off_abar, e * (size_t)T.abar_doubles);
     std::memcpy(img + L.off_objidx, ti + T.off_objidx, 4 * (size_t)T.n_obj);
     std::memcpy(img + L.off_objc, ti + T.off_objc, 8 * (size_t)T.n_obj);
     // per-scenario operator blocks: the template block with each load subsystem's triangle and b-bar
     // replaced by the scenario's (same packing, so the per-slot metadata stays valid)
-    const double* tpool = (const double*)(ti + T.off_abar);
-    double* vpool = (double*)(img + L.off_bvar);
+    const uint8_t* tpool = ti + T.off_abar;
+    uint8_t* vpool = img + L.off_bvar;
+    auto put = [e](uint8_t* base, size_t i, double v) {
+        if (e == 8) reinterpret_cast<double*>(base)[i] = v;
+        else reinterpret_cast<float*>(base)[i] = (float)v;
+    };
     for (int64_t t = 0; t < NT; ++t) {
         if (var_off[t] < 0) continue;
         const int4 tr = T.trec[t];
         for (int64_t sc = 0; sc < NSC; ++sc) {
-            double* dst = vpool + (size_t)sc * VP + var_off[t];
-            std::memcpy(dst, tpool + tr.y, 8 * (size_t)tr.z);
+            const size_t dst = (size_t)sc * VP + var_off[t];
+            std::memcpy(vpool + e * dst, tpool + e * (size_t)tr.y, e * (size_t)tr.z);
             for (int32_t j = T.tsub_ptr[t]; j < T.tsub_ptr[t + 1]; ++j) {
                 const int64_t s = T.tsub_s[j];
                 const int32_t v = bo.vidx[s];
@@ -111,13 +118,13 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
                 const int ns = P.n_s[s];
                 const double* A = &bo.abar[(size_t)sc * bo.VA + bo.va_off[v]];
                 const double* b = &bo.bbar[(size_t)sc * bo.VB + bo.vb_off[v]];
-                double* blk = dst + T.tsub_poff[j];
+                const size_t blk = dst + T.tsub_poff[j];
                 bool has_b = false;
                 for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) has_b |= P.bbar[k] != 0.0;
                 for (int r = 0; r < ns; ++r)
-                    for (int k = r; k < ns; ++k) blk[r * ns - r * (r - 1) / 2 + (k - r)] = A[(size_t)r * ns + k];
+                    for (int k = r; k < ns; ++k) put(vpool, blk + r * ns - r * (r - 1) / 2 + (k - r), A[(size_t)r * ns + k]);
                 if (has_b)
-                    for (int r = 0; r < ns; ++r) blk[ns * (ns + 1) / 2 + r] = b[r];
+                    for (int r = 0; r < ns; ++r) put(vpool, blk + ns * (ns + 1) / 2 + r, b[r]);
             }
         }
     }

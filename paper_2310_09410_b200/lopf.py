@@ -44,7 +44,7 @@ class Network(C.Structure):
 class Options(C.Structure):
     _fields_ = [("rho", _f64), ("eps_rel", _f64), ("max_iter", _i64), ("trace_every", _i32), ("trace_cap", _i32),
                 ("single", _i32), ("kernel", _i32), ("block_threads", _i32), ("max_ctas", _i32), ("grid_cap", _i32),
-                ("reserved", _i32 * 3)]
+                ("reserved", _i32 * 2), ("precision", _i32)]
 
 
 class Sizes(C.Structure):
@@ -172,7 +172,9 @@ class Lopf:
     @classmethod
     def setup(cls, feeder, rho: float = 100.0, eps_rel: float = 1e-3, max_iter: int = 1_000_000,
               trace_every: int = 0, trace_cap: int = 4096, single: bool = False, kernel: int = 0,
-              grid_cap: int = 0, max_ctas: int = 0, diag_profile: bool = False, diag_skip: int = 0) -> "Lopf":
+              grid_cap: int = 0, max_ctas: int = 0, diag_profile: bool = False, diag_skip: int = 0,
+              precision: int = 64) -> "Lopf":
+        """lopf_setup; precision 32 selects the fp32 variant (the paper's GPU precision)."""
         lib = load_library()
         o = Options()
         _check(lib.lopf_options_default(C.byref(o)), "lopf_options_default")
@@ -180,6 +182,7 @@ class Lopf:
         o.trace_every, o.trace_cap, o.single, o.kernel = int(trace_every), int(trace_cap), int(bool(single)), int(kernel)
         o.grid_cap, o.max_ctas = int(grid_cap), int(max_ctas)
         o.reserved[0], o.reserved[1] = int(bool(diag_profile)), int(diag_skip)
+        o.precision = int(precision)
         net, keep = _network(feeder)
         h = _vp()
         _check(lib.lopf_setup(C.byref(net), C.byref(o), C.byref(h)), "lopf_setup")
@@ -187,12 +190,14 @@ class Lopf:
         return cls(h.value, o)
 
     @classmethod
-    def setup_batch(cls, feeder, load_scale, rho: float = 100.0, eps_rel: float = 1e-3, max_iter: int = 1_000_000) -> "Lopf":
+    def setup_batch(cls, feeder, load_scale, rho: float = 100.0, eps_rel: float = 1e-3, max_iter: int = 1_000_000,
+                    precision: int = 64) -> "Lopf":
         """lopf_setup_batch: load_scale [n_scen, n_load] (> 0) scales every load's (a, b) per scenario."""
         lib = load_library()
         o = Options()
         _check(lib.lopf_options_default(C.byref(o)), "lopf_options_default")
         o.rho, o.eps_rel, o.max_iter = float(rho), float(eps_rel), int(max_iter)
+        o.precision = int(precision)
         net, keep = _network(feeder)
         sc = np.ascontiguousarray(load_scale, dtype=np.float64)
         if sc.ndim != 2 or sc.shape[1] != feeder.n_load:
@@ -204,12 +209,13 @@ class Lopf:
 
     @classmethod
     def setup_part(cls, feeder, rank: int, world: int, bus_owner=None, rho: float = 100.0, eps_rel: float = 1e-3,
-                   max_iter: int = 1_000_000) -> "Lopf":
+                   max_iter: int = 1_000_000, precision: int = 64) -> "Lopf":
         """lopf_setup_part: this rank's share of a feeder partitioned over `world` ranks (config 5)."""
         lib = load_library()
         o = Options()
         _check(lib.lopf_options_default(C.byref(o)), "lopf_options_default")
         o.rho, o.eps_rel, o.max_iter, o.kernel = float(rho), float(eps_rel), int(max_iter), 1
+        o.precision = int(precision)
         net, keep = _network(feeder)
         own = None if bus_owner is None else np.ascontiguousarray(bus_owner, dtype=np.int32)
         h = _vp()

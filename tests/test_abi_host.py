@@ -24,7 +24,7 @@ def test_exports_every_declared_symbol():
     assert len(names) >= 20
     for n in sorted(names):
         assert hasattr(lib, n), n
-    assert lib.lopf_abi_version() == 1
+    assert lib.lopf_abi_version() == 2
 
 
 @pytest.mark.parametrize("make", [lambda: fg.make_feeder("13"), lambda: fg.make_feeder("123"), fx.four_bus,
@@ -145,3 +145,17 @@ def test_kernel_selection():
     assert Lopf.setup(fg.make_feeder("123"), kernel=1).sizes.kernel == 1
     with pytest.raises(LopfError):
         Lopf.setup(fg.make_feeder("8500"), kernel=2, max_ctas=16)        # does not fit 16 CTAs
+
+
+def test_precision_option():
+    """fp32 variant (reading F1): selects the streaming layout, halves the (T) bytes of the byte model;
+    an unknown precision or fp32 on the fp64-only resident kernel is LOPF_E_ARG."""
+    f = fg.make_feeder("123")
+    s64 = Lopf.setup(f, kernel=1).sizes
+    s32 = Lopf.setup(f, precision=32).sizes
+    assert s32.kernel == 1 and s32.device_bytes < s64.device_bytes
+    int_bytes = 4 * (2 * s64.n_copies + s64.n + 1)
+    assert (s32.alg_bytes - int_bytes) * 2 == s64.alg_bytes - int_bytes
+    for bad in (dict(precision=16), dict(precision=32, kernel=2)):
+        with pytest.raises(Exception):
+            Lopf.setup(f, **bad)
