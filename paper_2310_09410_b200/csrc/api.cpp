@@ -292,7 +292,7 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
         sz->reserved[1] = h->lay.max_smem;
     }
     sz->grid = h->resident() ? h->lay.G : h->grid;
-    sz->block = h->resident() ? kResBlock : stream_block(h->lay.rmax);
+    sz->block = h->resident() ? kResBlock : stream_block(h->lay.rmax, h->lay.esz);
     sz->n_scen = h->batch() ? h->lay.n_scen : 0;
     return LOPF_OK;
 }

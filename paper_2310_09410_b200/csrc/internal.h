@@ -76,9 +76,9 @@ constexpr int kTaskVar = 1 << 6;           // batch: the task's operator block i
 constexpr int kTaskUsedShift = 16;         // packed task: slots in use (rounded up to 4), bits 16..23 of .w
 constexpr int kTaskHalves = 2;             // streaming packer: max 32-slot halves per packed task
 #ifndef LOPF_PACK_BUDGET
-#define LOPF_PACK_BUDGET 224
+#define LOPF_PACK_BUDGET 448
 #endif
-constexpr int kPackBudget = LOPF_PACK_BUDGET;  // doubles of operator block per staged task (per-warp SMEM stage)
+constexpr int kPackBudget = LOPF_PACK_BUDGET;  // operator-block entries (fp64 or fp32) per staged task (per-warp SMEM stage)
 
 struct DevCtrl {                           // 256 B, device-resident control block
     unsigned long long arrive;             // barrier arrivals of this launch
@@ -274,12 +274,19 @@ lopf_status pack_resident(const Net& net, const Canon& cp, const lopf_options& o
 lopf_status pack_batch(const Net& N, const Canon& cp, const BatchOps& bo, const lopf_options& opt, Layout& lay,
                        std::string& err);
 // kernels.cu
-#ifndef LOPF_STREAM_WARPS
-#define LOPF_STREAM_WARPS 24
+// Streaming / batch CTA (one per SM): warps x 2 SMEM stages of kPackBudget operator entries each.  Measured
+// (tools/ab_stream.py): the best split keeps ~448 entries per stage and as many warps as SMEM then allows --
+// 16 warps for fp64 (3.5 KB of operators per stage), 24 for fp32 (1.75 KB).
+#ifndef LOPF_STREAM_WARPS_F64
+#define LOPF_STREAM_WARPS_F64 16
 #endif
-constexpr int kStreamWarps = LOPF_STREAM_WARPS;  // streaming CTA (one per SM): 24 warps x 2 SMEM stages
-constexpr int kStreamWarpsWide = 16;         // ... when tasks of R > 2 exist (n_s > 64)
-int stream_block(int rmax);
+#ifndef LOPF_STREAM_WARPS_F32
+#define LOPF_STREAM_WARPS_F32 24
+#endif
+constexpr int kStreamWarpsF64 = LOPF_STREAM_WARPS_F64;
+constexpr int kStreamWarpsF32 = LOPF_STREAM_WARPS_F32;
+constexpr int kStreamWarpsWide = 12;         // ... when tasks of R > 2 exist (n_s > 64, the S = 1 path)
+int stream_block(int rmax, int esz);
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
 lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err);
 lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err);

@@ -41,15 +41,15 @@ constexpr int kInvNu = 64;                 // SMEM table of 1 / nu (the host's 1
 // elected lane copies them into one of the warp's two SMEM stages with cp.async.bulk, completing
 // on that stage's mbarrier, one task ahead of the compute.
 // T = double (the parity path) or float (the paper's GPU precision; reading F1): the
-// operator block budget is the same 8 * kPackBudget bytes, per-slot iterate entries are sizeof(T).
-constexpr int kOffInfo = 8 * kPackBudget;
-constexpr int kOffG = kOffInfo + 4 * 64;
-constexpr int kOffNbr = kOffG + 4 * 64;
-constexpr int kOffLam = kOffNbr + 16 * 64;
+// operator block holds kPackBudget entries of T, then the per-slot inputs of 64 slots.
 template <class T> struct Stg {
+    static constexpr int kOffInfo = (int)sizeof(T) * kPackBudget;
+    static constexpr int kOffG = kOffInfo + 4 * 64;
+    static constexpr int kOffNbr = kOffG + 4 * 64;
+    static constexpr int kOffLam = kOffNbr + 16 * 64;
     static constexpr int kOffXl = kOffLam + (int)sizeof(T) * 64;
     static constexpr int kBytes = kOffXl + (int)sizeof(T) * 64;
-    static_assert(kBytes % 16 == 0, "bulk copies need 16-byte alignment");
+    static_assert(kOffInfo % 16 == 0 && kBytes % 16 == 0, "bulk copies need 16-byte alignment");
 };
 template <class T> struct Vec2;
 template <> struct Vec2<double> { using type = double2; };
@@ -95,10 +95,10 @@ __device__ __forceinline__ void issue_task(const DevProblem& P, Stage& st, const
         else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
         if (ablk) bulk_g2s(sb, reinterpret_cast<const T*>(P.abar) + tr.y, E * (uint32_t)tr.z, m);
-        bulk_g2s(sb + kOffInfo, P.s_info + tr.x, 4u * n, m);
-        bulk_g2s(sb + kOffG, P.s_g + tr.x, 4u * n, m);
-        bulk_g2s(sb + kOffNbr, P.s_nbr + tr.x, 16u * n, m);
-        bulk_g2s(sb + kOffLam, reinterpret_cast<const T*>(P.lam) + tr.x, E * n, m);
+        bulk_g2s(sb + Stg<T>::kOffInfo, P.s_info + tr.x, 4u * n, m);
+        bulk_g2s(sb + Stg<T>::kOffG, P.s_g + tr.x, 4u * n, m);
+        bulk_g2s(sb + Stg<T>::kOffNbr, P.s_nbr + tr.x, 16u * n, m);
+        bulk_g2s(sb + Stg<T>::kOffLam, reinterpret_cast<const T*>(P.lam) + tr.x, E * n, m);
         bulk_g2s(sb + Stg<T>::kOffXl, reinterpret_cast<const T*>(P.xl) + tr.x, E * n, m);
     }
 }
@@ -164,10 +164,10 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
     mbar_wait(st.bar + b, (st.consumed >> 1) & 1);
     ++st.consumed;
     const char* sb = st.buf + b * kStageBytes;
-    const int* s_info = reinterpret_cast<const int*>(sb + kOffInfo);
-    const int* s_g = reinterpret_cast<const int*>(sb + kOffG);
-    const int4* s_nbr = reinterpret_cast<const int4*>(sb + kOffNbr);
-    const T* s_lam = reinterpret_cast<const T*>(sb + kOffLam);
+    const int* s_info = reinterpret_cast<const int*>(sb + Stg<T>::kOffInfo);
+    const int* s_g = reinterpret_cast<const int*>(sb + Stg<T>::kOffG);
+    const int4* s_nbr = reinterpret_cast<const int4*>(sb + Stg<T>::kOffNbr);
+    const T* s_lam = reinterpret_cast<const T*>(sb + Stg<T>::kOffLam);
     const T* s_xl = reinterpret_cast<const T*>(sb + Stg<T>::kOffXl);
     const T* S = (tr.w & kTaskDirect) ? reinterpret_cast<const T*>(P.abar) + tr.y : reinterpret_cast<const T*>(sb);
     const int used = (tr.w >> kTaskUsedShift) & 0xFF;       // stage entries past `used` are stale
@@ -297,12 +297,14 @@ __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, co
     __syncwarp();
 }
 
-template <int RMAX>
-struct StreamWarps { static constexpr int value = RMAX <= 2 ? kStreamWarps : kStreamWarpsWide; };
+template <int RMAX, class T>
+struct StreamWarps {
+    static constexpr int value = RMAX > 2 ? kStreamWarpsWide : sizeof(T) == 8 ? kStreamWarpsF64 : kStreamWarpsF32;
+};
 
 template <int RMAX, class T>   // largest task width in the problem (RMAX > 2 only with n_s > 64: the S = 1 path)
-__global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_stream_kernel(DevProblem P) {
-    constexpr int kWarps = StreamWarps<RMAX>::value;
+__global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stream_kernel(DevProblem P) {
+    constexpr int kWarps = StreamWarps<RMAX, T>::value;
     constexpr int kStageBytes = Stg<T>::kBytes;
     extern __shared__ __align__(128) char sdyn[];      // [kWarps][2][kStageBytes] stages, [kWarps][32*RMAX] d
     __shared__ double red[kWarps][5];
@@ -520,8 +522,8 @@ __device__ __forceinline__ int next_active(const uint32_t* m, const int W, const
 constexpr int kBatchMaskWords = kBatchMaxScen / 32;
 
 template <int RMAX, class T>
-__global__ void __launch_bounds__(32 * StreamWarps<RMAX>::value, 1) admm_batch_kernel(DevProblem P, BatchProblem B) {
-    constexpr int kWarps = StreamWarps<RMAX>::value;
+__global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_batch_kernel(DevProblem P, BatchProblem B) {
+    constexpr int kWarps = StreamWarps<RMAX, T>::value;
     constexpr int kStageBytes = Stg<T>::kBytes;
     extern __shared__ __align__(128) char sdyn[];
     __shared__ uint64_t sbar[kWarps][2];
@@ -755,10 +757,12 @@ static const void* stream_kernel_for(int rmax, int esz) {
 static int stream_smem(int rmax, int esz) {
     const int r = rmax <= 1 ? 1 : rmax <= 2 ? 2 : rmax <= 4 ? 4 : 8;
     const int stage = esz == 4 ? Stg<float>::kBytes : Stg<double>::kBytes;
-    return (rmax <= 2 ? kStreamWarps : kStreamWarpsWide) * (2 * stage + esz * 32 * r);
+    return stream_block(rmax, esz) / 32 * (2 * stage + esz * 32 * r);
 }
 
-int stream_block(int rmax) { return 32 * (rmax <= 2 ? kStreamWarps : kStreamWarpsWide); }
+int stream_block(int rmax, int esz) {
+    return 32 * (rmax > 2 ? kStreamWarpsWide : esz == 8 ? kStreamWarpsF64 : kStreamWarpsF32);
+}
 
 lopf_status query_grid(int rmax, int esz, int* grid, std::string& err) {
     int dev = 0, sms = 0, per = 0;
@@ -767,7 +771,7 @@ lopf_status query_grid(int rmax, int esz, int* grid, std::string& err) {
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem(rmax, esz));
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, stream_block(rmax), stream_smem(rmax, esz));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, stream_block(rmax, esz), stream_smem(rmax, esz));
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     if (per < 1) { err = "streaming kernel cannot be resident (occupancy 0)"; return LOPF_E_CUDA; }
     *grid = sms * per;
@@ -781,7 +785,7 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
     if (e == cudaSuccess && P.max_iter > 0) {
         DevProblem Q = P;
         void* args[] = {&Q};
-        e = cudaLaunchCooperativeKernel(stream_kernel_for(P.rmax, P.esz), dim3(grid), dim3(stream_block(P.rmax)), args,
+        e = cudaLaunchCooperativeKernel(stream_kernel_for(P.rmax, P.esz), dim3(grid), dim3(stream_block(P.rmax, P.esz)), args,
                                         stream_smem(P.rmax, P.esz), s);
     }
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
@@ -807,7 +811,7 @@ lopf_status launch_batch(const DevProblem& P, const BatchProblem& B, int grid, v
         DevProblem Q = P;
         BatchProblem C = B;
         void* args[] = {&Q, &C};
-        e = cudaLaunchCooperativeKernel(k, dim3(grid), dim3(stream_block(P.rmax)), args, smem, s);
+        e = cudaLaunchCooperativeKernel(k, dim3(grid), dim3(stream_block(P.rmax, P.esz)), args, smem, s);
     }
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;

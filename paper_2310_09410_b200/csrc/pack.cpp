@@ -24,10 +24,10 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
                            std::string& err, const PartSpec* part, int32_t rank) {
     L = Layout();
     L.kernel = 1;
-    // element size of operators / iterate / globals (fp32 variant: reading F1); the SMEM stage keeps its
-    // byte budget, so an fp32 task packs twice the operator entries; bulk copies stay 16-byte aligned
+    // element size of operators / iterate / globals (fp32 variant: reading F1); a stage holds kPackBudget
+    // operator entries of either type; bulk copies stay 16-byte aligned
     const int esz = opt.precision == 32 ? 4 : 8;
-    const int budget = kPackBudget * 8 / esz, al = 16 / esz;
+    const int budget = kPackBudget, al = 16 / esz;
     L.esz = esz;
     // partitioned mode: only this rank's subsystems; remote copies its globals read become ghost slots
     auto local_sub = [&](int64_t s) { return !part || part->sub_owner[s] == rank; };
