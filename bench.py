@@ -233,7 +233,7 @@ def main():
         mean_kern_ms = statistics.mean(kern_ms)
         mean_iters = statistics.mean(iters)
         achieved = sz.alg_bytes * mean_iters / (mean_kern_ms / 1e3) / 1e9
-        dram, ncu_iters = _ncu_traffic()
+        dram, ncu_iters = _ncu_traffic() if sz.kernel == 2 else (None, None)   # the summary is the resident kernel's
         traffic = (dram / ncu_iters * mean_iters) if (dram and ncu_iters) else None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -420,7 +420,8 @@ def bench_stitched(args):
                              f"to the full instance (extrapolated, linear in size)"}
         dram = None
         try:
-            with open(os.path.join(ROOT, "profiles", "ncu_summary_config5.json")) as fh:
+            suffix = "_f32" if args.precision == 32 else ""
+            with open(os.path.join(ROOT, "profiles", f"ncu_summary_config5{suffix}.json")) as fh:
                 dram = json.load(fh).get("dram_bytes_per_sweep")
         except Exception:
             pass
@@ -530,6 +531,13 @@ def bench_batch(args):
         batch_sweeps = float(allv[:, 4].max())                 # launch length = slowest scenario
         us_per_batch_sweep = 1e3 * (max_ms / args.steps) / batch_sweeps
         achieved = sz.alg_bytes / (us_per_batch_sweep * 1e-6) / 1e9
+        traffic = None                                  # ncu dram bytes per batch sweep (committed summary)
+        try:
+            suffix = "_f32" if args.precision == 32 else ""
+            with open(os.path.join(ROOT, "profiles", f"ncu_summary_config4{suffix}.json")) as fh:
+                traffic = json.load(fh).get("dram_bytes_per_sweep")
+        except Exception:
+            pass
         out = {
             "metric": METRIC, "value": value, "unit": "scenario-iterations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
@@ -540,7 +548,7 @@ def bench_batch(args):
                        "mean_iters": float(allv[:, 3].sum()) / args.n_scen, "time_to_tolerance_ms": max_ms / args.steps,
                        "l2": "flushed between steps (512 MiB write)", "setup_s": round(setup_s, 1)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_src, "kernel": "admm_batch_kernel",
+                         "traffic": traffic, "peak_source": peak_src, "kernel": "admm_batch_kernel",
                          "alg_bytes_per_batch_sweep": int(sz.alg_bytes), "us_per_batch_sweep": us_per_batch_sweep},
             "cpu_baseline": None,
             "e2e": {"value": float(allv[:, 3].sum()) * e2e_steps / float(allv[:, 2].max()), "unit": "scenario-iterations/s",

@@ -9,8 +9,9 @@ import feedergen as fg  # noqa: E402
 from paper_2310_09410_b200 import Lopf  # noqa: E402
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+prec = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 f = fg.make_feeder("123")
-h = Lopf.setup_batch(f, fg.scenario_scales(f, 4096)).bind("cuda")
+h = Lopf.setup_batch(f, fg.scenario_scales(f, 4096), precision=prec).bind("cuda")
 h.run(K)
 h.run(K)
 torch.cuda.synchronize()

@@ -10,7 +10,8 @@ import feedergen as fg  # noqa: E402
 from paper_2310_09410_b200 import Lopf  # noqa: E402
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-h = Lopf.setup(fg.make_stitched(64, "8500")).bind("cuda")
+prec = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+h = Lopf.setup(fg.make_stitched(64, "8500"), kernel=1, precision=prec).bind("cuda")
 h.run(K)
 h.run(K)
 torch.cuda.synchronize()
