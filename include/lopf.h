@@ -235,7 +235,8 @@ lopf_status lopf_set_state(lopf_handle *h, void *cuda_stream, const double *x_lo
 lopf_status lopf_get_trace(lopf_handle *h, void *cuda_stream, double *buf, int64_t cap, int64_t *n_rows);
 
 /* Diagnostics (resident kernel, options.reserved[0] = 1): per-CTA cycle counters of the last launch,
- * rows {work, publish + neighbour wait, 0, sweeps}: buf [cap*4].  The counters perturb the timing. */
+ * rows {work, publish + neighbour wait, 0, sweeps}: buf [cap*4].  The counters perturb the timing.
+ * Rows G .. 33G-1 (cap > G) hold the event timeline of a LOPF_RES_TIMELINE diagnostics build. */
 lopf_status lopf_get_profile(lopf_handle *h, void *cuda_stream, int64_t *buf, int64_t cap, int64_t *n_rows);
 
 void lopf_destroy(lopf_handle *h);

@@ -778,7 +778,7 @@ lopf_status lopf_get_profile(lopf_handle* h, void* stream, int64_t* buf, int64_t
     if (!h) return fail(LOPF_E_ARG, "NULL handle");
     if (!h->bound || !h->resident() || !h->rp.prof) return fail(LOPF_E_STATE, "profiling needs the resident kernel with diagnostics enabled");
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t rows = std::min<int64_t>(h->lay.G, cap);
+    const int64_t rows = std::min<int64_t>(41 * (int64_t)h->lay.G, cap);   // G counter rows, then timeline events
     CUDA_TRY(cudaMemcpyAsync(buf, h->rp.prof, sizeof(int64_t) * 4 * rows, cudaMemcpyDeviceToHost, s), "profile D2H");
     CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     if (n_rows) *n_rows = rows;

@@ -98,6 +98,63 @@ std::vector<TaskR> make_tasks(const Canon& P, const std::vector<int64_t>& subs) 
     return tasks;
 }
 
+// Use the chunk's idle worker warps: the most expensive 64-row tasks whose subsystems fit two 32-row
+// halves become two R = 1 tasks (lane l: row l only) run by two warps.  The period of the kernel is set by
+// the slowest warp of the slowest CTA (tools/res_timeline2.py: a warp's cycles ~ 45 per tile column + 90
+// per boundary read, issue-bound), so halving the longest tasks shortens the critical path.  The split
+// never grows the SMEM footprint (same slots, tiles of 32 x kmax_half <= 64 x kmax).
+// Measured and OFF by default: the widest tasks (two n_s = 18..26 subsystems plus a small one) do not fit
+// two 32-row halves, so the split lands on cheaper tasks; the extra active warps raise the issue
+// contention for every warp (median worker 4.2k -> 5.9k cycles) and the period grows 5.22 -> 5.31 us.
+#ifndef LOPF_RES_SPLIT_TASKS
+#define LOPF_RES_SPLIT_TASKS 0
+#endif
+void split_tasks(const Canon& P, std::vector<TaskR>& tasks, const std::vector<int32_t>& copy_chunk, int c,
+                 int workers) {
+    if (!LOPF_RES_SPLIT_TASKS) return;
+    auto cost = [&](const TaskR& t) {
+        int64_t xr = 0;
+        for (int64_t s : t.subs)
+            for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) {
+                const int32_t g = P.copy_global[k];
+                for (int64_t q = P.seg_ptr[g]; q < P.seg_ptr[g + 1]; ++q) xr += copy_chunk[P.seg_copy[q]] != c;
+            }
+        return 45.0 * t.kmax + 90.0 * (double)xr;
+    };
+    std::vector<int> idx(tasks.size());
+    std::vector<double> cs(tasks.size());
+    for (size_t i = 0; i < tasks.size(); ++i) { idx[i] = (int)i; cs[i] = cost(tasks[i]); }
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cs[a] > cs[b]; });
+    int idle = workers - (int)tasks.size();
+    std::vector<TaskR> out;
+    std::vector<char> split(tasks.size(), 0);
+    std::vector<std::pair<TaskR, TaskR>> halves(tasks.size());
+    for (int i : idx) {
+        if (idle <= 0) break;
+        const TaskR& t = tasks[i];
+        if (t.R != 2) continue;
+        TaskR a{1, 0, {}}, b{1, 0, {}};
+        int ra = 32, rb = 32;
+        bool ok = true;
+        for (int64_t s : t.subs) {                        // first fit decreasing (subs are in n_s order)
+            const int ns = P.n_s[s];
+            if (ns <= ra) { a.subs.push_back(s); a.kmax = std::max(a.kmax, ns); ra -= ns; }
+            else if (ns <= rb) { b.subs.push_back(s); b.kmax = std::max(b.kmax, ns); rb -= ns; }
+            else { ok = false; break; }
+        }
+        if (!ok || a.subs.empty()) continue;
+        split[i] = 1;
+        halves[i] = {a, b};
+        if (!b.subs.empty()) --idle;                       // (<= 32 rows: one R = 1 task, no extra warp)
+    }
+    for (size_t i = 0; i < tasks.size(); ++i) {
+        if (!split[i]) { out.push_back(tasks[i]); continue; }
+        out.push_back(halves[i].first);
+        if (!halves[i].second.subs.empty()) out.push_back(halves[i].second);
+    }
+    tasks.swap(out);
+}
+
 // exact SMEM bytes of a chunk (blob + xg scratch); mirrors the blob layout built below
 int64_t chunk_bytes(const Canon& P, const std::vector<int64_t>& subs, std::vector<int32_t>& cnt) {
     auto tasks = make_tasks(P, subs);
@@ -211,15 +268,16 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     std::vector<int32_t> gl_of(P.n, -1);
     for (int c = 0; c < L.G; ++c) {
         auto tasks = make_tasks(P, chunks[c].subs);
+        split_tasks(P, tasks, copy_chunk, c, kResBlock / 32 - 1);
         CtaHdr& h = B[c].h;
         std::memset(&h, 0, sizeof(h));
         int64_t NS = 0, pool = 0;
         std::vector<int4> trec;
         int kpad = 0;
-        for (auto& t : tasks) {                              // task tile: kmax columns x 64 rows, zero padded
-            trec.push_back(make_int4((int)NS, t.kmax, (int)pool, 0));
-            NS += 64;
-            pool += (int64_t)t.kmax * 64;
+        for (auto& t : tasks) {                              // task tile: kmax columns x 32R rows, zero padded
+            trec.push_back(make_int4((int)NS, t.kmax, (int)pool, t.R));
+            NS += 32 * t.R;
+            pool += (int64_t)t.kmax * 32 * t.R;
             kpad = std::max(kpad, t.kmax);
         }
         std::vector<int32_t> gl_list;
@@ -285,8 +343,9 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
             for (int64_t s : tasks[t].subs) {
                 const int ns = P.n_s[s];
                 const double* Ab = &P.abar[P.abar_ptr[s]];
+                const int rows = 32 * tasks[t].R;
                 for (int r = 0; r < ns; ++r)             // row base+r of the tile: tile[k][base + r] = Abar_s[r][k]
-                    for (int k = 0; k < ns; ++k) abar[(size_t)trec[t].z + (size_t)k * 64 + base + r] = Ab[(size_t)r * ns + k];
+                    for (int k = 0; k < ns; ++k) abar[(size_t)trec[t].z + (size_t)k * rows + base + r] = Ab[(size_t)r * ns + k];
                 for (int r = 0; r < ns; ++r) {
                     const int64_t slot = trec[t].x + base + r;
                     const int64_t copy = P.sub_ptr[s] + r;
@@ -352,7 +411,7 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     L.off_partial = take(8 * 8 * 4 * (size_t)L.G);     // 4 sweep slots (lagged decision, see resident.cu)
     L.off_ctrl = take(sizeof(DevCtrl));
     L.off_trace = take(8 * 5 * (size_t)L.trace_cap);
-    L.off_prof = take(8 * 4 * (size_t)L.G);
+    L.off_prof = take(8 * 4 * (size_t)L.G + 8 * 5 * 32 * (size_t)L.G);   // counters + LOPF_RES_TIMELINE=2 events
     L.off_objidx = take(4 * obj_idx.size());
     L.off_objc = take(8 * obj_c.size());
     L.bytes = off;

@@ -88,12 +88,13 @@ __device__ __forceinline__ double seg_u(const Ctx& C, const int e) {
     return e >= 0 ? u_of(Dd(C.xl_c, e), Dd(C.lam_c, e), C.inv_rho) : ld_entry(C.xch_c + (-e - 1), C.tag_c);
 }
 
-// one 64-row task; lane l owns rows l and l + 32 (two independent dependency chains)
+// one task of 32R rows (tr.w = R): lane l owns rows l (and l + 32 when R = 2: two dependency chains)
+template <int R>
 __device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double (&acc)[5], const int lane) {
     double v[2], lam[2], xo[2];
     int info[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < R; ++h) {
         const int slot = tr.x + h * 32 + lane;
         info[h] = Ii(C.sinfo, slot);
         double d = 0.0;
@@ -129,35 +130,22 @@ __device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double (
     // per column; d indices beyond the subsystem land on finite d values or the zeroed staging tail.
     const int kmax = tr.y;
     const int at = C.sabar + 8 * (tr.z + lane);                          // byte offset of tile[0][lane]
-    const int d0 = C.dst + 8 * (info[0] & 0x3F), d1 = C.dst + 8 * (info[1] & 0x3F);
-#if LOPF_RES_SPLIT
-    // even and odd columns in separate chains (half the dependent-FMA latency), added at the end
-    double ax0 = 0.0, ax1 = 0.0, bx0 = 0.0, bx1 = 0.0;
-    int k = 0;
-#pragma unroll 2
-    for (; k + 1 < kmax; k += 2) {
-        ax0 = fma(Dd(at, 64 * k), Dd(d0, k), ax0);
-        ax1 = fma(Dd(at, 64 * k + 32), Dd(d1, k), ax1);
-        bx0 = fma(Dd(at, 64 * k + 64), Dd(d0, k + 1), bx0);
-        bx1 = fma(Dd(at, 64 * k + 96), Dd(d1, k + 1), bx1);
-    }
-    if (k < kmax) {
-        ax0 = fma(Dd(at, 64 * k), Dd(d0, k), ax0);
-        ax1 = fma(Dd(at, 64 * k + 32), Dd(d1, k), ax1);
-    }
-    const double axr[2] = {ax0 + bx0, ax1 + bx1};
-#else
+    const int d0 = C.dst + 8 * (info[0] & 0x3F), d1 = C.dst + 8 * (info[R - 1] & 0x3F);
     double ax0 = 0.0, ax1 = 0.0;
+    if (R == 2) {
 #pragma unroll 4
-    for (int k = 0; k < kmax; ++k) {
-        ax0 = fma(Dd(at, 64 * k), Dd(d0, k), ax0);
-        ax1 = fma(Dd(at, 64 * k + 32), Dd(d1, k), ax1);
+        for (int k = 0; k < kmax; ++k) {
+            ax0 = fma(Dd(at, 64 * k), Dd(d0, k), ax0);
+            ax1 = fma(Dd(at, 64 * k + 32), Dd(d1, k), ax1);
+        }
+    } else {
+#pragma unroll 4
+        for (int k = 0; k < kmax; ++k) ax0 = fma(Dd(at, 32 * k), Dd(d0, k), ax0);
     }
     const double axr[2] = {ax0, ax1};
-#endif
     __syncwarp();                                                        // dst is reused by the next task
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < R; ++h) {
         if (!(info[h] & kResValid)) continue;
         const int slot = tr.x + h * 32 + lane;
         const double xn = fma(axr[h], C.inv_rho, Dd(C.sbbar, slot));         // (1/rho) Abar d + bbar
@@ -177,9 +165,15 @@ __device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double (
 
 constexpr int kFlagStride = 32;                    // one flag per 256-byte line (no L2 hot spot)
 
-#if LOPF_RES_TIMELINE   // diagnostics build: per-warp clock64 events of CTA G/2, sweeps 500..502, into P.prof
+#if LOPF_RES_TIMELINE == 1   // diagnostics build: per-warp clock64 events of CTA G/2, sweeps 500..502, into P.prof
 #define TL(e) do { if (P.prof && cta == G / 2 && t >= 500 && t < 503 && lane == 0) \
     P.prof[((t - 500) * RW + wid) * 8 + (e)] = clock64(); } while (0)
+#elif LOPF_RES_TIMELINE == 2  // every CTA, sweeps 500..503: cycles from each warp's loop top to its work end
+                              // (event 1; slot = warp) and, for warp 0, to the end-of-iteration barrier (slot 31)
+#define TL(e) do { if (P.prof && t >= 500 && t < 504 && lane == 0) { \
+    if ((e) == 0) tl_top = clock64(); \
+    else if ((e) == 1) P.prof[4 * G + ((t - 500) * G + cta) * 32 + wid] = clock64() - tl_top; \
+    else if ((e) == 7 && wid == 0) P.prof[4 * G + ((t - 500) * G + cta) * 32 + 31] = clock64() - tl_top; } } while (0)
 #else
 #define TL(e) do { } while (0)
 #endif
@@ -231,6 +225,9 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     __syncthreads();
 
     long long t = 0;                                   // sweeps completed; state t in buffer t & 1
+#if LOPF_RES_TIMELINE == 2
+    long long tl_top = 0;
+#endif
     for (;;) {
         const int cur = (int)(t & 1);
         if (prof && tid == 0) s_prof[2] = clock64();
@@ -308,8 +305,33 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                 C.tag_c = tag_of(t);
                 C.tag_n = tag_of(t + 1);
                 for (int task = wid; task < NT; task += NWORK) {
-                    task_sweep(C, reinterpret_cast<const int4*>(sm + H.off_tasks)[task], acc, lane);
+                    const int4 tr = reinterpret_cast<const int4*>(sm + H.off_tasks)[task];
+                    if (tr.w == 1) task_sweep<1>(C, tr, acc, lane);
+                    else task_sweep<2>(C, tr, acc, lane);
                 }
+#if LOPF_RES_TIMELINE == 2
+                if (P.prof && t == 500) {   // task signature of this warp: kmax | tasks << 8 | rows << 16 | xreads << 32
+                    long long sig = 0, rows = 0, xr = 0, km = 0, nt = 0;
+                    for (int task = wid; task < NT; task += NWORK) {
+                        const int4 tr = reinterpret_cast<const int4*>(sm + H.off_tasks)[task];
+                        km = km > tr.y ? km : tr.y;
+                        ++nt;
+                        for (int h = 0; h < (tr.w == 1 ? 1 : 2); ++h) {
+                            const int inf = Ii(C.sinfo, tr.x + h * 32 + lane);
+                            if (!(inf & kResValid)) continue;
+                            ++rows;
+                            const int gl = inf >> kResGlShift;
+                            for (int q = Ii(C.gsegoff, gl); q < Ii(C.gsegoff, gl + 1); ++q) xr += Ii(C.gseg, q) < 0;
+                        }
+                    }
+                    for (int off = 16; off > 0; off >>= 1) {
+                        rows += __shfl_xor_sync(kFull, rows, off);
+                        xr += __shfl_xor_sync(kFull, xr, off);
+                    }
+                    sig = km | (nt << 8) | (rows << 16) | (xr << 32);
+                    if (lane == 0) P.prof[4 * G + 128 * G + cta * 32 + wid] = sig;
+                }
+#endif
             }
             TL(1);
             if (busy) {                                // idle warps contribute exact zeros without shuffling

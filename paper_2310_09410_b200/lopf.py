@@ -388,10 +388,11 @@ class Lopf:
                "lopf_get_trace")
         return buf[: n.value].copy()
 
-    def get_profile(self, stream=None) -> np.ndarray:
-        """Diagnostics: per-CTA cycles {work, publish + neighbour wait, -, sweeps} of the last resident launch.
+    def get_profile(self, stream=None, timeline: bool = False) -> np.ndarray:
+        """Diagnostics: per-CTA cycles {work, publish + neighbour wait, -, sweeps} of the last resident launch
+        (timeline=True: followed by the 32 G rows of a LOPF_RES_TIMELINE build's events).
         The counters perturb the kernel: use them for relative shares, not absolute times."""
-        g = int(self.sizes.grid)
+        g = int(self.sizes.grid) * (41 if timeline else 1)
         buf = np.zeros((g, 4), np.int64)
         n = _i64(0)
         _check(load_library().lopf_get_profile(self._h, _vp(_stream_handle(stream)), _ptr(buf), g, C.byref(n)),
