@@ -163,6 +163,33 @@ __device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double (
     }
 }
 
+// Warp sums of five doubles by a reduce-scatter butterfly (fixed order, deterministic): 18 shuffles and
+// 9 adds instead of 50 and 25.  Returns the total of value (lane >> 2) on lanes with (lane >> 2) < 5.
+__device__ __forceinline__ double warp_sum5(const double (&v)[5], const int lane) {
+    const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+    double w[4];                                   // xor 16: lanes keep values 0-3 (b16 = 0) or 4-7
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double lo = v[i], hi = i == 0 ? v[4] : 0.0;
+        const double send = b16 ? lo : hi, keep = b16 ? hi : lo;
+        w[i] = keep + __shfl_xor_sync(kFull, send, 16);
+    }
+    double x[2];                                   // xor 8: keep 2 of the 4
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double send = b8 ? w[i] : w[i + 2], keep = b8 ? w[i + 2] : w[i];
+        x[i] = keep + __shfl_xor_sync(kFull, send, 8);
+    }
+    double y;                                      // xor 4: keep 1 of the 2
+    {
+        const double send = b4 ? x[0] : x[1], keep = b4 ? x[1] : x[0];
+        y = keep + __shfl_xor_sync(kFull, send, 4);
+    }
+    y += __shfl_xor_sync(kFull, y, 2);
+    y += __shfl_xor_sync(kFull, y, 1);
+    return y;                                      // value index 4 b16 + 2 b8 + b4 = lane >> 2
+}
+
 constexpr int kFlagStride = 32;                    // one flag per 256-byte line (no L2 hot spot)
 
 #if LOPF_RES_TIMELINE == 1   // diagnostics build: per-warp clock64 events of CTA G/2, sweeps 500..502, into P.prof
@@ -334,17 +361,9 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
 #endif
             }
             TL(1);
-            if (busy) {                                // idle warps contribute exact zeros without shuffling
-#pragma unroll
-                for (int k = 0; k < 5; ++k) {
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(kFull, acc[k], off);
-                }
-            }
-            if (lane == 0) {
-#pragma unroll
-                for (int k = 0; k < 5; ++k) red[cur ^ 1][wid][k] = acc[k];   // sums of sweep t+1
-            }
+            // the five warp sums of sweep t+1 (idle warps contribute exact zeros without shuffling)
+            const double wsum = busy ? warp_sum5(acc, lane) : 0.0;
+            if ((lane & 3) == 0 && (lane >> 2) < 5) red[cur ^ 1][wid][lane >> 2] = wsum;
             TL(2);
         }
         __syncthreads();                               // sweep t+1 computed; decision for sweep t known
