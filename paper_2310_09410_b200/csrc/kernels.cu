@@ -182,7 +182,9 @@ __device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, 
 
 // Packed task (R <= 2 halves): inputs from the SMEM stage; operator block from the stage or, for a
 // lone large subsystem (kTaskDirect), straight from the pool.
-template <int R, class T>
+// SRC: where the operator block is read -- 1 the pool (direct task), 2 the SMEM stage (shared-space
+// loads), 0 decided per task at run time (one code path: the batch kernel, whose registers are tighter)
+template <int R, class T, int SRC>
 __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, const T* __restrict__ ucur,
                                             T* __restrict__ unext, double (&acc)[5], const int lane,
                                             T* __restrict__ dsm, Stage& st, const T* __restrict__ inv_nu) {
@@ -196,7 +198,8 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
     const int4* s_nbr = reinterpret_cast<const int4*>(sb + Stg<T>::kOffNbr);
     const T* s_lam = reinterpret_cast<const T*>(sb + Stg<T>::kOffLam);
     const T* s_xl = reinterpret_cast<const T*>(sb + Stg<T>::kOffXl);
-    const T* S = (tr.w & kTaskDirect) ? reinterpret_cast<const T*>(P.abar) + tr.y : reinterpret_cast<const T*>(sb);
+    const bool direct = SRC == 1 || (SRC == 0 && (tr.w & kTaskDirect));
+    const T* S = direct ? reinterpret_cast<const T*>(P.abar) + tr.y : reinterpret_cast<const T*>(sb);
     const int used = (tr.w >> kTaskUsedShift) & 0xFF;       // stage entries past `used` are stale
     const T rho = (T)P.rho;
     T v[R], ax[R];
@@ -365,8 +368,14 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
             const int4 tr2 = task + 2 * nw < P.n_tasks ? __ldg(P.tasks + task + 2 * nw) : make_int4(0, 0, 0, 0);
             if (task + nw < P.n_tasks) issue_task<T>(P, st, tr1, lane, false);   // one task ahead
             if (tr.w & kTaskPacked) {
-                if ((tr.w & 0xF) == 1) task_packed<1, T>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
-                else if constexpr (RMAX >= 2) task_packed<2, T>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
+                const bool dir = tr.w & kTaskDirect;
+                if ((tr.w & 0xF) == 1) {
+                    if (dir) task_packed<1, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
+                    else task_packed<1, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
+                } else if constexpr (RMAX >= 2) {
+                    if (dir) task_packed<2, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
+                    else task_packed<2, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
+                }
             } else {
                 switch (tr.w & 0xF) {
                     case 2: if constexpr (RMAX >= 2) task_full<2, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
@@ -545,7 +554,7 @@ constexpr int kBatchMaskWords = kBatchMaxScen / 32;
 
 template <int RMAX, class T>
 __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_batch_kernel(DevProblem P, BatchProblem B) {
-    constexpr int kWarps = StreamWarps<RMAX, T>::value;
+    constexpr int kWarps = StreamWarps<RMAX, T>::value;   // fp32: 24 warps beat 16 (390 vs 466 us/batch sweep)
     constexpr int kStageBytes = Stg<T>::kBytes;
     extern __shared__ __align__(128) char sdyn[];
     __shared__ uint64_t sbar[kWarps][2];
@@ -622,8 +631,8 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_batc
                 }
                 const size_t so = (size_t)sc * B.ns_stride;
                 const DevProblem Q = batch_view<T>(P, B, sc, tr);
-                if ((tr.w & 0xF) == 1) task_packed<1, T>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
-                else if constexpr (RMAX >= 2) task_packed<2, T>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+                if ((tr.w & 0xF) == 1) task_packed<1, T, 0>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+                else if constexpr (RMAX >= 2) task_packed<2, T, 0>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
                 double* pp = B.partial + ((size_t)sc * NT + tk) * 8;
                 if (more && sc1 == sc) {                       // the run goes on: this item's slot holds 0
                     if (lane < 5) pp[lane] = 0.0;
@@ -804,6 +813,7 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;
 }
+
 
 static const void* batch_kernel_for(int rmax, int esz) {
     if (esz == 4) return rmax <= 1 ? (const void*)admm_batch_kernel<1, float> : (const void*)admm_batch_kernel<2, float>;

@@ -36,6 +36,9 @@ constexpr int RW = RB / 32;
 constexpr int NWORK = RW - 1;              // worker warps 0 .. RW-2
 constexpr int RED = RW - 1;                // reducer warp
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef LOPF_RES_SLEEP
+#define LOPF_RES_SLEEP 20                  // reducer poll back-off (ns)
+#endif
 constexpr int kPer = 5;                    // flags / partials per reducer lane per round (G <= 160 in one round)
 
 __device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p) {
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                     asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pub) : "memory");
                 }
                 const unsigned long long need = (unsigned long long)G * (unsigned long long)t;
-                while (ld_rlx(pub) < need) __nanosleep(20);
+                while (ld_rlx(pub) < need) __nanosleep(LOPF_RES_SLEEP);
                 __syncwarp();
                 fence_acq_rel();
                 double ps[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
