@@ -528,6 +528,13 @@ def bench_batch(args):
     value = float(allv[:, 1].sum()) / (max_ms / 1e3)
     if rank == 0:
         peak, peak_src = _peaks()
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:          # the oracle on a bounded sample: one scenario
+            n_cpu = 10 * args.cpu_sweeps
+            rate, secs = cpu_oracle_rate(fg.scale_loads(f, scales[0]), n_cpu)
+            cpu = {"value": rate, "unit": "scenario-iterations/s", "cores": 1, "kind": "oracle",
+                   "sample": f"{n_cpu} oracle sweeps (O6 loop, plain C, -O2, one thread) of scenario 0 from the "
+                             f"initial point; {secs:.1f} s; the oracle solves scenarios one after another"}
         batch_sweeps = float(allv[:, 4].max())                 # launch length = slowest scenario
         us_per_batch_sweep = 1e3 * (max_ms / args.steps) / batch_sweeps
         achieved = sz.alg_bytes / (us_per_batch_sweep * 1e-6) / 1e9
@@ -550,7 +557,7 @@ def bench_batch(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_src, "kernel": "admm_batch_kernel",
                          "alg_bytes_per_batch_sweep": int(sz.alg_bytes), "us_per_batch_sweep": us_per_batch_sweep},
-            "cpu_baseline": None,
+            "cpu_baseline": cpu,
             "e2e": {"value": float(allv[:, 3].sum()) * e2e_steps / float(allv[:, 2].max()), "unit": "scenario-iterations/s",
                     "h2d_bytes_per_step": int(sz.device_bytes), "d2h_bytes_per_step": 64 * (hi - lo), "steps": e2e_steps},
             "clocks": clk.summary(),
