@@ -74,9 +74,9 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def _ncu_traffic():
+def _ncu_traffic(precision: int = 64):
     """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json" if precision == 64 else "ncu_summary_f32.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
@@ -233,7 +233,7 @@ def main():
         mean_kern_ms = statistics.mean(kern_ms)
         mean_iters = statistics.mean(iters)
         achieved = sz.alg_bytes * mean_iters / (mean_kern_ms / 1e3) / 1e9
-        dram, ncu_iters = _ncu_traffic() if sz.kernel == 2 else (None, None)   # the summary is the resident kernel's
+        dram, ncu_iters = _ncu_traffic(args.precision) if sz.kernel == 2 else (None, None)   # resident kernel's
         traffic = (dram / ncu_iters * mean_iters) if (dram and ncu_iters) else None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:

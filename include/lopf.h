@@ -99,8 +99,7 @@ typedef struct {
                               mask (bit 0 global update, bit 1 local/dual update) — results are then NOT the method */
     int32_t precision;     /* 0 or 64: fp64 (the parity path); 32: fp32 operators, iterate and arithmetic — the
                               paper's GPU precision (reading F1).  Residual sums,
-                              the termination test and the objective stay fp64.  Streaming and batch kernels only
-                              (kernel = 2 with precision 32 is LOPF_E_ARG; auto selects streaming). */
+                              the termination test and the objective stay fp64.  All three kernels. */
 } lopf_options;
 
 typedef struct {

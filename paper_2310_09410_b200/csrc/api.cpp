@@ -106,8 +106,6 @@ lopf_status lopf_setup(const lopf_network* net, const lopf_options* opt, lopf_ha
     if (o.trace_every < 0) return fail(LOPF_E_ARG, "trace_every must be >= 0");
     if (o.kernel < 0 || o.kernel > 2) return fail(LOPF_E_ARG, "kernel must be 0 (auto), 1 or 2");
     if (check_precision(o) != LOPF_OK) return LOPF_E_ARG;
-    if (o.precision == 32 && o.kernel == 2)
-        return fail(LOPF_E_ARG, "the resident kernel is fp64 only: use kernel 0 / 1 with precision 32");
     lopf_handle* h = new (std::nothrow) lopf_handle();
     if (!h) return fail(LOPF_E_ARG, "out of host memory");
     h->opt = o;
@@ -122,7 +120,7 @@ lopf_status lopf_setup(const lopf_network* net, const lopf_options* opt, lopf_ha
                 st = pack_streaming(h->net, h->cp, h->opt, kMaxGrid, h->lay, err);
             } else {                                      // auto: operators on chip when they fit (fp64)
                 std::string e2;
-                st = h->opt.precision == 32 ? LOPF_E_ARG : pack_resident(h->net, h->cp, h->opt, h->lay, e2);
+                st = pack_resident(h->net, h->cp, h->opt, h->lay, e2);
                 if (st != LOPF_OK) st = pack_streaming(h->net, h->cp, h->opt, kMaxGrid, h->lay, err);
             }
         }
@@ -388,10 +386,10 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         R.partial = (double*)(b + L.off_partial);
         R.ctrl = (DevCtrl*)(b + L.off_ctrl);
         R.trace = (double*)(b + L.off_trace);
-        R.x = (double*)(b + L.off_x);
+        R.x = b + L.off_x;
         R.obj_idx = (const int32_t*)(b + L.off_objidx);
         R.obj_c = (const double*)(b + L.off_objc);
-        R.x0 = (const double*)(b + L.off_x0r);
+        R.x0 = b + L.off_x0r;
         R.n_exp = L.n_exp;
         R.G = L.G;
         R.n_obj = (int32_t)L.n_obj;
@@ -404,6 +402,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         R.eps_rel = h->opt.eps_rel;
         R.prof = h->opt.reserved[0] ? (long long*)(b + L.off_prof) : nullptr;   // diagnostics switch
         R.skip = h->opt.reserved[1];
+        R.esz = L.esz;
         h->dp = DevProblem{};
         h->dp.ctrl = R.ctrl;
         h->dp.x = R.x;
@@ -644,8 +643,8 @@ static lopf_status fetch_slots(lopf_handle* h, cudaStream_t s, std::vector<doubl
         for (int c = 0; c < L.G; ++c) {
             const CtaHdr& H = L.hdr[c];
             const uint8_t* blob = h->rp.blobs + H.blob_off;
-            CUDA_TRY(cudaMemcpyAsync(xl.data() + H.slot_base, blob + H.off_xl0, 8 * (size_t)H.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
-            CUDA_TRY(cudaMemcpyAsync(lm.data() + H.slot_base, blob + H.off_lam0, 8 * (size_t)H.n_slots, cudaMemcpyDeviceToHost, s), "state D2H");
+            CUDA_TRY(d2h_elems(xl.data() + H.slot_base, blob + H.off_xl0, H.n_slots, L.esz, s), "state D2H");
+            CUDA_TRY(d2h_elems(lm.data() + H.slot_base, blob + H.off_lam0, H.n_slots, L.esz, s), "state D2H");
         }
     }
     CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
@@ -698,9 +697,8 @@ lopf_status lopf_set_state(lopf_handle* h, void* stream, const double* x_loc, co
         for (int c = 0; c < L.G; ++c) {
             const CtaHdr& H = L.hdr[c];
             uint8_t* blob = h->rp.blobs + H.blob_off;
-            const size_t nb = 8 * (size_t)H.n_slots;
-            CUDA_TRY(cudaMemcpyAsync(blob + H.off_xl0, xl.data() + H.slot_base, nb, cudaMemcpyHostToDevice, s), "state H2D");
-            CUDA_TRY(cudaMemcpyAsync(blob + H.off_lam0, lm.data() + H.slot_base, nb, cudaMemcpyHostToDevice, s), "state H2D");
+            CUDA_TRY(h2d_elems(blob + H.off_xl0, xl.data() + H.slot_base, H.n_slots, L.esz, s), "state H2D");
+            CUDA_TRY(h2d_elems(blob + H.off_lam0, lm.data() + H.slot_base, H.n_slots, L.esz, s), "state H2D");
         }
     }
     CUDA_TRY(cudaMemsetAsync(&h->dp.ctrl->total, 0, sizeof(long long), s), "state memset");

@@ -169,10 +169,10 @@ struct ResProblem {                           // resident kernel argument
     unsigned long long* flags;                // [G] sweeps published by each CTA (+1), zeroed per launch
     DevCtrl* ctrl;
     double* trace;
-    double* x;                                // [n] solution
+    void* x;                                  // (T) [n] solution
     const int32_t* obj_idx;
     const double* obj_c;
-    const double* x0;                         // [total slots] initial x_s, blob slot order
+    const void* x0;                           // (T) [total slots] initial x_s, blob slot order
     int32_t n_exp, G, n_obj, test;
     int32_t trace_cap, trace_every, total_slots, max_smem;
     double rho, inv_rho, eps_rel;
@@ -180,6 +180,7 @@ struct ResProblem {                           // resident kernel argument
     long long* prof;                          // diagnostics: [G][4] cycles (work, publish+wait, -, sweeps) or NULL
     int32_t skip;                             // diagnostics: bit 1 skips the update work (sync cost only)
     uint32_t epoch;                           // launch number (> 0): high half of the exchange tags
+    int32_t esz;                              // element size of the SMEM state / blob arrays: 8 fp64, 4 fp32 (F1)
 };
 
 // ---- batch kernel (config 4: lane = scenario, 32 scenarios per CTA group) -----------------------

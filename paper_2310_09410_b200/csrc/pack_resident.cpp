@@ -156,7 +156,7 @@ void split_tasks(const Canon& P, std::vector<TaskR>& tasks, const std::vector<in
 }
 
 // exact SMEM bytes of a chunk (blob + xg scratch); mirrors the blob layout built below
-int64_t chunk_bytes(const Canon& P, const std::vector<int64_t>& subs, std::vector<int32_t>& cnt) {
+int64_t chunk_bytes(const Canon& P, const std::vector<int64_t>& subs, std::vector<int32_t>& cnt, const int64_t E) {
     auto tasks = make_tasks(P, subs);
     int64_t NS = 0, pool = 0, NG = 0, NSEG = 0;
     int kpad = 0;
@@ -170,8 +170,8 @@ int64_t chunk_bytes(const Canon& P, const std::vector<int64_t>& subs, std::vecto
         for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) cnt[P.copy_global[k]] = 0;
     const int64_t NT = (int64_t)tasks.size();
     int64_t b = 0;
-    for (int64_t sz : {8 * pool, 8 * NS, 32 * NG, 16 * NT, 4 * NS, 4 * NS, 4 * (NG + 1), 4 * NSEG, 4 * NG,
-                       (int64_t)4 * 64, 8 * NS, 8 * NS, 8 * NS, 8 * NS, 16 * NG, (int64_t)8 * (64 + kpad) * (kResBlock / 32)})
+    for (int64_t sz : {E * pool, E * NS, 4 * E * NG, 16 * NT, 4 * NS, 4 * NS, 4 * (NG + 1), 4 * NSEG, 4 * NG,
+                       (int64_t)4 * 64, E * NS, E * NS, E * NS, E * NS, 2 * E * NG, E * (64 + kpad) * (kResBlock / 32)})
         b = a16(b + sz);
     return b;
 }
@@ -180,6 +180,8 @@ int64_t chunk_bytes(const Canon& P, const std::vector<int64_t>& subs, std::vecto
 lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt, Layout& L, std::string& err) {
     L = Layout();
     L.kernel = 2;
+    const int64_t E = opt.precision == 32 ? 4 : 8;           // element size of the SMEM state (reading F1)
+    L.esz = (int32_t)E;
     const int max_ctas = opt.max_ctas > 0 ? opt.max_ctas : 148;
     for (int64_t s = 0; s < P.S; ++s)
         if (P.n_s[s] > 64) { err = "resident kernel supports n_s <= 64 (use the streaming kernel)"; return LOPF_E_ARG; }
@@ -190,7 +192,7 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     std::vector<int64_t> est(P.S);
     int64_t total = 0;
     for (int64_t s = 0; s < P.S; ++s) {
-        est[s] = 8LL * P.n_s[s] * P.n_s[s] + 72LL * P.n_s[s];
+        est[s] = E * P.n_s[s] * P.n_s[s] + (40 + 4 * E) * P.n_s[s];
         total += est[s];
     }
     const int warps = kResBlock / 32;
@@ -204,7 +206,7 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         approx_tasks = (rows + 31) / 32;
         G = std::max<int>(G, (int)((approx_tasks + 3 * warps - 1) / (3 * warps)));
     }
-    if (G > max_ctas / 2) G = max_ctas;              // large problems: use every SM
+    if (G > max_ctas / (E == 8 ? 2 : 4)) G = max_ctas;   // large problems: use every SM
     std::vector<Chunk> chunks;
     auto cut = [&](int64_t T, int64_t cap) {
         chunks.assign(1, Chunk{});
@@ -232,7 +234,7 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         if (grew) continue;
         bool ok = true;
         for (auto& c : chunks)
-            if (chunk_bytes(P, c.subs, cnt) > kResSmemBudget) { ok = false; break; }
+            if (chunk_bytes(P, c.subs, cnt, E) > kResSmemBudget) { ok = false; break; }
         if (ok) done = true;
         else if (margin > 0.5) margin *= 0.95;
         else ++G;
@@ -303,9 +305,9 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         std::sort(nbrs.begin(), nbrs.end());
         const int64_t NNB = (int64_t)nbrs.size();
         int32_t o = 0;
-        h.off_abar = o;     o = a16(o + 8 * pool);
-        h.off_bbar = o;     o = a16(o + 8 * NS);
-        h.off_gpar = o;     o = a16(o + 32 * NG);
+        h.off_abar = o;     o = a16(o + E * pool);
+        h.off_bbar = o;     o = a16(o + E * NS);
+        h.off_gpar = o;     o = a16(o + 4 * E * NG);
         h.off_tasks = o;    o = a16(o + 16 * NT);
         h.off_sinfo = o;    o = a16(o + 4 * NS);
         h.off_sexp = o;     o = a16(o + 4 * NS);
@@ -313,13 +315,13 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         h.off_gseg = o;     o = a16(o + 4 * NSEG);
         h.off_gown = o;     o = a16(o + 4 * NG);
         h.off_nbr = o;      o = a16(o + 4 * std::max<int64_t>(NNB, 64));
-        h.off_xl0 = o;      o = a16(o + 8 * NS);
-        h.off_lam0 = o;     o = a16(o + 8 * NS);
+        h.off_xl0 = o;      o = a16(o + E * NS);
+        h.off_lam0 = o;     o = a16(o + E * NS);
         h.blob_bytes = o;
-        h.off_xl1 = o;      o = a16(o + 8 * NS);
-        h.off_lam1 = o;     o = a16(o + 8 * NS);
-        h.off_xout = o;     o = a16(o + 16 * NG);
-        h.off_dst = o;      o = a16(o + 8 * (64 + kpad) * (kResBlock / 32));   // d staging; tail stays 0
+        h.off_xl1 = o;      o = a16(o + E * NS);
+        h.off_lam1 = o;     o = a16(o + E * NS);
+        h.off_xout = o;     o = a16(o + 2 * E * NG);
+        h.off_dst = o;      o = a16(o + E * (64 + kpad) * (kResBlock / 32));   // d staging; tail stays 0
         h.dst_stride = 64 + kpad;
         h.smem_bytes = o;
         if (h.smem_bytes > kResSmemBudget) { err = "internal: chunk exceeds the SMEM budget"; return LOPF_E_ARG; }
@@ -329,11 +331,14 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         max_smem = std::max(max_smem, h.smem_bytes);
         std::vector<uint8_t>& blob = B[c].blob;
         blob.assign(h.blob_bytes, 0);
-        auto D = [&](int32_t off) { return (double*)(blob.data() + off); };
+        auto put = [&](int32_t off, size_t i, double v) {          // (T) arrays: fp64, or rounded once to fp32
+            if (E == 8) reinterpret_cast<double*>(blob.data() + off)[i] = v;
+            else reinterpret_cast<float*>(blob.data() + off)[i] = (float)v;
+        };
         auto I = [&](int32_t off) { return (int32_t*)(blob.data() + off); };
         std::memcpy(blob.data() + h.off_tasks, trec.data(), 16 * NT);
         std::memcpy(blob.data() + h.off_nbr, nbrs.data(), 4 * NNB);
-        double* abar = D(h.off_abar);
+
         int32_t* sinfo = I(h.off_sinfo);
         int32_t* sexp = I(h.off_sexp);
         B[c].x0.assign(NS, 0.0);
@@ -345,7 +350,7 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
                 const double* Ab = &P.abar[P.abar_ptr[s]];
                 const int rows = 32 * tasks[t].R;
                 for (int r = 0; r < ns; ++r)             // row base+r of the tile: tile[k][base + r] = Abar_s[r][k]
-                    for (int k = 0; k < ns; ++k) abar[(size_t)trec[t].z + (size_t)k * rows + base + r] = Ab[(size_t)r * ns + k];
+                    for (int k = 0; k < ns; ++k) put(h.off_abar, (size_t)trec[t].z + (size_t)k * rows + base + r, Ab[(size_t)r * ns + k]);
                 for (int r = 0; r < ns; ++r) {
                     const int64_t slot = trec[t].x + base + r;
                     const int64_t copy = P.sub_ptr[s] + r;
@@ -354,15 +359,15 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
                     sinfo[slot] = (base & 0x3F) | kResValid | (first ? kResFirst : 0) | (ns << kResNsShift) |
                                   (gl_of[g] << kResGlShift);
                     sexp[slot] = xidx[copy];
-                    D(h.off_bbar)[slot] = P.bbar[copy];
-                    D(h.off_xl0)[slot] = P.x0[copy];
+                    put(h.off_bbar, slot, P.bbar[copy]);
+                    put(h.off_xl0, slot, P.x0[copy]);
                     B[c].x0[slot] = P.x0[copy];
                     L.slot_of_copy[copy] = slot_base + (int32_t)slot;
                 }
                 base += ns;
             }
         }
-        double4* gpar = (double4*)(blob.data() + h.off_gpar);
+
         int32_t* segoff = I(h.off_gsegoff);
         int32_t* seg = I(h.off_gseg);
         int32_t* gown = I(h.off_gown);
@@ -370,7 +375,10 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         for (int64_t j = 0; j < NG; ++j) {
             const int32_t g = gl_list[j];
             const double nu = (double)(P.seg_ptr[g + 1] - P.seg_ptr[g]);
-            gpar[j] = make_double4(P.c[g] / opt.rho, 1.0 / nu, P.lo[g], P.hi[g]);
+            put(h.off_gpar, 4 * j, P.c[g] / opt.rho);
+            put(h.off_gpar, 4 * j + 1, 1.0 / nu);
+            put(h.off_gpar, 4 * j + 2, P.lo[g]);
+            put(h.off_gpar, 4 * j + 3, P.hi[g]);
             segoff[j] = q;
             for (int64_t p = P.seg_ptr[g]; p < P.seg_ptr[g + 1]; ++p) {
                 const int32_t k = P.seg_copy[p];                 // canonical ascending copy order
@@ -387,7 +395,7 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     L.n_slots = slot_base;
     for (auto& b : B) L.n_tasks += b.h.n_tasks;
     int64_t pool_all = 0;
-    for (int c = 0; c < L.G; ++c) pool_all += (B[c].h.off_bbar - B[c].h.off_abar) / 8;
+    for (int c = 0; c < L.G; ++c) pool_all += (B[c].h.off_bbar - B[c].h.off_abar) / E;
     L.abar_doubles = pool_all;
 
     // ---- objective, arena ---------------------------------------------------------------------------
@@ -406,8 +414,8 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     L.off_blobs = take(blobs_total);
     L.off_xchg = take(16 * 2 * (size_t)std::max(n_exp, 1));   // {u, tag} per boundary copy and parity
     L.off_flags = take(8 * 32 * (size_t)(L.G + 1));   // one flag per 256-byte line + the published count
-    L.off_x0r = take(8 * (size_t)L.total_slots);
-    L.off_x = take(8 * (size_t)P.n);
+    L.off_x0r = take(E * (size_t)L.total_slots);
+    L.off_x = take(E * (size_t)P.n);
     L.off_partial = take(8 * 8 * 4 * (size_t)L.G);     // 4 sweep slots (lagged decision, see resident.cu)
     L.off_ctrl = take(sizeof(DevCtrl));
     L.off_trace = take(8 * 5 * (size_t)L.trace_cap);
@@ -422,7 +430,11 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     for (int c = 0; c < L.G; ++c) {
         L.hdr[c] = B[c].h;
         std::memcpy(img + L.off_blobs + B[c].h.blob_off, B[c].blob.data(), B[c].blob.size());
-        std::memcpy(img + L.off_x0r + 8 * (size_t)B[c].h.slot_base, B[c].x0.data(), 8 * B[c].x0.size());
+        for (size_t i = 0; i < B[c].x0.size(); ++i) {
+            const size_t at = L.off_x0r + (size_t)E * ((size_t)B[c].h.slot_base + i);
+            if (E == 8) *reinterpret_cast<double*>(img + at) = B[c].x0[i];
+            else *reinterpret_cast<float*>(img + at) = (float)B[c].x0[i];
+        }
         for (int i = 0; i < B[c].h.n_slots; ++i) L.slot_cta[B[c].h.slot_base + i] = c;
     }
     std::memcpy(img + L.off_hdr, L.hdr.data(), sizeof(CtaHdr) * L.G);

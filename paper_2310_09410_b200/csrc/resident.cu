@@ -54,23 +54,28 @@ __device__ __forceinline__ unsigned long long ld_rlx(const unsigned long long* p
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // consensus input u = x_s - lambda / rho, formed with the same rounding wherever it is needed
-__device__ __forceinline__ double u_of(const double x, const double l, const double inv_rho) {
-    return __fma_rn(-l, inv_rho, x);
+template <class T>
+__device__ __forceinline__ T u_of(const T x, const T l, const T inv_rho) {
+    return fma(-l, inv_rho, x);
 }
 
 extern __shared__ __align__(16) uint8_t sm[];
 
 // SMEM accessors on 32-bit byte offsets (LDS/STS with 32-bit addresses, no 64-bit generic pointers)
-__device__ __forceinline__ double& Dd(int off, int i) { return reinterpret_cast<double*>(sm + off)[i]; }
+template <class T> __device__ __forceinline__ T& Dt(int off, int i) { return reinterpret_cast<T*>(sm + off)[i]; }
+template <class T> struct V2;                      // {x, y} pair of T (global parameters in SMEM)
+template <> struct V2<double> { using type = double2; };
+template <> struct V2<float> { using type = float2; };
 __device__ __forceinline__ int Ii(int off, int i) { return reinterpret_cast<const int*>(sm + off)[i]; }
 
+template <class T>                                 // T: element type of the SMEM state (fp64, or fp32: reading F1)
 struct Ctx {                                       // byte offsets into SMEM + the two exchange slots
     int sinfo, sexp, sabar, sbbar, gsegoff, gseg, gpar;
     int xl_c, lam_c, xl_n, lam_n, xout_n, dst;
-    const double2* xch_c;                          // {u, tag} entries of state t / t+1
+    const double2* xch_c;                          // {u, tag} entries of state t / t+1 (u widened to fp64)
     double2* xch_n;
     unsigned long long tag_c, tag_n;
-    double rho, inv_rho;
+    T rho, inv_rho;
 };
 
 __device__ __forceinline__ void st_entry(double2* p, const double u, const unsigned long long tag) {
@@ -87,82 +92,85 @@ __device__ __forceinline__ double ld_entry(const double2* p, const unsigned long
 }
 
 // value of one consensus-segment entry: u of an own copy (SMEM) or of a boundary copy (exchange buffer)
-__device__ __forceinline__ double seg_u(const Ctx& C, const int e) {
-    return e >= 0 ? u_of(Dd(C.xl_c, e), Dd(C.lam_c, e), C.inv_rho) : ld_entry(C.xch_c + (-e - 1), C.tag_c);
+template <class T>
+__device__ __forceinline__ T seg_u(const Ctx<T>& C, const int e) {
+    return e >= 0 ? u_of<T>(Dt<T>(C.xl_c, e), Dt<T>(C.lam_c, e), C.inv_rho) : (T)ld_entry(C.xch_c + (-e - 1), C.tag_c);
 }
 
 // one task of 32R rows (tr.w = R): lane l owns rows l (and l + 32 when R = 2: two dependency chains)
-template <int R>
-__device__ __forceinline__ void task_sweep(const Ctx& C, const int4 tr, double (&acc)[5], const int lane) {
-    double v[2], lam[2], xo[2];
+template <int R, class T>
+__device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, double (&acc)[5], const int lane) {
+    constexpr int E = sizeof(T);
+    using T2 = typename V2<T>::type;
+    T v[2], lam[2], xo[2];
     int info[2];
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         const int slot = tr.x + h * 32 + lane;
         info[h] = Ii(C.sinfo, slot);
-        double d = 0.0;
-        v[h] = lam[h] = xo[h] = 0.0;
+        T d = T(0);
+        v[h] = lam[h] = xo[h] = T(0);
         if (info[h] & kResValid) {
             const int gl = info[h] >> kResGlShift;
             const int q0 = Ii(C.gsegoff, gl), nq = Ii(C.gsegoff, gl + 1) - q0;
             int e[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) e[j] = j < nq ? Ii(C.gseg, q0 + j) : 0;
-            double u[4];
+            T u[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) u[j] = j < nq ? seg_u(C, e[j]) : 0.0;
-            double sigma = 0.0;                                          // canonical copy order
+            for (int j = 0; j < 4; ++j) u[j] = j < nq ? seg_u<T>(C, e[j]) : T(0);
+            T sigma = T(0);                                              // canonical copy order
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 if (j < nq) sigma += u[j];
-            for (int q = 4; q < nq; ++q) sigma += seg_u(C, Ii(C.gseg, q0 + q));
-            const double2 g0 = reinterpret_cast<const double2*>(sm + C.gpar)[2 * gl];       // {c/rho, 1/nu}
-            const double2 g1 = reinterpret_cast<const double2*>(sm + C.gpar)[2 * gl + 1];   // {lo, hi}
-            const double xg = fmin(fmax((sigma - g0.x) * g0.y, g1.x), g1.y);   // IEEE +-inf = no clamp
-            if (info[h] & kResFirst) Dd(C.xout_n, gl) = xg;
+            for (int q = 4; q < nq; ++q) sigma += seg_u<T>(C, Ii(C.gseg, q0 + q));
+            const T2 g0 = reinterpret_cast<const T2*>(sm + C.gpar)[2 * gl];       // {c/rho, 1/nu}
+            const T2 g1 = reinterpret_cast<const T2*>(sm + C.gpar)[2 * gl + 1];   // {lo, hi}
+            const T xg = fmin(fmax((sigma - g0.x) * g0.y, g1.x), g1.y);   // IEEE +-inf = no clamp
+            if (info[h] & kResFirst) Dt<T>(C.xout_n, gl) = xg;
             v[h] = xg;
-            lam[h] = Dd(C.lam_c, slot);
-            xo[h] = Dd(C.xl_c, slot);
+            lam[h] = Dt<T>(C.lam_c, slot);
+            xo[h] = Dt<T>(C.xl_c, slot);
             d = -C.rho * xg - lam[h];
         }
-        Dd(C.dst, h * 32 + lane) = d;
+        Dt<T>(C.dst, h * 32 + lane) = d;
     }
     __syncwarp();
     // local update: x_s = (1/rho) Abar_s d + bbar_s.  The task tile is zero-padded (tile[k][row] = 0 for
-    // k >= n_s of the row's subsystem), so the loop has no masks: 2 tile loads + 2 staged-d loads + 2 DFMA
+    // k >= n_s of the row's subsystem), so the loop has no masks: 2 tile loads + 2 staged-d loads + 2 FMA
     // per column; d indices beyond the subsystem land on finite d values or the zeroed staging tail.
     const int kmax = tr.y;
-    const int at = C.sabar + 8 * (tr.z + lane);                          // byte offset of tile[0][lane]
-    const int d0 = C.dst + 8 * (info[0] & 0x3F), d1 = C.dst + 8 * (info[R - 1] & 0x3F);
-    double ax0 = 0.0, ax1 = 0.0;
+    const int at = C.sabar + E * (tr.z + lane);                          // byte offset of tile[0][lane]
+    const int d0 = C.dst + E * (info[0] & 0x3F), d1 = C.dst + E * (info[R - 1] & 0x3F);
+    T ax0 = T(0), ax1 = T(0);
     if (R == 2) {
 #pragma unroll 4
         for (int k = 0; k < kmax; ++k) {
-            ax0 = fma(Dd(at, 64 * k), Dd(d0, k), ax0);
-            ax1 = fma(Dd(at, 64 * k + 32), Dd(d1, k), ax1);
+            ax0 = fma(Dt<T>(at, 64 * k), Dt<T>(d0, k), ax0);
+            ax1 = fma(Dt<T>(at, 64 * k + 32), Dt<T>(d1, k), ax1);
         }
     } else {
 #pragma unroll 4
-        for (int k = 0; k < kmax; ++k) ax0 = fma(Dd(at, 32 * k), Dd(d0, k), ax0);
+        for (int k = 0; k < kmax; ++k) ax0 = fma(Dt<T>(at, 32 * k), Dt<T>(d0, k), ax0);
     }
-    const double axr[2] = {ax0, ax1};
+    const T axr[2] = {ax0, ax1};
     __syncwarp();                                                        // dst is reused by the next task
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         if (!(info[h] & kResValid)) continue;
         const int slot = tr.x + h * 32 + lane;
-        const double xn = fma(axr[h], C.inv_rho, Dd(C.sbbar, slot));         // (1/rho) Abar d + bbar
-        const double ln = lam[h] + C.rho * (v[h] - xn);                  // ADMM-3
-        Dd(C.xl_n, slot) = xn;
-        Dd(C.lam_n, slot) = ln;
+        const T xn = fma(axr[h], C.inv_rho, Dt<T>(C.sbbar, slot));       // (1/rho) Abar d + bbar
+        const T ln = lam[h] + C.rho * (v[h] - xn);                       // ADMM-3
+        Dt<T>(C.xl_n, slot) = xn;
+        Dt<T>(C.lam_n, slot) = ln;
         const int e = Ii(C.sexp, slot);
-        if (e >= 0) st_entry(C.xch_n + e, u_of(xn, ln, C.inv_rho), C.tag_n);   // boundary copy -> exchange
-        const double r = v[h] - xn, dx = xn - xo[h];
-        acc[0] += r * r;
-        acc[1] += dx * dx;
-        acc[2] += v[h] * v[h];
-        acc[3] += xn * xn;
-        acc[4] += ln * ln;
+        if (e >= 0) st_entry(C.xch_n + e, (double)u_of<T>(xn, ln, C.inv_rho), C.tag_n);   // boundary copy -> exchange
+        const T r = v[h] - xn, dx = xn - xo[h];                          // terms in T, sums in fp64 (F1)
+        acc[0] += (double)(r * r);
+        acc[1] += (double)(dx * dx);
+        acc[2] += (double)(v[h] * v[h]);
+        acc[3] += (double)(xn * xn);
+        acc[4] += (double)(ln * ln);
     }
 }
 
@@ -208,7 +216,9 @@ constexpr int kFlagStride = 32;                    // one flag per 256-byte line
 #define TL(e) do { } while (0)
 #endif
 
+template <class T>
 __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
+    constexpr int E = sizeof(T);
     __shared__ CtaHdr H;
     __shared__ double red[2][RW][5];               // worker sums by sweep parity (reducer reads the older)
     __shared__ double s_res[2][4];                 // decision records double-buffered by sweep parity: the
@@ -231,13 +241,13 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     __syncthreads();
     const int NS = H.n_slots, NG = H.n_glob, NT = H.n_tasks;
     const int dst_stride = H.dst_stride;                              // 64 + largest task width, doubles
-    for (int i = tid; i < RW * dst_stride; i += RB) Dd(H.off_dst, i) = 0.0;   // zero tail of the d staging
-    Ctx C;
+    for (int i = tid; i < RW * dst_stride; i += RB) Dt<T>(H.off_dst, i) = T(0);   // zero tail of the d staging
+    Ctx<T> C;
     C.sinfo = H.off_sinfo; C.sexp = H.off_sexp; C.sabar = H.off_abar; C.sbbar = H.off_bbar;
     C.gsegoff = H.off_gsegoff; C.gseg = H.off_gseg; C.gpar = H.off_gpar;
-    C.dst = H.off_dst + 8 * wid * dst_stride;
-    C.rho = P.rho;
-    C.inv_rho = P.inv_rho;
+    C.dst = H.off_dst + E * wid * dst_stride;
+    C.rho = (T)P.rho;
+    C.inv_rho = (T)P.inv_rho;
     unsigned long long* pub = P.flags + (size_t)G * kFlagStride;       // CTAs x sweeps published
     const long long total0 = *(volatile long long*)&P.ctrl->total;
     const bool prof = P.prof != nullptr;
@@ -250,7 +260,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     // state 0: boundary u into exchange slot 0
     for (int i = tid; i < NS; i += RB) {
         const int e = Ii(H.off_sexp, i);
-        if (e >= 0) st_entry(xchg + e, u_of(Dd(H.off_xl0, i), Dd(H.off_lam0, i), P.inv_rho), tag_of(0));
+        if (e >= 0) st_entry(xchg + e, (double)u_of<T>(Dt<T>(H.off_xl0, i), Dt<T>(H.off_lam0, i), C.inv_rho), tag_of(0));
     }
     __syncthreads();
 
@@ -329,15 +339,15 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                 C.lam_c = cur ? H.off_lam1 : H.off_lam0;
                 C.xl_n = cur ? H.off_xl0 : H.off_xl1;
                 C.lam_n = cur ? H.off_lam0 : H.off_lam1;
-                C.xout_n = H.off_xout + (cur ? 0 : 8 * NG);
+                C.xout_n = H.off_xout + (cur ? 0 : E * NG);
                 C.xch_c = xchg + (size_t)cur * P.n_exp;
                 C.xch_n = xchg + (size_t)(cur ^ 1) * P.n_exp;
                 C.tag_c = tag_of(t);
                 C.tag_n = tag_of(t + 1);
                 for (int task = wid; task < NT; task += NWORK) {
                     const int4 tr = reinterpret_cast<const int4*>(sm + H.off_tasks)[task];
-                    if (tr.w == 1) task_sweep<1>(C, tr, acc, lane);
-                    else task_sweep<2>(C, tr, acc, lane);
+                    if (tr.w == 1) task_sweep<1, T>(C, tr, acc, lane);
+                    else task_sweep<2, T>(C, tr, acc, lane);
                 }
 #if LOPF_RES_TIMELINE == 2
                 if (P.prof && t == 500) {   // task signature of this warp: kmax | tasks << 8 | rows << 16 | xreads << 32
@@ -379,17 +389,17 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     // exit: state t (buffer t & 1) back to the blob, this CTA's x, then one grid barrier for the result
     const int fin = (int)(t & 1);
     {
-        double* gx = (double*)(blob + H.off_xl0);
-        double* gl = (double*)(blob + H.off_lam0);
+        T* gx = (T*)(blob + H.off_xl0);
+        T* gl = (T*)(blob + H.off_lam0);
         const int oxl = fin ? H.off_xl1 : H.off_xl0, olm = fin ? H.off_lam1 : H.off_lam0;
         for (int i = tid; i < NS; i += RB) {
-            __stcg(gx + i, Dd(oxl, i));
-            __stcg(gl + i, Dd(olm, i));
+            __stcg(gx + i, Dt<T>(oxl, i));
+            __stcg(gl + i, Dt<T>(olm, i));
         }
     }
     for (int j = tid; j < NG; j += RB) {
         const int g = Ii(H.off_gown, j);
-        if (g >= 0) __stcg(P.x + g, Dd(H.off_xout, fin * NG + j));
+        if (g >= 0) __stcg(reinterpret_cast<T*>(P.x) + g, Dt<T>(H.off_xout, fin * NG + j));
     }
 #if !LOPF_RES_TIMELINE
     if (prof && tid == 0) {
@@ -405,7 +415,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
             while (ld_acq(&P.ctrl->arrive) < (unsigned long long)G) {
             }
             double obj = 0.0;
-            for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * __ldcg(P.x + P.obj_idx[j]);
+            for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * (double)__ldcg(reinterpret_cast<const T*>(P.x) + P.obj_idx[j]);
             DevCtrl* c = P.ctrl;
             const int q = (int)(t & 1);
             c->res[0] = s_res[q][0]; c->res[1] = s_res[q][1]; c->res[2] = s_res[q][2]; c->res[3] = s_res[q][3];
@@ -419,15 +429,16 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
 }
 
 // a3 for the resident layout: x_s = x0, lambda = 0 in every blob; sweep counter 0.
+template <class T>
 __global__ void reset_resident_kernel(ResProblem P) {
     const CtaHdr& H = P.hdr[blockIdx.x];
     uint8_t* blob = P.blobs + H.blob_off;
-    double* xl = (double*)(blob + H.off_xl0);
-    double* lam = (double*)(blob + H.off_lam0);
-    const double* x0 = P.x0 + H.slot_base;
+    T* xl = (T*)(blob + H.off_xl0);
+    T* lam = (T*)(blob + H.off_lam0);
+    const T* x0 = reinterpret_cast<const T*>(P.x0) + H.slot_base;
     for (int i = threadIdx.x; i < H.n_slots; i += blockDim.x) {
         xl[i] = x0[i];
-        lam[i] = 0.0;
+        lam[i] = T(0);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         P.ctrl->arrive = 0; P.ctrl->flag = 0; P.ctrl->total = 0; P.ctrl->iters = 0; P.ctrl->trace_rows = 0;
@@ -447,21 +458,23 @@ lopf_status resident_capacity(int* sms, int* smem_optin, std::string& err) {
 
 lopf_status launch_resident(const ResProblem& P, void* stream, std::string& err) {
     cudaStream_t s = (cudaStream_t)stream;
-    cudaError_t e = cudaFuncSetAttribute(admm_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P.max_smem);
+    const void* k = P.esz == 4 ? (const void*)admm_resident_kernel<float> : (const void*)admm_resident_kernel<double>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, P.max_smem);
     if (e == cudaSuccess) e = cudaMemsetAsync(P.ctrl, 0, 2 * sizeof(unsigned long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(&P.ctrl->trace_rows, 0, sizeof(long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(P.flags, 0, sizeof(unsigned long long) * 32 * (P.G + 1), s);
     if (e == cudaSuccess && P.max_iter > 0) {
         ResProblem Q = P;
         void* args[] = {&Q};
-        e = cudaLaunchCooperativeKernel((const void*)admm_resident_kernel, dim3(P.G), dim3(RB), args, P.max_smem, s);
+        e = cudaLaunchCooperativeKernel(k, dim3(P.G), dim3(RB), args, P.max_smem, s);
     }
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;
 }
 
 lopf_status launch_reset_resident(const ResProblem& P, void* stream, std::string& err) {
-    reset_resident_kernel<<<P.G, 256, 0, (cudaStream_t)stream>>>(P);
+    if (P.esz == 4) reset_resident_kernel<float><<<P.G, 256, 0, (cudaStream_t)stream>>>(P);
+    else reset_resident_kernel<double><<<P.G, 256, 0, (cudaStream_t)stream>>>(P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;

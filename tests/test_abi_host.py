@@ -148,14 +148,14 @@ def test_kernel_selection():
 
 
 def test_precision_option():
-    """fp32 variant (reading F1): selects the streaming layout, halves the (T) bytes of the byte model;
-    an unknown precision or fp32 on the fp64-only resident kernel is LOPF_E_ARG."""
+    """fp32 variant (reading F1): every kernel has an fp32 layout with half the (T) bytes of the byte model
+    and a smaller arena; an unknown precision is LOPF_E_ARG."""
     f = fg.make_feeder("123")
-    s64 = Lopf.setup(f, kernel=1).sizes
-    s32 = Lopf.setup(f, precision=32).sizes
-    assert s32.kernel == 1 and s32.device_bytes < s64.device_bytes
-    int_bytes = 4 * (2 * s64.n_copies + s64.n + 1)
-    assert (s32.alg_bytes - int_bytes) * 2 == s64.alg_bytes - int_bytes
-    for bad in (dict(precision=16), dict(precision=32, kernel=2)):
-        with pytest.raises(Exception):
-            Lopf.setup(f, **bad)
+    for kernel in (1, 2):
+        s64 = Lopf.setup(f, kernel=kernel).sizes
+        s32 = Lopf.setup(f, kernel=kernel, precision=32).sizes
+        assert s32.kernel == s64.kernel == kernel and s32.device_bytes < s64.device_bytes
+        int_bytes = 4 * (2 * s64.n_copies + s64.n + 1)
+        assert (s32.alg_bytes - int_bytes) * 2 == s64.alg_bytes - int_bytes
+    with pytest.raises(Exception):
+        Lopf.setup(f, precision=16)

@@ -1,5 +1,5 @@
 """fp32 variant on the GPU (reading F1): the paper's GPU precision
-(PAPER.md:414, 499-501).  The streaming and batch kernels instantiated for float are compared with the
+(PAPER.md:414, 499-501).  The resident, streaming and batch kernels instantiated for float are compared with the
 oracle's binary32 loop (`oracle.run_k_f32` / `solve_f32`, pinned in tests/test_oracle_f32.py) on the
 same seeded inputs.
 
@@ -54,12 +54,16 @@ def _rel(a, b):
     return float(np.abs(a - b).max() / max(1.0, np.abs(b).max()))
 
 
+KERNELS = [1, 2]          # 1 streaming, 2 resident
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("shape,ks", [("13", (1, 10, 100)), ("123", (1, 10, 100)), ("8500", (1, 20))])
-def test_f32_fixed_k_iterates(torch_cuda, shape, ks):
+def test_f32_fixed_k_iterates(torch_cuda, shape, ks, kernel):
     from paper_2310_09410_b200 import Lopf
     f, p = _problem(shape)
-    h = Lopf.setup(f, precision=32).bind("cuda")
-    assert h.sizes.kernel == 1                     # fp32 runs on the streaming kernel
+    h = Lopf.setup(f, precision=32, kernel=kernel).bind("cuda")
+    assert h.sizes.kernel == kernel
     done = 0
     for k in ks:
         h.run(k - done)
@@ -76,12 +80,13 @@ def test_f32_fixed_k_iterates(torch_cuda, shape, ks):
         assert np.all(xl.astype(np.float32).astype(np.float64) == xl)
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("shape", ["13", "123", "8500"])
-def test_f32_iterations_to_tolerance(torch_cuda, shape):
+def test_f32_iterations_to_tolerance(torch_cuda, shape, kernel):
     from paper_2310_09410_b200 import CONVERGED, Lopf
     f, p = _problem(shape)
     g = GOLD[shape]
-    h = Lopf.setup(f, precision=32).bind("cuda")
+    h = Lopf.setup(f, precision=32, kernel=kernel).bind("cuda")
     r = h.solve()
     o = oracle.solve_f32(p)
     assert r.outcome == CONVERGED and o.converged
@@ -108,9 +113,3 @@ def test_f32_batch_fixed_k(torch_cuda):
         tol = _bound(p, 100)
         assert _rel(x, o.x) <= tol and _rel(xl, o.x_loc) <= tol and _rel(lam / 100.0, o.lam / 100.0) <= tol, sc
 
-
-def test_f32_resident_rejected(torch_cuda):
-    from paper_2310_09410_b200 import Lopf
-    f, _ = _problem("13")
-    with pytest.raises(Exception):
-        Lopf.setup(f, precision=32, kernel=2)
