@@ -54,3 +54,30 @@ def test_solve_to_tolerance_per_scenario(batch):
         assert abs(r["objective"][sc] - o.objective) <= 1e-6 * abs(o.objective)
         x, _, _ = h.get_state_scen(sc)
         assert np.all(x >= p.lp.lo) and np.all(x <= p.lp.hi)
+
+
+def test_full_4096_batch_sampled():
+    """BASELINE configs[3] at full size in the bench's launch configuration: 4096 scenarios in one batch
+    handle; sampled scenarios (first, middle, last) against the oracle run on that scenario alone --
+    iterates after a fixed K (1e-9 relative) and the iteration count to (termination), bit-exact."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2310_09410_b200 import Lopf
+    f = fg.make_feeder("123")
+    K = fg.scenario_scales(f, 4096)
+    h = Lopf.setup_batch(f, K).bind("cuda")
+    h.run(60)
+    samples = (0, 2047, 4095)
+    probs = {sc: oracle.build_problem(fg.scale_loads(f, K[sc])) for sc in samples}
+    for sc in samples:
+        o = oracle.run_k(probs[sc], 60)
+        x, xl, lam = h.get_state_scen(sc)
+        assert _rel(x, o.x) <= TOL and _rel(xl, o.x_loc) <= TOL and _rel(lam, o.lam) <= TOL, sc
+    h.reset()
+    h.solve()
+    r = h.get_batch_results()
+    assert np.all(r["outcome"] == 0)
+    for sc in (0, 4095):
+        o = oracle.solve(probs[sc])
+        assert int(r["iters"][sc]) == o.iters, (sc, int(r["iters"][sc]), o.iters)
