@@ -104,36 +104,44 @@ __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, doubl
     using T2 = typename V2<T>::type;
     T v[2], lam[2], xo[2];
     int info[2];
+    // a4 for both rows without per-row branches (invalid rows read global 0 and are discarded), so the
+    // SMEM dependency chains of the two rows interleave; only a boundary entry leaves the straight line
+    int gl[2], q0[2], nq[2], e[2][4];
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        info[h] = Ii(C.sinfo, tr.x + h * 32 + lane);
+        const bool val = info[h] & kResValid;
+        gl[h] = val ? info[h] >> kResGlShift : 0;
+        q0[h] = Ii(C.gsegoff, gl[h]);
+        nq[h] = val ? Ii(C.gsegoff, gl[h] + 1) - q0[h] : 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) e[h][j] = Ii(C.gseg, q0[h] + (j < nq[h] ? j : 0));
+    }
+    T sig[2];
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        sig[h] = T(0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int ee = e[h][j] >= 0 ? e[h][j] : 0;
+            T u = u_of<T>(Dt<T>(C.xl_c, ee), Dt<T>(C.lam_c, ee), C.inv_rho);
+            if (j < nq[h] && e[h][j] < 0) u = (T)ld_entry(C.xch_c + (-e[h][j] - 1), C.tag_c);
+            if (j < nq[h]) sig[h] += u;                                  // canonical copy order
+        }
+    }
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         const int slot = tr.x + h * 32 + lane;
-        info[h] = Ii(C.sinfo, slot);
-        T d = T(0);
-        v[h] = lam[h] = xo[h] = T(0);
-        if (info[h] & kResValid) {
-            const int gl = info[h] >> kResGlShift;
-            const int q0 = Ii(C.gsegoff, gl), nq = Ii(C.gsegoff, gl + 1) - q0;
-            int e[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) e[j] = j < nq ? Ii(C.gseg, q0 + j) : 0;
-            T u[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) u[j] = j < nq ? seg_u<T>(C, e[j]) : T(0);
-            T sigma = T(0);                                              // canonical copy order
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (j < nq) sigma += u[j];
-            for (int q = 4; q < nq; ++q) sigma += seg_u<T>(C, Ii(C.gseg, q0 + q));
-            const T2 g0 = reinterpret_cast<const T2*>(sm + C.gpar)[2 * gl];       // {c/rho, 1/nu}
-            const T2 g1 = reinterpret_cast<const T2*>(sm + C.gpar)[2 * gl + 1];   // {lo, hi}
-            const T xg = fmin(fmax((sigma - g0.x) * g0.y, g1.x), g1.y);   // IEEE +-inf = no clamp
-            if (info[h] & kResFirst) Dt<T>(C.xout_n, gl) = xg;
-            v[h] = xg;
-            lam[h] = Dt<T>(C.lam_c, slot);
-            xo[h] = Dt<T>(C.xl_c, slot);
-            d = -C.rho * xg - lam[h];
-        }
-        Dt<T>(C.dst, h * 32 + lane) = d;
+        for (int q = 4; q < nq[h]; ++q) sig[h] += seg_u<T>(C, Ii(C.gseg, q0[h] + q));
+        const T2 g0 = reinterpret_cast<const T2*>(sm + C.gpar)[2 * gl[h]];       // {c/rho, 1/nu}
+        const T2 g1 = reinterpret_cast<const T2*>(sm + C.gpar)[2 * gl[h] + 1];   // {lo, hi}
+        const T xg = fmin(fmax((sig[h] - g0.x) * g0.y, g1.x), g1.y);   // IEEE +-inf = no clamp
+        const bool val = info[h] & kResValid;
+        if (val && (info[h] & kResFirst)) Dt<T>(C.xout_n, gl[h]) = xg;
+        v[h] = val ? xg : T(0);
+        lam[h] = val ? Dt<T>(C.lam_c, slot) : T(0);
+        xo[h] = val ? Dt<T>(C.xl_c, slot) : T(0);
+        Dt<T>(C.dst, h * 32 + lane) = val ? -C.rho * xg - lam[h] : T(0);
     }
     __syncwarp();
     // local update: x_s = (1/rho) Abar_s d + bbar_s.  The task tile is zero-padded (tile[k][row] = 0 for
@@ -156,9 +164,8 @@ __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, doubl
     const T axr[2] = {ax0, ax1};
     __syncwarp();                                                        // dst is reused by the next task
 #pragma unroll
-    for (int h = 0; h < R; ++h) {
-        if (!(info[h] & kResValid)) continue;
-        const int slot = tr.x + h * 32 + lane;
+    for (int h = 0; h < R; ++h) {      // no branch on validity: an empty row has a zero tile row, b-bar and d,
+        const int slot = tr.x + h * 32 + lane;   // so it stores zeros and adds exact zeros to the sums
         const T xn = fma(axr[h], C.inv_rho, Dt<T>(C.sbbar, slot));       // (1/rho) Abar d + bbar
         const T ln = lam[h] + C.rho * (v[h] - xn);                       // ADMM-3
         Dt<T>(C.xl_n, slot) = xn;
