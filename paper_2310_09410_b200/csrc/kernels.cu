@@ -163,14 +163,16 @@ __device__ __forceinline__ T consensus(const DevProblem& P, const int inf, const
 template <class T>
 __device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, const int slot, const T ax, const T bb,
                                             const T v, const T lam, const T xo, T* __restrict__ unext,
-                                            double (&acc)[5]) {
+                                            double (&acc)[5], const bool val = true) {
     const T rho = (T)P.rho, inv_rho = (T)P.inv_rho;
     const T xn = fma(ax, inv_rho, bb);                                 // (1/rho) Abar d + bbar
     const T ln = lam + rho * (v - xn);                                 // ADMM-3
-    __stcs(reinterpret_cast<T*>(P.xl) + slot, xn);
-    __stcs(reinterpret_cast<T*>(P.lam) + slot, ln);
     const T un = xn - ln * inv_rho;                                    // next consensus input
-    unext[slot] = un;
+    if (val) {
+        __stcs(reinterpret_cast<T*>(P.xl) + slot, xn);
+        __stcs(reinterpret_cast<T*>(P.lam) + slot, ln);
+        unext[slot] = un;
+    }
     if (inf & kInfoExport) __stcg(P.xbuf + __ldg(P.s_exp + slot), (double)un);   // partitioned: to the other ranks
     const T rr = v - xn, dx = xn - xo;
     acc[0] += (double)(rr * rr);
@@ -227,30 +229,21 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
         cr[h] = val && (info[h] & kInfoCost) ? __ldg(reinterpret_cast<const T*>(P.gcost) + g[h]) : T(0);
     }
 #pragma unroll
-    for (int h = 0; h < R; ++h) {
+    for (int h = 0; h < R; ++h) {      // branch-free for the inline case (absent entries are exact zeros)
         const int j = h * 32 + lane;
-        v[h] = T(0);
-        T d = T(0);
-        if (info[h] & kInfoValid) {
-            T sigma, inv;
-            if (info[h] & kInfoInline) {
-                const int nu = (info[h] >> kInfoNuShift) & 0xF;
-                sigma = ua[h][0];                                  // ascending canonical copy order
-                if (nu > 1) sigma += ua[h][1];
-                if (nu > 2) sigma += ua[h][2];
-                if (nu > 3) sigma += ua[h][3];
-                inv = inv_nu[nu];
-            } else {
-                const int q0 = __ldg(P.seg_ptr + g[h]), q1 = __ldg(P.seg_ptr + g[h] + 1);
-                sigma = T(0);
-                for (int q = q0; q < q1; ++q) sigma += __ldcg(ucur + __ldg(P.seg_slot + q));
-                inv = q1 - q0 < kInvNu ? inv_nu[q1 - q0] : T(1) / (T)(q1 - q0);
-            }
-            v[h] = fmin(fmax((sigma - cr[h]) * inv, lo[h]), hi[h]);   // closed_1; IEEE +-inf = no clamp
-            if (info[h] & kInfoFirst) reinterpret_cast<T*>(P.x)[g[h]] = v[h];
-            d = -rho * v[h] - s_lam[j];
+        const bool val = info[h] & kInfoValid;
+        const int nu = (info[h] >> kInfoNuShift) & 0xF;
+        T sigma = ((ua[h][0] + ua[h][1]) + ua[h][2]) + ua[h][3];      // ascending canonical copy order
+        T inv = inv_nu[nu];
+        if (val && !(info[h] & kInfoInline)) {                         // nu > 4: the CSR segment
+            const int q0 = __ldg(P.seg_ptr + g[h]), q1 = __ldg(P.seg_ptr + g[h] + 1);
+            sigma = T(0);
+            for (int q = q0; q < q1; ++q) sigma += __ldcg(ucur + __ldg(P.seg_slot + q));
+            inv = q1 - q0 < kInvNu ? inv_nu[q1 - q0] : T(1) / (T)(q1 - q0);
         }
-        dsm[j] = d;
+        v[h] = fmin(fmax((sigma - cr[h]) * inv, lo[h]), hi[h]);       // closed_1; IEEE +-inf = no clamp
+        if (val && (info[h] & kInfoFirst)) reinterpret_cast<T*>(P.x)[g[h]] = v[h];
+        dsm[j] = val ? -rho * v[h] - s_lam[j] : T(0);
         ax[h] = T(0);
     }
     __syncwarp();
@@ -276,13 +269,14 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
         }
     }
 #pragma unroll
-    for (int h = 0; h < R; ++h) {
-        if (!(info[h] & kInfoValid)) continue;
+    for (int h = 0; h < R; ++h) {      // an empty slot has ax = b-bar = v = lambda = 0: exact zeros, no stores
         const int j = h * 32 + lane;
+        const bool val = info[h] & kInfoValid;
         // b-bar follows the subsystem's triangle in the block when nonzero
         const T bb = (info[h] & kInfoBbar)
                          ? S[((unsigned)info[h] >> kInfoPoffShift) + ns[h] * (ns[h] + 1) / 2 + r[h]] : T(0);
-        finish_slot<T>(P, info[h], tr.x + j, ax[h], bb, v[h], s_lam[j], s_xl[j], unext, acc);
+        finish_slot<T>(P, info[h], tr.x + j, ax[h], bb, v[h], val ? s_lam[j] : T(0), val ? s_xl[j] : T(0), unext,
+                       acc, val);
     }
     __syncwarp();
 }
