@@ -80,6 +80,8 @@ def _ncu_traffic(precision: int = 64):
     try:
         with open(p) as fh:
             d = json.load(fh)
+        if "dram_bytes_per_sweep" in d:                   # tools/ncu_json.py summaries
+            return d["dram_bytes_per_sweep"] * d["sweeps_per_launch"], d["sweeps_per_launch"]
         return d.get("dram_bytes_per_launch"), d.get("iters_per_launch")
     except Exception:
         return None, None

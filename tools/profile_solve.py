@@ -14,8 +14,9 @@ ap.add_argument("--shape", default="8500")
 ap.add_argument("--kernel", type=int, default=0)
 ap.add_argument("--solves", type=int, default=3)
 ap.add_argument("--iters", type=int, default=0, help="fixed sweeps per launch (0 = solve to tolerance)")
+ap.add_argument("--precision", type=int, default=64)
 a = ap.parse_args()
-h = Lopf.setup(fg.make_feeder(a.shape), kernel=a.kernel).bind("cuda")
+h = Lopf.setup(fg.make_feeder(a.shape), kernel=a.kernel, precision=a.precision).bind("cuda")
 for i in range(a.solves):
     h.reset()
     r = h.run(a.iters, test=False) if a.iters else h.solve()
