@@ -109,7 +109,7 @@ def main():
     ap.add_argument("--kernel", type=int, default=0)
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="32: the fp32 variant (the paper's GPU precision, PAPER.md:414; streaming/batch kernels)")
-    ap.add_argument("--cpu-sweeps", type=int, default=2000, help="oracle sweeps timed for cpu_baseline")
+    ap.add_argument("--cpu-sweeps", type=int, default=6000, help="oracle sweeps timed for cpu_baseline (~10 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sweeps", type=int, default=100, help="oracle sweeps per step for --impl reference")
     ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5],
@@ -411,14 +411,15 @@ def bench_stitched(args):
         if world == 1 and not args.no_cpu_baseline:
             import oracle
             sub = fg.make_stitched(2, "8500")
+            n5 = max(1, args.cpu_sweeps // 3)              # ~3 ms per oracle sweep of 2 x 8500: ~6-10 s
             p = oracle.build_problem(sub)
             x0 = oracle.initial_state(p)
             tt = time.perf_counter()
-            oracle.run_k(p, 20, state=x0)
+            oracle.run_k(p, n5, state=x0)
             dt = time.perf_counter() - tt
-            rate = 20 / dt * (2.0 / args.n_sub)
+            rate = n5 / dt * (2.0 / args.n_sub)
             cpu = {"value": rate, "unit": "iterations/s", "cores": 1, "kind": "oracle",
-                   "sample": f"20 oracle sweeps of the 2 x 8500 stitched feeder ({dt:.1f} s), rate scaled by 2/{args.n_sub} "
+                   "sample": f"{n5} oracle sweeps of the 2 x 8500 stitched feeder ({dt:.1f} s), rate scaled by 2/{args.n_sub} "
                              f"to the full instance (extrapolated, linear in size)"}
         dram = None
         try:
@@ -532,14 +533,17 @@ def bench_batch(args):
         peak, peak_src = _peaks()
         cpu = None
         if world == 1 and not args.no_cpu_baseline:          # the oracle on a bounded sample: one scenario
-            n_cpu = 10 * args.cpu_sweeps
+            n_cpu = 50 * args.cpu_sweeps
             rate, secs = cpu_oracle_rate(fg.scale_loads(f, scales[0]), n_cpu)
             cpu = {"value": rate, "unit": "scenario-iterations/s", "cores": 1, "kind": "oracle",
                    "sample": f"{n_cpu} oracle sweeps (O6 loop, plain C, -O2, one thread) of scenario 0 from the "
                              f"initial point; {secs:.1f} s; the oracle solves scenarios one after another"}
         batch_sweeps = float(allv[:, 4].max())                 # launch length = slowest scenario
         us_per_batch_sweep = 1e3 * (max_ms / args.steps) / batch_sweeps
-        achieved = sz.alg_bytes / (us_per_batch_sweep * 1e-6) / 1e9
+        # bytes actually moved: converged scenarios freeze, so a batch sweep carries the active share of the
+        # per-scenario bytes (sum of per-scenario K over scenarios x max K); the shared operators are <2%
+        active = float(allv[:, 3].sum()) / (args.n_scen * batch_sweeps)
+        achieved = sz.alg_bytes * active / (us_per_batch_sweep * 1e-6) / 1e9
         traffic = None                                  # ncu dram bytes per batch sweep (committed summary)
         try:
             suffix = "_f32" if args.precision == 32 else ""
@@ -558,7 +562,8 @@ def bench_batch(args):
                        "l2": "flushed between steps (512 MiB write)", "setup_s": round(setup_s, 1)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_src, "kernel": "admm_batch_kernel",
-                         "alg_bytes_per_batch_sweep": int(sz.alg_bytes), "us_per_batch_sweep": us_per_batch_sweep},
+                         "alg_bytes_per_batch_sweep": int(sz.alg_bytes), "active_fraction": active,
+                         "us_per_batch_sweep": us_per_batch_sweep},
             "cpu_baseline": cpu,
             "e2e": {"value": float(allv[:, 3].sum()) * e2e_steps / float(allv[:, 2].max()), "unit": "scenario-iterations/s",
                     "h2d_bytes_per_step": int(sz.device_bytes), "d2h_bytes_per_step": 64 * (hi - lo), "steps": e2e_steps},
