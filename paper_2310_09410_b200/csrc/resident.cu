@@ -91,6 +91,11 @@ __device__ __forceinline__ double ld_entry(const double2* p, const unsigned long
     return __longlong_as_double(lo);
 }
 
+__device__ __forceinline__ void ld_entry_once(const double2* p, unsigned long long& lo, unsigned long long& hi) {
+    asm volatile("{\n .reg .b128 v;\n ld.relaxed.gpu.global.b128 v, [%2];\n mov.b128 {%0, %1}, v;\n}"
+                 : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
+}
+
 // value of one consensus-segment entry: u of an own copy (SMEM) or of a boundary copy (exchange buffer)
 template <class T>
 __device__ __forceinline__ T seg_u(const Ctx<T>& C, const int e) {
@@ -117,6 +122,21 @@ __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, doubl
 #pragma unroll
         for (int j = 0; j < 4; ++j) e[h][j] = Ii(C.gseg, q0[h] + (j < nq[h] ? j : 0));
     }
+    // the first boundary entry of each row is requested before any is consumed (one L2 round trip for
+    // both rows instead of one per row; a second boundary entry of a row, rare, is read on its own)
+    int jx[2], ex[2];
+    unsigned long long xlo[2], xhi[2];
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+        jx[h] = 4;
+        ex[h] = -1;
+#pragma unroll
+        for (int j = 3; j >= 0; --j)
+            if (j < nq[h] && e[h][j] < 0) { jx[h] = j; ex[h] = e[h][j]; }
+        xlo[h] = 0ull;
+        xhi[h] = C.tag_c;
+        if (jx[h] < 4) ld_entry_once(C.xch_c + (-ex[h] - 1), xlo[h], xhi[h]);
+    }
     T sig[2];
 #pragma unroll
     for (int h = 0; h < R; ++h) {
@@ -125,7 +145,12 @@ __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, doubl
         for (int j = 0; j < 4; ++j) {
             const int ee = e[h][j] >= 0 ? e[h][j] : 0;
             T u = u_of<T>(Dt<T>(C.xl_c, ee), Dt<T>(C.lam_c, ee), C.inv_rho);
-            if (j < nq[h] && e[h][j] < 0) u = (T)ld_entry(C.xch_c + (-e[h][j] - 1), C.tag_c);
+            if (j == jx[h]) {
+                while (xhi[h] != C.tag_c) ld_entry_once(C.xch_c + (-ex[h] - 1), xlo[h], xhi[h]);
+                u = (T)__longlong_as_double((long long)xlo[h]);
+            } else if (j < nq[h] && e[h][j] < 0) {
+                u = (T)ld_entry(C.xch_c + (-e[h][j] - 1), C.tag_c);
+            }
             if (j < nq[h]) sig[h] += u;                                  // canonical copy order
         }
     }
