@@ -117,6 +117,8 @@ def main():
                          "123 shape, sharded; 5: 64 x 8500 stitched feeder, partitioned over the ranks")
     ap.add_argument("--sweeps", type=int, default=500, help="config 5: sweeps per step (fixed K, test off)")
     ap.add_argument("--n-sub", type=int, default=64, help="config 5: stitched subfeeders")
+    ap.add_argument("--graph-block", type=int, default=50,
+                    help="config 5 under torchrun: sweeps per captured CUDA graph (0 = host-launched sweeps)")
     ap.add_argument("--n-scen", type=int, default=4096, help="config 4: scenarios")
     args = ap.parse_args()
     if args.config == 5:
@@ -341,7 +343,7 @@ def bench_stitched(args):
         solver = None
     else:
         solver = PartitionedSolver(feeder, device=dev, bus_owner=fg.stitched_bus_owner(feeder, world), max_iter=100_000,
-                                   precision=args.precision)
+                                   precision=args.precision, graph_block=args.graph_block)
         h = solver.h
     setup_s = time.perf_counter() - t0
     sz = h.sizes
@@ -357,8 +359,7 @@ def bench_stitched(args):
         if solver is None:
             h.solve_async(k, False)
         else:
-            for _ in range(k):
-                solver.sweep()
+            solver.sweeps(k)
 
     for _ in range(args.warmup):
         step(args.sweeps)
@@ -395,8 +396,7 @@ def bench_stitched(args):
         if solver is None:
             h.run(args.sweeps)
         else:
-            for _ in range(args.sweeps):
-                solver.sweep()
+            solver.sweeps(args.sweeps)
         x = h.get_x()
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t

@@ -22,10 +22,17 @@ class PartitionedSolver:
     """This rank's share of a partitioned feeder.  All ranks construct it with the same feeder and
     options; `solve` / `run` are collective calls."""
 
-    def __init__(self, feeder, group=None, device=None, bus_owner=None, rank=None, world=None, **opts):
+    def __init__(self, feeder, group=None, device=None, bus_owner=None, rank=None, world=None, graph_block=0,
+                 always_reduce=False, **opts):
+        """graph_block > 0: `sweeps` / `run` replay a CUDA graph of `graph_block` captured sweeps (launch,
+        allreduce, import per sweep) instead of launching every sweep from the host.  always_reduce: run the
+        allreduce even with one rank (tests the captured collective on a single GPU)."""
         import torch
         import torch.distributed as dist
         self.group = group
+        self.graph_block = int(graph_block)
+        self.always_reduce = bool(always_reduce)
+        self._graph = None
         if rank is None:
             rank = dist.get_rank(group) if dist.is_initialized() else 0
             world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -36,7 +43,7 @@ class PartitionedSolver:
         self.xbuf = self.h.exchange()
 
     def _allreduce(self):
-        if self.world > 1:
+        if self.world > 1 or self.always_reduce:
             import torch.distributed as dist
             dist.all_reduce(self.xbuf, group=self.group)
 
@@ -49,15 +56,47 @@ class PartitionedSolver:
     def reset(self, stream=None):
         self.h.reset(stream)
 
+    def _captured(self):
+        """The CUDA graph of graph_block sweeps (captured once; the arena, and so every kernel argument,
+        stays where bind put it).  The sweep count lives on the device, so replays continue the iteration,
+        and after (termination) every captured kernel returns at once."""
+        import torch
+        if self._graph is None:
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):                # warm the collective outside the capture
+                self._allreduce()
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            self.xbuf.zero_()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(self.graph_block):
+                    self.sweep()
+            self._graph = g
+        return self._graph
+
+    def sweeps(self, k: int, stream=None):
+        """k sweeps on every rank (collective): graph replays of graph_block sweeps, then single sweeps."""
+        done = 0
+        if self.graph_block > 0:
+            g = self._captured()
+            while k - done >= self.graph_block:
+                g.replay()
+                done += self.graph_block
+        for _ in range(k - done):
+            self.sweep(stream)
+
     def run(self, k: int, check_every: int = 64, stream=None):
         """Up to k sweeps, stopping early at (termination); polls the device result every
         `check_every` sweeps (the kernels become no-ops once the test has fired)."""
+        if self.graph_block > 0:
+            check_every = max(self.graph_block, check_every // self.graph_block * self.graph_block)
         done = 0
         r = None
         while done < k:
             n = min(check_every, k - done)
-            for _ in range(n):
-                self.sweep(stream)
+            self.sweeps(n, stream)
             done += n
             r = self.h.result_get(stream)
             if r.outcome == CONVERGED:

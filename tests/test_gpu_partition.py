@@ -78,3 +78,36 @@ def test_partitioned_k_to_tolerance(torch_cuda, key, world):
     obj = sum(r.objective for r in rs)
     assert abs(obj - g["objective"]) <= 1e-6 * abs(g["objective"])
     assert len({(r.pres, r.dres, r.eps_prim, r.eps_dual) for r in rs}) == 1        # one decision everywhere
+
+
+def test_graph_captured_sweeps_with_nccl(torch_cuda):
+    """The partitioned loop as a CUDA graph (PartitionedSolver(graph_block=...)): per captured sweep the
+    cooperative sweep launch, an NCCL sum-allreduce of the exchange buffer (a one-rank NCCL group, so no
+    kernel waits on another GPU) and the import launch.  Graph replays must equal host-launched sweeps bit
+    for bit, and the solve must stop at the golden K with the golden objective."""
+    import socket
+
+    import torch.distributed as dist
+    from paper_2310_09410_b200.partition import PartitionedSolver
+    own = not dist.is_initialized()
+    if own:
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        f = _feeder("s2x8500")
+        g = GOLD["s2x8500"]
+        eager = PartitionedSolver(f, rank=0, world=1, always_reduce=True)
+        graph = PartitionedSolver(f, rank=0, world=1, always_reduce=True, graph_block=25)
+        eager.sweeps(60)
+        graph.sweeps(60)                                  # two replays + ten host-launched sweeps
+        for a, b in zip(eager.h.get_state(), graph.h.get_state()):
+            assert np.array_equal(a, b)
+        graph.reset()
+        r = graph.run(200_000, check_every=500)
+        assert r.outcome == CONVERGED and r.iters == g["iters"], (r.outcome, r.iters)
+        assert abs(r.objective - g["objective"]) <= 1e-6 * abs(g["objective"])
+    finally:
+        if own:
+            dist.destroy_process_group()
