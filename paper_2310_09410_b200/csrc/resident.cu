@@ -36,9 +36,13 @@ constexpr int RW = RB / 32;
 constexpr int NWORK = RW - 1;              // worker warps 0 .. RW-2
 constexpr int RED = RW - 1;                // reducer warp
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef LOPF_RES_UNROLL
+#define LOPF_RES_UNROLL 8                  // mat-vec column loop unroll (A/B: 1 4.83, 2 4.63, 4 4.59, 8 4.54 us)
+#endif
 #ifndef LOPF_RES_SLEEP
 #define LOPF_RES_SLEEP 20                  // reducer poll back-off (ns)
 #endif
+constexpr int kUnroll = LOPF_RES_UNROLL;
 constexpr int kPer = 5;                    // flags / partials per reducer lane per round (G <= 160 in one round)
 
 __device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p) {
@@ -177,13 +181,13 @@ __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, doubl
     const int d0 = C.dst + E * (info[0] & 0x3F), d1 = C.dst + E * (info[R - 1] & 0x3F);
     T ax0 = T(0), ax1 = T(0);
     if (R == 2) {
-#pragma unroll 4
+#pragma unroll kUnroll
         for (int k = 0; k < kmax; ++k) {
             ax0 = fma(Dt<T>(at, 64 * k), Dt<T>(d0, k), ax0);
             ax1 = fma(Dt<T>(at, 64 * k + 32), Dt<T>(d1, k), ax1);
         }
     } else {
-#pragma unroll 4
+#pragma unroll kUnroll
         for (int k = 0; k < kmax; ++k) ax0 = fma(Dt<T>(at, 32 * k), Dt<T>(d0, k), ax0);
     }
     const T axr[2] = {ax0, ax1};
