@@ -33,6 +33,10 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+#ifndef LOPF_STREAM_UNROLL
+#define LOPF_STREAM_UNROLL 4
+#endif
+constexpr int kStreamUnroll = LOPF_STREAM_UNROLL;   // packed-task column loop unroll
 constexpr int kInvNu = 64;                 // SMEM table of 1 / nu (the host's 1.0 / nu, bit for bit)
 
 // ---- bulk-copy (TMA) staging ---------------------------------------------------------------------
@@ -259,6 +263,7 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
         p[h] = ((unsigned)info[h] >> kInfoPoffShift) + r[h];
     }
     const int kmax = (tr.w >> kTaskKmaxShift) & 0xFF;
+#pragma unroll kStreamUnroll
     for (int k = 0; k < kmax; ++k) {
 #pragma unroll
         for (int h = 0; h < R; ++h) {
