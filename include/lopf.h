@@ -92,7 +92,7 @@ typedef struct {
     int32_t trace_cap;     /* rows of trace kept on the device (0 = default 4096) */
     int32_t single;        /* 1: one subsystem holding every row (S = 1) */
     int32_t kernel;        /* 0 auto, 1 streaming (operators in HBM/L2), 2 resident (operators in SMEM) */
-    int32_t block_threads; /* 0 = default */
+    int32_t block_threads; /* must be 0: block sizes are fixed per kernel at build time (lopf_sizes.block) */
     int32_t max_ctas;      /* resident kernel: CTAs available (one per SM; 0 = 148, the B200 SM count) */
     int32_t grid_cap;      /* streaming kernel: cap on the persistent grid (0 = occupancy x SMs; test hook) */
     int32_t reserved[2];   /* [0] = 1: per-CTA phase cycle counters (lopf_get_profile); [1]: diagnostics phase-skip

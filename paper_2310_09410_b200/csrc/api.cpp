@@ -75,6 +75,8 @@ static cudaError_t h2d_elems(void* dev, const double* in, size_t n, int esz, cud
 static lopf_status check_precision(const lopf_options& o) {
     if (o.precision != 0 && o.precision != 32 && o.precision != 64)
         return fail(LOPF_E_ARG, "precision must be 0 / 64 (fp64) or 32 (fp32)");
+    if (o.block_threads != 0)
+        return fail(LOPF_E_ARG, "block_threads must be 0 (block sizes are fixed per kernel; see lopf_sizes.block)");
     return LOPF_OK;
 }
 
