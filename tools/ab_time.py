@@ -8,7 +8,8 @@ from paper_2310_09410_b200 import Lopf  # noqa: E402
 
 shape = sys.argv[1] if len(sys.argv) > 1 else "8500"
 mixed = len(sys.argv) > 2 and sys.argv[2] == "mixed"
-h = Lopf.setup(fg.make_feeder(shape), kernel=2)
+prec = int(sys.argv[3]) if len(sys.argv) > 3 else 64
+h = Lopf.setup(fg.make_feeder(shape), kernel=2, precision=prec)
 if mixed:
     h.destroy()
     from paper_2310_09410_b200.lopf import Options  # noqa: F401
@@ -24,4 +25,4 @@ for _ in range(5):
     h.reset()
     r = h.run(3000)
     best = min(best, 1e3 * r.solve_ms / 3000)
-print(f"{os.environ.get('LOPF_LIB', 'current')}{' mixed' if mixed else ''}: {shape} G={h.sizes.grid} best {best:.3f} us/sweep", flush=True)
+print(f"{os.environ.get('LOPF_LIB', 'current')}{' mixed' if mixed else ''}: {shape} p{prec} G={h.sizes.grid} best {best:.3f} us/sweep", flush=True)
