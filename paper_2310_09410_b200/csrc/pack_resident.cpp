@@ -103,14 +103,15 @@ std::vector<TaskR> make_tasks(const Canon& P, const std::vector<int64_t>& subs) 
 // the slowest warp of the slowest CTA (tools/res_timeline2.py: a warp's cycles ~ 45 per tile column + 90
 // per boundary read, issue-bound), so halving the longest tasks shortens the critical path.  The split
 // never grows the SMEM footprint (same slots, tiles of 32 x kmax_half <= 64 x kmax).
-// Measured and OFF by default: the widest tasks (two n_s = 18..26 subsystems plus a small one) do not fit
-// two 32-row halves, so the split lands on cheaper tasks; the extra active warps raise the issue
-// contention for every warp (median worker 4.2k -> 5.9k cycles) and the period grows 5.22 -> 5.31 us.
+// A task's subsystems are re-packed first-fit-decreasing into as many 32-row tasks as the idle warps and
+// the SMEM margin allow.  Measured (profiles/r01_ab_resident_split*.log): the 123 shape (G = 4) gains
+// 3.43 -> 3.31 us/sweep, the 8500 shape (G = 145) loses 4.53 -> 4.73 (the extra active warps raise the
+// issue contention of every warp), so it is applied to small feeders (G <= 16) only.
 #ifndef LOPF_RES_SPLIT_TASKS
-#define LOPF_RES_SPLIT_TASKS 0
+#define LOPF_RES_SPLIT_TASKS 1
 #endif
 void split_tasks(const Canon& P, std::vector<TaskR>& tasks, const std::vector<int32_t>& copy_chunk, int c,
-                 int workers) {
+                 int workers, int64_t smem_room, int64_t E) {
     if (!LOPF_RES_SPLIT_TASKS) return;
     auto cost = [&](const TaskR& t) {
         int64_t xr = 0;
@@ -126,31 +127,39 @@ void split_tasks(const Canon& P, std::vector<TaskR>& tasks, const std::vector<in
     for (size_t i = 0; i < tasks.size(); ++i) { idx[i] = (int)i; cs[i] = cost(tasks[i]); }
     std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cs[a] > cs[b]; });
     int idle = workers - (int)tasks.size();
-    std::vector<TaskR> out;
-    std::vector<char> split(tasks.size(), 0);
-    std::vector<std::pair<TaskR, TaskR>> halves(tasks.size());
+    const int64_t per_slot = 5 * E + 8;                  // bbar, x_s and lambda (two parities), sinfo, sexp
+    std::vector<std::vector<TaskR>> parts(tasks.size());
     for (int i : idx) {
         if (idle <= 0) break;
         const TaskR& t = tasks[i];
         if (t.R != 2) continue;
-        TaskR a{1, 0, {}}, b{1, 0, {}};
-        int ra = 32, rb = 32;
+        std::vector<TaskR> bins;                          // first fit decreasing into 32-row R = 1 tasks
+        std::vector<int> room;
         bool ok = true;
-        for (int64_t s : t.subs) {                        // first fit decreasing (subs are in n_s order)
+        for (int64_t s : t.subs) {                        // (subs are in decreasing n_s order)
             const int ns = P.n_s[s];
-            if (ns <= ra) { a.subs.push_back(s); a.kmax = std::max(a.kmax, ns); ra -= ns; }
-            else if (ns <= rb) { b.subs.push_back(s); b.kmax = std::max(b.kmax, ns); rb -= ns; }
-            else { ok = false; break; }
+            if (ns > 32) { ok = false; break; }
+            size_t b = 0;
+            while (b < bins.size() && room[b] < ns) ++b;
+            if (b == bins.size()) { bins.push_back(TaskR{1, 0, {}}); room.push_back(32); }
+            bins[b].subs.push_back(s);
+            bins[b].kmax = std::max(bins[b].kmax, ns);
+            room[b] -= ns;
         }
-        if (!ok || a.subs.empty()) continue;
-        split[i] = 1;
-        halves[i] = {a, b};
-        if (!b.subs.empty()) --idle;                       // (<= 32 rows: one R = 1 task, no extra warp)
+        const int extra = (int)bins.size() - 1;
+        if (!ok || extra > idle) continue;
+        int64_t grow = 32 * per_slot * ((int64_t)bins.size() - 2);     // 32 slots per R = 1 task (64 before)
+        for (auto& b : bins) grow += E * 32 * b.kmax;
+        grow -= E * 64 * t.kmax;
+        if (grow > smem_room) continue;
+        smem_room -= grow;
+        parts[i] = bins;
+        idle -= extra;
     }
+    std::vector<TaskR> out;
     for (size_t i = 0; i < tasks.size(); ++i) {
-        if (!split[i]) { out.push_back(tasks[i]); continue; }
-        out.push_back(halves[i].first);
-        if (!halves[i].second.subs.empty()) out.push_back(halves[i].second);
+        if (parts[i].empty()) { out.push_back(tasks[i]); continue; }
+        for (auto& b : parts[i]) out.push_back(b);
     }
     tasks.swap(out);
 }
@@ -270,7 +279,9 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     std::vector<int32_t> gl_of(P.n, -1);
     for (int c = 0; c < L.G; ++c) {
         auto tasks = make_tasks(P, chunks[c].subs);
-        split_tasks(P, tasks, copy_chunk, c, kResBlock / 32 - 1);
+        if (L.G <= 16)          // small feeders only: 123 shape 3.43 -> 3.31 us/sweep, 8500 shape 4.53 -> 4.73
+            split_tasks(P, tasks, copy_chunk, c, kResBlock / 32 - 1,
+                        kResSmemBudget - 512 - chunk_bytes(P, chunks[c].subs, cnt, E), E);
         CtaHdr& h = B[c].h;
         std::memset(&h, 0, sizeof(h));
         int64_t NS = 0, pool = 0;
