@@ -159,3 +159,17 @@ def test_precision_option():
         assert (s32.alg_bytes - int_bytes) * 2 == s64.alg_bytes - int_bytes
     with pytest.raises(Exception):
         Lopf.setup(f, precision=16)
+
+
+def test_block_threads_must_be_zero():
+    """lopf_options.block_threads is fixed per kernel at build time: a nonzero value is LOPF_E_ARG."""
+    import ctypes as C
+    from paper_2310_09410_b200 import lopf as L
+    lib = L.load_library()
+    o = L.Options()
+    lib.lopf_options_default(C.byref(o))
+    o.block_threads = 256
+    net, keep = L._network(fg.make_feeder("13"))
+    h = C.c_void_p()
+    assert lib.lopf_setup(C.byref(net), C.byref(o), C.byref(h)) == 1          # LOPF_E_ARG
+    assert b"block_threads" in lib.lopf_last_error()
