@@ -205,16 +205,22 @@ def main():
     dev_ms = sum(step_ms)
     tot_iters = sum(iters)
 
-    # end to end through the public API with host buffers: H2D of the packed problem (pinned host
-    # image), solve, D2H of the solution x and the result record
+    # end to end through the public API with host buffers: every step uploads the packed problem from its
+    # pinned host image (H2D), solves, and reads the solution x and the result record back (D2H).  Two
+    # handles on two streams: step i+1's upload runs on the copy engines while step i solves.
     e2e_steps = max(3, min(args.steps, 10))
+    h2 = Lopf.setup(feeder, kernel=args.kernel, precision=args.precision).bind(dev)
+    hs, ss = (h, h2), (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
     barrier()
     t = time.perf_counter()
     e2e_iters = 0
-    for _ in range(e2e_steps):
-        h.bind(dev)
-        r = h.solve()
-        x = h.get_x()
+    hs[0].bind(dev, stream=ss[0])
+    for i in range(e2e_steps):
+        a, sa = hs[i % 2], ss[i % 2]
+        if i + 1 < e2e_steps:
+            hs[(i + 1) % 2].bind(dev, stream=ss[(i + 1) % 2])      # next step's H2D, overlapped
+        r = a.solve(stream=sa)
+        x = a.get_x(stream=sa)
         e2e_iters += int(r.iters)
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t
