@@ -53,14 +53,42 @@ static lopf_status cuda_fail(cudaError_t e, const char* where) {
 
 static constexpr int kMaxGrid = 4096;
 
-// (T) device arrays (reading F1) <-> host fp64: n elements of esz bytes at `dev`.
+// Pinned staging for device -> host reads into caller (pageable) memory: a DMA into pinned memory plus a
+// host copy is several times faster than a staged pageable copy (x of the 8500 shape: ~0.05 vs 0.3 ms).
+static thread_local void* g_pin = nullptr;
+static thread_local size_t g_pin_bytes = 0;
+static void* pinned(size_t bytes) {
+    if (bytes > g_pin_bytes) {
+        if (g_pin) cudaFreeHost(g_pin);
+        g_pin = nullptr;
+        g_pin_bytes = 0;
+        if (cudaMallocHost(&g_pin, bytes) != cudaSuccess) { cudaGetLastError(); g_pin = nullptr; return nullptr; }
+        g_pin_bytes = bytes;
+    }
+    return g_pin;
+}
+
+// (T) device arrays (reading F1) <-> host fp64: n elements of esz bytes at `dev`.  Synchronous.
 static cudaError_t d2h_elems(double* out, const void* dev, size_t n, int esz, cudaStream_t s) {
-    if (esz == 8) return cudaMemcpyAsync(out, dev, 8 * n, cudaMemcpyDeviceToHost, s);
-    std::vector<float> tmp(n);
-    cudaError_t e = cudaMemcpyAsync(tmp.data(), dev, 4 * n, cudaMemcpyDeviceToHost, s);
+    void* stage = pinned((size_t)esz * n);
+    cudaError_t e;
+    if (!stage) {                                              // no pinned memory: direct (staged) copy
+        if (esz == 8) {
+            e = cudaMemcpyAsync(out, dev, 8 * n, cudaMemcpyDeviceToHost, s);
+            return e == cudaSuccess ? cudaStreamSynchronize(s) : e;
+        }
+        std::vector<float> tmp(n);
+        e = cudaMemcpyAsync(tmp.data(), dev, 4 * n, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        for (size_t i = 0; e == cudaSuccess && i < n; ++i) out[i] = (double)tmp[i];
+        return e;
+    }
+    e = cudaMemcpyAsync(stage, dev, (size_t)esz * n, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    for (size_t i = 0; e == cudaSuccess && i < n; ++i) out[i] = (double)tmp[i];
-    return e;
+    if (e != cudaSuccess) return e;
+    if (esz == 8) std::memcpy(out, stage, 8 * n);
+    else for (size_t i = 0; i < n; ++i) out[i] = (double)static_cast<const float*>(stage)[i];
+    return cudaSuccess;
 }
 static cudaError_t h2d_elems(void* dev, const double* in, size_t n, int esz, cudaStream_t s) {
     if (esz == 8) {
