@@ -352,9 +352,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         P.esz = L.esz;
         P.n = h->cp.n;
         P.tasks = (const int4*)(b + L.off_tasks);
-        P.s_info = (const int32_t*)(b + L.off_info);
-        P.s_g = (const int32_t*)(b + L.off_g);
-        P.s_nbr = (const int4*)(b + L.off_nbr);
+        P.s_meta = (const SlotMeta*)(b + L.off_meta);
         P.s_bbar = (const double*)(b + L.off_bbar);
         P.xl = (double*)(b + L.off_xl);
         P.lam = (double*)(b + L.off_lam);
@@ -450,9 +448,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     P.n_slots = (int32_t)L.n_slots;
     P.n = h->cp.n;
     P.tasks = (const int4*)(b + L.off_tasks);
-    P.s_info = (const int32_t*)(b + L.off_info);
-    P.s_g = (const int32_t*)(b + L.off_g);
-    P.s_nbr = (const int4*)(b + L.off_nbr);
+    P.s_meta = (const SlotMeta*)(b + L.off_meta);
     P.s_bbar = (const double*)(b + L.off_bbar);
     P.xl = (double*)(b + L.off_xl);
     P.lam = (double*)(b + L.off_lam);

@@ -93,6 +93,14 @@ struct DevCtrl {                           // 256 B, device-resident control blo
     double pad[18];
 };
 
+// Per-slot metadata of the streaming / batch layouts, one 24-byte record (one bulk copy per task):
+// the inline segment slots (nu <= 4, canonical copy order), the info bit field and the global index.
+struct alignas(8) SlotMeta {
+    int2 n01, n23;
+    int32_t info, g;
+};
+static_assert(sizeof(SlotMeta) == 24, "SlotMeta is 24 bytes");
+
 // Arrays marked (T) hold doubles when esz == 8 and floats when esz == 4 (the fp32 variant, reading F1:
 // the paper's GPU precision); the kernels cast them to the element type they were
 // instantiated for.  Residual sums, partials, trace, objective coefficients and the exchange are fp64.
@@ -101,9 +109,7 @@ struct DevProblem {                        // kernel argument (pointers into the
     int32_t esz;                           // element size of operators / iterate / globals: 8 (fp64) or 4 (fp32)
     int64_t n;
     const int4* tasks;                     // {slot_off, abar_off, kmax, R}
-    const int32_t* s_info;
-    const int32_t* s_g;
-    const int4* s_nbr;
+    const SlotMeta* s_meta;                // per-slot {inline segment slots, info, global}: one record
     const void* s_bbar;                    // (T)
     void* xl;                              // (T)
     void* lam;                             // (T)
@@ -216,7 +222,7 @@ struct Layout {
     // partitioned mode
     int32_t part = 0, rank = 0, world = 1, n_bnd = 0, n_imp = 0, ghost0 = 0;
     size_t off_sexp = 0, off_imp = 0, off_xbuf = 0;
-    size_t off_tasks = 0, off_info = 0, off_g = 0, off_nbr = 0, off_bbar = 0, off_xl = 0, off_lam = 0,
+    size_t off_tasks = 0, off_meta = 0, off_bbar = 0, off_xl = 0, off_lam = 0,
            off_u0 = 0, off_u1 = 0, off_x0 = 0, off_gpar = 0, off_gcost = 0, off_segptr = 0, off_segslot = 0, off_x = 0, off_abar = 0,
            off_partial = 0, off_ctrl = 0, off_trace = 0, off_objidx = 0, off_objc = 0;
     size_t bytes = 0;

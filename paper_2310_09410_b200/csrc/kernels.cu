@@ -47,13 +47,11 @@ constexpr int kInvNu = 64;                 // SMEM table of 1 / nu (the host's 1
 // T = double (the parity path) or float (the paper's GPU precision; reading F1): the
 // operator block holds kPackBudget entries of T, then the per-slot inputs of 64 slots.
 template <class T> struct Stg {
-    static constexpr int kOffInfo = (int)sizeof(T) * kPackBudget;
-    static constexpr int kOffG = kOffInfo + 4 * 64;
-    static constexpr int kOffNbr = kOffG + 4 * 64;
-    static constexpr int kOffLam = kOffNbr + 16 * 64;
+    static constexpr int kOffMeta = (int)sizeof(T) * kPackBudget;
+    static constexpr int kOffLam = kOffMeta + (int)sizeof(SlotMeta) * 64;
     static constexpr int kOffXl = kOffLam + (int)sizeof(T) * 64;
     static constexpr int kBytes = kOffXl + (int)sizeof(T) * 64;
-    static_assert(kOffInfo % 16 == 0 && kBytes % 16 == 0, "bulk copies need 16-byte alignment");
+    static_assert(kOffMeta % 16 == 0 && kBytes % 16 == 0, "bulk copies need 16-byte alignment");
 };
 template <class T> struct Vec2;
 template <> struct Vec2<double> { using type = double2; };
@@ -93,15 +91,13 @@ __device__ __forceinline__ void issue_task(const DevProblem& P, Stage& st, const
         const uint32_t n = (uint32_t)(tr.w >> kTaskUsedShift) & 0xFFu;
         const bool ablk = !(tr.w & kTaskDirect);
         constexpr uint32_t E = sizeof(T);
-        const uint32_t bytes = (24u + 2u * E) * n + (ablk ? E * (uint32_t)tr.z : 0u);
+        const uint32_t bytes = ((uint32_t)sizeof(SlotMeta) + 2u * E) * n + (ablk ? E * (uint32_t)tr.z : 0u);
         uint64_t* m = st.bar + b;
         if (full_fence) asm volatile("fence.proxy.async;" ::: "memory");
         else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
         if (ablk) bulk_g2s(sb, reinterpret_cast<const T*>(P.abar) + tr.y, E * (uint32_t)tr.z, m);
-        bulk_g2s(sb + Stg<T>::kOffInfo, P.s_info + tr.x, 4u * n, m);
-        bulk_g2s(sb + Stg<T>::kOffG, P.s_g + tr.x, 4u * n, m);
-        bulk_g2s(sb + Stg<T>::kOffNbr, P.s_nbr + tr.x, 16u * n, m);
+        bulk_g2s(sb + Stg<T>::kOffMeta, P.s_meta + tr.x, (uint32_t)sizeof(SlotMeta) * n, m);
         bulk_g2s(sb + Stg<T>::kOffLam, reinterpret_cast<const T*>(P.lam) + tr.x, E * n, m);
         bulk_g2s(sb + Stg<T>::kOffXl, reinterpret_cast<const T*>(P.xl) + tr.x, E * n, m);
     }
@@ -199,9 +195,7 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
     mbar_wait(st.bar + b, (st.consumed >> 1) & 1);
     ++st.consumed;
     const char* sb = st.buf + b * kStageBytes;
-    const int* s_info = reinterpret_cast<const int*>(sb + Stg<T>::kOffInfo);
-    const int* s_g = reinterpret_cast<const int*>(sb + Stg<T>::kOffG);
-    const int4* s_nbr = reinterpret_cast<const int4*>(sb + Stg<T>::kOffNbr);
+    const SlotMeta* s_meta = reinterpret_cast<const SlotMeta*>(sb + Stg<T>::kOffMeta);
     const T* s_lam = reinterpret_cast<const T*>(sb + Stg<T>::kOffLam);
     const T* s_xl = reinterpret_cast<const T*>(sb + Stg<T>::kOffXl);
     const bool direct = SRC == 1 || (SRC == 0 && (tr.w & kTaskDirect));
@@ -216,11 +210,12 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         const int j = h * 32 + lane;
-        info[h] = j < used ? s_info[j] : 0;
+        info[h] = j < used ? s_meta[j].info : 0;
         const bool val = info[h] & kInfoValid, inl = val && (info[h] & kInfoInline);
         const int nu = (info[h] >> kInfoNuShift) & 0xF;
-        g[h] = s_g[j];
-        const int4 nb = s_nbr[j];
+        g[h] = s_meta[j].g;
+        const int2 n01 = s_meta[j].n01, n23 = s_meta[j].n23;
+        const int4 nb = make_int4(n01.x, n01.y, n23.x, n23.y);
         ua[h][0] = inl ? __ldcg(ucur + nb.x) : T(0);
         ua[h][1] = inl && nu > 1 ? __ldcg(ucur + nb.y) : T(0);
         ua[h][2] = inl && nu > 2 ? __ldcg(ucur + nb.z) : T(0);
@@ -299,11 +294,13 @@ __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, co
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         const int slot = tr.x + h * 32 + lane;
-        info[h] = __ldg(P.s_info + slot);
+        info[h] = __ldg(&P.s_meta[slot].info);
         v[h] = T(0);
         T d = T(0);
         if (info[h] & kInfoValid) {
-            v[h] = consensus<T>(P, info[h], __ldg(P.s_g + slot), __ldg(P.s_nbr + slot), ucur, inv_nu);
+            const int2 n01 = __ldg(&P.s_meta[slot].n01), n23 = __ldg(&P.s_meta[slot].n23);
+            v[h] = consensus<T>(P, info[h], __ldg(&P.s_meta[slot].g), make_int4(n01.x, n01.y, n23.x, n23.y), ucur,
+                                inv_nu);
             d = -rho * v[h] - lamp[slot];
         }
         dsm[h * 32 + lane] = d;

@@ -147,9 +147,7 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     auto take = [&](size_t bytes) { size_t r = o; o = align256(o + std::max<size_t>(bytes, 1)); return r; };
     const size_t NS = (size_t)slots, NG = (size_t)P.n, NC = (size_t)P.nc;
     L.off_tasks = take(sizeof(int4) * L.n_tasks);
-    L.off_info = take(4 * NS);
-    L.off_g = take(4 * NS);
-    L.off_nbr = take(16 * NS);
+    L.off_meta = take(sizeof(SlotMeta) * NS);
     L.off_bbar = take(esz * NS);
     L.off_xl = take(esz * NS);
     L.off_lam = take(esz * NS);
@@ -178,9 +176,9 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     auto at = [&](size_t off) { return img + off; };
 
     std::memcpy(at(L.off_tasks), trec.data(), sizeof(int4) * trec.size());
-    int32_t* info = (int32_t*)at(L.off_info);
-    int32_t* gs = (int32_t*)at(L.off_g);
-    int4* nbr = (int4*)at(L.off_nbr);
+    SlotMeta* meta = (SlotMeta*)at(L.off_meta);
+    std::vector<int32_t> info(NS, 0), gs(NS, -1);
+    std::vector<int4> nbr(NS, make_int4(0, 0, 0, 0));
     // (T) arrays: values computed in fp64, stored as T (fp32: each rounded once to nearest)
     auto put = [esz](uint8_t* base, size_t i, double v) {
         if (esz == 8) reinterpret_cast<double*>(base)[i] = v;
@@ -188,7 +186,6 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     };
     uint8_t* bbar = at(L.off_bbar);
     uint8_t* abar = at(L.off_abar);
-    for (size_t i = 0; i < NS; ++i) { gs[i] = -1; nbr[i] = make_int4(0, 0, 0, 0); }
 
     L.slot_of_copy.assign(NC, -1);
     L.trec = trec;
@@ -259,6 +256,8 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
             nbr[slot] = make_int4(v[0], v[1], v[2], v[3]);
         }
     }
+    for (size_t i = 0; i < NS; ++i)
+        meta[i] = SlotMeta{make_int2(nbr[i].x, nbr[i].y), make_int2(nbr[i].z, nbr[i].w), info[i], gs[i]};
     uint8_t* gbnd = at(L.off_gpar);                   // {lo, hi} pairs (IEEE +-inf kept in fp32 too)
     uint8_t* gcost = at(L.off_gcost);
     for (int64_t i = 0; i < P.n; ++i) {

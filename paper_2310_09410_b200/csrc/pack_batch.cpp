@@ -54,9 +54,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = a256b(o + std::max<size_t>(bytes, 1)); return r; };
     L.off_tasks = take(16 * NT);
-    L.off_info = take(4 * NS);
-    L.off_g = take(4 * NS);
-    L.off_nbr = take(16 * NS);
+    L.off_meta = take(sizeof(SlotMeta) * NS);
     L.off_bbar = take(e * NS);
     L.off_x0 = take(e * NS);
     L.off_gpar = take(2 * e * NG);
@@ -85,9 +83,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     uint8_t* img = L.image.data();
     const uint8_t* ti = T.image.data();
     std::memcpy(img + L.off_tasks, trec.data(), 16 * NT);
-    std::memcpy(img + L.off_info, ti + T.off_info, 4 * NS);
-    std::memcpy(img + L.off_g, ti + T.off_g, 4 * NS);
-    std::memcpy(img + L.off_nbr, ti + T.off_nbr, 16 * NS);
+    std::memcpy(img + L.off_meta, ti + T.off_meta, sizeof(SlotMeta) * NS);
     std::memcpy(img + L.off_bbar, ti + T.off_bbar, e * NS);
     std::memcpy(img + L.off_x0, ti + T.off_x0, e * NS);
     std::memcpy(img + L.off_gpar, ti + T.off_gpar, 2 * e * NG);
