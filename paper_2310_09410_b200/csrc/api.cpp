@@ -320,7 +320,7 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
         sz->reserved[1] = h->lay.max_smem;
     }
     sz->grid = h->resident() ? h->lay.G : h->grid;
-    sz->block = h->resident() ? kResBlock : stream_block(h->lay.rmax, h->lay.esz);
+    sz->block = h->resident() ? kResBlock : h->batch() ? batch_block(h->lay.esz) : stream_block(h->lay.rmax, h->lay.esz);
     sz->n_scen = h->batch() ? h->lay.n_scen : 0;
     return LOPF_OK;
 }
@@ -388,7 +388,8 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         B.amask = (uint32_t*)(b + L.off_bmask);
         std::string err;
         int grid = 0;
-        lopf_status st = query_grid(L.rmax, L.esz, &grid, err);
+        B.staged = L.staged;
+        lopf_status st = query_batch_grid(L.rmax, L.esz, L.staged, &grid, err);
         if (st != LOPF_OK) return fail(st, err);
         h->grid = grid;
         st = launch_reset_batch(P, B, stream, err);

@@ -210,6 +210,7 @@ struct BatchProblem {                          // config 4: streaming kernel ove
     double* partial;                           // [n_scen][n_tasks][8] residual sums per item
     unsigned long long* cnt;                   // [2]: barrier arrivals, cumulative active count
     uint32_t* amask;                           // [2][ceil(n_scen/32)] active-scenario bits by sweep parity
+    int32_t staged;                            // 1: no kTaskDirect task (every operator block from the SMEM stage)
 };
 constexpr int kBatchMaxScen = 8192;            // scenarios per batch handle (SMEM active-set tables)
 
@@ -218,6 +219,7 @@ struct Layout {
     int32_t kernel = 1;
     int64_t n_tasks = 0, n_slots = 0, abar_doubles = 0, n_obj = 0;
     int32_t rmax = 1;                     // streaming: widest task (R)
+    int32_t staged = 0;                   // batch: 1 when no task reads its operator block from HBM (kTaskDirect)
     int32_t esz = 8;                      // streaming / batch: element size of the (T) arrays (8 fp64, 4 fp32)
     // partitioned mode
     int32_t part = 0, rank = 0, world = 1, n_bnd = 0, n_imp = 0, ghost0 = 0;
@@ -293,7 +295,18 @@ lopf_status pack_batch(const Net& N, const Canon& cp, const BatchOps& bo, const 
 constexpr int kStreamWarpsF64 = LOPF_STREAM_WARPS_F64;
 constexpr int kStreamWarpsF32 = LOPF_STREAM_WARPS_F32;
 constexpr int kStreamWarpsWide = 12;         // ... when tasks of R > 2 exist (n_s > 64, the S = 1 path)
+// Batch kernel (config 4): its own warp count per element type (same stage size as streaming).
+#ifndef LOPF_BATCH_WARPS_F64
+#define LOPF_BATCH_WARPS_F64 LOPF_STREAM_WARPS_F64
+#endif
+#ifndef LOPF_BATCH_WARPS_F32
+#define LOPF_BATCH_WARPS_F32 LOPF_STREAM_WARPS_F32
+#endif
+constexpr int kBatchWarpsF64 = LOPF_BATCH_WARPS_F64;
+constexpr int kBatchWarpsF32 = LOPF_BATCH_WARPS_F32;
 int stream_block(int rmax, int esz);
+int batch_block(int esz);
+lopf_status query_batch_grid(int rmax, int esz, int staged, int* grid, std::string& err);
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
 lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err);
 lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err);

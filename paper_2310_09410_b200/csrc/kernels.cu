@@ -548,9 +548,17 @@ __device__ __forceinline__ int next_active(const uint32_t* m, const int W, const
 
 constexpr int kBatchMaskWords = kBatchMaxScen / 32;
 
-template <int RMAX, class T>
-__global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_batch_kernel(DevProblem P, BatchProblem B) {
-    constexpr int kWarps = StreamWarps<RMAX, T>::value;   // fp32: 24 warps beat 16 (390 vs 466 us/batch sweep)
+template <class T>
+struct BatchWarps {
+    static constexpr int value = sizeof(T) == 8 ? kBatchWarpsF64 : kBatchWarpsF32;
+};
+
+// SRC (task_packed): 0 operator block from HBM or the stage, decided per task (generic loads); 2 every
+// block from the stage (the problem has no kTaskDirect task: shared-space loads); 3 a branch per task
+// between the two specialised paths
+template <int RMAX, class T, int SRC>
+__global__ void __launch_bounds__(32 * BatchWarps<T>::value, 1) admm_batch_kernel(DevProblem P, BatchProblem B) {
+    constexpr int kWarps = BatchWarps<T>::value;
     constexpr int kStageBytes = Stg<T>::kBytes;
     extern __shared__ __align__(128) char sdyn[];
     __shared__ uint64_t sbar[kWarps][2];
@@ -627,8 +635,18 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_batc
                 }
                 const size_t so = (size_t)sc * B.ns_stride;
                 const DevProblem Q = batch_view<T>(P, B, sc, tr);
-                if ((tr.w & 0xF) == 1) task_packed<1, T, 0>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
-                else if constexpr (RMAX >= 2) task_packed<2, T, 0>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+                if constexpr (SRC == 3) {                      // split: HBM-block tasks on their own path
+                    if (tr.w & kTaskDirect) {
+                        if ((tr.w & 0xF) == 1) task_packed<1, T, 1>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+                        else if constexpr (RMAX >= 2) task_packed<2, T, 1>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+                    } else {
+                        if ((tr.w & 0xF) == 1) task_packed<1, T, 2>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+                        else if constexpr (RMAX >= 2) task_packed<2, T, 2>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+                    }
+                } else {
+                    if ((tr.w & 0xF) == 1) task_packed<1, T, SRC>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+                    else if constexpr (RMAX >= 2) task_packed<2, T, SRC>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
+                }
                 double* pp = B.partial + ((size_t)sc * NT + tk) * 8;
                 if (more && sc1 == sc) {                       // the run goes on: this item's slot holds 0
                     if (lane < 5) pp[lane] = 0.0;
@@ -811,15 +829,46 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
 }
 
 
-static const void* batch_kernel_for(int rmax, int esz) {
-    if (esz == 4) return rmax <= 1 ? (const void*)admm_batch_kernel<1, float> : (const void*)admm_batch_kernel<2, float>;
-    return rmax <= 1 ? (const void*)admm_batch_kernel<1, double> : (const void*)admm_batch_kernel<2, double>;
+template <int SRC>
+static const void* batch_kernel_src(int rmax, int esz) {
+    if (esz == 4)
+        return rmax <= 1 ? (const void*)admm_batch_kernel<1, float, SRC> : (const void*)admm_batch_kernel<2, float, SRC>;
+    return rmax <= 1 ? (const void*)admm_batch_kernel<1, double, SRC> : (const void*)admm_batch_kernel<2, double, SRC>;
+}
+// A problem with kTaskDirect tasks: fp64 takes the split kernel (SRC 3: staged blocks by shared-space
+// loads, the direct ones by global loads; 512 vs 519 us per batch sweep of config 4), fp32 the per-task
+// select (SRC 0: the split spills at its 80-register cap, 433 vs 384 us; profiles/r01_ab_batch_split.log).
+static const void* batch_kernel_for(int rmax, int esz, int staged) {
+    if (staged) return batch_kernel_src<2>(rmax, esz);
+    if (esz == 8) return rmax <= 1 ? (const void*)admm_batch_kernel<1, double, 3> : (const void*)admm_batch_kernel<2, double, 3>;
+    return rmax <= 1 ? (const void*)admm_batch_kernel<1, float, 0> : (const void*)admm_batch_kernel<2, float, 0>;
+}
+
+int batch_block(int esz) { return 32 * (esz == 8 ? kBatchWarpsF64 : kBatchWarpsF32); }
+
+static int batch_smem(int rmax, int esz) {
+    const int r = rmax <= 1 ? 1 : 2;
+    const int stage = esz == 4 ? Stg<float>::kBytes : Stg<double>::kBytes;
+    return batch_block(esz) / 32 * (2 * stage + esz * 32 * r);
+}
+
+lopf_status query_batch_grid(int rmax, int esz, int staged, int* grid, std::string& err) {
+    int dev = 0, sms = 0, per = 0;
+    const void* k = batch_kernel_for(rmax, esz, staged);
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, batch_smem(rmax, esz));
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, batch_block(esz), batch_smem(rmax, esz));
+    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
+    if (per < 1) { err = "batch kernel cannot be resident (occupancy 0)"; return LOPF_E_CUDA; }
+    *grid = sms * per;
+    return LOPF_OK;
 }
 
 lopf_status launch_batch(const DevProblem& P, const BatchProblem& B, int grid, void* stream, std::string& err) {
     cudaStream_t s = (cudaStream_t)stream;
-    const void* k = batch_kernel_for(P.rmax, P.esz);
-    const int smem = stream_smem(P.rmax, P.esz);
+    const void* k = batch_kernel_for(P.rmax, P.esz, B.staged);
+    const int smem = batch_smem(P.rmax, P.esz);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) e = cudaMemsetAsync(B.cnt, 0, 2 * sizeof(unsigned long long), s);
     if (e == cudaSuccess) {
@@ -830,7 +879,7 @@ lopf_status launch_batch(const DevProblem& P, const BatchProblem& B, int grid, v
         DevProblem Q = P;
         BatchProblem C = B;
         void* args[] = {&Q, &C};
-        e = cudaLaunchCooperativeKernel(k, dim3(grid), dim3(stream_block(P.rmax, P.esz)), args, smem, s);
+        e = cudaLaunchCooperativeKernel(k, dim3(grid), dim3(batch_block(P.esz)), args, smem, s);
     }
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;

@@ -46,6 +46,9 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     L.n_tasks = NT;
     L.n_slots = NS;
     L.rmax = T.rmax;
+    L.staged = 1;
+    for (const int4& tr : trec)
+        if (tr.w & kTaskDirect) L.staged = 0;
     L.VP = VP;
     L.n_obj = T.n_obj;
     L.slot_of_copy = T.slot_of_copy;

@@ -81,3 +81,27 @@ def test_full_4096_batch_sampled():
     for sc in (0, 4095):
         o = oracle.solve(probs[sc])
         assert int(r["iters"][sc]) == o.iters, (sc, int(r["iters"][sc]), o.iters)
+
+
+def test_staged_only_batch():
+    """A feeder whose every operator block fits the SMEM stage (max n_s = 10: no kTaskDirect task) runs
+    the batch kernel's staged-only instantiation (SRC 2, shared-space operator loads): iterates after a
+    fixed K, across two launches, within 1e-9 of the oracle per scenario."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    import fixtures as fx
+    from paper_2310_09410_b200 import Lopf
+    f = fx.chain_1ph(24)
+    K = fg.scenario_scales(f, 37)
+    h = Lopf.setup_batch(f, K).bind("cuda")
+    assert h.sizes.max_ns * (h.sizes.max_ns + 3) // 2 <= 448      # triangle + b-bar fit one stage
+    h.run(300)
+    h.run(200)
+    for sc in (0, 17, 36):
+        o = oracle.run_k(oracle.build_problem(fg.scale_loads(f, K[sc])), 500)
+        x, xl, lam = h.get_state_scen(sc)
+        assert _rel(x, o.x) <= TOL and _rel(xl, o.x_loc) <= TOL and _rel(lam, o.lam) <= TOL, sc
