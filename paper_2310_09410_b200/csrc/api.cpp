@@ -386,6 +386,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         B.partial = (double*)(b + L.off_bpart);
         B.cnt = (unsigned long long*)(b + L.off_bcnt);
         B.amask = (uint32_t*)(b + L.off_bmask);
+        B.wpre = (const long long*)(b + L.off_bwpre);
         std::string err;
         int grid = 0;
         B.staged = L.staged;

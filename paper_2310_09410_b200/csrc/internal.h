@@ -211,7 +211,11 @@ struct BatchProblem {                          // config 4: streaming kernel ove
     unsigned long long* cnt;                   // [2]: barrier arrivals, cumulative active count
     uint32_t* amask;                           // [2][ceil(n_scen/32)] active-scenario bits by sweep parity
     int32_t staged;                            // 1: no kTaskDirect task (every operator block from the SMEM stage)
+    const long long* wpre;                     // [n_tasks + 1] prefix of the per-task cost weights (work split)
 };
+#ifndef LOPF_BATCH_WBASE
+#define LOPF_BATCH_WBASE 16                    // per-item fixed cost in units of one mat-vec column per half
+#endif
 constexpr int kBatchMaxScen = 8192;            // scenarios per batch handle (SMEM active-set tables)
 
 // Arena layout: byte offsets of every array (all 256-byte aligned).
@@ -242,7 +246,7 @@ struct Layout {
     // batch kernel (config 4): the streaming layout of one scenario, replicated over the scenarios
     int32_t n_scen = 0, n_grp = 0, ns_max = 0;
     int64_t VP = 0;                        // doubles of per-scenario operator blocks (tasks holding a load)
-    size_t off_bvar = 0, off_bres = 0, off_bstop = 0, off_bpart = 0, off_bcnt = 0, off_bmask = 0;
+    size_t off_bvar = 0, off_bres = 0, off_bstop = 0, off_bpart = 0, off_bcnt = 0, off_bmask = 0, off_bwpre = 0;
 };
 
 // Scenario batches (config 4): per-scenario operators of the subsystems that hold a load (their

@@ -548,6 +548,19 @@ __device__ __forceinline__ int next_active(const uint32_t* m, const int W, const
 
 constexpr int kBatchMaskWords = kBatchMaxScen / 32;
 
+// first item (active rank * NT + task) whose start weight (rank * WS + wpre[task]) is >= w
+__device__ __forceinline__ long long batch_item_at(const long long* __restrict__ wpre, const int NT, const long long WS,
+                                                   const long long w) {
+    const long long ar = w / WS, rem = w - ar * WS;
+    if (rem == 0) return ar * NT;
+    int lo = 1, hi = NT;                                   // smallest t with wpre[t] >= rem (wpre[NT] = WS > rem)
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(wpre + mid) >= rem) hi = mid; else lo = mid + 1;
+    }
+    return ar * NT + lo;
+}
+
 template <class T>
 struct BatchWarps {
     static constexpr int value = sizeof(T) == 8 ? kBatchWarpsF64 : kBatchWarpsF32;
@@ -607,9 +620,10 @@ __global__ void __launch_bounds__(32 * BatchWarps<T>::value, 1) admm_batch_kerne
             for (int w = threadIdx.x; w < W; w += blockDim.x) B.amask[(size_t)((it + 1) & 1) * W + w] = 0u;
         __syncthreads();
         const int NA = s_wpre[W];
-        const long long items = (long long)NA * NT;
-        const long long C = (items + nw - 1) / nw;
-        long long a0 = (long long)gw * C, a1 = a0 + C < items ? a0 + C : items;
+        // warp gw takes the items whose start weight lies in [gw, gw + 1) * WT / nw (weights: B.wpre)
+        const long long WS = __ldg(B.wpre + NT), WT = (long long)NA * WS;
+        const long long a0 = batch_item_at(B.wpre, NT, WS, (WT * gw + nw - 1) / nw);
+        const long long a1 = batch_item_at(B.wpre, NT, WS, (WT * (gw + 1) + nw - 1) / nw);
         if (a0 < a1) {
             // scenario of active rank a0 / NT: its mask word by binary search on the prefix, then the bit
             const int ar = (int)(a0 / NT);

@@ -78,6 +78,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     L.off_bpart = take(8 * 8 * (size_t)NT * NSC);
     L.off_bcnt = take(8 * 4);
     L.off_bmask = take(4 * 2 * (((size_t)NSC + 31) / 32));
+    L.off_bwpre = take(8 * ((size_t)NT + 1));
     L.off_partial = take(8 * 8 * 4096);
     L.off_ctrl = take(sizeof(DevCtrl));
     L.off_trace = take(8 * 5);
@@ -86,6 +87,12 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     uint8_t* img = L.image.data();
     const uint8_t* ti = T.image.data();
     std::memcpy(img + L.off_tasks, trec.data(), 16 * NT);
+    {   // work-split weights: a fixed per-item cost plus the mat-vec columns x halves (kmax * R)
+        long long* wp = reinterpret_cast<long long*>(img + L.off_bwpre);
+        wp[0] = 0;
+        for (int64_t t = 0; t < NT; ++t)
+            wp[t + 1] = wp[t] + LOPF_BATCH_WBASE + (long long)((trec[t].w >> kTaskKmaxShift) & 0xFF) * (trec[t].w & 0xF);
+    }
     std::memcpy(img + L.off_meta, ti + T.off_meta, sizeof(SlotMeta) * NS);
     std::memcpy(img + L.off_bbar, ti + T.off_bbar, e * NS);
     std::memcpy(img + L.off_x0, ti + T.off_x0, e * NS);
