@@ -547,6 +547,10 @@ __device__ __forceinline__ int next_active(const uint32_t* m, const int W, const
 }
 
 constexpr int kBatchMaskWords = kBatchMaxScen / 32;
+#ifndef LOPF_BATCH_SMEM_TASKS
+#define LOPF_BATCH_SMEM_TASKS 256
+#endif
+constexpr int kBatchSmemTasks = LOPF_BATCH_SMEM_TASKS;   // task records kept in SMEM (else read through L1)
 
 // first item (active rank * NT + task) whose start weight (rank * WS + wpre[task]) is >= w
 __device__ __forceinline__ long long batch_item_at(const long long* __restrict__ wpre, const int NT, const long long WS,
@@ -578,6 +582,7 @@ __global__ void __launch_bounds__(32 * BatchWarps<T>::value, 1) admm_batch_kerne
     __shared__ T inv_nu[kInvNu];
     __shared__ uint32_t s_mask[kBatchMaskWords];           // active scenarios of this sweep
     __shared__ uint16_t s_wpre[kBatchMaskWords + 1];       // active scenarios before word w
+    __shared__ int4 s_tasks[kBatchSmemTasks];               // the (scenario-independent) task records
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
     Stage st{sdyn + (size_t)wid * 2 * kStageBytes, sbar[wid], 0u, 0u};
@@ -591,6 +596,10 @@ __global__ void __launch_bounds__(32 * BatchWarps<T>::value, 1) admm_batch_kerne
     __syncthreads();
     const long long total0 = *(volatile long long*)&P.ctrl->total;
     const int NT = B.n_tasks, W = (B.n_scen + 31) >> 5;
+    const bool tasks_smem = NT <= kBatchSmemTasks;
+    if (tasks_smem)
+        for (int i = threadIdx.x; i < NT; i += blockDim.x) s_tasks[i] = __ldg(P.tasks + i);
+    __syncthreads();
     const volatile int32_t* stopped = B.stopped;
     unsigned long long bars = 0, seen = 0;
     long long it = 0;
@@ -634,7 +643,7 @@ __global__ void __launch_bounds__(32 * BatchWarps<T>::value, 1) admm_batch_kerne
                 if (s_wpre[mid] <= ar) lo = mid; else hi = mid - 1;
             }
             int sc = (lo << 5) + (int)__fns(s_mask[lo], 0, ar - s_wpre[lo] + 1);
-            int4 tr = __ldg(P.tasks + tk);
+            int4 tr = tasks_smem ? s_tasks[tk] : __ldg(P.tasks + tk);
             issue_task<T>(batch_view<T>(P, B, sc, tr), st, tr, lane, true);
             double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
             for (long long a = a0; a < a1; ++a) {
@@ -644,7 +653,7 @@ __global__ void __launch_bounds__(32 * BatchWarps<T>::value, 1) admm_batch_kerne
                 const bool more = a + 1 < a1;
                 int4 tr1 = make_int4(0, 0, 0, 0);
                 if (more) {
-                    tr1 = __ldg(P.tasks + tk1);
+                    tr1 = tasks_smem ? s_tasks[tk1] : __ldg(P.tasks + tk1);
                     issue_task<T>(batch_view<T>(P, B, sc1, tr1), st, tr1, lane, false);
                 }
                 const size_t so = (size_t)sc * B.ns_stride;
