@@ -292,15 +292,18 @@ class Shape:
     delta_frac: float          # fraction of 3-phase loads that are delta-connected
     n_caps: int                # capacitor buses
     lat_load_every: int = 0    # also put a 1-phase load on every k-th internal lateral node (0 = leaves only)
+    n_lat2: int = 0            # laterals widened to 2 phases (IEEE13 684-611/652 style)
+    n_gsh: int = 0             # load-free pass-through buses given a shunt conductance g^sh (Table I)
+    gs_frac: float = 0.0       # fraction of primary lines with line shunt conductances g^s at both ends
 
 
 SHAPES = {
     # 13-shaped: 29 nodes, 28 lines, 7 leaves, S = 50 target; ~15 load-phases.
     "13": Shape(n3=25, n1=3, n_lat=3, window=4, r3=(0.002, 0.008), r1=(0.004, 0.016), load_a=(0.005, 0.03),
-                n_extra3=1, delta_frac=0.35, n_caps=2),
+                n_extra3=1, delta_frac=0.35, n_caps=2, n_lat2=1, n_gsh=2, gs_frac=0.3),
     # 123-shaped: 147 nodes, 146 lines, 43 leaves, S = 250 target.
     "123": Shape(n3=73, n1=73, n_lat=43, window=6, r3=(0.002, 0.008), r1=(0.004, 0.016), load_a=(0.002, 0.01),
-                 n_extra3=8, delta_frac=0.4, n_caps=4, lat_load_every=3),
+                 n_extra3=8, delta_frac=0.4, n_caps=4, lat_load_every=3, n_lat2=10, n_gsh=6, gs_frac=0.3),
     # 8500-shaped: N3=1566, N1=11545, 1222 leaves => S = 25001 (SURVEY.md App. B closed form).
     "8500": Shape(n3=1566, n1=11545, n_lat=1222, window=40, r3=(0.0002, 0.0008), r1=(0.004, 0.016),
                   load_a=(0.0005, 0.002), n_extra3=0, delta_frac=0.0, n_caps=8),
@@ -355,7 +358,7 @@ def make_radial(shape: Shape, seed: int, name: str) -> Feeder:
         fb.lines[0]["tau"] = [tau, tau, tau]
 
     # --- 1-phase chain laterals ---------------------------------------------------------------
-    lat_leaves = []
+    lat_leaves, lat_chains = [], []
     if shape.n_lat > 0 and shape.n1 >= shape.n_lat:
         extra = rng.multinomial(shape.n1 - shape.n_lat, np.full(shape.n_lat, 1.0 / shape.n_lat))
         lengths = 1 + extra
@@ -367,15 +370,18 @@ def make_radial(shape: Shape, seed: int, name: str) -> Feeder:
         for li in range(shape.n_lat):                       # chain of lengths[li] nodes, random phase
             ph = 1 << int(rng.integers(3))
             prev = hosts[li]
+            chain = (ph, [], [])
             for k in range(int(lengths[li])):
                 b = fb.bus(ph)
                 r = rng.uniform(*shape.r1)
                 x = rng.uniform(2.0, 3.0) * r
-                fb.line(prev, b, ph, np.eye(3) * r, np.eye(3) * x)
+                chain[2].append(fb.line(prev, b, ph, np.eye(3) * r, np.eye(3) * x))
+                chain[1].append(b)
                 if shape.lat_load_every and k < lengths[li] - 1 and (k + 1) % shape.lat_load_every == 0:
                     _add_load(fb, rng, b, ph, WYE, shape)
                 prev = b
             lat_leaves.append(prev)
+            lat_chains.append(chain)
 
     # --- loads ----------------------------------------------------------------------------------
     covered = set(lat_leaves)
@@ -400,9 +406,66 @@ def make_radial(shape: Shape, seed: int, name: str) -> Feeder:
         bsh = rng.uniform(0.005, 0.02, size=3) * (0.1 if shape.n3 > 1000 else 1.0)
         fb.buses[b]["bsh"] = [float(v) for v in bsh]
 
+    _widen_and_shunts(fb, shape, seed, root, lat_chains)
     f = fb.build()
     f.meta = dict(shape=name, seed=seed, n_prim_leaves=len(prim_leaves))
     return f
+
+
+def _widen_and_shunts(fb: FeederBuilder, shape: Shape, seed: int, root: int, lat_chains: list):
+    """The Table I input classes the base recipe leaves out, drawn from a second stream (seed + 7919) so
+    the rest of the feeder is unchanged: `n_lat2` laterals widened to 2 phases (the second phase gets
+    its own self r/x ~ the lateral range and mutuals U[0.25, 0.4] r / U[0.35, 0.5] x; loads on the chain
+    get a second-phase a, b, alpha, beta), `n_gsh` load- and capacitor-free non-leaf buses with
+    g^sh ~ U[1e-4, 5e-4], and a `gs_frac` share of the 3-phase lines with
+    g^s ~ U[1e-6, 1e-5] at both ends."""
+    if not (shape.n_lat2 or shape.n_gsh or shape.gs_frac):
+        return
+    rng = np.random.default_rng(seed + 7919)
+    loads_at = {}
+    for l, d in enumerate(fb.loads):
+        loads_at.setdefault(d["bus"], []).append(l)
+    n2 = min(shape.n_lat2, len(lat_chains))
+    for ci in (rng.choice(len(lat_chains), n2, replace=False) if n2 else []):
+        ph, buses, lines = lat_chains[int(ci)]
+        p0 = phase_list(ph)[0]
+        p1 = [p for p in range(3) if p != p0][int(rng.integers(2))]
+        mask = ph | (1 << p1)
+        for b in buses:
+            d = fb.buses[b]
+            d["phases"] = mask
+            d["wmin"][p1], d["wmax"][p1] = d["wmin"][p0], d["wmax"][p0]
+            for l in loads_at.get(b, []):
+                ld = fb.loads[l]
+                ld["phases"] = mask
+                a = rng.uniform(*shape.load_a)
+                ld["a"][p1] = float(a)
+                ld["b"][p1] = float(a * np.tan(np.arccos(rng.uniform(0.85, 0.98))))
+                ld["alpha"][p1] = float(rng.integers(0, 3))
+                ld["beta"][p1] = float(rng.integers(0, 3))
+        for e in lines:
+            d = fb.lines[e]
+            d["phases"] = mask
+            r = np.array(d["r"]).reshape(3, 3)
+            x = np.array(d["x"]).reshape(3, 3)
+            r[p1, p1] = rng.uniform(*shape.r1)
+            x[p1, p1] = rng.uniform(2.0, 3.0) * r[p1, p1]
+            r[p0, p1] = r[p1, p0] = rng.uniform(0.25, 0.4) * 0.5 * (r[p0, p0] + r[p1, p1])
+            x[p0, p1] = x[p1, p0] = rng.uniform(0.35, 0.5) * 0.5 * (x[p0, p0] + x[p1, p1])
+            d["r"], d["x"] = r.ravel().tolist(), x.ravel().tolist()
+            d["pmin"][p1], d["pmax"][p1] = d["pmin"][p0], d["pmax"][p0]
+            d["qmin"][p1], d["qmax"][p1] = d["qmin"][p0], d["qmax"][p0]
+            d["tau"][p1] = d["tau"][p0]
+    has_child = {int(d["f"]) for d in fb.lines}
+    cand = [b for b in range(len(fb.buses)) if b != root and b in has_child and b not in loads_at
+            and not any(fb.buses[b]["bsh"])]
+    for b in (rng.choice(cand, min(shape.n_gsh, len(cand)), replace=False) if shape.n_gsh and cand else []):
+        d = fb.buses[int(b)]
+        d["gsh"] = [float(rng.uniform(1e-4, 5e-4)) if p in phase_list(d["phases"]) else 0.0 for p in range(3)]
+    for d in fb.lines:
+        if d["phases"] == ALL3 and rng.uniform() < shape.gs_frac:
+            d["gs_from"] = [float(v) for v in rng.uniform(1e-6, 1e-5, size=3)]
+            d["gs_to"] = [float(v) for v in rng.uniform(1e-6, 1e-5, size=3)]
 
 
 def _add_load(fb: FeederBuilder, rng, bus: int, phases: int, conn: int, shape: Shape):

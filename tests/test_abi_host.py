@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol():
 
 
 @pytest.mark.parametrize("make", [lambda: fg.make_feeder("13"), lambda: fg.make_feeder("123"), fx.four_bus,
-                                  lambda: fx.two_bus_3ph(fg.DELTA), fx.one_bus_wye])
+                                  lambda: fx.two_bus_3ph(fg.DELTA), fx.one_bus_wye, fx.physical])
 def test_setup_matches_oracle(make):
     f = make()
     h = Lopf.setup(f)

@@ -89,8 +89,9 @@ def test_iterations_to_tolerance_bit_exact(torch_cuda, shape, kernel):
 
 @pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("make", [lambda: fx.chain_1ph(4), lambda: fx.two_bus_3ph(fg.DELTA), fx.four_bus,
-                                  fx.one_bus_wye, fx.two_bus_line, lambda: fx.two_bus_3ph(fg.WYE)],
-                         ids=["chain4", "2bus-delta", "4bus", "1bus (S=1, no line)", "2bus-no-load (c=0)", "2bus-wye"])
+                                  fx.one_bus_wye, fx.two_bus_line, lambda: fx.two_bus_3ph(fg.WYE), fx.physical],
+                         ids=["chain4", "2bus-delta", "4bus", "1bus (S=1, no line)", "2bus-no-load (c=0)", "2bus-wye",
+                              "physical (tau, g^s, g^sh, 2-phase)"])
 def test_fixtures_fixed_k_and_solve(torch_cuda, make, kernel):
     f = make()
     p = oracle.build_problem(f)
