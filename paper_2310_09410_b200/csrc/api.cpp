@@ -193,6 +193,9 @@ lopf_status lopf_setup_batch(const lopf_network* net, const lopf_options* opt, i
     } catch (const std::bad_alloc&) {
         delete h;
         return fail(LOPF_E_ARG, "out of host memory during setup");
+    } catch (const std::exception& ex) {
+        delete h;
+        return fail(LOPF_E_ARG, std::string("setup failed: ") + ex.what());
     }
     *out = h;
     return LOPF_OK;
@@ -224,6 +227,9 @@ lopf_status lopf_setup_part(const lopf_network* net, const lopf_options* opt, in
     } catch (const std::bad_alloc&) {
         delete h;
         return fail(LOPF_E_ARG, "out of host memory during setup");
+    } catch (const std::exception& ex) {
+        delete h;
+        return fail(LOPF_E_ARG, std::string("setup failed: ") + ex.what());
     }
     *out = h;
     return LOPF_OK;
@@ -706,6 +712,8 @@ lopf_status lopf_get_state(lopf_handle* h, void* stream, double* x, double* x_lo
 lopf_status lopf_set_state(lopf_handle* h, void* stream, const double* x_loc, const double* lam) {
     if (!h || !x_loc || !lam) return fail(LOPF_E_ARG, "NULL argument");
     if (h->parted()) return fail(LOPF_E_STATE, "lopf_set_state is not supported on a partitioned handle");
+    if (h->batch()) return fail(LOPF_E_STATE, "lopf_set_state is not supported on a batch handle (the u parity is "
+                                              "shared by all scenarios)");
     if (!h->bound) return fail(LOPF_E_STATE, "set_state before lopf_bind");
     cudaStream_t s = (cudaStream_t)stream;
     const Layout& L = h->lay;

@@ -468,35 +468,43 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
 }
 
 // Partitioned mode, after the exchange-buffer allreduce of sweep t: the other ranks' boundary u into
-// this rank's ghost slots of the buffer sweep t+1 reads, then the termination test of sweep t on the
-// residual sums added in rank order (identical on every rank).  One launch of one CTA per 256 ghosts.
+// this rank's ghost slots of the buffer sweep t+1 reads.  One CTA per 256 ghosts.  It only READS the
+// control block (sweep count, stop flag); the decision that changes them is a separate one-thread launch
+// after it (part_decide_kernel), so no block of a large import can see a half-updated control block.
 template <class T>
 __global__ void part_import_kernel(DevProblem P) {
-    DevCtrl* c = P.ctrl;
-    if (*(volatile long long*)&c->stopped) return;
-    const long long t = *(volatile long long*)&c->total;
+    const DevCtrl* c = P.ctrl;
+    if (*(volatile const long long*)&c->stopped) return;
+    const long long t = *(volatile const long long*)&c->total;
     T* dst = reinterpret_cast<T*>((t & 1) ? P.u0 : P.u1);               // = unext of sweep t
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_imp; i += gridDim.x * blockDim.x)
         dst[P.ghost0 + i] = (T)__ldcg(P.xbuf + P.imp[i]);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        for (int r = 0; r < P.world; ++r)
-            for (int k = 0; k < 5; ++k) s[k] += __ldcg(P.xbuf + P.n_bnd + (size_t)r * 8 + k);
-        const double pres = sqrt(s[0]), dres = P.rho * sqrt(s[1]);
-        const double ep = P.eps_rel * fmax(sqrt(s[2]), sqrt(s[3])), ed = P.eps_rel * sqrt(s[4]);
-        const int numeric = !(isfinite(s[0]) && isfinite(s[1]) && isfinite(s[2]) && isfinite(s[3]) && isfinite(s[4]));
-        const int conv = P.test && (pres <= ep) && (dres <= ed);
-        double obj = 0.0;                                              // this rank's share of c^T x
-        const T* xg = reinterpret_cast<const T*>(P.x);
-        for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * (double)__ldcg(xg + P.obj_idx[j]);
-        c->res[0] = pres; c->res[1] = dres; c->res[2] = ep; c->res[3] = ed;
-        c->objective = obj;
-        c->iters = c->iters + 1;
-        c->total = t + 1;
-        c->outcome = conv ? LOPF_CONVERGED : LOPF_MAX_ITER;
-        c->numeric = numeric;
-        if (conv || numeric) c->stopped = 1;
-    }
+}
+
+// ... then the termination test of sweep t on the residual sums added in rank order (identical on every
+// rank) and the sweep count / stop flag of the next sweep.
+template <class T>
+__global__ void part_decide_kernel(DevProblem P) {
+    DevCtrl* c = P.ctrl;
+    if (*(volatile long long*)&c->stopped) return;
+    const long long t = *(volatile long long*)&c->total;
+    double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int r = 0; r < P.world; ++r)
+        for (int k = 0; k < 5; ++k) s[k] += __ldcg(P.xbuf + P.n_bnd + (size_t)r * 8 + k);
+    const double pres = sqrt(s[0]), dres = P.rho * sqrt(s[1]);
+    const double ep = P.eps_rel * fmax(sqrt(s[2]), sqrt(s[3])), ed = P.eps_rel * sqrt(s[4]);
+    const int numeric = !(isfinite(s[0]) && isfinite(s[1]) && isfinite(s[2]) && isfinite(s[3]) && isfinite(s[4]));
+    const int conv = P.test && (pres <= ep) && (dres <= ed);
+    double obj = 0.0;                                              // this rank's share of c^T x
+    const T* xg = reinterpret_cast<const T*>(P.x);
+    for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * (double)__ldcg(xg + P.obj_idx[j]);
+    c->res[0] = pres; c->res[1] = dres; c->res[2] = ep; c->res[3] = ed;
+    c->objective = obj;
+    c->iters = c->iters + 1;
+    c->total = t + 1;
+    c->outcome = conv ? LOPF_CONVERGED : LOPF_MAX_ITER;
+    c->numeric = numeric;
+    if (conv || numeric) c->stopped = 1;
 }
 
 // ---- batch mode (config 4): (scenario, task) items over the one-scenario streaming layout ---------
@@ -918,8 +926,14 @@ lopf_status launch_reset_batch(const DevProblem& P, const BatchProblem& B, void*
 
 lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err) {
     const int nb = P.n_imp > 0 ? (P.n_imp + 255) / 256 : 1;
-    if (P.esz == 4) part_import_kernel<float><<<nb < 148 ? nb : 148, 256, 0, (cudaStream_t)stream>>>(P);
-    else part_import_kernel<double><<<nb < 148 ? nb : 148, 256, 0, (cudaStream_t)stream>>>(P);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (P.esz == 4) {
+        part_import_kernel<float><<<nb < 148 ? nb : 148, 256, 0, s>>>(P);
+        part_decide_kernel<float><<<1, 1, 0, s>>>(P);
+    } else {
+        part_import_kernel<double><<<nb < 148 ? nb : 148, 256, 0, s>>>(P);
+        part_decide_kernel<double><<<1, 1, 0, s>>>(P);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;

@@ -670,7 +670,7 @@ lopf_status build_batch_ops(const Net& base, const Canon& P, int32_t n_scen, con
     out.abar.assign((size_t)n_scen * out.VA, 0.0);
     out.bbar.assign((size_t)n_scen * out.VB, 0.0);
     std::vector<int> status(n_scen, 0);
-    auto work = [&](int32_t s0, int32_t s1) {
+    auto work_body = [&](int32_t s0, int32_t s1) {
         Net N = base;                                  // this thread's scaled copy
         Builder B(N);
         for (int32_t sc = s0; sc < s1; ++sc) {
@@ -713,22 +713,38 @@ lopf_status build_batch_ops(const Net& base, const Canon& P, int32_t n_scen, con
             }
         }
     };
+    // no exception may leave a worker thread (it would terminate the process): a failure marks the
+    // thread's scenarios with -2 and is reported after the join
+    auto work = [&](int32_t s0, int32_t s1) {
+        try {
+            work_body(s0, s1);
+        } catch (...) {
+            for (int32_t sc = s0; sc < s1; ++sc)
+                if (!status[sc]) status[sc] = -2;
+        }
+    };
     unsigned nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
     nt = (unsigned)std::min<int64_t>(nt, n_scen);
     std::vector<std::thread> th;
     const int32_t chunk = (n_scen + (int32_t)nt - 1) / (int32_t)nt;
-    for (unsigned t = 0; t < nt; ++t) {
-        const int32_t s0 = (int32_t)t * chunk, s1 = std::min(n_scen, s0 + chunk);
-        if (s0 < s1) th.emplace_back(work, s0, s1);
+    int32_t ran = 0;                                   // scenarios handed to threads; the rest run here
+    try {
+        for (unsigned t = 0; t < nt; ++t) {
+            const int32_t s0 = (int32_t)t * chunk, s1 = std::min(n_scen, s0 + chunk);
+            if (s0 < s1) { th.emplace_back(work, s0, s1); ran = s1; }
+        }
+    } catch (...) {                                    // thread creation failed: finish on this thread
     }
     for (auto& t : th) t.join();
+    if (ran < n_scen) work(ran, n_scen);
     for (int32_t sc = 0; sc < n_scen; ++sc)
         if (status[sc]) {
             err = "batch scenario " + std::to_string(sc) + ": " +
-                  (status[sc] == -1 ? std::string("row outside the structural column set")
+                  (status[sc] == -2 ? std::string("host failure (out of memory?) in the precompute")
+                   : status[sc] == -1 ? std::string("row outside the structural column set")
                                     : status[sc] == LOPF_E_RANK ? std::string("A_s A_s^T singular")
                                                                 : std::string("inconsistent equality rows"));
-            return status[sc] == -1 ? LOPF_E_NETWORK : (lopf_status)status[sc];
+            return status[sc] == -2 ? LOPF_E_ARG : status[sc] == -1 ? LOPF_E_NETWORK : (lopf_status)status[sc];
         }
     return LOPF_OK;
 }

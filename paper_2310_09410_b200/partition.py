@@ -48,10 +48,20 @@ class PartitionedSolver:
             dist.all_reduce(self.xbuf, group=self.group)
 
     def sweep(self, stream=None):
-        """One sweep on every rank (collective)."""
-        self.h.part_sweep(stream)
-        self._allreduce()
-        self.h.part_import(stream)
+        """One sweep on every rank (collective).  The three steps are ordered on one stream: a given
+        stream becomes torch's current stream for the allreduce too."""
+        import contextlib
+        import torch
+        if stream is None:
+            ctx = contextlib.nullcontext()
+        elif isinstance(stream, int):
+            ctx = torch.cuda.stream(torch.cuda.ExternalStream(stream))
+        else:
+            ctx = torch.cuda.stream(stream)
+        with ctx:                                     # everything on torch's current stream
+            self.h.part_sweep(None)
+            self._allreduce()
+            self.h.part_import(None)
 
     def reset(self, stream=None):
         self.h.reset(stream)
