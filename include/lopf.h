@@ -95,8 +95,7 @@ typedef struct {
     int32_t block_threads; /* must be 0: block sizes are fixed per kernel at build time (lopf_sizes.block) */
     int32_t max_ctas;      /* resident kernel: CTAs available (one per SM; 0 = 148, the B200 SM count) */
     int32_t grid_cap;      /* streaming kernel: cap on the persistent grid (0 = occupancy x SMs; test hook) */
-    int32_t reserved[2];   /* [0] = 1: per-CTA phase cycle counters (lopf_get_profile); [1]: diagnostics phase-skip
-                              mask (bit 0 global update, bit 1 local/dual update) — results are then NOT the method */
+    int32_t reserved[2];   /* [0] = 1: per-CTA phase cycle counters (lopf_get_profile); [1] must be 0 */
     int32_t precision;     /* 0 or 64: fp64 (the parity path); 32: fp32 operators, iterate and arithmetic — the
                               paper's GPU precision (reading F1).  Residual sums,
                               the termination test and the objective stay fp64.  All three kernels. */

@@ -7,8 +7,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "liblopf.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("setup.cpp", "partition.cpp", "pack.cpp", "pack_resident.cpp", "pack_batch.cpp", "api.cpp", "kernels.cu",
-                                                  "resident.cu")]
-HEADERS = [os.path.join(HERE, "csrc", "internal.h"), os.path.join(ROOT, "include", "lopf.h")]
+                                                  "resident.cu", "batch.cu")]
+HEADERS = [os.path.join(HERE, "csrc", "internal.h"), os.path.join(HERE, "csrc", "device.cuh"), os.path.join(ROOT, "include", "lopf.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -105,6 +105,8 @@ static lopf_status check_precision(const lopf_options& o) {
         return fail(LOPF_E_ARG, "precision must be 0 / 64 (fp64) or 32 (fp32)");
     if (o.block_threads != 0)
         return fail(LOPF_E_ARG, "block_threads must be 0 (block sizes are fixed per kernel; see lopf_sizes.block)");
+    if (o.reserved[1] != 0)
+        return fail(LOPF_E_ARG, "options.reserved[1] must be 0 (the phase-skip diagnostics are a build flag, LOPF_DIAG_SKIP)");
     return LOPF_OK;
 }
 
@@ -326,7 +328,7 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
         sz->reserved[1] = h->lay.max_smem;
     }
     sz->grid = h->resident() ? h->lay.G : h->grid;
-    sz->block = h->resident() ? kResBlock : h->batch() ? batch_block(h->lay.esz) : stream_block(h->lay.rmax, h->lay.esz);
+    sz->block = h->resident() ? kResBlock : h->batch() ? batch_block() : stream_block(h->lay.rmax, h->lay.esz);
     sz->n_scen = h->batch() ? h->lay.n_scen : 0;
     return LOPF_OK;
 }
@@ -346,60 +348,55 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         CUDA_TRY(cudaEventCreate(&h->ev0), "cudaEventCreate");
         CUDA_TRY(cudaEventCreate(&h->ev1), "cudaEventCreate");
     }
-    CUDA_TRY(cudaMemcpyAsync(arena, h->lay.image.data(), h->lay.bytes, cudaMemcpyHostToDevice, s), "bind H2D");
+    CUDA_TRY(cudaMemcpyAsync(arena, h->lay.image.data(), h->lay.image.size(), cudaMemcpyHostToDevice, s), "bind H2D");
     const Layout& L = h->lay;
     uint8_t* b = (uint8_t*)arena;
-    if (h->batch()) {                              // streaming template + per-scenario arrays
-        DevProblem& P = h->dp;
-        P = DevProblem{};
-        P.n_tasks = (int32_t)L.n_tasks;
-        P.n_slots = (int32_t)L.n_slots;
-        P.rmax = L.rmax;
-        P.esz = L.esz;
-        P.n = h->cp.n;
-        P.tasks = (const int4*)(b + L.off_tasks);
-        P.s_meta = (const SlotMeta*)(b + L.off_meta);
-        P.s_bbar = (const double*)(b + L.off_bbar);
-        P.xl = (double*)(b + L.off_xl);
-        P.lam = (double*)(b + L.off_lam);
-        P.u0 = (double*)(b + L.off_u0);
-        P.u1 = (double*)(b + L.off_u1);
-        P.x0 = (const double*)(b + L.off_x0);
-        P.gbnd = (const double2*)(b + L.off_gpar);
-        P.gcost = (const double*)(b + L.off_gcost);
-        P.seg_ptr = (const int32_t*)(b + L.off_segptr);
-        P.seg_slot = (const int32_t*)(b + L.off_segslot);
-        P.x = (double*)(b + L.off_x);
-        P.abar = (const double*)(b + L.off_abar);
-        P.partial = (double*)(b + L.off_partial);
-        P.ctrl = (DevCtrl*)(b + L.off_ctrl);
-        P.trace = (double*)(b + L.off_trace);
-        P.obj_idx = (const int32_t*)(b + L.off_objidx);
-        P.obj_c = (const double*)(b + L.off_objc);
-        P.n_obj = (int32_t)L.n_obj;
-        P.rho = h->opt.rho;
-        P.inv_rho = 1.0 / h->opt.rho;
-        P.eps_rel = h->opt.eps_rel;
+    if (h->batch()) {                              // lane = scenario layout (pack_batch.cpp, batch.cu)
         BatchProblem& B = h->bp;
+        B = BatchProblem{};
         B.n_scen = L.n_scen;
+        B.n_grp = L.n_grp;
+        B.n_rows = L.n_rows;
         B.n_tasks = (int32_t)L.n_tasks;
-        B.ns_stride = (int32_t)L.n_slots;
-        B.n_stride = (int32_t)h->cp.n;
-        B.vp_stride = L.VP;
-        B.var_pool = (const double*)(b + L.off_bvar);
+        B.ve = L.ve;
+        B.ns_max = L.ns_max;
+        B.esz = L.esz;
+        B.n_obj = (int32_t)L.n_obj;
+        B.n = h->cp.n;
+        B.rows = (const BRow*)(b + L.off_brow);
+        B.subs = (const BSub*)(b + L.off_bsub);
+        B.tasks = (const BTask*)(b + L.off_btask);
+        B.seg_rows = (const int32_t*)(b + L.off_bseg);
+        B.gpar = b + L.off_gpar;
+        B.spool = b + L.off_bspool;
+        B.vpool = b + L.off_bvpool;
+        B.x0 = b + L.off_x0;
+        B.xl = b + L.off_xl;
+        B.lam = b + L.off_lam;
+        B.u0 = b + L.off_u0;
+        B.u1 = b + L.off_u1;
+        B.x = b + L.off_x;
+        B.partial = (double*)(b + L.off_bpart);
         B.res = (ScenResult*)(b + L.off_bres);
         B.stopped = (int32_t*)(b + L.off_bstop);
-        B.partial = (double*)(b + L.off_bpart);
+        B.gact = (uint32_t*)(b + L.off_bgact);
         B.cnt = (unsigned long long*)(b + L.off_bcnt);
-        B.amask = (uint32_t*)(b + L.off_bmask);
         B.wpre = (const long long*)(b + L.off_bwpre);
+        B.obj_idx = (const int32_t*)(b + L.off_objidx);
+        B.obj_c = (const double*)(b + L.off_objc);
+        B.ctrl = (DevCtrl*)(b + L.off_ctrl);
+        B.stage = (double*)(b + L.off_bstage);
+        B.rho = h->opt.rho;
+        B.inv_rho = 1.0 / h->opt.rho;
+        B.eps_rel = h->opt.eps_rel;
+        h->dp = DevProblem{};
+        h->dp.ctrl = B.ctrl;
         std::string err;
         int grid = 0;
-        B.staged = L.staged;
-        lopf_status st = query_batch_grid(L.rmax, L.esz, L.staged, &grid, err);
+        lopf_status st = query_batch_grid(L.ns_max, L.esz, &grid, err);
         if (st != LOPF_OK) return fail(st, err);
         h->grid = grid;
-        st = launch_reset_batch(P, B, stream, err);
+        st = launch_reset_batch(B, stream, err);
         if (st != LOPF_OK) return fail(st, err);
         h->arena = arena;
         h->arena_bytes = bytes;
@@ -437,7 +434,6 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         R.inv_rho = 1.0 / h->opt.rho;
         R.eps_rel = h->opt.eps_rel;
         R.prof = h->opt.reserved[0] ? (long long*)(b + L.off_prof) : nullptr;   // diagnostics switch
-        R.skip = h->opt.reserved[1];
         R.esz = L.esz;
         h->dp = DevProblem{};
         h->dp.ctrl = R.ctrl;
@@ -504,7 +500,7 @@ lopf_status lopf_reset(lopf_handle* h, void* stream) {
     if (!h->bound) return fail(LOPF_E_STATE, "lopf_reset before lopf_bind");
     std::string err;
     lopf_status st = h->resident() ? launch_reset_resident(h->rp, stream, err)
-                     : h->batch() ? launch_reset_batch(h->dp, h->bp, stream, err)
+                     : h->batch() ? launch_reset_batch(h->bp, stream, err)
                                   : launch_reset(h->dp, stream, err);
     if (st == LOPF_OK && h->parted())
         CUDA_TRY(cudaMemsetAsync(h->dp.xbuf, 0, sizeof(double) * ((size_t)h->lay.n_bnd + 8 * (size_t)h->lay.world),
@@ -528,10 +524,10 @@ lopf_status lopf_solve_async(lopf_handle* h, int64_t max_iter, int32_t test, voi
         R.epoch = ++h->epoch;
         st = launch_resident(R, stream, err);
     } else if (h->batch()) {
-        DevProblem P = h->dp;
-        P.max_iter = max_iter;
-        P.test = test ? 1 : 0;
-        st = launch_batch(P, h->bp, h->grid, stream, err);
+        BatchProblem B = h->bp;
+        B.max_iter = max_iter;
+        B.test = test ? 1 : 0;
+        st = launch_batch(B, h->grid, stream, err);
     } else {
         DevProblem P = h->dp;
         P.max_iter = max_iter;
@@ -688,6 +684,7 @@ static lopf_status fetch_slots(lopf_handle* h, cudaStream_t s, std::vector<doubl
 lopf_status lopf_get_state(lopf_handle* h, void* stream, double* x, double* x_loc, double* lam) {
     if (!h) return fail(LOPF_E_ARG, "NULL handle");
     if (!h->bound) return fail(LOPF_E_STATE, "get_state before lopf_bind");
+    if (h->batch()) return fail(LOPF_E_STATE, "batch handle: use lopf_get_state_scen");
     cudaStream_t s = (cudaStream_t)stream;
     const Layout& L = h->lay;
     if (x) CUDA_TRY(d2h_elems(x, h->dp.x, h->cp.n, L.esz, s), "state D2H");
@@ -780,17 +777,17 @@ lopf_status lopf_get_state_scen(lopf_handle* h, void* stream, int32_t scen, doub
     if (scen < 0 || scen >= h->lay.n_scen) return fail(LOPF_E_ARG, "scenario index out of range");
     cudaStream_t s = (cudaStream_t)stream;
     const Layout& L = h->lay;
-    const size_t NS = (size_t)L.n_slots, N = (size_t)h->cp.n;
-    std::vector<double> xl(NS), lm(NS);
-    const size_t E = (size_t)L.esz;
-    CUDA_TRY(d2h_elems(xl.data(), (const uint8_t*)h->dp.xl + E * scen * NS, NS, L.esz, s), "state D2H");
-    CUDA_TRY(d2h_elems(lm.data(), (const uint8_t*)h->dp.lam + E * scen * NS, NS, L.esz, s), "state D2H");
-    if (x) CUDA_TRY(d2h_elems(x, (const uint8_t*)h->dp.x + E * scen * N, N, L.esz, s), "state D2H");
-    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    std::string err;
+    lopf_status st = launch_gather_scen(h->bp, scen, stream, err);     // one gather kernel, one D2H
+    if (st != LOPF_OK) return fail(st, err);
+    const size_t nr = (size_t)L.n_rows, n = (size_t)h->cp.n;
+    std::vector<double> stage(2 * nr + n);
+    CUDA_TRY(d2h_elems(stage.data(), h->bp.stage, stage.size(), 8, s), "state D2H");
     for (int64_t k = 0; k < h->cp.nc; ++k) {
-        if (x_loc) x_loc[k] = xl[L.slot_of_copy[k]];
-        if (lam) lam[k] = lm[L.slot_of_copy[k]];
+        if (x_loc) x_loc[k] = stage[L.slot_of_copy[k]];
+        if (lam) lam[k] = stage[nr + L.slot_of_copy[k]];
     }
+    if (x) std::copy(stage.begin() + 2 * nr, stage.end(), x);
     return LOPF_OK;
 }
 

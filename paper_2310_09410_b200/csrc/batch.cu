@@ -1,0 +1,368 @@
+// Batch kernel for sm_100a (config 4): many load scenarios of one feeder, each an
+// independent run of Algorithm 1 with its own (termination) test.
+//
+// Lane = scenario.  Scenarios form groups of 32 and every per-scenario array is [group][entry][32], so a
+// warp instruction moves one 256-byte line for 32 scenarios while everything structural -- rows, segment
+// lists, bounds, the operators of subsystems without a load -- is the same address for all 32 lanes
+// (uniform loads).  A work item is (group, task), a task a depth-first run of subsystems; per item and
+// subsystem s the warp computes, for its 32 scenarios at once,
+//   a4  x_g = clamp((sum_{k in seg(g)} u_k - c_g/rho) / nu_g, lo_g, hi_g) for each row (closed_1, rho
+//       restored, reading C1), canonical copy order; d = -rho v - lambda staged in SMEM [row][lane]
+//   a5  y = Abar_s d, four rows at a time (k ascending, FMA); Abar_s from the shared dense pool (uniform
+//       loads) or, for a load subsystem, the scenario's packed upper triangle ([entry][lane], coalesced)
+//   a6  x_s = y / rho + bbar_s, lambda += rho (v - x_s), u = x_s - lambda / rho     (closed_2, ADMM-3)
+//   a7  five residual sums per lane (scenario), written per item
+// The ACTIVE items of a sweep (groups with a scenario still running, times tasks) are cut into one
+// contiguous chunk per warp by a per-task cost weight.  Grid barrier; one warp per active group then
+// sums each scenario's item partials in task order (deterministic) and takes its decision; converged
+// scenarios freeze (their lanes stop storing), a group leaves the item list when all 32 have; grid barrier.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "device.cuh"
+#include "internal.h"
+
+namespace lopf {
+
+namespace {
+
+using dev::grid_sync;
+using dev::kFull;
+
+constexpr int BW = kBatchWarps;
+constexpr int BB = 32 * BW;
+
+template <class T> struct V2;                 // {c/rho, lo}, {hi, 1/nu} per global
+template <> struct V2<double> { using type = double2; };
+template <> struct V2<float> { using type = float2; };
+
+// first item (active-group rank * NT + task) whose start weight (rank * WS + wpre[task]) is >= w
+__device__ __forceinline__ long long item_at(const long long* __restrict__ wpre, const int NT, const long long WS,
+                                             const long long w) {
+    const long long ar = w / WS, rem = w - ar * WS;
+    if (rem == 0) return ar * NT;
+    int lo = 1, hi = NT;                       // smallest t with wpre[t] >= rem (wpre[NT] = WS > rem)
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(wpre + mid) >= rem) hi = mid; else lo = mid + 1;
+    }
+    return ar * NT + lo;
+}
+
+// One (group, task) item for the 32 scenarios of the group (lane = scenario; `act`: the lane's scenario
+// is running -- frozen or padding lanes compute but store nothing and add nothing).
+template <class T>
+__device__ __forceinline__ void batch_item(const BatchProblem& B, const int grp, const int task,
+                                           const T* __restrict__ ucur, T* __restrict__ unext, T* __restrict__ dsm,
+                                           const int lane, const bool act, double (&acc)[5]) {
+    using T2 = typename V2<T>::type;
+    const T rho = (T)B.rho, inv_rho = (T)B.inv_rho;
+    const int4 tk = __ldg(reinterpret_cast<const int4*>(B.tasks) + task);
+    const size_t gb = (size_t)grp * B.n_rows;                        // first row of this group
+    T* __restrict__ xlp = reinterpret_cast<T*>(B.xl);
+    T* __restrict__ lmp = reinterpret_cast<T*>(B.lam);
+    T* __restrict__ xg = reinterpret_cast<T*>(B.x) + (size_t)grp * B.n * 32 + lane;
+    const T2* __restrict__ gpar = reinterpret_cast<const T2*>(B.gpar);
+    const int2* __restrict__ rows = reinterpret_cast<const int2*>(B.rows);
+    for (int s = tk.x; s < tk.y; ++s) {
+        const int4 sm = __ldg(reinterpret_cast<const int4*>(B.subs) + s);   // {row0, ns, op, flags}
+        const int row0 = sm.x, ns = sm.y;
+        // a4: consensus of every row's global; v parked in unext (replaced by u below), d in SMEM
+#pragma unroll 2
+        for (int r = 0; r < ns; ++r) {
+            const int row = row0 + r;
+            const int2 gi = __ldg(rows + 3 * row);                     // {g, info}
+            const int2 n01 = __ldg(rows + 3 * row + 1);
+            T sig;
+            if (gi.y & kBInline) {                                      // nu <= 4: rows inline
+                const int nu = (gi.y >> kBNuShift) & 0xFF;
+                const int2 n23 = __ldg(rows + 3 * row + 2);
+                const T a0 = __ldcg(ucur + (gb + n01.x) * 32 + lane);
+                const T a1 = nu > 1 ? __ldcg(ucur + (gb + n01.y) * 32 + lane) : T(0);
+                const T a2 = nu > 2 ? __ldcg(ucur + (gb + n23.x) * 32 + lane) : T(0);
+                const T a3 = nu > 3 ? __ldcg(ucur + (gb + n23.y) * 32 + lane) : T(0);
+                sig = ((a0 + a1) + a2) + a3;                            // ascending canonical copy order
+            } else {
+                sig = T(0);
+                for (int q = 0; q < n01.y; ++q) sig += __ldcg(ucur + (gb + __ldg(B.seg_rows + n01.x + q)) * 32 + lane);
+            }
+            const T2 ga = __ldg(gpar + 2 * gi.x), gb2 = __ldg(gpar + 2 * gi.x + 1);
+            const T v = fmin(fmax((sig - ga.x) * gb2.y, ga.y), gb2.x);  // IEEE +-inf bounds = no clamp
+            const size_t at = (gb + row) * 32 + lane;
+            if (act && (gi.y & kBFirst)) __stcg(xg + (size_t)gi.x * 32, v);
+            dsm[r * 32 + lane] = -rho * v - __ldcg(lmp + at);
+            if (act) __stcg(unext + at, v);
+        }
+        __syncwarp();
+        // a5-a7, four rows at a time: y_r = sum_k Abar[r][k] d_k with k ascending
+        const bool var = sm.w & kBVar;
+        const T* __restrict__ V = reinterpret_cast<const T*>(B.vpool) + ((size_t)grp * B.ve + (var ? sm.z : 0)) * 32 + lane;
+        const T* __restrict__ A = reinterpret_cast<const T*>(B.spool) + (var ? 0 : sm.z);
+        for (int r0 = 0; r0 < ns; r0 += 4) {
+            int rr[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rr[i] = min(r0 + i, ns - 1);    // rows past n_s: discarded
+            T y[4] = {T(0), T(0), T(0), T(0)};
+            if (var) {
+                // packed upper triangle, row-major: (i, j >= i) at i n - i (i - 1) / 2 + j - i; row r reads
+                // (min(r, k), max(r, k)): the walk steps by n - k - 1 while k < r, then by 1
+                int p[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) p[i] = rr[i];
+#pragma unroll 2
+                for (int k = 0; k < ns; ++k) {
+                    const T dk = dsm[k * 32 + lane];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        y[i] = fma(__ldg(V + (size_t)p[i] * 32), dk, y[i]);
+                        p[i] += k < rr[i] ? ns - k - 1 : 1;
+                    }
+                }
+            } else {
+#pragma unroll 2
+                for (int k = 0; k < ns; ++k) {                          // Abar is exactly symmetric: A[k][r]
+                    const T dk = dsm[k * 32 + lane];
+                    const T* __restrict__ Ak = A + k * ns;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) y[i] = fma(__ldg(Ak + rr[i]), dk, y[i]);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = r0 + i;
+                if (r >= ns) break;
+                const size_t at = (gb + row0 + r) * 32 + lane;
+                const T bb = (sm.w & kBBbar) ? __ldg(V + (size_t)(ns * (ns + 1) / 2 + r) * 32) : T(0);
+                const T xn = fma(y[i], inv_rho, bb);                    // (1/rho) Abar d + bbar
+                const T v = __ldcg(unext + at);
+                const T lam = __ldcg(lmp + at), xo = __ldcg(xlp + at);
+                const T ln = lam + rho * (v - xn);                      // ADMM-3
+                const T un = xn - ln * inv_rho;                         // next consensus input
+                if (act) {
+                    __stcg(xlp + at, xn);
+                    __stcg(lmp + at, ln);
+                    __stcg(unext + at, un);
+                    const T rs = v - xn, dx = xn - xo;                  // terms in T, sums in fp64 (F1)
+                    acc[0] += (double)(rs * rs);
+                    acc[1] += (double)(dx * dx);
+                    acc[2] += (double)(v * v);
+                    acc[3] += (double)(xn * xn);
+                    acc[4] += (double)(ln * ln);
+                }
+            }
+        }
+        __syncwarp();                                                  // dsm is reused by the next subsystem
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(BB, 1) admm_batch_kernel(BatchProblem B) {
+    extern __shared__ __align__(16) unsigned char bsm[];
+    __shared__ int s_gl[kBatchMaxGrp];                  // active groups of this sweep, ascending
+    __shared__ int s_na;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int gw = blockIdx.x * BW + wid, nw = gridDim.x * BW;
+    T* dsm = reinterpret_cast<T*>(bsm) + (size_t)wid * B.ns_max * 32;
+    const long long total0 = *(volatile long long*)&B.ctrl->total;
+    const int NT = B.n_tasks, NG = B.n_grp;
+    const long long WS = __ldg(B.wpre + NT);
+    unsigned long long bars = 0;
+    long long it = 0;
+    while (it < B.max_iter) {
+        const long long t = total0 + it;
+        const T* ucur = reinterpret_cast<const T*>((t & 1) ? B.u1 : B.u0);
+        T* unext = reinterpret_cast<T*>((t & 1) ? B.u0 : B.u1);
+        const uint32_t* gcur = B.gact + (size_t)(it & 1) * NG;
+        if (wid == 0) {
+            int run = 0;
+            for (int g0 = 0; g0 < NG; g0 += 32) {
+                const int g = g0 + lane;
+                const bool a = g < NG && __ldcg(gcur + g) != 0u;
+                const unsigned m = __ballot_sync(kFull, a);
+                if (a) s_gl[run + __popc(m & ((1u << lane) - 1u))] = g;
+                run += __popc(m);
+            }
+            if (lane == 0) s_na = run;
+        }
+        if (blockIdx.x == 0)
+            for (int g = threadIdx.x; g < NG; g += blockDim.x) B.gact[(size_t)((it + 1) & 1) * NG + g] = 0u;
+        __syncthreads();
+        const int NA = s_na;
+        if (NA == 0) break;                             // every scenario has stopped (same view in every CTA)
+        // warp gw takes the items whose start weight lies in [gw, gw + 1) * WT / nw
+        const long long WT = (long long)NA * WS;
+        const long long a0 = item_at(B.wpre, NT, WS, (WT * gw + nw - 1) / nw);
+        const long long a1 = item_at(B.wpre, NT, WS, (WT * (gw + 1) + nw - 1) / nw);
+        int cur = -1;
+        bool act = false;
+        for (long long a = a0; a < a1; ++a) {
+            const int ag = (int)(a / NT), task = (int)(a - (long long)ag * NT);
+            const int grp = s_gl[ag];
+            if (grp != cur) {
+                cur = grp;
+                const int sc = grp * 32 + lane;
+                act = sc < B.n_scen && __ldcg(B.stopped + sc) == 0;
+            }
+            double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+            batch_item<T>(B, grp, task, ucur, unext, dsm, lane, act, acc);
+            double* pp = B.partial + ((size_t)grp * NT + task) * 5 * 32 + lane;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) __stcg(pp + k * 32, acc[k]);
+        }
+        grid_sync(B.cnt, (++bars) * gridDim.x);
+        // per-scenario (termination): warp per active group, lane = scenario
+        uint32_t* gnext = B.gact + (size_t)((it + 1) & 1) * NG;
+        for (int ag = gw; ag < NA; ag += nw) {
+            const int grp = s_gl[ag], sc = grp * 32 + lane;
+            const bool act = sc < B.n_scen && __ldcg(B.stopped + sc) == 0;
+            double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+            const double* pp = B.partial + (size_t)grp * NT * 160 + lane;
+            for (int k2 = 0; k2 < NT; ++k2)                      // task order: fixed
+#pragma unroll
+                for (int k = 0; k < 5; ++k) s5[k] += __ldcg(pp + (size_t)k2 * 160 + k * 32);
+            const double pres = sqrt(s5[0]), dres = B.rho * sqrt(s5[1]);
+            const double ep = B.eps_rel * fmax(sqrt(s5[2]), sqrt(s5[3])), ed = B.eps_rel * sqrt(s5[4]);
+            const int num = !(isfinite(s5[0]) && isfinite(s5[1]) && isfinite(s5[2]) && isfinite(s5[3]) && isfinite(s5[4]));
+            const int conv = B.test && pres <= ep && dres <= ed;
+            const bool fin = conv || num || it + 1 == B.max_iter;
+            if (act) {
+                ScenResult& R = B.res[sc];
+                R.iters = it + 1;
+                R.total = t + 1;
+                R.res[0] = pres; R.res[1] = dres; R.res[2] = ep; R.res[3] = ed;
+                R.status = conv ? 1 : num ? 3 : (fin ? 2 : 0);
+                if (fin) {
+                    double obj = 0.0;
+                    const T* xs = reinterpret_cast<const T*>(B.x) + (size_t)grp * B.n * 32 + lane;
+                    for (int j = 0; j < B.n_obj; ++j) obj += B.obj_c[j] * (double)__ldcg(xs + (size_t)B.obj_idx[j] * 32);
+                    R.objective = obj;
+                }
+                if (conv || num) B.stopped[sc] = 1;
+            }
+            if (__any_sync(kFull, act && !(conv || num)) && lane == 0) gnext[grp] = 1u;
+        }
+        grid_sync(B.cnt, (++bars) * gridDim.x);
+        ++it;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        B.ctrl->total = total0 + it;
+        B.ctrl->iters = it;
+    }
+}
+
+// Before each launch: the first sweep's active groups from the stopped flags (scenarios stopped in an
+// earlier launch stay frozen); the other parity cleared.
+__global__ void batch_gact_kernel(BatchProblem B) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < B.n_grp; g += gridDim.x * blockDim.x) {
+        uint32_t any = 0u;
+        for (int l = 0; l < 32; ++l) {
+            const int sc = g * 32 + l;
+            if (sc < B.n_scen && !B.stopped[sc]) any = 1u;
+        }
+        B.gact[g] = any;
+        B.gact[B.n_grp + g] = 0u;
+    }
+}
+
+// a3 for every scenario: x_s = x0, lambda = 0, u = x0; x = 0; results cleared.
+template <class T>
+__global__ void reset_batch_kernel(BatchProblem B) {
+    const T* x0 = reinterpret_cast<const T*>(B.x0);
+    const size_t nr = (size_t)B.n_grp * B.n_rows * 32, nx = (size_t)B.n_grp * B.n * 32;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += stride) {
+        const T v = x0[(i >> 5) % B.n_rows];
+        reinterpret_cast<T*>(B.xl)[i] = v;
+        reinterpret_cast<T*>(B.lam)[i] = T(0);
+        reinterpret_cast<T*>(B.u0)[i] = v;
+        reinterpret_cast<T*>(B.u1)[i] = T(0);
+    }
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nx; i += stride) reinterpret_cast<T*>(B.x)[i] = T(0);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < (size_t)B.n_scen; i += stride) {
+        ScenResult& R = B.res[i];
+        R.iters = 0; R.total = 0; R.status = 0; R.pad = 0; R.objective = 0.0;
+        R.res[0] = R.res[1] = R.res[2] = R.res[3] = 0.0;
+        B.stopped[i] = 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        B.ctrl->total = 0;
+        B.ctrl->iters = 0;
+    }
+}
+
+// Scenario scen's x_s, lambda (rows) and x (globals) widened to fp64 into the staging area:
+// stage[0 .. n_rows) = x_s, [n_rows .. 2 n_rows) = lambda, [2 n_rows .. 2 n_rows + n) = x.
+template <class T>
+__global__ void gather_scen_kernel(BatchProblem B, int32_t scen) {
+    const int grp = scen >> 5, lane = scen & 31;
+    const size_t gb = (size_t)grp * B.n_rows;
+    const int stride = gridDim.x * blockDim.x;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < B.n_rows; r += stride) {
+        B.stage[r] = (double)reinterpret_cast<const T*>(B.xl)[(gb + r) * 32 + lane];
+        B.stage[B.n_rows + r] = (double)reinterpret_cast<const T*>(B.lam)[(gb + r) * 32 + lane];
+    }
+    for (int64_t g = blockIdx.x * blockDim.x + threadIdx.x; g < B.n; g += stride)
+        B.stage[2 * (size_t)B.n_rows + g] = (double)reinterpret_cast<const T*>(B.x)[((size_t)grp * B.n + g) * 32 + lane];
+}
+
+const void* batch_kernel_for(int esz) {
+    return esz == 4 ? (const void*)admm_batch_kernel<float> : (const void*)admm_batch_kernel<double>;
+}
+
+}  // namespace
+
+int batch_block() { return BB; }
+
+int batch_smem(int ns_max, int esz) { return BW * ns_max * 32 * esz; }
+
+lopf_status query_batch_grid(int ns_max, int esz, int* grid, std::string& err) {
+    int dev = 0, sms = 0, per = 0;
+    const void* k = batch_kernel_for(esz);
+    const int smem = batch_smem(ns_max, esz);
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, BB, smem);
+    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
+    if (per < 1) { err = "batch kernel cannot be resident (occupancy 0)"; return LOPF_E_CUDA; }
+    *grid = sms * per;
+    return LOPF_OK;
+}
+
+lopf_status launch_batch(const BatchProblem& B, int grid, void* stream, std::string& err) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const void* k = batch_kernel_for(B.esz);
+    const int smem = batch_smem(B.ns_max, B.esz);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaMemsetAsync(B.cnt, 0, sizeof(unsigned long long), s);
+    if (e == cudaSuccess) {
+        batch_gact_kernel<<<(B.n_grp + 255) / 256, 256, 0, s>>>(B);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && B.max_iter > 0) {
+        BatchProblem C = B;
+        void* args[] = {&C};
+        e = cudaLaunchCooperativeKernel(k, dim3(grid), dim3(BB), args, smem, s);
+    }
+    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
+    return LOPF_OK;
+}
+
+lopf_status launch_reset_batch(const BatchProblem& B, void* stream, std::string& err) {
+    if (B.esz == 4) reset_batch_kernel<float><<<1184, 256, 0, (cudaStream_t)stream>>>(B);
+    else reset_batch_kernel<double><<<1184, 256, 0, (cudaStream_t)stream>>>(B);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
+    return LOPF_OK;
+}
+
+lopf_status launch_gather_scen(const BatchProblem& B, int32_t scen, void* stream, std::string& err) {
+    if (B.esz == 4) gather_scen_kernel<float><<<64, 256, 0, (cudaStream_t)stream>>>(B, scen);
+    else gather_scen_kernel<double><<<64, 256, 0, (cudaStream_t)stream>>>(B, scen);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
+    return LOPF_OK;
+}
+
+}  // namespace lopf

@@ -184,13 +184,16 @@ struct ResProblem {                           // resident kernel argument
     double rho, inv_rho, eps_rel;
     long long max_iter;
     long long* prof;                          // diagnostics: [G][4] cycles (work, publish+wait, -, sweeps) or NULL
-    int32_t skip;                             // diagnostics: bit 1 skips the update work (sync cost only)
     uint32_t epoch;                           // launch number (> 0): high half of the exchange tags
     int32_t esz;                              // element size of the SMEM state / blob arrays: 8 fp64, 4 fp32 (F1)
 };
 
-// ---- batch kernel (config 4: lane = scenario, 32 scenarios per CTA group) -----------------------
-
+// ---- batch kernel (config 4): lane = scenario ------------------------------------
+// Scenarios form groups of 32 (group g, lane l = scenario 32 g + l).  Every per-scenario array is
+// [group][entry][32]: one warp instruction touches one 256-byte line for 32 scenarios, and every
+// structural datum (rows, subsystems, shared operators) is the same for the 32 lanes (uniform loads).
+// Rows are the copies in depth-first subsystem order; a work item is (group, task), a task a DFS run
+// of subsystems.
 
 struct ScenResult {                            // 64 B per scenario (device)
     long long iters;                           // sweeps executed in the last launch
@@ -201,22 +204,60 @@ struct ScenResult {                            // 64 B per scenario (device)
     double objective;
 };
 
-struct BatchProblem {                          // config 4: streaming kernel over (scenario, task) items
-    int32_t n_scen, n_tasks, ns_stride, n_stride;  // scenarios; tasks per scenario; slot / global strides
-    int64_t vp_stride;                         // doubles of per-scenario operator blocks
-    const void* var_pool;                      // (T) [n_scen][vp_stride] blocks of tasks flagged kTaskVar
-    ScenResult* res;                           // [n_scen]
-    int32_t* stopped;                          // [n_scen] converged / non-finite: no more sweeps
-    double* partial;                           // [n_scen][n_tasks][8] residual sums per item
-    unsigned long long* cnt;                   // [2]: barrier arrivals, cumulative active count
-    uint32_t* amask;                           // [2][ceil(n_scen/32)] active-scenario bits by sweep parity
-    int32_t staged;                            // 1: no kTaskDirect task (every operator block from the SMEM stage)
-    const long long* wpre;                     // [n_tasks + 1] prefix of the per-task cost weights (work split)
+constexpr int kBFirst = 1;                     // BRow.info: canonical first copy of its global (writes x_g)
+constexpr int kBInline = 2;                    // segment rows inline (nu <= 4), else {offset, count} in seg_rows
+constexpr int kBNuShift = 8;                   // nu in bits 8..15 (inline rows)
+struct alignas(8) BRow {                       // 24 B per row (copy)
+    int32_t g, info;
+    int32_t n0, n1, n2, n3;                    // the segment's rows in canonical copy order (inline), or n0 = offset,
+};                                             // n1 = count into seg_rows
+static_assert(sizeof(BRow) == 24, "BRow is 24 bytes");
+constexpr int kBVar = 1;                       // BSub.flags: per-scenario operator (the subsystem holds a load)
+constexpr int kBBbar = 2;                      // ... with a nonzero b-bar after the triangle
+struct BSub {                                  // 16 B per subsystem (DFS order)
+    int32_t row0, ns, op, flags;               // op: shared dense Abar offset (T entries) or var-pool entry offset
 };
-#ifndef LOPF_BATCH_WBASE
-#define LOPF_BATCH_WBASE 16                    // per-item fixed cost in units of one mat-vec column per half
+struct BTask {                                 // 16 B per task: a DFS run of subsystems
+    int32_t sub0, sub1, row0, row1;
+};
+
+struct BatchProblem {
+    int32_t n_scen, n_grp, n_rows, n_tasks, ve, ns_max, esz, n_obj;
+    int64_t n;                                 // globals
+    const BRow* rows;
+    const BSub* subs;
+    const BTask* tasks;
+    const int32_t* seg_rows;                   // segments of nu > 4
+    const void* gpar;                          // (T) [n][4] {c/rho, lo, hi, 1/nu}
+    const void* spool;                         // (T) dense n_s x n_s Abar of the shared subsystems
+    const void* vpool;                         // (T) [group][ve][32] packed upper triangle (+ b-bar) of load subsystems
+    const void* x0;                            // (T) [n_rows] initial x_s
+    void *xl, *lam, *u0, *u1;                  // (T) [group][n_rows][32]
+    void* x;                                   // (T) [group][n][32]
+    double* partial;                           // [group][n_tasks][5][32] residual sums per item
+    ScenResult* res;                           // [n_scen]
+    int32_t* stopped;                          // [n_scen] converged / non-finite: frozen
+    uint32_t* gact;                            // [2][n_grp] group has an active scenario, by sweep parity
+    unsigned long long* cnt;                   // barrier arrivals
+    const long long* wpre;                     // [n_tasks + 1] prefix of the per-task cost weights (work split)
+    const int32_t* obj_idx;
+    const double* obj_c;
+    DevCtrl* ctrl;
+    double* stage;                             // gather staging for the per-scenario getters
+    double rho, inv_rho, eps_rel;
+    long long max_iter;
+    int32_t test, pad;
+};
+constexpr int kBatchMaxScen = 8192;            // scenarios per batch handle
+constexpr int kBatchMaxGrp = kBatchMaxScen / 32;
+#ifndef LOPF_BATCH_WARPS
+#define LOPF_BATCH_WARPS 16
 #endif
-constexpr int kBatchMaxScen = 8192;            // scenarios per batch handle (SMEM active-set tables)
+constexpr int kBatchWarps = LOPF_BATCH_WARPS;  // warps per CTA of the batch kernel
+#ifndef LOPF_BATCH_TASK_ROWS
+#define LOPF_BATCH_TASK_ROWS 32
+#endif
+constexpr int kBatchTaskRows = LOPF_BATCH_TASK_ROWS;   // rows per task (target; whole subsystems)
 
 // Arena layout: byte offsets of every array (all 256-byte aligned).
 struct Layout {
@@ -243,10 +284,12 @@ struct Layout {
     // streaming task composition (kept for the batch packer): subsystems and block offsets per task
     std::vector<int4> trec;
     std::vector<int32_t> tsub_ptr, tsub_s, tsub_poff;
-    // batch kernel (config 4): the streaming layout of one scenario, replicated over the scenarios
-    int32_t n_scen = 0, n_grp = 0, ns_max = 0;
-    int64_t VP = 0;                        // doubles of per-scenario operator blocks (tasks holding a load)
-    size_t off_bvar = 0, off_bres = 0, off_bstop = 0, off_bpart = 0, off_bcnt = 0, off_bmask = 0, off_bwpre = 0;
+    // batch kernel (config 4, lane = scenario)
+    int32_t n_scen = 0, n_grp = 0, ns_max = 0, n_rows = 0, n_bsub = 0, ve = 0;
+    size_t off_brow = 0, off_bsub = 0, off_btask = 0, off_bseg = 0, off_bspool = 0, off_bvpool = 0, off_bpart = 0,
+           off_bres = 0, off_bstop = 0, off_bgact = 0, off_bcnt = 0, off_bwpre = 0, off_bstage = 0;
+    size_t image_bytes = 0;                // bytes of `image` uploaded by bind (0: the whole arena); the rest is
+                                           // device state initialised by the reset kernels
 };
 
 // Scenario batches (config 4): per-scenario operators of the subsystems that hold a load (their
@@ -299,18 +342,7 @@ lopf_status pack_batch(const Net& N, const Canon& cp, const BatchOps& bo, const 
 constexpr int kStreamWarpsF64 = LOPF_STREAM_WARPS_F64;
 constexpr int kStreamWarpsF32 = LOPF_STREAM_WARPS_F32;
 constexpr int kStreamWarpsWide = 12;         // ... when tasks of R > 2 exist (n_s > 64, the S = 1 path)
-// Batch kernel (config 4): its own warp count per element type (same stage size as streaming).
-#ifndef LOPF_BATCH_WARPS_F64
-#define LOPF_BATCH_WARPS_F64 LOPF_STREAM_WARPS_F64
-#endif
-#ifndef LOPF_BATCH_WARPS_F32
-#define LOPF_BATCH_WARPS_F32 LOPF_STREAM_WARPS_F32
-#endif
-constexpr int kBatchWarpsF64 = LOPF_BATCH_WARPS_F64;
-constexpr int kBatchWarpsF32 = LOPF_BATCH_WARPS_F32;
 int stream_block(int rmax, int esz);
-int batch_block(int esz);
-lopf_status query_batch_grid(int rmax, int esz, int staged, int* grid, std::string& err);
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
 lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err);
 lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err);
@@ -319,7 +351,11 @@ lopf_status launch_resident(const ResProblem& P, void* stream, std::string& err)
 lopf_status launch_reset_resident(const ResProblem& P, void* stream, std::string& err);
 lopf_status resident_capacity(int* sms, int* smem_optin, std::string& err);
 // batch.cu
-lopf_status launch_batch(const DevProblem& P, const BatchProblem& B, int grid, void* stream, std::string& err);
-lopf_status launch_reset_batch(const DevProblem& P, const BatchProblem& B, void* stream, std::string& err);
+int batch_block();
+int batch_smem(int ns_max, int esz);
+lopf_status query_batch_grid(int ns_max, int esz, int* grid, std::string& err);
+lopf_status launch_batch(const BatchProblem& B, int grid, void* stream, std::string& err);
+lopf_status launch_reset_batch(const BatchProblem& B, void* stream, std::string& err);
+lopf_status launch_gather_scen(const BatchProblem& B, int32_t scen, void* stream, std::string& err);
 
 }  // namespace lopf

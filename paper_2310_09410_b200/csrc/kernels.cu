@@ -16,22 +16,17 @@
 
 #include <cmath>
 
+#include "device.cuh"
 #include "internal.h"
 
 namespace lopf {
 
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
-
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
+using dev::kFull;
+using dev::ld_acquire_u64;
+using dev::st_release_u64;
+using dev::warp_sum5;
 
 #ifndef LOPF_STREAM_UNROLL
 #define LOPF_STREAM_UNROLL 4
@@ -101,33 +96,6 @@ __device__ __forceinline__ void issue_task(const DevProblem& P, Stage& st, const
         bulk_g2s(sb + Stg<T>::kOffLam, reinterpret_cast<const T*>(P.lam) + tr.x, E * n, m);
         bulk_g2s(sb + Stg<T>::kOffXl, reinterpret_cast<const T*>(P.xl) + tr.x, E * n, m);
     }
-}
-
-// Warp sums of five doubles by a reduce-scatter butterfly (fixed order, deterministic): 18 shuffles and
-// 9 adds instead of 50 and 25.  Returns the total of value (lane >> 2) on lanes with (lane >> 2) < 5.
-__device__ __forceinline__ double warp_sum5(const double (&v)[5], const int lane) {
-    const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
-    double w[4];                                   // xor 16: lanes keep values 0-3 (b16 = 0) or 4-7
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double lo = v[i], hi = i == 0 ? v[4] : 0.0;
-        const double send = b16 ? lo : hi, keep = b16 ? hi : lo;
-        w[i] = keep + __shfl_xor_sync(kFull, send, 16);
-    }
-    double x[2];                                   // xor 8: keep 2 of the 4
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const double send = b8 ? w[i] : w[i + 2], keep = b8 ? w[i + 2] : w[i];
-        x[i] = keep + __shfl_xor_sync(kFull, send, 8);
-    }
-    double y;                                      // xor 4: keep 1 of the 2
-    {
-        const double send = b4 ? x[0] : x[1], keep = b4 ? x[1] : x[0];
-        y = keep + __shfl_xor_sync(kFull, send, 4);
-    }
-    y += __shfl_xor_sync(kFull, y, 2);
-    y += __shfl_xor_sync(kFull, y, 1);
-    return y;                                      // value index 4 b16 + 2 b8 + b4 = lane >> 2
 }
 
 // a4 for one slot: the global's consensus value from the ping-pong copies (closed_1, rho restored)
@@ -507,290 +475,6 @@ __global__ void part_decide_kernel(DevProblem P) {
     if (conv || numeric) c->stopped = 1;
 }
 
-// ---- batch mode (config 4): (scenario, task) items over the one-scenario streaming layout ---------
-// The ACTIVE items of a sweep (tasks of scenarios not yet stopped, scenario-major, tasks in DFS order)
-// are cut into nw contiguous chunks, one per warp: a warp walks consecutive tasks of one scenario
-// (neighbouring subsystems: its u gathers hit lines the previous task fetched), with the same TMA
-// pipeline and task code as the streaming kernel on a view whose iterate / solution / varying-operator
-// pointers are offset to the scenario.  Residual sums accumulate in registers over a warp's RUN of
-// one scenario; the run's last item gets the warp-reduced sums in partial[scenario][task], its other
-// items exact zeros.  Grid barrier; then warp w decides scenarios w, w + nw, ... (partials summed in
-// task order: deterministic), freezing converged ones and setting the next sweep's active bits; grid
-// barrier.  As scenarios converge the chunks shrink, so the active work stays spread over every warp.
-__device__ __forceinline__ void grid_sync(unsigned long long* cnt, const unsigned long long target) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(cnt, 1ULL);
-        while (ld_acquire_u64(cnt) < target) {
-        }
-    }
-    __syncthreads();
-}
-
-template <class T>
-__device__ __forceinline__ DevProblem batch_view(const DevProblem& P, const BatchProblem& B, const int sc,
-                                                 const int4 tr) {
-    DevProblem Q = P;
-    const size_t so = (size_t)sc * B.ns_stride;
-    Q.xl = reinterpret_cast<T*>(P.xl) + so;
-    Q.lam = reinterpret_cast<T*>(P.lam) + so;
-    Q.u0 = reinterpret_cast<T*>(P.u0) + so;
-    Q.u1 = reinterpret_cast<T*>(P.u1) + so;
-    Q.x = reinterpret_cast<T*>(P.x) + (size_t)sc * B.n_stride;
-    if (tr.w & kTaskVar) Q.abar = reinterpret_cast<const T*>(B.var_pool) + (size_t)sc * B.vp_stride;
-    return Q;
-}
-
-// next active scenario after sc (its bit set in the SMEM copy of the active mask), or -1
-__device__ __forceinline__ int next_active(const uint32_t* m, const int W, const int sc) {
-    int w = (sc + 1) >> 5;
-    if (w >= W) return -1;
-    uint32_t bits = m[w] & (0xffffffffu << ((sc + 1) & 31));
-    while (bits == 0) {
-        if (++w >= W) return -1;
-        bits = m[w];
-    }
-    return (w << 5) + __ffs(bits) - 1;
-}
-
-constexpr int kBatchMaskWords = kBatchMaxScen / 32;
-#ifndef LOPF_BATCH_SMEM_TASKS
-#define LOPF_BATCH_SMEM_TASKS 256
-#endif
-constexpr int kBatchSmemTasks = LOPF_BATCH_SMEM_TASKS;   // task records kept in SMEM (else read through L1)
-
-// first item (active rank * NT + task) whose start weight (rank * WS + wpre[task]) is >= w
-__device__ __forceinline__ long long batch_item_at(const long long* __restrict__ wpre, const int NT, const long long WS,
-                                                   const long long w) {
-    const long long ar = w / WS, rem = w - ar * WS;
-    if (rem == 0) return ar * NT;
-    int lo = 1, hi = NT;                                   // smallest t with wpre[t] >= rem (wpre[NT] = WS > rem)
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(wpre + mid) >= rem) hi = mid; else lo = mid + 1;
-    }
-    return ar * NT + lo;
-}
-
-template <class T>
-struct BatchWarps {
-    static constexpr int value = sizeof(T) == 8 ? kBatchWarpsF64 : kBatchWarpsF32;
-};
-
-// SRC (task_packed): 0 operator block from HBM or the stage, decided per task (generic loads); 2 every
-// block from the stage (the problem has no kTaskDirect task: shared-space loads); 3 a branch per task
-// between the two specialised paths
-template <int RMAX, class T, int SRC>
-__global__ void __launch_bounds__(32 * BatchWarps<T>::value, 1) admm_batch_kernel(DevProblem P, BatchProblem B) {
-    constexpr int kWarps = BatchWarps<T>::value;
-    constexpr int kStageBytes = Stg<T>::kBytes;
-    extern __shared__ __align__(128) char sdyn[];
-    __shared__ uint64_t sbar[kWarps][2];
-    __shared__ T inv_nu[kInvNu];
-    __shared__ uint32_t s_mask[kBatchMaskWords];           // active scenarios of this sweep
-    __shared__ uint16_t s_wpre[kBatchMaskWords + 1];       // active scenarios before word w
-    __shared__ int4 s_tasks[kBatchSmemTasks];               // the (scenario-independent) task records
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
-    Stage st{sdyn + (size_t)wid * 2 * kStageBytes, sbar[wid], 0u, 0u};
-    T* dsm = reinterpret_cast<T*>(sdyn + (size_t)kWarps * 2 * kStageBytes) + (size_t)wid * 32 * RMAX;
-    for (int i = threadIdx.x; i < kInvNu; i += blockDim.x) inv_nu[i] = i > 0 ? T(1) / (T)i : T(0);
-    if (lane == 0) {
-        mbar_init(st.bar);
-        mbar_init(st.bar + 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const long long total0 = *(volatile long long*)&P.ctrl->total;
-    const int NT = B.n_tasks, W = (B.n_scen + 31) >> 5;
-    const bool tasks_smem = NT <= kBatchSmemTasks;
-    if (tasks_smem)
-        for (int i = threadIdx.x; i < NT; i += blockDim.x) s_tasks[i] = __ldg(P.tasks + i);
-    __syncthreads();
-    const volatile int32_t* stopped = B.stopped;
-    unsigned long long bars = 0, seen = 0;
-    long long it = 0;
-    while (it < P.max_iter) {
-        const long long t = total0 + it;
-        const T* ucur = reinterpret_cast<const T*>((t & 1) ? P.u1 : P.u0);
-        T* unext = reinterpret_cast<T*>((t & 1) ? P.u0 : P.u1);
-        const uint32_t* mcur = B.amask + (size_t)(it & 1) * W;
-        // the active set of this sweep into SMEM (warp 0), and the next sweep's mask cleared (CTA 0)
-        if (wid == 0) {
-            int run = 0;
-            for (int w0 = 0; w0 < W; w0 += 32) {
-                const int w = w0 + lane;
-                const uint32_t m = w < W ? __ldcg(mcur + w) : 0u;
-                int c = __popc(m), inc = c;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int y = __shfl_up_sync(kFull, inc, off);
-                    if (lane >= off) inc += y;
-                }
-                if (w < W) { s_mask[w] = m; s_wpre[w] = (uint16_t)(run + inc - c); }
-                run += __shfl_sync(kFull, inc, 31);
-            }
-            if (lane == 0) s_wpre[W] = (uint16_t)run;
-        }
-        if (blockIdx.x == 0)
-            for (int w = threadIdx.x; w < W; w += blockDim.x) B.amask[(size_t)((it + 1) & 1) * W + w] = 0u;
-        __syncthreads();
-        const int NA = s_wpre[W];
-        // warp gw takes the items whose start weight lies in [gw, gw + 1) * WT / nw (weights: B.wpre)
-        const long long WS = __ldg(B.wpre + NT), WT = (long long)NA * WS;
-        const long long a0 = batch_item_at(B.wpre, NT, WS, (WT * gw + nw - 1) / nw);
-        const long long a1 = batch_item_at(B.wpre, NT, WS, (WT * (gw + 1) + nw - 1) / nw);
-        if (a0 < a1) {
-            // scenario of active rank a0 / NT: its mask word by binary search on the prefix, then the bit
-            const int ar = (int)(a0 / NT);
-            int tk = (int)(a0 - (long long)ar * NT);
-            int lo = 0, hi = W - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s_wpre[mid] <= ar) lo = mid; else hi = mid - 1;
-            }
-            int sc = (lo << 5) + (int)__fns(s_mask[lo], 0, ar - s_wpre[lo] + 1);
-            int4 tr = tasks_smem ? s_tasks[tk] : __ldg(P.tasks + tk);
-            issue_task<T>(batch_view<T>(P, B, sc, tr), st, tr, lane, true);
-            double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            for (long long a = a0; a < a1; ++a) {
-                // the next item: the next task of this scenario or task 0 of the next active one
-                int sc1 = sc, tk1 = tk + 1;
-                if (tk1 == NT) { tk1 = 0; sc1 = next_active(s_mask, W, sc); }
-                const bool more = a + 1 < a1;
-                int4 tr1 = make_int4(0, 0, 0, 0);
-                if (more) {
-                    tr1 = tasks_smem ? s_tasks[tk1] : __ldg(P.tasks + tk1);
-                    issue_task<T>(batch_view<T>(P, B, sc1, tr1), st, tr1, lane, false);
-                }
-                const size_t so = (size_t)sc * B.ns_stride;
-                const DevProblem Q = batch_view<T>(P, B, sc, tr);
-                if constexpr (SRC == 3) {                      // split: HBM-block tasks on their own path
-                    if (tr.w & kTaskDirect) {
-                        if ((tr.w & 0xF) == 1) task_packed<1, T, 1>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
-                        else if constexpr (RMAX >= 2) task_packed<2, T, 1>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
-                    } else {
-                        if ((tr.w & 0xF) == 1) task_packed<1, T, 2>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
-                        else if constexpr (RMAX >= 2) task_packed<2, T, 2>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
-                    }
-                } else {
-                    if ((tr.w & 0xF) == 1) task_packed<1, T, SRC>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
-                    else if constexpr (RMAX >= 2) task_packed<2, T, SRC>(Q, tr, ucur + so, unext + so, acc, lane, dsm, st, inv_nu);
-                }
-                double* pp = B.partial + ((size_t)sc * NT + tk) * 8;
-                if (more && sc1 == sc) {                       // the run goes on: this item's slot holds 0
-                    if (lane < 5) pp[lane] = 0.0;
-                } else {                                       // end of the run: its sums
-                    const double ws = warp_sum5(acc, lane);
-                    if ((lane & 3) == 0 && (lane >> 2) < 5) pp[lane >> 2] = ws;
-#pragma unroll
-                    for (int k = 0; k < 5; ++k) acc[k] = 0.0;
-                }
-                sc = sc1;
-                tk = tk1;
-                tr = tr1;
-            }
-        }
-        grid_sync(B.cnt, (++bars) * gridDim.x);
-        // per-scenario (termination)
-        uint32_t* mnext = B.amask + (size_t)((it + 1) & 1) * W;
-        unsigned long long active = 0;
-        for (int sc = gw; sc < B.n_scen; sc += nw) {
-            if (stopped[sc]) continue;
-            double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            for (int k2 = lane; k2 < NT; k2 += 32) {
-                const double* pp = B.partial + ((size_t)sc * NT + k2) * 8;
-#pragma unroll
-                for (int k = 0; k < 5; ++k) s5[k] += __ldcg(pp + k);
-            }
-#pragma unroll
-            for (int k = 0; k < 5; ++k) {
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) s5[k] += __shfl_xor_sync(kFull, s5[k], off);
-            }
-            const double pres = sqrt(s5[0]), dres = P.rho * sqrt(s5[1]);
-            const double ep = P.eps_rel * fmax(sqrt(s5[2]), sqrt(s5[3])), ed = P.eps_rel * sqrt(s5[4]);
-            const int num = !(isfinite(s5[0]) && isfinite(s5[1]) && isfinite(s5[2]) && isfinite(s5[3]) && isfinite(s5[4]));
-            const int conv = P.test && pres <= ep && dres <= ed;
-            const bool fin = conv || num || it + 1 == P.max_iter;
-            if (lane == 0) {
-                ScenResult& R = B.res[sc];
-                R.iters = it + 1;
-                R.total = t + 1;
-                R.res[0] = pres; R.res[1] = dres; R.res[2] = ep; R.res[3] = ed;
-                R.status = conv ? 1 : num ? 3 : (fin ? 2 : 0);
-                if (fin) {
-                    double obj = 0.0;
-                    const T* xs = reinterpret_cast<const T*>(P.x) + (size_t)sc * B.n_stride;
-                    for (int j = 0; j < P.n_obj; ++j) obj += P.obj_c[j] * (double)__ldcg(xs + P.obj_idx[j]);
-                    R.objective = obj;
-                }
-                if (conv || num) B.stopped[sc] = 1;
-                else atomicOr(mnext + (sc >> 5), 1u << (sc & 31));
-            }
-            active += (conv || num) ? 0ULL : 1ULL;
-        }
-        if (lane == 0 && active) atomicAdd(B.cnt + 1, active);
-        grid_sync(B.cnt, (++bars) * gridDim.x);
-        const unsigned long long cum = *(volatile unsigned long long*)(B.cnt + 1);
-        const unsigned long long act = cum - seen;
-        seen = cum;
-        ++it;
-        if (act == 0) break;
-    }
-    while (st.consumed < st.issued) {
-        mbar_wait(st.bar + (st.consumed & 1), (st.consumed >> 1) & 1);
-        ++st.consumed;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        P.ctrl->total = total0 + it;
-        P.ctrl->iters = it;
-    }
-}
-
-// Before each batch launch: the active mask of its first sweep from the stopped flags (scenarios that
-// converged in an earlier launch stay frozen); the other parity cleared.
-__global__ void batch_mask_kernel(BatchProblem B) {
-    const int W = (B.n_scen + 31) >> 5;
-    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) {
-        uint32_t m = 0;
-        for (int b = 0; b < 32; ++b) {
-            const int sc = (w << 5) + b;
-            if (sc < B.n_scen && !B.stopped[sc]) m |= 1u << b;
-        }
-        B.amask[w] = m;
-        B.amask[W + w] = 0u;
-    }
-}
-
-// a3 for every scenario: x_s = x0 (template slots), lambda = 0, u = x0; decisions cleared.
-template <class T>
-__global__ void reset_batch_kernel(DevProblem P, BatchProblem B) {
-    const size_t n = (size_t)B.n_scen * B.ns_stride;
-    const T* x0p = reinterpret_cast<const T*>(P.x0);
-    T* xl = reinterpret_cast<T*>(P.xl);
-    T* lam = reinterpret_cast<T*>(P.lam);
-    T* u0 = reinterpret_cast<T*>(P.u0);
-    T* u1 = reinterpret_cast<T*>(P.u1);
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const T x0 = x0p[i % B.ns_stride];
-        xl[i] = x0;
-        lam[i] = T(0);
-        u0[i] = x0;
-        u1[i] = T(0);
-    }
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < (size_t)B.n_scen; i += (size_t)gridDim.x * blockDim.x) {
-        ScenResult& R = B.res[i];
-        R.iters = 0; R.total = 0; R.status = 0; R.objective = 0.0;
-        R.res[0] = R.res[1] = R.res[2] = R.res[3] = 0.0;
-        B.stopped[i] = 0;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        P.ctrl->total = 0; P.ctrl->iters = 0;
-    }
-}
-
 // a3: reset the iterate to the initial point: x_s = x0, lambda = 0, u = x0.
 template <class T>
 __global__ void reset_kernel(DevProblem P) {
@@ -859,70 +543,6 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
     return LOPF_OK;
 }
 
-
-template <int SRC>
-static const void* batch_kernel_src(int rmax, int esz) {
-    if (esz == 4)
-        return rmax <= 1 ? (const void*)admm_batch_kernel<1, float, SRC> : (const void*)admm_batch_kernel<2, float, SRC>;
-    return rmax <= 1 ? (const void*)admm_batch_kernel<1, double, SRC> : (const void*)admm_batch_kernel<2, double, SRC>;
-}
-// A problem with kTaskDirect tasks: fp64 takes the split kernel (SRC 3: staged blocks by shared-space
-// loads, the direct ones by global loads; 512 vs 519 us per batch sweep of config 4), fp32 the per-task
-// select (SRC 0: the split spills at its 80-register cap, 433 vs 384 us; profiles/r01_ab_batch_split.log).
-static const void* batch_kernel_for(int rmax, int esz, int staged) {
-    if (staged) return batch_kernel_src<2>(rmax, esz);
-    if (esz == 8) return rmax <= 1 ? (const void*)admm_batch_kernel<1, double, 3> : (const void*)admm_batch_kernel<2, double, 3>;
-    return rmax <= 1 ? (const void*)admm_batch_kernel<1, float, 0> : (const void*)admm_batch_kernel<2, float, 0>;
-}
-
-int batch_block(int esz) { return 32 * (esz == 8 ? kBatchWarpsF64 : kBatchWarpsF32); }
-
-static int batch_smem(int rmax, int esz) {
-    const int r = rmax <= 1 ? 1 : 2;
-    const int stage = esz == 4 ? Stg<float>::kBytes : Stg<double>::kBytes;
-    return batch_block(esz) / 32 * (2 * stage + esz * 32 * r);
-}
-
-lopf_status query_batch_grid(int rmax, int esz, int staged, int* grid, std::string& err) {
-    int dev = 0, sms = 0, per = 0;
-    const void* k = batch_kernel_for(rmax, esz, staged);
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, batch_smem(rmax, esz));
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, batch_block(esz), batch_smem(rmax, esz));
-    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
-    if (per < 1) { err = "batch kernel cannot be resident (occupancy 0)"; return LOPF_E_CUDA; }
-    *grid = sms * per;
-    return LOPF_OK;
-}
-
-lopf_status launch_batch(const DevProblem& P, const BatchProblem& B, int grid, void* stream, std::string& err) {
-    cudaStream_t s = (cudaStream_t)stream;
-    const void* k = batch_kernel_for(P.rmax, P.esz, B.staged);
-    const int smem = batch_smem(P.rmax, P.esz);
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) e = cudaMemsetAsync(B.cnt, 0, 2 * sizeof(unsigned long long), s);
-    if (e == cudaSuccess) {
-        batch_mask_kernel<<<((B.n_scen + 31) / 32 + 255) / 256, 256, 0, s>>>(B);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess && P.max_iter > 0) {
-        DevProblem Q = P;
-        BatchProblem C = B;
-        void* args[] = {&Q, &C};
-        e = cudaLaunchCooperativeKernel(k, dim3(grid), dim3(batch_block(P.esz)), args, smem, s);
-    }
-    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
-    return LOPF_OK;
-}
-
-lopf_status launch_reset_batch(const DevProblem& P, const BatchProblem& B, void* stream, std::string& err) {
-    if (P.esz == 4) reset_batch_kernel<float><<<1184, 256, 0, (cudaStream_t)stream>>>(P, B);
-    else reset_batch_kernel<double><<<1184, 256, 0, (cudaStream_t)stream>>>(P, B);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
-    return LOPF_OK;
-}
 
 lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err) {
     const int nb = P.n_imp > 0 ? (P.n_imp + 255) / 256 : 1;

@@ -1,13 +1,15 @@
-// Device layout of the batch mode (config 4): the streaming layout of ONE scenario
-// (pack_streaming: DFS-ordered tasks, packed operator blocks, per-slot metadata) is the template; every
-// scenario gets its own iterate arrays ([scenario][slot]) and solution ([scenario][global]), and the
-// tasks that hold a load subsystem -- whose A_s depends on the load level (VDLM-1/2)
-// -- get a per-scenario operator block in `var_pool` ([scenario][VP]).  Metadata and the operators of
-// every other task are shared by all scenarios (they stay in L2).
+// Device layout of the batch mode (config 4; kernel in batch.cu).
+//
+// Lane = scenario: scenarios form groups of 32 and every per-scenario array is [group][entry][32].
+// Rows are the copies in depth-first subsystem order (neighbouring subsystems share globals, so the
+// u lines a subsystem gathers were touched moments earlier).  Shared by all scenarios: per-row records
+// (global, first-copy flag, the segment's rows in canonical copy order), per-subsystem records, the
+// {c/rho, lo, hi, 1/nu} of every global and the dense Abar of every subsystem without a load.  Per
+// scenario: the packed upper triangle and b-bar of every subsystem that holds a load (its A_s depends on
+// the load level through VDLM-1/2), and the iterate.  Tasks are depth-first runs of
+// whole subsystems of about kBatchTaskRows rows; a work item is (group, task).
 #include <algorithm>
 #include <cstring>
-
-#include <vector_functions.h>
 
 #include "internal.h"
 
@@ -17,124 +19,174 @@ static size_t a256b(size_t x) { return (x + 255) & ~(size_t)255; }
 
 lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const lopf_options& opt, Layout& L,
                        std::string& err) {
-    Layout T;
-    lopf_status st = pack_streaming(N, P, opt, 4096, T, err);
-    if (st != LOPF_OK) return st;
-    for (const int4& tr : T.trec)
-        if (!(tr.w & kTaskPacked)) { err = "batch mode supports n_s <= 63"; return LOPF_E_ARG; }
-    const int64_t NT = T.n_tasks, NS = T.n_slots, NG = P.n, NSC = bo.n_scen;
-    // per-scenario blocks: tasks holding at least one varying (load) subsystem
-    std::vector<int4> trec = T.trec;
-    std::vector<int64_t> var_off(NT, -1);
-    int64_t VP = 0;
-    for (int64_t t = 0; t < NT; ++t) {
-        bool var = false;
-        for (int32_t j = T.tsub_ptr[t]; j < T.tsub_ptr[t + 1]; ++j) var |= bo.vidx[T.tsub_s[j]] >= 0;
-        if (!var) continue;
-        var_off[t] = VP;
-        trec[t].y = (int)VP;
-        trec[t].w |= kTaskVar;
-        VP += trec[t].z;                                     // block length (entries, 16-byte multiple)
-    }
-    if (VP * NSC > ((int64_t)1 << 40)) { err = "batch: per-scenario operators too large"; return LOPF_E_ARG; }
-
     L = Layout();
     L.kernel = 3;
-    const size_t e = (size_t)T.esz;                          // (T) element size (fp32 variant: reading F1)
-    L.esz = T.esz;
-    L.n_scen = (int32_t)NSC;
+    const int64_t E = opt.precision == 32 ? 4 : 8;            // (T) element size (fp32 variant: reading F1)
+    L.esz = (int32_t)E;
+    int ns_max = 1;
+    for (int64_t s = 0; s < P.S; ++s) ns_max = std::max(ns_max, P.n_s[s]);
+    if ((int64_t)kBatchWarps * ns_max * 32 * E > 200 * 1024) {
+        err = "batch mode: n_s = " + std::to_string(ns_max) + " needs more shared memory for the d staging than a CTA of " +
+              std::to_string(kBatchWarps) + " warps has";
+        return LOPF_E_ARG;
+    }
+    const int32_t NSC = bo.n_scen, NG = (NSC + 31) / 32;
+    const std::vector<int64_t> order = dfs_order(N, P);
+
+    // ---- rows (copies in DFS subsystem order), subsystems, segments ---------------------------------
+    std::vector<int32_t> row_of_copy(P.nc, -1);
+    int32_t nr = 0;
+    for (int64_t s : order)
+        for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) row_of_copy[k] = nr++;
+    std::vector<BRow> rows(nr);
+    std::vector<int32_t> seg_rows;
+    for (int64_t k = 0; k < P.nc; ++k) {
+        const int32_t g = P.copy_global[k];
+        const int64_t q0 = P.seg_ptr[g], q1 = P.seg_ptr[g + 1], nu = q1 - q0;
+        BRow& R = rows[row_of_copy[k]];
+        R.g = g;
+        R.info = (P.seg_copy[q0] == k ? kBFirst : 0);
+        R.n0 = R.n1 = R.n2 = R.n3 = 0;
+        if (nu <= 4) {
+            R.info |= kBInline | (int32_t)(nu << kBNuShift);
+            int32_t* n = &R.n0;
+            for (int64_t q = q0; q < q1; ++q) n[q - q0] = row_of_copy[P.seg_copy[q]];
+        } else {
+            R.n0 = (int32_t)seg_rows.size();
+            R.n1 = (int32_t)nu;
+            for (int64_t q = q0; q < q1; ++q) seg_rows.push_back(row_of_copy[P.seg_copy[q]]);
+        }
+    }
+    std::vector<BSub> subs;
+    std::vector<double> spool;                                     // dense Abar of shared subsystems
+    std::vector<int64_t> var_op(P.S, -1);
+    int64_t ve = 0;
+    std::vector<char> has_b(P.S, 0);
+    for (int64_t s = 0; s < P.S; ++s)
+        for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) has_b[s] |= P.bbar[k] != 0.0;
+    int32_t r0 = 0;
+    for (int64_t s : order) {
+        const int ns = P.n_s[s];
+        BSub b{r0, ns, 0, 0};
+        if (bo.vidx[s] >= 0) {
+            b.flags = kBVar | kBBbar;
+            b.op = (int32_t)ve;
+            var_op[s] = ve;
+            ve += (int64_t)ns * (ns + 1) / 2 + ns;
+        } else {
+            if (has_b[s]) { err = "batch mode: a subsystem without a load has a nonzero b-bar"; return LOPF_E_ARG; }
+            b.op = (int32_t)spool.size();
+            spool.insert(spool.end(), P.abar.begin() + P.abar_ptr[s], P.abar.begin() + P.abar_ptr[s + 1]);
+        }
+        subs.push_back(b);
+        r0 += ns;
+    }
+    if ((int64_t)NG * ve * 32 * E > ((int64_t)1 << 40)) { err = "batch: per-scenario operators too large"; return LOPF_E_ARG; }
+    // tasks: DFS runs of whole subsystems of ~kBatchTaskRows rows; cost weight = consensus rows + the
+    // mat-vec entries (a per-scenario operator entry is a coalesced line, a shared one a uniform load)
+    std::vector<BTask> tasks;
+    std::vector<long long> wpre(1, 0);
+    for (size_t i = 0; i < subs.size();) {
+        BTask t{(int32_t)i, (int32_t)i, subs[i].row0, subs[i].row0};
+        long long w = 0;
+        while (i < subs.size() && (t.row1 - t.row0 < kBatchTaskRows || t.sub1 == t.sub0)) {
+            const long long ns = subs[i].ns;
+            w += 16 + 12 * ns + ns * ns * ((subs[i].flags & kBVar) ? 2 : 1);
+            t.row1 += subs[i].ns;
+            t.sub1 = (int32_t)++i;
+        }
+        tasks.push_back(t);
+        wpre.push_back(wpre.back() + w);
+    }
+    const int64_t NT = (int64_t)tasks.size();
+
+    // ---- arena -----------------------------------------------------------------------------------
+    std::vector<int32_t> obj_idx;
+    std::vector<double> obj_c;
+    for (int64_t i = 0; i < P.n; ++i)
+        if (P.c[i] != 0.0) { obj_idx.push_back((int32_t)i); obj_c.push_back(P.c[i]); }
+    L.n_scen = NSC;
+    L.n_grp = NG;
+    L.ns_max = ns_max;
+    L.n_rows = nr;
+    L.n_bsub = (int32_t)subs.size();
+    L.ve = (int32_t)ve;
     L.n_tasks = NT;
-    L.n_slots = NS;
-    L.rmax = T.rmax;
-    L.staged = 1;
-    for (const int4& tr : trec)
-        if (tr.w & kTaskDirect) L.staged = 0;
-    L.VP = VP;
-    L.n_obj = T.n_obj;
-    L.slot_of_copy = T.slot_of_copy;
+    L.n_slots = nr;
+    L.n_obj = (int64_t)obj_idx.size();
+    L.abar_doubles = (int64_t)spool.size() + ve;
+    L.slot_of_copy = row_of_copy;
     L.max_grid = 4096;
     L.trace_cap = 1;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = a256b(o + std::max<size_t>(bytes, 1)); return r; };
-    L.off_tasks = take(16 * NT);
-    L.off_meta = take(sizeof(SlotMeta) * NS);
-    L.off_bbar = take(e * NS);
-    L.off_x0 = take(e * NS);
-    L.off_gpar = take(2 * e * NG);
-    L.off_gcost = take(e * NG);
-    L.off_segptr = take(4 * (NG + 1));
-    L.off_segslot = take(4 * P.nc);
-    L.off_abar = take(e * (size_t)T.abar_doubles);
-    L.off_objidx = take(4 * (size_t)T.n_obj);
-    L.off_objc = take(8 * (size_t)T.n_obj);
-    L.off_bvar = take(e * (size_t)VP * NSC);
-    L.off_xl = take(e * (size_t)NS * NSC);
-    L.off_lam = take(e * (size_t)NS * NSC);
-    L.off_u0 = take(e * (size_t)NS * NSC);
-    L.off_u1 = take(e * (size_t)NS * NSC);
-    L.off_x = take(e * (size_t)NG * NSC);
+    // inputs (uploaded by bind)
+    L.off_brow = take(sizeof(BRow) * (size_t)nr);
+    L.off_bsub = take(sizeof(BSub) * subs.size());
+    L.off_btask = take(sizeof(BTask) * (size_t)NT);
+    L.off_bseg = take(4 * seg_rows.size());
+    L.off_gpar = take(4 * E * (size_t)P.n);
+    L.off_bspool = take(E * spool.size());
+    L.off_x0 = take(E * (size_t)nr);
+    L.off_bwpre = take(8 * (size_t)(NT + 1));
+    L.off_objidx = take(4 * obj_idx.size());
+    L.off_objc = take(8 * obj_c.size());
+    L.off_bvpool = take(E * (size_t)NG * ve * 32);
+    L.image_bytes = o;
+    // device state (initialised by the reset kernel)
+    const size_t per = E * (size_t)NG * nr * 32;
+    L.off_xl = take(per);
+    L.off_lam = take(per);
+    L.off_u0 = take(per);
+    L.off_u1 = take(per);
+    L.off_x = take(E * (size_t)NG * P.n * 32);
+    L.off_bpart = take(8 * 160 * (size_t)NG * NT);
     L.off_bres = take(sizeof(ScenResult) * (size_t)NSC);
     L.off_bstop = take(4 * (size_t)NSC);
-    L.off_bpart = take(8 * 8 * (size_t)NT * NSC);
+    L.off_bgact = take(4 * 2 * (size_t)NG);
     L.off_bcnt = take(8 * 4);
-    L.off_bmask = take(4 * 2 * (((size_t)NSC + 31) / 32));
-    L.off_bwpre = take(8 * ((size_t)NT + 1));
-    L.off_partial = take(8 * 8 * 4096);
     L.off_ctrl = take(sizeof(DevCtrl));
+    L.off_bstage = take(8 * (2 * (size_t)nr + (size_t)P.n));
     L.off_trace = take(8 * 5);
     L.bytes = o;
-    L.image.assign(L.bytes, 0);
+    L.image.assign(L.image_bytes, 0);
     uint8_t* img = L.image.data();
-    const uint8_t* ti = T.image.data();
-    std::memcpy(img + L.off_tasks, trec.data(), 16 * NT);
-    {   // work-split weights: a fixed per-item cost plus the mat-vec columns x halves (kmax * R)
-        long long* wp = reinterpret_cast<long long*>(img + L.off_bwpre);
-        wp[0] = 0;
-        for (int64_t t = 0; t < NT; ++t)
-            wp[t + 1] = wp[t] + LOPF_BATCH_WBASE + (long long)((trec[t].w >> kTaskKmaxShift) & 0xFF) * (trec[t].w & 0xF);
-    }
-    std::memcpy(img + L.off_meta, ti + T.off_meta, sizeof(SlotMeta) * NS);
-    std::memcpy(img + L.off_bbar, ti + T.off_bbar, e * NS);
-    std::memcpy(img + L.off_x0, ti + T.off_x0, e * NS);
-    std::memcpy(img + L.off_gpar, ti + T.off_gpar, 2 * e * NG);
-    std::memcpy(img + L.off_gcost, ti + T.off_gcost, e * NG);
-    std::memcpy(img + L.off_segptr, ti + T.off_segptr, 4 * (NG + 1));
-    std::memcpy(img + L.off_segslot, ti + T.off_segslot, 4 * P.nc);
-    std::memcpy(img + L.off_abar, ti + T.off_abar, e * (size_t)T.abar_doubles);
-    std::memcpy(img + L.off_objidx, ti + T.off_objidx, 4 * (size_t)T.n_obj);
-    std::memcpy(img + L.off_objc, ti + T.off_objc, 8 * (size_t)T.n_obj);
-    // per-scenario operator blocks: the template block with each load subsystem's triangle and b-bar
-    // replaced by the scenario's (same packing, so the per-slot metadata stays valid)
-    const uint8_t* tpool = ti + T.off_abar;
-    uint8_t* vpool = img + L.off_bvar;
-    auto put = [e](uint8_t* base, size_t i, double v) {
-        if (e == 8) reinterpret_cast<double*>(base)[i] = v;
+    auto put = [E](uint8_t* base, size_t i, double v) {
+        if (E == 8) reinterpret_cast<double*>(base)[i] = v;
         else reinterpret_cast<float*>(base)[i] = (float)v;
     };
-    for (int64_t t = 0; t < NT; ++t) {
-        if (var_off[t] < 0) continue;
-        const int4 tr = T.trec[t];
-        for (int64_t sc = 0; sc < NSC; ++sc) {
-            const size_t dst = (size_t)sc * VP + var_off[t];
-            std::memcpy(vpool + e * dst, tpool + e * (size_t)tr.y, e * (size_t)tr.z);
-            for (int32_t j = T.tsub_ptr[t]; j < T.tsub_ptr[t + 1]; ++j) {
-                const int64_t s = T.tsub_s[j];
-                const int32_t v = bo.vidx[s];
-                if (v < 0) continue;
-                const int ns = P.n_s[s];
-                const double* A = &bo.abar[(size_t)sc * bo.VA + bo.va_off[v]];
-                const double* b = &bo.bbar[(size_t)sc * bo.VB + bo.vb_off[v]];
-                const size_t blk = dst + T.tsub_poff[j];
-                bool has_b = false;
-                for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) has_b |= P.bbar[k] != 0.0;
-                for (int r = 0; r < ns; ++r)
-                    for (int k = r; k < ns; ++k) put(vpool, blk + r * ns - r * (r - 1) / 2 + (k - r), A[(size_t)r * ns + k]);
-                if (has_b)
-                    for (int r = 0; r < ns; ++r) put(vpool, blk + ns * (ns + 1) / 2 + r, b[r]);
-            }
+    std::memcpy(img + L.off_brow, rows.data(), sizeof(BRow) * (size_t)nr);
+    std::memcpy(img + L.off_bsub, subs.data(), sizeof(BSub) * subs.size());
+    std::memcpy(img + L.off_btask, tasks.data(), sizeof(BTask) * (size_t)NT);
+    std::memcpy(img + L.off_bseg, seg_rows.data(), 4 * seg_rows.size());
+    for (int64_t g = 0; g < P.n; ++g) {
+        const double nu = (double)(P.seg_ptr[g + 1] - P.seg_ptr[g]);
+        put(img + L.off_gpar, 4 * g, P.c[g] / opt.rho);
+        put(img + L.off_gpar, 4 * g + 1, P.lo[g]);
+        put(img + L.off_gpar, 4 * g + 2, P.hi[g]);
+        put(img + L.off_gpar, 4 * g + 3, 1.0 / nu);
+    }
+    for (size_t i = 0; i < spool.size(); ++i) put(img + L.off_bspool, i, spool[i]);
+    for (int64_t k = 0; k < P.nc; ++k) put(img + L.off_x0, row_of_copy[k], P.x0[k]);
+    std::memcpy(img + L.off_bwpre, wpre.data(), 8 * wpre.size());
+    std::memcpy(img + L.off_objidx, obj_idx.data(), 4 * obj_idx.size());
+    std::memcpy(img + L.off_objc, obj_c.data(), 8 * obj_c.size());
+    // per-scenario operators: [group][entry][lane]; padding lanes of the last group stay zero
+    uint8_t* vp = img + L.off_bvpool;
+    for (int64_t v = 0; v < (int64_t)bo.vsub.size(); ++v) {
+        const int64_t s = bo.vsub[v];
+        const int ns = P.n_s[s];
+        const int64_t op = var_op[s];
+        for (int32_t sc = 0; sc < NSC; ++sc) {
+            const double* A = &bo.abar[(size_t)sc * bo.VA + bo.va_off[v]];
+            const double* b = &bo.bbar[(size_t)sc * bo.VB + bo.vb_off[v]];
+            const size_t base = ((size_t)(sc >> 5) * ve + op) * 32 + (sc & 31);
+            int64_t e = 0;
+            for (int i = 0; i < ns; ++i)
+                for (int j = i; j < ns; ++j, ++e) put(vp, base + 32 * (size_t)e, A[(size_t)i * ns + j]);
+            for (int i = 0; i < ns; ++i, ++e) put(vp, base + 32 * (size_t)e, b[i]);
         }
     }
-    (void)opt;
     return LOPF_OK;
 }
 

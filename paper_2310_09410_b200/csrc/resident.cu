@@ -25,6 +25,7 @@
 
 #include <cmath>
 
+#include "device.cuh"
 #include "internal.h"
 
 namespace lopf {
@@ -39,23 +40,19 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef LOPF_RES_UNROLL
 #define LOPF_RES_UNROLL 8                  // mat-vec column loop unroll (A/B: 1 4.83, 2 4.63, 4 4.59, 8 4.54 us)
 #endif
+#ifndef LOPF_DIAG_SKIP
+#define LOPF_DIAG_SKIP 0                   // diagnostics builds only: bit 1 skips the update work (sync cost alone)
+#endif
 #ifndef LOPF_RES_SLEEP
 #define LOPF_RES_SLEEP 20                  // reducer poll back-off (ns)
 #endif
 constexpr int kUnroll = LOPF_RES_UNROLL;
 constexpr int kPer = 5;                    // flags / partials per reducer lane per round (G <= 160 in one round)
 
-__device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ unsigned long long ld_rlx(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p) { return dev::ld_acquire_u64(p); }
+__device__ __forceinline__ unsigned long long ld_rlx(const unsigned long long* p) { return dev::ld_relaxed_u64(p); }
+using dev::fence_acq_rel;
+using dev::warp_sum5;
 
 // consensus input u = x_s - lambda / rho, formed with the same rounding wherever it is needed
 template <class T>
@@ -210,33 +207,6 @@ __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, doubl
     }
 }
 
-// Warp sums of five doubles by a reduce-scatter butterfly (fixed order, deterministic): 18 shuffles and
-// 9 adds instead of 50 and 25.  Returns the total of value (lane >> 2) on lanes with (lane >> 2) < 5.
-__device__ __forceinline__ double warp_sum5(const double (&v)[5], const int lane) {
-    const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
-    double w[4];                                   // xor 16: lanes keep values 0-3 (b16 = 0) or 4-7
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double lo = v[i], hi = i == 0 ? v[4] : 0.0;
-        const double send = b16 ? lo : hi, keep = b16 ? hi : lo;
-        w[i] = keep + __shfl_xor_sync(kFull, send, 16);
-    }
-    double x[2];                                   // xor 8: keep 2 of the 4
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const double send = b8 ? w[i] : w[i + 2], keep = b8 ? w[i + 2] : w[i];
-        x[i] = keep + __shfl_xor_sync(kFull, send, 8);
-    }
-    double y;                                      // xor 4: keep 1 of the 2
-    {
-        const double send = b4 ? x[0] : x[1], keep = b4 ? x[1] : x[0];
-        y = keep + __shfl_xor_sync(kFull, send, 4);
-    }
-    y += __shfl_xor_sync(kFull, y, 2);
-    y += __shfl_xor_sync(kFull, y, 1);
-    return y;                                      // value index 4 b16 + 2 b8 + b4 = lane >> 2
-}
-
 constexpr int kFlagStride = 32;                    // one flag per 256-byte line (no L2 hot spot)
 
 #if LOPF_RES_TIMELINE == 1   // diagnostics build: per-warp clock64 events of CTA G/2, sweeps 500..502, into P.prof
@@ -369,7 +339,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
             TL(1);
         } else {                                       // workers: sweep t+1 (speculative until decided)
             double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            const bool busy = t < P.max_iter && !(P.skip & 2) && wid < NT;
+            const bool busy = t < P.max_iter && !(LOPF_DIAG_SKIP & 2) && wid < NT;
             if (busy) {
                 C.xl_c = cur ? H.off_xl1 : H.off_xl0;
                 C.lam_c = cur ? H.off_lam1 : H.off_lam0;

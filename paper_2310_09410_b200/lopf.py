@@ -172,7 +172,7 @@ class Lopf:
     @classmethod
     def setup(cls, feeder, rho: float = 100.0, eps_rel: float = 1e-3, max_iter: int = 1_000_000,
               trace_every: int = 0, trace_cap: int = 4096, single: bool = False, kernel: int = 0,
-              grid_cap: int = 0, max_ctas: int = 0, diag_profile: bool = False, diag_skip: int = 0,
+              grid_cap: int = 0, max_ctas: int = 0, diag_profile: bool = False,
               precision: int = 64) -> "Lopf":
         """lopf_setup; precision 32 selects the fp32 variant (the paper's GPU precision)."""
         lib = load_library()
@@ -181,7 +181,7 @@ class Lopf:
         o.rho, o.eps_rel, o.max_iter = float(rho), float(eps_rel), int(max_iter)
         o.trace_every, o.trace_cap, o.single, o.kernel = int(trace_every), int(trace_cap), int(bool(single)), int(kernel)
         o.grid_cap, o.max_ctas = int(grid_cap), int(max_ctas)
-        o.reserved[0], o.reserved[1] = int(bool(diag_profile)), int(diag_skip)
+        o.reserved[0] = int(bool(diag_profile))
         o.precision = int(precision)
         net, keep = _network(feeder)
         h = _vp()
