@@ -377,6 +377,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         B.u1 = b + L.off_u1;
         B.x = b + L.off_x;
         B.partial = (double*)(b + L.off_bpart);
+        B.dscr = b + L.off_bdscr;
         B.res = (ScenResult*)(b + L.off_bres);
         B.stopped = (int32_t*)(b + L.off_bstop);
         B.gact = (uint32_t*)(b + L.off_bgact);

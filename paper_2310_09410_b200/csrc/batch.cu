@@ -30,7 +30,18 @@ namespace {
 using dev::grid_sync;
 using dev::kFull;
 
+#ifndef LOPF_BATCH_KUNROLL
+#define LOPF_BATCH_KUNROLL 4                  // mat-vec column unroll (operator loads in flight: 4 rows x this)
+#endif
+#ifndef LOPF_BATCH_CROWS
+#define LOPF_BATCH_CROWS 4                    // consensus rows whose gathers are issued together
+#endif
+#ifndef LOPF_BATCH_L2PF
+#define LOPF_BATCH_L2PF 1                     // per-subsystem lane-parallel L2 prefetch of x_s and the operator
+#endif
 constexpr int BW = kBatchWarps;
+constexpr int CR = LOPF_BATCH_CROWS;
+constexpr int KU = LOPF_BATCH_KUNROLL;
 constexpr int BB = 32 * BW;
 
 template <class T> struct V2;                 // {c/rho, lo}, {hi, 1/nu} per global
@@ -50,109 +61,183 @@ __device__ __forceinline__ long long item_at(const long long* __restrict__ wpre,
     return ar * NT + lo;
 }
 
-// One (group, task) item for the 32 scenarios of the group (lane = scenario; `act`: the lane's scenario
-// is running -- frozen or padding lanes compute but store nothing and add nothing).
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Per-warp shared memory: d of the current subsystem [kBatchDMax][32] (a subsystem with more rows keeps
+// its d in the global scratch `dscr` instead, an L2-resident [group][row][32] array), and the records of
+// up to 32 rows ({g, info, n0..n3} and {c/rho, lo, hi, 1/nu}) staged by one coalesced load per lane, so
+// the row loop reads its uniform metadata with shared-memory broadcasts instead of dependent global loads.
 template <class T>
-__device__ __forceinline__ void batch_item(const BatchProblem& B, const int grp, const int task,
-                                           const T* __restrict__ ucur, T* __restrict__ unext, T* __restrict__ dsm,
-                                           const int lane, const bool act, double (&acc)[5]) {
+struct WarpSmem {
+    T* d;                                      // [kBatchDMax][32]
+    int* mi;                                   // [32][6]
+    T* mp;                                     // [32][4]
+};
+template <class T>
+__host__ __device__ constexpr int warp_smem_bytes() {
+    return kBatchDMax * 32 * (int)sizeof(T) + 32 * 6 * 4 + 32 * 4 * (int)sizeof(T);
+}
+
+// One subsystem of a (group, task) item for the 32 scenarios of the group (lane = scenario; `act`: the
+// lane's scenario is running -- frozen or padding lanes compute but store nothing and add nothing).  Every
+// loop keeps many independent loads in flight: four rows' gathers at a time, the mat-vec's operator loads
+// of four rows x four columns, the four rows' finish loads.  BIG: d in the global scratch.
+template <class T, bool BIG>
+__device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, const size_t gb,
+                                          const T* __restrict__ ucur, T* __restrict__ unext, const WarpSmem<T>& W,
+                                          const int lane, const bool act, double (&acc)[5], const size_t grp) {
     using T2 = typename V2<T>::type;
     const T rho = (T)B.rho, inv_rho = (T)B.inv_rho;
-    const int4 tk = __ldg(reinterpret_cast<const int4*>(B.tasks) + task);
-    const size_t gb = (size_t)grp * B.n_rows;                        // first row of this group
-    T* __restrict__ xlp = reinterpret_cast<T*>(B.xl);
-    T* __restrict__ lmp = reinterpret_cast<T*>(B.lam);
-    T* __restrict__ xg = reinterpret_cast<T*>(B.x) + (size_t)grp * B.n * 32 + lane;
+    // this group's lane views: element (row r) at [32 r] (32-bit indices on 64-bit bases)
+    const T* __restrict__ ug = ucur + gb * 32 + lane;
+    T* __restrict__ ung = unext + gb * 32 + lane;
+    T* __restrict__ xlg = reinterpret_cast<T*>(B.xl) + gb * 32 + lane;
+    T* __restrict__ lmg = reinterpret_cast<T*>(B.lam) + gb * 32 + lane;
+    T* __restrict__ xg = reinterpret_cast<T*>(B.x) + grp * B.n * 32 + lane;
     const T2* __restrict__ gpar = reinterpret_cast<const T2*>(B.gpar);
     const int2* __restrict__ rows = reinterpret_cast<const int2*>(B.rows);
-    for (int s = tk.x; s < tk.y; ++s) {
-        const int4 sm = __ldg(reinterpret_cast<const int4*>(B.subs) + s);   // {row0, ns, op, flags}
-        const int row0 = sm.x, ns = sm.y;
-        // a4: consensus of every row's global; v parked in unext (replaced by u below), d in SMEM
-#pragma unroll 2
-        for (int r = 0; r < ns; ++r) {
-            const int row = row0 + r;
-            const int2 gi = __ldg(rows + 3 * row);                     // {g, info}
-            const int2 n01 = __ldg(rows + 3 * row + 1);
-            T sig;
-            if (gi.y & kBInline) {                                      // nu <= 4: rows inline
-                const int nu = (gi.y >> kBNuShift) & 0xFF;
-                const int2 n23 = __ldg(rows + 3 * row + 2);
-                const T a0 = __ldcg(ucur + (gb + n01.x) * 32 + lane);
-                const T a1 = nu > 1 ? __ldcg(ucur + (gb + n01.y) * 32 + lane) : T(0);
-                const T a2 = nu > 2 ? __ldcg(ucur + (gb + n23.x) * 32 + lane) : T(0);
-                const T a3 = nu > 3 ? __ldcg(ucur + (gb + n23.y) * 32 + lane) : T(0);
-                sig = ((a0 + a1) + a2) + a3;                            // ascending canonical copy order
-            } else {
-                sig = T(0);
-                for (int q = 0; q < n01.y; ++q) sig += __ldcg(ucur + (gb + __ldg(B.seg_rows + n01.x + q)) * 32 + lane);
-            }
-            const T2 ga = __ldg(gpar + 2 * gi.x), gb2 = __ldg(gpar + 2 * gi.x + 1);
-            const T v = fmin(fmax((sig - ga.x) * gb2.y, ga.y), gb2.x);  // IEEE +-inf bounds = no clamp
-            const size_t at = (gb + row) * 32 + lane;
-            if (act && (gi.y & kBFirst)) __stcg(xg + (size_t)gi.x * 32, v);
-            dsm[r * 32 + lane] = -rho * v - __ldcg(lmp + at);
-            if (act) __stcg(unext + at, v);
+    const int row0 = sm.x, ns = sm.y;
+    T* __restrict__ dd = BIG ? reinterpret_cast<T*>(B.dscr) + (gb + row0) * 32 + lane : W.d + lane;   // d_r at dd[32 r]
+    const bool var = sm.w & kBVar;
+    const T* __restrict__ V = reinterpret_cast<const T*>(B.vpool) + (grp * B.ve + (var ? sm.z : 0)) * 32 + lane;
+    if (LOPF_BATCH_L2PF) {
+        // lane-parallel L2 prefetch of the lines this subsystem streams from HBM (x_s read in the finish, the
+        // per-scenario operator in the mat-vec), issued before the consensus so they arrive while it runs
+        const char* xb = reinterpret_cast<const char*>(xlg - lane);
+        for (int e = lane; e < 2 * ns; e += 32) prefetch_l2_line(xb + (size_t)(32 * row0) * sizeof(T) + 128 * e);
+        if (var) {
+            const char* vb = reinterpret_cast<const char*>(V - lane);
+            const int nl = (ns * (ns + 1) / 2 + ns) * (int)(32 * sizeof(T) / 128);
+            for (int e = lane; e < nl; e += 32) prefetch_l2_line(vb + 128 * e);
+        }
+    }
+    // a4: consensus of every row's global, 32 rows per chunk; v parked in unext (replaced by u below)
+    for (int c0 = 0; c0 < ns; c0 += 32) {
+        const int nrow = min(32, ns - c0);
+        if (lane < nrow) {                                              // lane l stages row c0 + l's records
+            const int row = row0 + c0 + lane;
+            const int2 a = __ldg(rows + 3 * row), b = __ldg(rows + 3 * row + 1), c = __ldg(rows + 3 * row + 2);
+            int* mi = W.mi + lane * 6;
+            mi[0] = a.x; mi[1] = a.y; mi[2] = b.x; mi[3] = b.y; mi[4] = c.x; mi[5] = c.y;
+            const T2 p0 = __ldg(gpar + 2 * a.x), p1 = __ldg(gpar + 2 * a.x + 1);
+            T* mp = W.mp + lane * 4;
+            mp[0] = p0.x; mp[1] = p0.y; mp[2] = p1.x; mp[3] = p1.y;
         }
         __syncwarp();
-        // a5-a7, four rows at a time: y_r = sum_k Abar[r][k] d_k with k ascending
-        const bool var = sm.w & kBVar;
-        const T* __restrict__ V = reinterpret_cast<const T*>(B.vpool) + ((size_t)grp * B.ve + (var ? sm.z : 0)) * 32 + lane;
-        const T* __restrict__ A = reinterpret_cast<const T*>(B.spool) + (var ? 0 : sm.z);
-        for (int r0 = 0; r0 < ns; r0 += 4) {
-            int rr[4];
+        for (int r = 0; r < nrow; r += CR) {
+            T ua[CR][4], lm[CR];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) rr[i] = min(r0 + i, ns - 1);    // rows past n_s: discarded
-            T y[4] = {T(0), T(0), T(0), T(0)};
-            if (var) {
-                // packed upper triangle, row-major: (i, j >= i) at i n - i (i - 1) / 2 + j - i; row r reads
-                // (min(r, k), max(r, k)): the walk steps by n - k - 1 while k < r, then by 1
-                int p[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) p[i] = rr[i];
-#pragma unroll 2
-                for (int k = 0; k < ns; ++k) {
-                    const T dk = dsm[k * 32 + lane];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        y[i] = fma(__ldg(V + (size_t)p[i] * 32), dk, y[i]);
-                        p[i] += k < rr[i] ? ns - k - 1 : 1;
-                    }
-                }
-            } else {
-#pragma unroll 2
-                for (int k = 0; k < ns; ++k) {                          // Abar is exactly symmetric: A[k][r]
-                    const T dk = dsm[k * 32 + lane];
-                    const T* __restrict__ Ak = A + k * ns;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) y[i] = fma(__ldg(Ak + rr[i]), dk, y[i]);
-                }
+            for (int i = 0; i < CR; ++i) {                              // every load of CR rows first
+                const int rr = min(r + i, nrow - 1);
+                const int* mi = W.mi + rr * 6;
+                const int inf = mi[1];
+                const bool inl = inf & kBInline;
+                const int nu = inl ? (inf >> kBNuShift) & 0xFF : 0;
+                const int self = row0 + c0 + rr;
+                ua[i][0] = __ldcg(ug + 32 * (inl ? mi[2] : self));
+                ua[i][1] = nu > 1 ? __ldcg(ug + 32 * mi[3]) : T(0);
+                ua[i][2] = nu > 2 ? __ldcg(ug + 32 * mi[4]) : T(0);
+                ua[i][3] = nu > 3 ? __ldcg(ug + 32 * mi[5]) : T(0);
+                lm[i] = __ldcg(lmg + 32 * self);
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int r = r0 + i;
-                if (r >= ns) break;
-                const size_t at = (gb + row0 + r) * 32 + lane;
-                const T bb = (sm.w & kBBbar) ? __ldg(V + (size_t)(ns * (ns + 1) / 2 + r) * 32) : T(0);
-                const T xn = fma(y[i], inv_rho, bb);                    // (1/rho) Abar d + bbar
-                const T v = __ldcg(unext + at);
-                const T lam = __ldcg(lmp + at), xo = __ldcg(xlp + at);
-                const T ln = lam + rho * (v - xn);                      // ADMM-3
-                const T un = xn - ln * inv_rho;                         // next consensus input
-                if (act) {
-                    __stcg(xlp + at, xn);
-                    __stcg(lmp + at, ln);
-                    __stcg(unext + at, un);
-                    const T rs = v - xn, dx = xn - xo;                  // terms in T, sums in fp64 (F1)
-                    acc[0] += (double)(rs * rs);
-                    acc[1] += (double)(dx * dx);
-                    acc[2] += (double)(v * v);
-                    acc[3] += (double)(xn * xn);
-                    acc[4] += (double)(ln * ln);
+            for (int i = 0; i < CR; ++i) {
+                if (r + i >= nrow) break;
+                const int* mi = W.mi + (r + i) * 6;
+                const T* mp = W.mp + (r + i) * 4;
+                const int g = mi[0], inf = mi[1];
+                T sig = ((ua[i][0] + ua[i][1]) + ua[i][2]) + ua[i][3];   // ascending canonical copy order
+                if (!(inf & kBInline)) {                                // nu > 4 (rare): the segment list
+                    sig = T(0);
+                    for (int q = 0; q < mi[3]; ++q) sig += __ldcg(ug + 32 * __ldg(B.seg_rows + mi[2] + q));
                 }
+                const T v = fmin(fmax((sig - mp[0]) * mp[3], mp[1]), mp[2]);   // IEEE +-inf = no clamp
+                const int at = 32 * (row0 + c0 + r + i);
+                if (act && (inf & kBFirst)) __stcg(xg + 32 * g, v);
+                const T d = -rho * v - lm[i];
+                if (BIG) __stcg(dd + (c0 + r + i) * 32, d);
+                else dd[(c0 + r + i) * 32] = d;
+                if (act) __stcg(ung + at, v);
             }
         }
-        __syncwarp();                                                  // dsm is reused by the next subsystem
+        __syncwarp();                                                   // the row records are restaged
+    }
+    // a5-a7, four rows at a time: y_r = sum_k Abar[r][k] d_k with k ascending
+    const T* __restrict__ A = reinterpret_cast<const T*>(B.spool) + (var ? 0 : sm.z);
+    for (int r0 = 0; r0 < ns; r0 += 4) {
+        int rr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) rr[i] = min(r0 + i, ns - 1);        // rows past n_s: discarded
+        T y[4] = {T(0), T(0), T(0), T(0)};
+        if (var) {
+            // packed upper triangle, row-major: (i, j >= i) at i n - i (i - 1) / 2 + j - i; row r reads
+            // (min(r, k), max(r, k)): the walk steps by n - k - 1 while k < r, then by 1
+            int p[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p[i] = rr[i];
+#pragma unroll KU
+            for (int k = 0; k < ns; ++k) {
+                const T dk = BIG ? __ldcg(dd + k * 32) : dd[k * 32];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    y[i] = fma(__ldg(V + 32 * p[i]), dk, y[i]);
+                    p[i] += k < rr[i] ? ns - k - 1 : 1;
+                }
+            }
+        } else {
+#pragma unroll KU
+            for (int k = 0; k < ns; ++k) {                              // Abar is exactly symmetric: A[k][r]
+                const T dk = BIG ? __ldcg(dd + k * 32) : dd[k * 32];
+                const T* __restrict__ Ak = A + k * ns;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) y[i] = fma(__ldg(Ak + rr[i]), dk, y[i]);
+            }
+        }
+        T vv[4], lam[4], xo[4], bb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {                                   // the four rows' loads first
+            const int at = 32 * (row0 + rr[i]);
+            vv[i] = __ldcg(ung + at);
+            lam[i] = __ldcg(lmg + at);
+            xo[i] = __ldcg(xlg + at);
+            bb[i] = (sm.w & kBBbar) ? __ldg(V + 32 * (ns * (ns + 1) / 2 + rr[i])) : T(0);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (r0 + i >= ns) break;
+            const int at = 32 * (row0 + r0 + i);
+            const T xn = fma(y[i], inv_rho, bb[i]);                     // (1/rho) Abar d + bbar
+            const T v = vv[i];
+            const T ln = lam[i] + rho * (v - xn);                       // ADMM-3
+            const T un = xn - ln * inv_rho;                             // next consensus input
+            if (act) {
+                __stcg(xlg + at, xn);
+                __stcg(lmg + at, ln);
+                __stcg(ung + at, un);
+                const T rs = v - xn, dx = xn - xo[i];                   // terms in T, sums in fp64 (F1)
+                acc[0] += (double)(rs * rs);
+                acc[1] += (double)(dx * dx);
+                acc[2] += (double)(v * v);
+                acc[3] += (double)(xn * xn);
+                acc[4] += (double)(ln * ln);
+            }
+        }
+    }
+    __syncwarp();                                                       // d is reused by the next subsystem
+}
+
+template <class T>
+__device__ __forceinline__ void batch_item(const BatchProblem& B, const int grp, const int task,
+                                           const T* __restrict__ ucur, T* __restrict__ unext, const WarpSmem<T>& W,
+                                           const int lane, const bool act, double (&acc)[5]) {
+    const int4 tk = __ldg(reinterpret_cast<const int4*>(B.tasks) + 2 * task);
+    const size_t gb = (size_t)grp * B.n_rows;                        // first row of this group
+    for (int s = tk.x; s < tk.y; ++s) {
+        const int4 sm = __ldg(reinterpret_cast<const int4*>(B.subs) + s);   // {row0, ns, op, flags}
+        if (sm.y <= kBatchDMax) batch_sub<T, false>(B, sm, gb, ucur, unext, W, lane, act, acc, grp);
+        else batch_sub<T, true>(B, sm, gb, ucur, unext, W, lane, act, acc, grp);
     }
 }
 
@@ -163,11 +248,18 @@ __global__ void __launch_bounds__(BB, 1) admm_batch_kernel(BatchProblem B) {
     __shared__ int s_na;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int gw = blockIdx.x * BW + wid, nw = gridDim.x * BW;
-    T* dsm = reinterpret_cast<T*>(bsm) + (size_t)wid * B.ns_max * 32;
+    WarpSmem<T> W;
+    {
+        unsigned char* base = bsm + (size_t)wid * warp_smem_bytes<T>();
+        W.d = reinterpret_cast<T*>(base);
+        unsigned char* meta = base + kBatchDMax * 32 * sizeof(T);
+        W.mp = reinterpret_cast<T*>(meta);
+        W.mi = reinterpret_cast<int*>(meta + 32 * 4 * sizeof(T));
+    }
     const long long total0 = *(volatile long long*)&B.ctrl->total;
     const int NT = B.n_tasks, NG = B.n_grp;
-    const long long WS = __ldg(B.wpre + NT);
     unsigned long long bars = 0;
+    const long long WS = __ldg(B.wpre + NT);
     long long it = 0;
     while (it < B.max_iter) {
         const long long t = total0 + it;
@@ -190,13 +282,17 @@ __global__ void __launch_bounds__(BB, 1) admm_batch_kernel(BatchProblem B) {
         __syncthreads();
         const int NA = s_na;
         if (NA == 0) break;                             // every scenario has stopped (same view in every CTA)
-        // warp gw takes the items whose start weight lies in [gw, gw + 1) * WT / nw
+        // warp gw takes the active items (active group rank * NT + task, group-major) whose start weight
+        // lies in [gw, gw + 1) WT / nw: consecutive tasks of one group, cost-balanced
+        const long long NI = (long long)NA * NT;
         const long long WT = (long long)NA * WS;
-        const long long a0 = item_at(B.wpre, NT, WS, (WT * gw + nw - 1) / nw);
-        const long long a1 = item_at(B.wpre, NT, WS, (WT * (gw + 1) + nw - 1) / nw);
+        long long a = item_at(B.wpre, NT, WS, (WT * gw + nw - 1) / nw);
+        const long long a_end = item_at(B.wpre, NT, WS, (WT * (gw + 1) + nw - 1) / nw);
+        if (a >= a_end) a = NI;
         int cur = -1;
         bool act = false;
-        for (long long a = a0; a < a1; ++a) {
+        while (a < NI) {
+            const long long an = a + 1 < a_end ? a + 1 : NI;
             const int ag = (int)(a / NT), task = (int)(a - (long long)ag * NT);
             const int grp = s_gl[ag];
             if (grp != cur) {
@@ -205,10 +301,11 @@ __global__ void __launch_bounds__(BB, 1) admm_batch_kernel(BatchProblem B) {
                 act = sc < B.n_scen && __ldcg(B.stopped + sc) == 0;
             }
             double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            batch_item<T>(B, grp, task, ucur, unext, dsm, lane, act, acc);
+            batch_item<T>(B, grp, task, ucur, unext, W, lane, act, acc);
             double* pp = B.partial + ((size_t)grp * NT + task) * 5 * 32 + lane;
 #pragma unroll
             for (int k = 0; k < 5; ++k) __stcg(pp + k * 32, acc[k]);
+            a = an;
         }
         grid_sync(B.cnt, (++bars) * gridDim.x);
         // per-scenario (termination): warp per active group, lane = scenario
@@ -314,7 +411,10 @@ const void* batch_kernel_for(int esz) {
 
 int batch_block() { return BB; }
 
-int batch_smem(int ns_max, int esz) { return BW * ns_max * 32 * esz; }
+int batch_smem(int ns_max, int esz) {
+    (void)ns_max;
+    return BW * (esz == 4 ? warp_smem_bytes<float>() : warp_smem_bytes<double>());
+}
 
 lopf_status query_batch_grid(int ns_max, int esz, int* grid, std::string& err) {
     int dev = 0, sms = 0, per = 0;

@@ -217,8 +217,10 @@ constexpr int kBBbar = 2;                      // ... with a nonzero b-bar after
 struct BSub {                                  // 16 B per subsystem (DFS order)
     int32_t row0, ns, op, flags;               // op: shared dense Abar offset (T entries) or var-pool entry offset
 };
-struct BTask {                                 // 16 B per task: a DFS run of subsystems
+struct BTask {                                 // 32 B per task: a DFS run of subsystems
     int32_t sub0, sub1, row0, row1;
+    int32_t vop0, vop1;                        // its per-scenario operator entries [vop0, vop1) (contiguous)
+    int32_t pad[2];
 };
 
 struct BatchProblem {
@@ -235,6 +237,7 @@ struct BatchProblem {
     void *xl, *lam, *u0, *u1;                  // (T) [group][n_rows][32]
     void* x;                                   // (T) [group][n][32]
     double* partial;                           // [group][n_tasks][5][32] residual sums per item
+    void* dscr;                                // (T) [group][n_rows][32] d of subsystems with n_s > kBatchDMax
     ScenResult* res;                           // [n_scen]
     int32_t* stopped;                          // [n_scen] converged / non-finite: frozen
     uint32_t* gact;                            // [2][n_grp] group has an active scenario, by sweep parity
@@ -251,9 +254,13 @@ struct BatchProblem {
 constexpr int kBatchMaxScen = 8192;            // scenarios per batch handle
 constexpr int kBatchMaxGrp = kBatchMaxScen / 32;
 #ifndef LOPF_BATCH_WARPS
-#define LOPF_BATCH_WARPS 16
+#define LOPF_BATCH_WARPS 20
 #endif
 constexpr int kBatchWarps = LOPF_BATCH_WARPS;  // warps per CTA of the batch kernel
+#ifndef LOPF_BATCH_DMAX
+#define LOPF_BATCH_DMAX 24
+#endif
+constexpr int kBatchDMax = LOPF_BATCH_DMAX;    // subsystems with more rows stage d in the global scratch
 #ifndef LOPF_BATCH_TASK_ROWS
 #define LOPF_BATCH_TASK_ROWS 32
 #endif
@@ -287,7 +294,7 @@ struct Layout {
     // batch kernel (config 4, lane = scenario)
     int32_t n_scen = 0, n_grp = 0, ns_max = 0, n_rows = 0, n_bsub = 0, ve = 0;
     size_t off_brow = 0, off_bsub = 0, off_btask = 0, off_bseg = 0, off_bspool = 0, off_bvpool = 0, off_bpart = 0,
-           off_bres = 0, off_bstop = 0, off_bgact = 0, off_bcnt = 0, off_bwpre = 0, off_bstage = 0;
+           off_bres = 0, off_bstop = 0, off_bgact = 0, off_bcnt = 0, off_bwpre = 0, off_bstage = 0, off_bdscr = 0;
     size_t image_bytes = 0;                // bytes of `image` uploaded by bind (0: the whole arena); the rest is
                                            // device state initialised by the reset kernels
 };

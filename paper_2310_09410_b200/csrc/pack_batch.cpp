@@ -25,11 +25,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     L.esz = (int32_t)E;
     int ns_max = 1;
     for (int64_t s = 0; s < P.S; ++s) ns_max = std::max(ns_max, P.n_s[s]);
-    if ((int64_t)kBatchWarps * ns_max * 32 * E > 200 * 1024) {
-        err = "batch mode: n_s = " + std::to_string(ns_max) + " needs more shared memory for the d staging than a CTA of " +
-              std::to_string(kBatchWarps) + " warps has";
-        return LOPF_E_ARG;
-    }
+    if (ns_max > 255) { err = "batch mode supports n_s <= 255"; return LOPF_E_ARG; }
     const int32_t NSC = bo.n_scen, NG = (NSC + 31) / 32;
     const std::vector<int64_t> order = dfs_order(N, P);
 
@@ -87,14 +83,20 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     std::vector<BTask> tasks;
     std::vector<long long> wpre(1, 0);
     for (size_t i = 0; i < subs.size();) {
-        BTask t{(int32_t)i, (int32_t)i, subs[i].row0, subs[i].row0};
+        BTask t{(int32_t)i, (int32_t)i, subs[i].row0, subs[i].row0, -1, -1, {0, 0}};
         long long w = 0;
         while (i < subs.size() && (t.row1 - t.row0 < kBatchTaskRows || t.sub1 == t.sub0)) {
             const long long ns = subs[i].ns;
             w += 16 + 12 * ns + ns * ns * ((subs[i].flags & kBVar) ? 2 : 1);
             t.row1 += subs[i].ns;
+            if (subs[i].flags & kBVar) {                           // var entries are assigned in DFS order
+                const int32_t e1 = subs[i].op + (int32_t)(ns * (ns + 1) / 2 + ns);
+                if (t.vop0 < 0) t.vop0 = subs[i].op;
+                t.vop1 = e1;
+            }
             t.sub1 = (int32_t)++i;
         }
+        if (t.vop0 < 0) t.vop0 = t.vop1 = 0;
         tasks.push_back(t);
         wpre.push_back(wpre.back() + w);
     }
@@ -141,6 +143,9 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     L.off_u1 = take(per);
     L.off_x = take(E * (size_t)NG * P.n * 32);
     L.off_bpart = take(8 * 160 * (size_t)NG * NT);
+    bool big = false;
+    for (int64_t s = 0; s < P.S; ++s) big |= P.n_s[s] > kBatchDMax;
+    L.off_bdscr = take(big ? per : 0);
     L.off_bres = take(sizeof(ScenResult) * (size_t)NSC);
     L.off_bstop = take(4 * (size_t)NSC);
     L.off_bgact = take(4 * 2 * (size_t)NG);
