@@ -74,12 +74,15 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def _ncu_traffic(precision: int = 64):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+def _ncu_traffic(precision: int = 64, shape: str = "8500"):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary of the SAME
+    workload (the summaries are of the 8500-shaped config 3; other shapes report null)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json" if precision == 64 else "ncu_summary_f32.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
+        if f"{shape}-shaped" not in d.get("workload", ""):
+            return None, None
         if "dram_bytes_per_sweep" in d:                   # tools/ncu_json.py summaries
             return d["dram_bytes_per_sweep"] * d["sweeps_per_launch"], d["sweeps_per_launch"]
         return d.get("dram_bytes_per_launch"), d.get("iters_per_launch")
@@ -87,16 +90,37 @@ def _ncu_traffic(precision: int = 64):
         return None, None
 
 
-def cpu_oracle_rate(feeder, sweeps: int):
-    """Oracle sweeps/s on this host (one thread), from the initial point; setup excluded."""
+def cpu_oracle_rate(feeder, sweeps: int, openmp: bool = False, prob=None):
+    """Oracle sweeps/s on this host from the initial point; setup excluded.  openmp=False: the parity oracle
+    (plain C, one thread); True: the same loop built with -fopenmp on every core of this process
+    (SURVEY §8(d) mode (ii), timing only)."""
     import oracle
-    p = oracle.build_problem(feeder)
+    from oracle.admm import run_k_omp
+    p = prob if prob is not None else oracle.build_problem(feeder)
     x0 = oracle.initial_state(p)
-    oracle.run_k(p, 5, state=x0)                         # warm the C library
+    run = run_k_omp if openmp else oracle.run_k
+    run(p, 5, state=x0)                                  # warm the C library / the thread pool
     t = time.perf_counter()
-    oracle.run_k(p, sweeps, state=x0)
+    run(p, sweeps, state=x0)
     dt = time.perf_counter() - t
     return sweeps / dt, dt
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _lp_optimum(feeder, shape):
+    """HiGHS optimum of the same LP (tests/golden/lp_optimum.json, written from oracle/ only), or None."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "lp_optimum.json")) as fh:
+            g = json.load(fh)["configs"][shape]
+        return g["objective"] if g["sha256"] == feeder.sha256() else None
+    except Exception:
+        return None
 
 
 def main():
@@ -111,6 +135,7 @@ def main():
                     help="32: the fp32 variant (the paper's GPU precision, PAPER.md:414; streaming/batch kernels)")
     ap.add_argument("--cpu-sweeps", type=int, default=6000, help="oracle sweeps timed for cpu_baseline (~10 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-paper-length", action="store_true", help="skip the fixed-K = 15817 run (PAPER.md:510)")
     ap.add_argument("--ref-sweeps", type=int, default=100, help="oracle sweeps per step for --impl reference")
     ap.add_argument("--config", type=int, default=3, choices=[3, 4, 5],
                     help="3: 8500-shaped single solve (default, the headline); 4: 4096 scenarios of the "
@@ -205,25 +230,64 @@ def main():
     dev_ms = sum(step_ms)
     tot_iters = sum(iters)
 
-    # end to end through the public API with host buffers: every step uploads the packed problem from its
-    # pinned host image (H2D), solves, and reads the solution x and the result record back (D2H).  Two
-    # handles on two streams: step i+1's upload runs on the copy engines while step i solves.
+    # end to end through the public API with host buffers, stream-ordered (no host synchronisation inside a
+    # step): step i uploads the packed problem from its pinned host image (lopf_bind, H2D), solves
+    # (lopf_solve_async) and copies the result record and x back into pinned host memory
+    # (lopf_fetch_async, D2H).  Two handles on two streams: step i+1's upload runs on the copy engine while
+    # step i solves; the host only waits for step i-2's fetch before reusing its buffer.
     e2e_steps = max(3, min(args.steps, 10))
     h2 = Lopf.setup(feeder, kernel=args.kernel, precision=args.precision).bind(dev)
     hs, ss = (h, h2), (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    fb = int(sz.fetch_bytes)
+    bufs = [torch.empty(fb, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    pending = [False, False]
     barrier()
     t = time.perf_counter()
     e2e_iters = 0
-    hs[0].bind(dev, stream=ss[0])
     for i in range(e2e_steps):
-        a, sa = hs[i % 2], ss[i % 2]
-        if i + 1 < e2e_steps:
-            hs[(i + 1) % 2].bind(dev, stream=ss[(i + 1) % 2])      # next step's H2D, overlapped
-        r = a.solve(stream=sa)
-        x = a.get_x(stream=sa)
-        e2e_iters += int(r.iters)
-    torch.cuda.synchronize(dev)
+        j = i % 2
+        if pending[j]:
+            done[j].synchronize()
+            e2e_iters += int(Lopf.decode_fetch(bufs[j], int(sz.n))[0].iters)
+        with torch.cuda.stream(ss[j]):
+            hs[j].bind(dev, stream=ss[j])
+            hs[j].solve_async(int(h.opts.max_iter), True, stream=ss[j])
+            hs[j].fetch_async(bufs[j], stream=ss[j])
+            done[j].record(ss[j])
+        pending[j] = True
+    for j in range(2):
+        if pending[j]:
+            done[j].synchronize()
+            e2e_iters += int(Lopf.decode_fetch(bufs[j], int(sz.n))[0].iters)
     e2e_s = time.perf_counter() - t
+    # breakdown of one step (events on one stream): upload, solve, read-back
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    evs[0].record(stream)
+    h.bind(dev, stream=stream)
+    evs[1].record(stream)
+    h.solve_async(int(h.opts.max_iter), True, stream=stream)
+    evs[2].record(stream)
+    h.fetch_async(bufs[0], stream=stream)
+    evs[3].record(stream)
+    torch.cuda.synchronize(dev)
+    breakdown = {"h2d_ms": evs[0].elapsed_time(evs[1]), "solve_ms": evs[1].elapsed_time(evs[2]),
+                 "d2h_ms": evs[2].elapsed_time(evs[3])}
+    r_last, _ = Lopf.decode_fetch(bufs[0], int(sz.n))
+    objective = float(r_last.objective)
+    # paper-length run (15817 sweeps on IEEE 8500): fixed K with the test off, so the sweep rate
+    # and the objective are not those of the early stop of the paper's criterion on this instance
+    paper = None
+    if args.shape == "8500" and not args.no_paper_length:
+        k_paper = 15817
+        h.reset()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        h.solve_async(k_paper, False, stream=stream)
+        b_.record(stream)
+        rp = h.result_get(stream=stream)
+        paper = {"sweeps": k_paper, "ms": a_.elapsed_time(b_), "us_per_sweep": 1e3 * a_.elapsed_time(b_) / k_paper,
+                 "objective": float(rp.objective)}
 
     # max over ranks
     vals = torch.tensor([dev_ms, float(tot_iters), e2e_s, float(e2e_iters)], dtype=torch.float64, device=dev)
@@ -243,14 +307,21 @@ def main():
         mean_kern_ms = statistics.mean(kern_ms)
         mean_iters = statistics.mean(iters)
         achieved = sz.alg_bytes * mean_iters / (mean_kern_ms / 1e3) / 1e9
-        dram, ncu_iters = _ncu_traffic(args.precision) if sz.kernel == 2 else (None, None)   # resident kernel's
+        dram, ncu_iters = _ncu_traffic(args.precision, args.shape) if sz.kernel == 2 else (None, None)   # resident
         traffic = (dram / ncu_iters * mean_iters) if (dram and ncu_iters) else None
-        cpu = None
+        cpu = cpu_omp = None
         if world == 1 and not args.no_cpu_baseline:
-            rate, secs = cpu_oracle_rate(feeder, args.cpu_sweeps)
+            import oracle
+            prob = oracle.build_problem(feeder)
+            rate, secs = cpu_oracle_rate(feeder, args.cpu_sweeps, prob=prob)
             cpu = {"value": rate, "unit": "iterations/s", "cores": 1, "kind": "oracle",
                    "sample": f"{args.cpu_sweeps} oracle sweeps (O6 loop, plain C, -O2, one thread) of the same "
                              f"ieee{args.shape}-shaped feeder from the initial point; {secs:.1f} s"}
+            rate2, secs2 = cpu_oracle_rate(feeder, args.cpu_sweeps, openmp=True, prob=prob)
+            cpu_omp = {"value": rate2, "unit": "iterations/s", "cores": _cores(), "kind": "oracle-openmp",
+                       "sample": f"{args.cpu_sweeps} sweeps of the oracle loop built with -fopenmp (static split of each "
+                                 f"step over {_cores()} cores, SURVEY 8(d) mode (ii)); {secs2:.1f} s"}
+        lp_opt = _lp_optimum(feeder, args.shape)
         out = {
             "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -259,7 +330,11 @@ def main():
                        "n_copies": int(sz.n_copies), "iters_to_tolerance": iters[0],
                        "time_to_tolerance_ms": statistics.median(step_ms), "l2": "flushed between steps (512 MiB write)",
                        "kernel": "streaming" if sz.kernel == 1 else "resident", "grid": int(sz.grid),
-                       "block": int(sz.block), "setup_s": round(setup_s, 3)},
+                       "block": int(sz.block), "setup_s": round(setup_s, 3), "objective": objective,
+                       "objective_lp": lp_opt,
+                       "objective_gap_vs_lp": None if lp_opt is None else (objective - lp_opt) / abs(lp_opt),
+                       "paper_length": None if paper is None else dict(paper, objective_gap_vs_lp=None if lp_opt is None
+                                                                       else (paper["objective"] - lp_opt) / abs(lp_opt))},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_src,
                          "kernel": ("admm_resident_kernel" if sz.kernel == 2 else "admm_stream_kernel")
@@ -267,11 +342,17 @@ def main():
                          "alg_bytes_per_sweep": int(sz.alg_bytes), "mean_kernel_ms": mean_kern_ms,
                          "us_per_sweep": 1e3 * mean_kern_ms / mean_iters},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": int(sz.device_bytes),
-                    "d2h_bytes_per_step": int(8 * sz.n + 256), "steps": e2e_steps},
+            "cpu_baseline_omp": cpu_omp,
+            "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": int(sz.upload_bytes),
+                    "d2h_bytes_per_step": int(sz.fetch_bytes), "steps": e2e_steps, "breakdown": breakdown,
+                    "pipeline": "2 handles x 2 streams: bind (H2D) / solve_async / fetch_async (D2H), no per-step sync"},
             "clocks": clk.summary(),
             "gpu_launches": 2 * args.steps,
         }
+        if sz.kernel == 2:
+            out["roofline"]["served_from"] = ("SMEM: the resident kernel keeps operators and iterate on chip, so "
+                                              "achieved is algorithmic bytes per second, not DRAM traffic")
+            out["roofline"]["dram_bytes_per_sweep"] = None if traffic is None else traffic / mean_iters
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
@@ -450,7 +531,7 @@ def bench_stitched(args):
                          "alg_bytes_per_sweep": int(sz.alg_bytes), "us_per_sweep": us},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_steps * args.sweeps / e2e_max, "unit": "iterations/s",
-                    "h2d_bytes_per_step": int(sz.device_bytes), "d2h_bytes_per_step": int(8 * sz.n), "steps": e2e_steps},
+                    "h2d_bytes_per_step": int(sz.upload_bytes), "d2h_bytes_per_step": int(8 * sz.n), "steps": e2e_steps},
             "clocks": clk.summary(),
             "gpu_launches": args.steps * (1 if world == 1 else 2 * args.sweeps),
         }
@@ -572,7 +653,7 @@ def bench_batch(args):
                          "us_per_batch_sweep": us_per_batch_sweep},
             "cpu_baseline": cpu,
             "e2e": {"value": float(allv[:, 3].sum()) * e2e_steps / float(allv[:, 2].max()), "unit": "scenario-iterations/s",
-                    "h2d_bytes_per_step": int(sz.device_bytes), "d2h_bytes_per_step": 64 * (hi - lo), "steps": e2e_steps},
+                    "h2d_bytes_per_step": int(sz.upload_bytes), "d2h_bytes_per_step": 64 * (hi - lo), "steps": e2e_steps},
             "clocks": clk.summary(),
             "gpu_launches": 2 * args.steps,
         }

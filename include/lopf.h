@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define LOPF_ABI_VERSION 2
+#define LOPF_ABI_VERSION 3
 
 typedef struct lopf_handle lopf_handle;
 
@@ -111,6 +111,8 @@ typedef struct {
     int32_t max_ns, max_ms;
     int32_t n_scen;        /* scenarios of a batch handle (lopf_setup_batch), else 0 */
     int32_t reserved[2];
+    int64_t upload_bytes;  /* bytes lopf_bind copies host -> device (the packed problem; device-only state excluded) */
+    int64_t fetch_bytes;   /* bytes of the host buffer lopf_fetch_async fills (single-problem handles) */
 } lopf_sizes;
 
 typedef struct {
@@ -201,6 +203,14 @@ lopf_status lopf_run(lopf_handle *h, int64_t k, int32_t test, void *cuda_stream,
  * without synchronising; fetch the result later with lopf_result_get. */
 lopf_status lopf_solve_async(lopf_handle *h, int64_t max_iter, int32_t test, void *cuda_stream);
 lopf_status lopf_result_get(lopf_handle *h, void *cuda_stream, lopf_result *res);
+
+/* Stream-ordered read-back of a solve (no host synchronisation): one small kernel gathers the result
+ * record and the solution x into the arena, one cudaMemcpyAsync copies them to `host_buf` (fetch_bytes
+ * from lopf_sizes; pinned memory makes the copy asynchronous).  Layout of host_buf: a lopf_result
+ * (solve_ms = 0: take it from lopf_result_get or your own events), padded to 64 bytes, then x as n
+ * doubles in canonical order.  The caller waits on its own event / stream before reading host_buf.
+ * LOPF_E_STATE on batch and partitioned handles (use lopf_get_batch_results / lopf_result_get). */
+lopf_status lopf_fetch_async(lopf_handle *h, void *cuda_stream, void *host_buf);
 
 /* Canonical decomposition: kind (0 BUS, 1 LINE, 2 LEAF), comp (bus or line index),
  * leaf_bus (-1 unless LEAF), m_s, n_s [S]; sub_ptr [S+1] copy offsets; copy_global [n_copies]. */

@@ -21,18 +21,21 @@ from .precompute import precompute
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "_build", "liboracle_admm.so")
+_SO_OMP = os.path.join(_HERE, "_build", "liboracle_admm_omp.so")
 _SRC = os.path.join(_HERE, "admm_loop.c")
 
 
-def build_lib(force: bool = False) -> str:
-    """Compile admm_loop.c (gcc -O2 -ffp-contract=off); the checker is built, never shipped."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        os.makedirs(os.path.dirname(_SO), exist_ok=True)
-        tmp = _SO + f".tmp{os.getpid()}"
+def build_lib(force: bool = False, openmp: bool = False) -> str:
+    """Compile admm_loop.c (gcc -O2 -ffp-contract=off); the checker is built, never shipped.  openmp=True:
+    the multi-core timing build of bench.py's cpu_baseline mode (ii) (not a parity reference)."""
+    so = _SO_OMP if openmp else _SO
+    if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(_SRC):
+        os.makedirs(os.path.dirname(so), exist_ok=True)
+        tmp = so + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-                               "-std=c11", "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _SO)
-    return _SO
+                               "-std=c11", *(["-fopenmp"] if openmp else []), "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, so)
+    return so
 
 
 class _Problem(C.Structure):
@@ -52,6 +55,36 @@ class _ProblemF32(C.Structure):
 
 
 _lib = None
+_lib_omp = None
+
+
+def _declare(lib_):
+    P = C.POINTER(_Problem)
+    vp = C.c_void_p
+    lib_.oracle_run.argtypes = [P, vp, vp, vp, C.c_int64, C.c_int32, vp, vp, vp, C.c_int64, C.c_int32, vp]
+    lib_.oracle_run.restype = C.c_int64
+    return lib_
+
+
+def lib_omp():
+    """The OpenMP build (timing only: its residual sums are reduced in a different order)."""
+    global _lib_omp
+    if _lib_omp is None:
+        _lib_omp = _declare(C.CDLL(build_lib(openmp=True)))
+    return _lib_omp
+
+
+def run_k_omp(prob: "OracleProblem", k: int, state=None) -> int:
+    """k sweeps of the OpenMP build from `state` (default: the initial point); returns k.  For timing."""
+    xl, lam = state if state is not None else initial_state(prob)
+    x = np.zeros(prob.n)
+    xl = np.array(xl, dtype=np.float64, copy=True)
+    lam = np.array(lam, dtype=np.float64, copy=True)
+    res = np.zeros(4)
+    conv = C.c_int32(0)
+    nrow = C.c_int64(0)
+    return int(lib_omp().oracle_run(C.byref(prob._st), _p(x), _p(xl), _p(lam), int(k), 0, _p(res), C.byref(conv), None,
+                                    0, 0, C.byref(nrow)))
 
 
 def lib():

@@ -3,7 +3,10 @@
  * TEST INFRASTRUCTURE ONLY: called from oracle/admm.py (ctypes) by tests/, smoke()
  * and bench.py's cpu_baseline leg.  Shares nothing with paper_2310_09410_b200/.
  * Built with: gcc -O2 -ffp-contract=off -fPIC -shared (no FMA contraction, IEEE
- * round-to-nearest-even, fixed summation orders as stated below).
+ * round-to-nearest-even, fixed summation orders as stated below).  The `omp` pragmas are inert in that
+ * (parity) build; the same file built with -fopenmp is the multi-core CPU baseline of bench.py (SURVEY
+ * §8(d) mode (ii)): each loop split statically over the host cores, residual sums by an OpenMP
+ * reduction (summation order then differs, so that build is for timing only, never for parity).
  *
  * Data (all in canonical order, DESIGN.md §3 C12):
  *   n globals: c, lo, hi                      (LP_model)
@@ -36,6 +39,7 @@ typedef struct {
  *          = (sum_k (x_k - lam_k/rho) - c_i/rho) / nu_i,   k over seg(i) ascending. */
 void oracle_global_update(const oracle_problem *p, const double *xl, const double *lam, double *x)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < p->n; ++i) {
         double sigma = 0.0;
         int64_t nu = p->seg_ptr[i + 1] - p->seg_ptr[i];
@@ -52,8 +56,11 @@ void oracle_global_update(const oracle_problem *p, const double *xl, const doubl
  *   v = B_s x,  d = -rho v - lam_s,  x_s[r] = (sum_k Abar[r][k] d[k]) / rho + bbar[r]  (k ascending). */
 void oracle_local_update(const oracle_problem *p, const double *x, const double *lam, double *xl_new)
 {
+#pragma omp parallel
+    {
     double *d = NULL;
     int64_t dcap = 0;
+#pragma omp for schedule(static)
     for (int64_t s = 0; s < p->S; ++s) {
         int64_t o = p->sub_ptr[s], ns = p->sub_ptr[s + 1] - o;
         if (ns > dcap) { free(d); dcap = ns; d = (double *)malloc(sizeof(double) * (size_t)dcap); }
@@ -69,11 +76,13 @@ void oracle_local_update(const oracle_problem *p, const double *x, const double 
         }
     }
     free(d);
+    }
 }
 
 /* Dual update ADMM-3: lam_s += rho (B_s x - x_s). */
 void oracle_dual_update(const oracle_problem *p, const double *x, const double *xl, double *lam)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t k = 0; k < p->nc; ++k) {
         double v = x[p->copy_global[k]];
         lam[k] = lam[k] + p->rho * (v - xl[k]);
@@ -88,6 +97,7 @@ void oracle_residuals(const oracle_problem *p, const double *x, const double *xl
                       const double *lam, double *out)
 {
     double sp = 0.0, sd = 0.0, sv = 0.0, sx = 0.0, sl = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : sp, sd, sv, sx, sl)
     for (int64_t k = 0; k < p->nc; ++k) {
         double v = x[p->copy_global[k]];
         double r = v - xl[k];

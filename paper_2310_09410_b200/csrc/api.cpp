@@ -110,6 +110,17 @@ static lopf_status check_precision(const lopf_options& o) {
     return LOPF_OK;
 }
 
+// The image uploaded by bind covers the packed problem; the fetch staging (lopf_fetch_async) goes after it.
+static void add_fetch_stage(lopf_handle* h) {
+    Layout& L = h->lay;
+    if (L.image_bytes == 0) L.image_bytes = L.image.size();
+    if (h->batch() || h->parted()) return;
+    L.off_fetch = (L.bytes + 255) & ~(size_t)255;
+    // also the slot-ordered x_s / lambda gather of the resident layout (lopf_get_state: one kernel, one copy)
+    const size_t res_gather = h->resident() ? 16 * (size_t)L.total_slots : 0;
+    L.bytes = L.off_fetch + std::max(64 + 8 * (size_t)h->cp.n, res_gather);
+}
+
 extern "C" {
 
 int32_t lopf_abi_version(void) { return LOPF_ABI_VERSION; }
@@ -157,6 +168,7 @@ lopf_status lopf_setup(const lopf_network* net, const lopf_options* opt, lopf_ha
             }
         }
         if (st != LOPF_OK) { delete h; return fail(st, err); }
+        add_fetch_stage(h);
     } catch (const std::bad_alloc&) {
         delete h;
         return fail(LOPF_E_ARG, "out of host memory during setup");
@@ -192,6 +204,7 @@ lopf_status lopf_setup_batch(const lopf_network* net, const lopf_options* opt, i
         if (st == LOPF_OK) st = build_batch_ops(h->net, h->cp, n_scen, load_scale, h->bo, err);
         if (st == LOPF_OK) st = pack_batch(h->net, h->cp, h->bo, h->opt, h->lay, err);
         if (st != LOPF_OK) { delete h; return fail(st, err); }
+        add_fetch_stage(h);
     } catch (const std::bad_alloc&) {
         delete h;
         return fail(LOPF_E_ARG, "out of host memory during setup");
@@ -226,6 +239,7 @@ lopf_status lopf_setup_part(const lopf_network* net, const lopf_options* opt, in
         if (st == LOPF_OK) st = build_partition(h->net, h->cp, world, bus_owner, h->part, err);
         if (st == LOPF_OK) st = pack_streaming(h->net, h->cp, h->opt, kMaxGrid, h->lay, err, &h->part, rank);
         if (st != LOPF_OK) { delete h; return fail(st, err); }
+        add_fetch_stage(h);
     } catch (const std::bad_alloc&) {
         delete h;
         return fail(LOPF_E_ARG, "out of host memory during setup");
@@ -330,6 +344,8 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
     sz->grid = h->resident() ? h->lay.G : h->grid;
     sz->block = h->resident() ? kResBlock : h->batch() ? batch_block() : stream_block(h->lay.rmax, h->lay.esz);
     sz->n_scen = h->batch() ? h->lay.n_scen : 0;
+    sz->upload_bytes = (int64_t)h->lay.image.size();
+    sz->fetch_bytes = (h->batch() || h->parted()) ? 0 : (int64_t)(64 + 8 * h->cp.n);
     return LOPF_OK;
 }
 
@@ -591,6 +607,19 @@ lopf_status lopf_result_get(lopf_handle* h, void* stream, lopf_result* res) {
     return LOPF_OK;
 }
 
+lopf_status lopf_fetch_async(lopf_handle* h, void* stream, void* host_buf) {
+    if (!h || !host_buf) return fail(LOPF_E_ARG, "NULL argument");
+    if (!h->bound) return fail(LOPF_E_STATE, "fetch before lopf_bind");
+    if (h->batch() || h->parted()) return fail(LOPF_E_STATE, "lopf_fetch_async serves single-problem handles");
+    uint8_t* stage = (uint8_t*)h->arena + h->lay.off_fetch;
+    std::string err;
+    lopf_status st = launch_fetch(h->dp.ctrl, h->dp.x, h->cp.n, h->lay.esz, stage, stream, err);
+    if (st != LOPF_OK) return fail(st, err);
+    CUDA_TRY(cudaMemcpyAsync(host_buf, stage, 64 + 8 * (size_t)h->cp.n, cudaMemcpyDeviceToHost, (cudaStream_t)stream),
+             "fetch D2H");
+    return LOPF_OK;
+}
+
 lopf_status lopf_run(lopf_handle* h, int64_t k, int32_t test, void* stream, lopf_result* res) {
     lopf_status st = lopf_solve_async(h, k, test, stream);
     if (st != LOPF_OK) return st;
@@ -670,13 +699,15 @@ static lopf_status fetch_slots(lopf_handle* h, cudaStream_t s, std::vector<doubl
     if (!h->resident()) {
         CUDA_TRY(d2h_elems(xl.data(), h->dp.xl, L.n_slots, L.esz, s), "state D2H");
         CUDA_TRY(d2h_elems(lm.data(), h->dp.lam, L.n_slots, L.esz, s), "state D2H");
-    } else {
-        for (int c = 0; c < L.G; ++c) {
-            const CtaHdr& H = L.hdr[c];
-            const uint8_t* blob = h->rp.blobs + H.blob_off;
-            CUDA_TRY(d2h_elems(xl.data() + H.slot_base, blob + H.off_xl0, H.n_slots, L.esz, s), "state D2H");
-            CUDA_TRY(d2h_elems(lm.data() + H.slot_base, blob + H.off_lam0, H.n_slots, L.esz, s), "state D2H");
-        }
+    } else {                                       // one gather kernel over the CTA blobs, one copy
+        uint8_t* stage = (uint8_t*)h->arena + L.off_fetch;
+        std::string err;
+        lopf_status st = launch_gather_resident(h->rp, stage, s, err);
+        if (st != LOPF_OK) return fail(st, err);
+        std::vector<double> both(2 * (size_t)L.n_slots);
+        CUDA_TRY(d2h_elems(both.data(), stage, both.size(), 8, s), "state D2H");
+        std::copy(both.begin(), both.begin() + L.n_slots, xl.begin());
+        std::copy(both.begin() + L.n_slots, both.end(), lm.begin());
     }
     CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     return LOPF_OK;

@@ -297,6 +297,7 @@ struct Layout {
            off_bres = 0, off_bstop = 0, off_bgact = 0, off_bcnt = 0, off_bwpre = 0, off_bstage = 0, off_bdscr = 0;
     size_t image_bytes = 0;                // bytes of `image` uploaded by bind (0: the whole arena); the rest is
                                            // device state initialised by the reset kernels
+    size_t off_fetch = 0;                  // staging of lopf_fetch_async (result record + x as fp64), after the image
 };
 
 // Scenario batches (config 4): per-scenario operators of the subsystems that hold a load (their
@@ -353,9 +354,11 @@ int stream_block(int rmax, int esz);
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
 lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err);
 lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err);
+lopf_status launch_fetch(const DevCtrl* ctrl, const void* x, int64_t n, int esz, void* stage, void* stream, std::string& err);
 lopf_status query_grid(int rmax, int esz, int* grid, std::string& err);
 lopf_status launch_resident(const ResProblem& P, void* stream, std::string& err);
 lopf_status launch_reset_resident(const ResProblem& P, void* stream, std::string& err);
+lopf_status launch_gather_resident(const ResProblem& P, void* stage, void* stream, std::string& err);
 lopf_status resident_capacity(int* sms, int* smem_optin, std::string& err);
 // batch.cu
 int batch_block();

@@ -14,6 +14,7 @@
 // One grid barrier per sweep; no host synchronisation inside the loop.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "device.cuh"
@@ -492,7 +493,34 @@ __global__ void reset_kernel(DevProblem P) {
     }
 }
 
+// lopf_fetch_async: the result record (lopf_result layout, solve_ms = 0) and x widened to fp64 into the
+// staging area: stage[0 .. 8) = the record (64 bytes), stage[8 .. 8 + n) = x.
+template <class T>
+__global__ void fetch_kernel(const DevCtrl* c, const T* x, int64_t n, double* stage) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        lopf_result r;
+        r.outcome = c->outcome;
+        r.reserved0 = c->numeric;
+        r.iters = c->iters;
+        r.pres = c->res[0]; r.dres = c->res[1]; r.eps_prim = c->res[2]; r.eps_dual = c->res[3];
+        r.objective = c->objective;
+        r.solve_ms = 0.0;
+        *reinterpret_cast<lopf_result*>(stage) = r;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        stage[8 + i] = (double)__ldcg(x + i);
+}
+
 }  // namespace
+
+lopf_status launch_fetch(const DevCtrl* ctrl, const void* x, int64_t n, int esz, void* stage, void* stream, std::string& err) {
+    const int nb = (int)std::min<int64_t>(148, (n + 255) / 256 + 1);
+    if (esz == 4) fetch_kernel<float><<<nb, 256, 0, (cudaStream_t)stream>>>(ctrl, (const float*)x, n, (double*)stage);
+    else fetch_kernel<double><<<nb, 256, 0, (cudaStream_t)stream>>>(ctrl, (const double*)x, n, (double*)stage);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
+    return LOPF_OK;
+}
 
 template <class T>
 static const void* stream_kernel_t(int rmax) {

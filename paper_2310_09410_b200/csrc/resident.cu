@@ -451,7 +451,29 @@ __global__ void reset_resident_kernel(ResProblem P) {
     }
 }
 
+// lopf_get_state on the resident layout: every CTA blob's x_s and lambda (state at the last exit) widened
+// to fp64 into the staging area in global slot order: stage[slot] = x_s, stage[total + slot] = lambda.
+template <class T>
+__global__ void gather_resident_kernel(ResProblem P, double* stage) {
+    const CtaHdr& H = P.hdr[blockIdx.x];
+    const uint8_t* blob = P.blobs + H.blob_off;
+    const T* xl = reinterpret_cast<const T*>(blob + H.off_xl0);
+    const T* lam = reinterpret_cast<const T*>(blob + H.off_lam0);
+    for (int i = threadIdx.x; i < H.n_slots; i += blockDim.x) {
+        stage[H.slot_base + i] = (double)xl[i];
+        stage[(size_t)P.total_slots + H.slot_base + i] = (double)lam[i];
+    }
+}
+
 }  // namespace
+
+lopf_status launch_gather_resident(const ResProblem& P, void* stage, void* stream, std::string& err) {
+    if (P.esz == 4) gather_resident_kernel<float><<<P.G, 256, 0, (cudaStream_t)stream>>>(P, (double*)stage);
+    else gather_resident_kernel<double><<<P.G, 256, 0, (cudaStream_t)stream>>>(P, (double*)stage);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
+    return LOPF_OK;
+}
 
 lopf_status resident_capacity(int* sms, int* smem_optin, std::string& err) {
     int dev = 0;

@@ -50,7 +50,8 @@ class Options(C.Structure):
 class Sizes(C.Structure):
     _fields_ = [(k, _i64) for k in ("S", "n", "m", "n_copies", "p_sym", "n_tasks", "n_slots", "device_bytes",
                                     "abar_doubles", "alg_bytes")] + \
-               [(k, _i32) for k in ("kernel", "grid", "block", "max_ns", "max_ms", "n_scen")] + [("reserved", _i32 * 2)]
+               [(k, _i32) for k in ("kernel", "grid", "block", "max_ns", "max_ms", "n_scen")] + [("reserved", _i32 * 2)] + \
+               [(k, _i64) for k in ("upload_bytes", "fetch_bytes")]
 
 
 class Result(C.Structure):
@@ -84,6 +85,7 @@ def load_library(path: str = LIB_PATH):
         "lopf_run": ([H, _i64, _i32, _vp, C.POINTER(Result)], _i32),
         "lopf_solve_async": ([H, _i64, _i32, _vp], _i32),
         "lopf_result_get": ([H, _vp, C.POINTER(Result)], _i32),
+        "lopf_fetch_async": ([H, _vp, _vp], _i32),
         "lopf_get_decomposition": ([H] + [_vp] * 7, _i32),
         "lopf_get_consensus": ([H, _vp, _vp], _i32),
         "lopf_get_globals": ([H] + [_vp] * 6, _i32),
@@ -315,6 +317,21 @@ class Lopf:
     def solve_async(self, max_iter: int, test: bool = True, stream=None):
         _check(load_library().lopf_solve_async(self._h, int(max_iter), int(bool(test)), _vp(_stream_handle(stream))),
                "lopf_solve_async")
+
+    def fetch_async(self, host_buf, stream=None):
+        """lopf_fetch_async into a host buffer of sizes.fetch_bytes bytes (a pinned torch uint8 tensor for a
+        truly asynchronous copy); decode it with `Lopf.decode_fetch` after the stream has reached it."""
+        ptr = host_buf.data_ptr() if hasattr(host_buf, "data_ptr") else host_buf.ctypes.data
+        _check(load_library().lopf_fetch_async(self._h, _vp(_stream_handle(stream)), _vp(ptr)), "lopf_fetch_async")
+
+    @staticmethod
+    def decode_fetch(host_buf, n: int):
+        """(Result, x) from a buffer filled by fetch_async."""
+        raw = host_buf.numpy() if hasattr(host_buf, "numpy") else np.asarray(host_buf)
+        raw = np.ascontiguousarray(raw).view(np.uint8)
+        r = Result.from_buffer_copy(raw[: C.sizeof(Result)].tobytes())
+        x = raw[64: 64 + 8 * n].view(np.float64).copy()
+        return r, x
 
     def result_get(self, stream=None) -> Result:
         r = Result()

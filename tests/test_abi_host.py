@@ -24,7 +24,7 @@ def test_exports_every_declared_symbol():
     assert len(names) >= 20
     for n in sorted(names):
         assert hasattr(lib, n), n
-    assert lib.lopf_abi_version() == 2
+    assert lib.lopf_abi_version() == 3
 
 
 @pytest.mark.parametrize("make", [lambda: fg.make_feeder("13"), lambda: fg.make_feeder("123"), fx.four_bus,

@@ -211,3 +211,25 @@ def test_resident_race_stress(torch_cuda, shape, k):
         for part in (1, k // 3, k - 1 - k // 3):
             h.run(part)
         _check_state(h, ref)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_fetch_async_matches_getters(torch_cuda, kernel):
+    """lopf_fetch_async (one gather kernel + one copy, stream-ordered) returns the same result record and x
+    as lopf_result_get / lopf_get_state; lopf_get_state of the resident layout (one gather kernel over the
+    CTA blobs) equals the oracle's iterate."""
+    import torch
+    from paper_2310_09410_b200 import Lopf
+    f, p = _problem("123")
+    h = _solver(f, kernel=kernel)
+    h.solve_async(333, False)
+    buf = torch.empty(int(h.sizes.fetch_bytes), dtype=torch.uint8, pin_memory=True)
+    h.fetch_async(buf)
+    torch.cuda.synchronize()
+    r, x = Lopf.decode_fetch(buf, int(h.sizes.n))
+    r2 = h.result_get()
+    assert (r.iters, r.outcome) == (r2.iters, r2.outcome) == (333, 2)
+    assert (r.pres, r.dres, r.objective) == (r2.pres, r2.dres, r2.objective)
+    xs, xl, lam = h.get_state()
+    assert np.array_equal(x, xs)
+    _check_state(h, oracle.run_k(p, 333))
