@@ -99,6 +99,15 @@ typedef struct {
     int32_t precision;     /* 0 or 64: fp64 (the parity path); 32: fp32 operators, iterate and arithmetic — the
                               paper's GPU precision (reading F1).  Residual sums,
                               the termination test and the objective stay fp64.  All three kernels. */
+    int32_t adapt_every;   /* 0: fixed rho (the paper's Algorithm 1).  k > 0: residual balancing (PAPER.md:394,
+                              DESIGN.md reading F2) — after a sweep t that fails the test with t % k == 0,
+                              rho <- adapt_tau rho if pres > adapt_mu dres, rho <- rho / adapt_tau if
+                              dres > adapt_mu pres.  Abar_s, bbar_s are rho-free, so only the scalar
+                              changes, on the device, with no host round trip.  Streaming kernel only (kernel 0 picks
+                              it; kernel 2, batch and partitioned handles are LOPF_E_ARG). */
+    int32_t reserved2;
+    double adapt_mu;       /* > 1 (0 = default 10) */
+    double adapt_tau;      /* > 1 (0 = default 2) */
 } lopf_options;
 
 typedef struct {
@@ -211,6 +220,10 @@ lopf_status lopf_result_get(lopf_handle *h, void *cuda_stream, lopf_result *res)
  * doubles in canonical order.  The caller waits on its own event / stream before reading host_buf.
  * LOPF_E_STATE on batch and partitioned handles (use lopf_get_batch_results / lopf_result_get). */
 lopf_status lopf_fetch_async(lopf_handle *h, void *cuda_stream, void *host_buf);
+
+/* The penalty in force on the device (the fixed rho, or the residual-balancing one after the last solve)
+ * and the number of changes since the last reset / bind. */
+lopf_status lopf_get_rho(lopf_handle *h, void *cuda_stream, double *rho, int64_t *changes);
 
 /* Canonical decomposition: kind (0 BUS, 1 LINE, 2 LEAF), comp (bus or line index),
  * leaf_bus (-1 unless LEAF), m_s, n_s [S]; sub_ptr [S+1] copy offsets; copy_global [n_copies]. */

@@ -25,4 +25,4 @@ the comparison with Table V's iteration counts (needs the real IEEE feeders).
 from .lp import assemble_lp, LP  # noqa: F401
 from .decompose import decompose, Decomposition  # noqa: F401
 from .precompute import precompute, row_rank_reduce  # noqa: F401
-from .admm import OracleProblem, build_problem, initial_state, solve, run_k, solve_f32, run_k_f32  # noqa: F401
+from .admm import OracleProblem, build_problem, initial_state, solve, run_k, solve_f32, run_k_f32, solve_adaptive  # noqa: F401

@@ -99,6 +99,9 @@ def lib():
         _lib.oracle_residuals.argtypes = [P, vp, vp, vp, vp, vp]
         _lib.oracle_run.argtypes = [P, vp, vp, vp, C.c_int64, C.c_int32, vp, vp, vp, C.c_int64, C.c_int32, vp]
         _lib.oracle_run.restype = C.c_int64
+        _lib.oracle_run_adaptive.argtypes = [P, vp, vp, vp, C.c_int64, C.c_int32, vp, vp, C.c_int32, C.c_double,
+                                             C.c_double, vp, vp]
+        _lib.oracle_run_adaptive.restype = C.c_int64
         _lib.oracle_run_f32.argtypes = [C.POINTER(_ProblemF32), vp, vp, vp, C.c_int64, C.c_int32, vp, vp]
         _lib.oracle_run_f32.restype = C.c_int64
     return _lib
@@ -263,6 +266,26 @@ def run_k(prob: OracleProblem, k: int, state=None) -> OracleResult:
     """Exactly k sweeps with the test disabled (fixed-K parity)."""
     xl, lam = state if state is not None else initial_state(prob)
     return _run(prob, xl, lam, k, False)
+
+
+# ---- residual balancing (SURVEY f2, PAPER.md:394; DESIGN.md reading F2) ---------------------------------
+def solve_adaptive(prob: OracleProblem, every: int = 10, mu: float = 10.0, tau: float = 2.0, max_iter: int = 1_000_000,
+                   test: bool = True, state=None):
+    """Algorithm 1 with residual balancing of rho every `every` sweeps (oracle_run_adaptive in admm_loop.c).
+    Returns (OracleResult, final rho, number of rho changes).  test=False: exactly max_iter sweeps."""
+    xl, lam = state if state is not None else initial_state(prob)
+    x = np.zeros(prob.n)
+    xl = np.array(xl, dtype=np.float64, copy=True)
+    lam = np.array(lam, dtype=np.float64, copy=True)
+    res = np.zeros(4)
+    conv = C.c_int32(0)
+    rho = C.c_double(0.0)
+    nch = C.c_int64(0)
+    k = lib().oracle_run_adaptive(C.byref(prob._st), _p(x), _p(xl), _p(lam), int(max_iter), int(bool(test)), _p(res),
+                                  C.byref(conv), int(every), float(mu), float(tau), C.byref(rho), C.byref(nch))
+    r = OracleResult(converged=bool(conv.value), iters=int(k), x=x, x_loc=xl, lam=lam, pres=res[0], dres=res[1],
+                     eps_prim=res[2], eps_dual=res[3], objective=float(prob.lp.c @ x), trace=np.zeros((0, 4)))
+    return r, rho.value, nch.value
 
 
 # ---- fp32 variant (PAPER.md:414, 499-501; DESIGN.md reading F1) ---------------------------------------

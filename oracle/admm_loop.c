@@ -145,6 +145,42 @@ int64_t oracle_run(const oracle_problem *p, double *x, double *xl, double *lam, 
     return t;
 }
 
+/* ---- residual balancing ("residual balancing [wohlberg2017admm]") ----------
+ * Algorithm 1 with the penalty adapted by the residual-balancing rule of Boyd et al. (2011) §3.4.1 /
+ * Wohlberg (2017): after the test of sweep t has failed, and if t is a multiple of `every`,
+ *     rho <- tau rho   if pres > mu dres,      rho <- rho / tau   if dres > mu pres,
+ * and rho is unchanged otherwise.  lambda is the unscaled multiplier, so nothing else is
+ * rescaled, and Abar_s, bbar_s contain no rho: only the scalar changes.  Sweep t uses
+ * the rho in force when it starts everywhere (u = x_s - lambda/rho and c/rho of closed_1, d = -rho v -
+ * lambda and the 1/rho of closed_2, ADMM-3, and dres = rho ||x_s - x_s_old||).  rho_out: the final rho. */
+int64_t oracle_run_adaptive(const oracle_problem *p, double *x, double *xl, double *lam, int64_t max_iter,
+                            int32_t test, double *res, int32_t *converged, int32_t every, double mu, double tau,
+                            double *rho_out, int64_t *n_changes)
+{
+    double *xl_old = (double *)malloc(sizeof(double) * (size_t)(p->nc > 0 ? p->nc : 1));
+    oracle_problem q = *p;
+    int64_t t = 0, nch = 0;
+    *converged = 0;
+    res[0] = res[1] = res[2] = res[3] = 0.0;
+    while (t < max_iter) {
+        memcpy(xl_old, xl, sizeof(double) * (size_t)p->nc);
+        oracle_global_update(&q, xl, lam, x);
+        oracle_local_update(&q, x, lam, xl);
+        oracle_dual_update(&q, x, xl, lam);
+        ++t;
+        oracle_residuals(&q, x, xl, xl_old, lam, res);
+        if (test && res[0] <= res[2] && res[1] <= res[3]) { *converged = 1; break; }
+        if (every > 0 && (t % every) == 0) {
+            if (res[0] > mu * res[1]) { q.rho = tau * q.rho; ++nch; }
+            else if (res[1] > mu * res[0]) { q.rho = q.rho / tau; ++nch; }
+        }
+    }
+    *rho_out = q.rho;
+    *n_changes = nch;
+    free(xl_old);
+    return t;
+}
+
 /* ---- fp32 variant (the paper's GPU precision; reading F1) --------
  * The same Algorithm 1 with every datum of the iteration in binary32: Abar_s, bbar_s, c, lo, hi, rho
  * and the initial point are the fp64 values rounded once to nearest (IEEE +-inf stays +-inf), and every

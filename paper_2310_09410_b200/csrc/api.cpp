@@ -107,6 +107,9 @@ static lopf_status check_precision(const lopf_options& o) {
         return fail(LOPF_E_ARG, "block_threads must be 0 (block sizes are fixed per kernel; see lopf_sizes.block)");
     if (o.reserved[1] != 0)
         return fail(LOPF_E_ARG, "options.reserved[1] must be 0 (the phase-skip diagnostics are a build flag, LOPF_DIAG_SKIP)");
+    if (o.adapt_every < 0) return fail(LOPF_E_ARG, "adapt_every must be >= 0");
+    if (o.adapt_every > 0 && ((o.adapt_mu != 0 && !(o.adapt_mu > 1)) || (o.adapt_tau != 0 && !(o.adapt_tau > 1))))
+        return fail(LOPF_E_ARG, "residual balancing needs adapt_mu > 1 and adapt_tau > 1");
     return LOPF_OK;
 }
 
@@ -156,6 +159,11 @@ lopf_status lopf_setup(const lopf_network* net, const lopf_options* opt, lopf_ha
     try {
         lopf_status st = copy_network(net, h->net, err);
         if (st == LOPF_OK) st = build_canon(h->net, h->opt, h->cp, err);
+        if (st == LOPF_OK && h->opt.adapt_every > 0) {
+            if (h->opt.adapt_mu == 0) h->opt.adapt_mu = 10.0;
+            if (h->opt.adapt_tau == 0) h->opt.adapt_tau = 2.0;
+            if (h->opt.kernel == 2) { st = LOPF_E_ARG; err = "residual balancing (adapt_every > 0) runs on the streaming kernel"; }
+        }
         if (st == LOPF_OK) {
             if (h->opt.kernel == 2) {
                 st = pack_resident(h->net, h->cp, h->opt, h->lay, err);
@@ -163,7 +171,7 @@ lopf_status lopf_setup(const lopf_network* net, const lopf_options* opt, lopf_ha
                 st = pack_streaming(h->net, h->cp, h->opt, kMaxGrid, h->lay, err);
             } else {                                      // auto: operators on chip when they fit (fp64)
                 std::string e2;
-                st = pack_resident(h->net, h->cp, h->opt, h->lay, e2);
+                st = h->opt.adapt_every > 0 ? LOPF_E_ARG : pack_resident(h->net, h->cp, h->opt, h->lay, e2);
                 if (st != LOPF_OK) st = pack_streaming(h->net, h->cp, h->opt, kMaxGrid, h->lay, err);
             }
         }
@@ -191,6 +199,7 @@ lopf_status lopf_setup_batch(const lopf_network* net, const lopf_options* opt, i
     if (!(o.eps_rel > 0) || !std::isfinite(o.eps_rel)) return fail(LOPF_E_ARG, "eps_rel must be > 0 (SPEC.md:186)");
     if (o.max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
     if (n_scen <= 0 || !load_scale) return fail(LOPF_E_ARG, "n_scen must be > 0 with a load_scale array");
+    if (o.adapt_every != 0) return fail(LOPF_E_ARG, "residual balancing is not available on batch handles");
     if (n_scen > kBatchMaxScen)
         return fail(LOPF_E_ARG, "n_scen > " + std::to_string(kBatchMaxScen) + " per handle: shard the scenarios");
     if (check_precision(o) != LOPF_OK) return LOPF_E_ARG;
@@ -227,6 +236,7 @@ lopf_status lopf_setup_part(const lopf_network* net, const lopf_options* opt, in
     if (!(o.eps_rel > 0) || !std::isfinite(o.eps_rel)) return fail(LOPF_E_ARG, "eps_rel must be > 0 (SPEC.md:186)");
     if (o.max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
     if (world < 1 || rank < 0 || rank >= world) return fail(LOPF_E_ARG, "need 0 <= rank < world");
+    if (o.adapt_every != 0) return fail(LOPF_E_ARG, "residual balancing is not available on partitioned handles");
     if (check_precision(o) != LOPF_OK) return LOPF_E_ARG;
     lopf_handle* h = new (std::nothrow) lopf_handle();
     if (!h) return fail(LOPF_E_ARG, "out of host memory");
@@ -493,6 +503,9 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     P.rho = h->opt.rho;
     P.inv_rho = 1.0 / h->opt.rho;
     P.eps_rel = h->opt.eps_rel;
+    P.adapt_every = h->opt.adapt_every;
+    P.adapt_mu = h->opt.adapt_mu;
+    P.adapt_tau = h->opt.adapt_tau;
     P.part = L.part; P.rank = L.rank; P.world = L.world; P.n_bnd = L.n_bnd;
     P.n_imp = L.n_imp; P.ghost0 = L.ghost0;
     P.xbuf = L.part ? (double*)(b + L.off_xbuf) : nullptr;
@@ -604,6 +617,22 @@ lopf_status lopf_result_get(lopf_handle* h, void* stream, lopf_result* res) {
     else cudaGetLastError();
     if (c.numeric) return fail(LOPF_E_NUMERIC, "non-finite residual sum detected on the device at sweep " +
                                                    std::to_string(c.iters));
+    return LOPF_OK;
+}
+
+lopf_status lopf_get_rho(lopf_handle* h, void* stream, double* rho, int64_t* changes) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->bound) return fail(LOPF_E_STATE, "get_rho before lopf_bind");
+    if (h->opt.adapt_every == 0 || h->resident() || h->batch()) {
+        if (rho) *rho = h->opt.rho;
+        if (changes) *changes = 0;
+        return LOPF_OK;
+    }
+    DevCtrl c;
+    CUDA_TRY(cudaMemcpyAsync(&c, h->dp.ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost, (cudaStream_t)stream), "rho D2H");
+    CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream), "cudaStreamSynchronize");
+    if (rho) *rho = c.rho_cur;
+    if (changes) *changes = c.rho_changes;
     return LOPF_OK;
 }
 

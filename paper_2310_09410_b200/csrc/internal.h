@@ -90,7 +90,10 @@ struct DevCtrl {                           // 256 B, device-resident control blo
     double objective;
     long long trace_rows;
     long long stopped;                     // partitioned mode: the termination test has fired
-    double pad[18];
+    double rho_cur;                        // residual balancing (F2): the penalty in force
+    long long rho_changes;                 // ... and how often it changed since the reset
+    unsigned long long arrive2;            // second barrier counter (u re-formed after a rho change)
+    double pad[15];
 };
 
 // Per-slot metadata of the streaming / batch layouts, one 24-byte record (one bulk copy per task):
@@ -130,6 +133,8 @@ struct DevProblem {                        // kernel argument (pointers into the
     int32_t n_obj, trace_cap, trace_every, test;
     double rho, inv_rho, eps_rel;
     long long max_iter;
+    int32_t adapt_every, pad_a;            // residual balancing every k sweeps (0 = fixed rho; F2)
+    double adapt_mu, adapt_tau;
     // partitioned mode (config 5): one sweep per launch, exchange through `xbuf`
     int32_t part, rank, world, n_bnd;      // n_bnd boundary-copy slots, then world x 8 residual slots
     double* xbuf;

@@ -102,9 +102,10 @@ __device__ __forceinline__ void issue_task(const DevProblem& P, Stage& st, const
 // a4 for one slot: the global's consensus value from the ping-pong copies (closed_1, rho restored)
 template <class T>
 __device__ __forceinline__ T consensus(const DevProblem& P, const int inf, const int g, const int4 nb,
-                                       const T* __restrict__ ucur, const T* __restrict__ inv_nu) {
+                                       const T* __restrict__ ucur, const T* __restrict__ inv_nu, const T rho) {
     const vec2_t<T> bd = __ldg(reinterpret_cast<const vec2_t<T>*>(P.gbnd) + g);        // {lo, hi}
-    const T cr = (inf & kInfoCost) ? __ldg(reinterpret_cast<const T*>(P.gcost) + g) : T(0);   // c / rho
+    T cr = (inf & kInfoCost) ? __ldg(reinterpret_cast<const T*>(P.gcost) + g) : T(0);   // c / rho
+    if (P.adapt_every) cr = cr / rho;                                   // adaptive rho: gcost holds c
     T sigma, inv;
     if (inf & kInfoInline) {                               // nu <= 4: neighbour slots inline
         const int nu = (inf >> kInfoNuShift) & 0xF;
@@ -132,8 +133,7 @@ __device__ __forceinline__ T consensus(const DevProblem& P, const int inf, const
 template <class T>
 __device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, const int slot, const T ax, const T bb,
                                             const T v, const T lam, const T xo, T* __restrict__ unext,
-                                            double (&acc)[5], const bool val = true) {
-    const T rho = (T)P.rho, inv_rho = (T)P.inv_rho;
+                                            double (&acc)[5], const T rho, const T inv_rho, const bool val = true) {
     const T xn = fma(ax, inv_rho, bb);                                 // (1/rho) Abar d + bbar
     const T ln = lam + rho * (v - xn);                                 // ADMM-3
     const T un = xn - ln * inv_rho;                                    // next consensus input
@@ -158,7 +158,8 @@ __device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, 
 template <int R, class T, int SRC>
 __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, const T* __restrict__ ucur,
                                             T* __restrict__ unext, double (&acc)[5], const int lane,
-                                            T* __restrict__ dsm, Stage& st, const T* __restrict__ inv_nu) {
+                                            T* __restrict__ dsm, Stage& st, const T* __restrict__ inv_nu,
+                                            const T rho, const T inv_rho) {
     constexpr int kStageBytes = Stg<T>::kBytes;
     const int b = st.consumed & 1;
     mbar_wait(st.bar + b, (st.consumed >> 1) & 1);
@@ -170,7 +171,6 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
     const bool direct = SRC == 1 || (SRC == 0 && (tr.w & kTaskDirect));
     const T* S = direct ? reinterpret_cast<const T*>(P.abar) + tr.y : reinterpret_cast<const T*>(sb);
     const int used = (tr.w >> kTaskUsedShift) & 0xFF;       // stage entries past `used` are stale
-    const T rho = (T)P.rho;
     T v[R], ax[R];
     int info[R];
     // a4, split so that every gather of both halves is in flight before the first is consumed
@@ -195,6 +195,7 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
         lo[h] = bd.x;
         hi[h] = bd.y;
         cr[h] = val && (info[h] & kInfoCost) ? __ldg(reinterpret_cast<const T*>(P.gcost) + g[h]) : T(0);
+        if (P.adapt_every) cr[h] = cr[h] / rho;                     // adaptive rho: gcost holds c
     }
 #pragma unroll
     for (int h = 0; h < R; ++h) {      // branch-free for the inline case (absent entries are exact zeros)
@@ -245,7 +246,7 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
         const T bb = (info[h] & kInfoBbar)
                          ? S[((unsigned)info[h] >> kInfoPoffShift) + ns[h] * (ns[h] + 1) / 2 + r[h]] : T(0);
         finish_slot<T>(P, info[h], tr.x + j, ax[h], bb, v[h], val ? s_lam[j] : T(0), val ? s_xl[j] : T(0), unext,
-                       acc, val);
+                       acc, rho, inv_rho, val);
     }
     __syncwarp();
 }
@@ -255,9 +256,9 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
 template <int R, class T>
 __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, const T* __restrict__ ucur,
                                           T* __restrict__ unext, double (&acc)[5], const int lane,
-                                          T* __restrict__ dsm, const T* __restrict__ inv_nu) {
+                                          T* __restrict__ dsm, const T* __restrict__ inv_nu, const T rho,
+                                          const T inv_rho) {
     const T* lamp = reinterpret_cast<const T*>(P.lam);
-    const T rho = (T)P.rho;
     T v[R], ax[R];
     int info[R];
 #pragma unroll
@@ -269,7 +270,7 @@ __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, co
         if (info[h] & kInfoValid) {
             const int2 n01 = __ldg(&P.s_meta[slot].n01), n23 = __ldg(&P.s_meta[slot].n23);
             v[h] = consensus<T>(P, info[h], __ldg(&P.s_meta[slot].g), make_int4(n01.x, n01.y, n23.x, n23.y), ucur,
-                                inv_nu);
+                                inv_nu, rho);
             d = -rho * v[h] - lamp[slot];
         }
         dsm[h * 32 + lane] = d;
@@ -287,7 +288,8 @@ __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, co
         if (!(info[h] & kInfoValid)) continue;
         const int slot = tr.x + h * 32 + lane;
         const T bb = (info[h] & kInfoBbar) ? __ldg(reinterpret_cast<const T*>(P.s_bbar) + slot) : T(0);
-        finish_slot<T>(P, info[h], slot, ax[h], bb, v[h], lamp[slot], reinterpret_cast<const T*>(P.xl)[slot], unext, acc);
+        finish_slot<T>(P, info[h], slot, ax[h], bb, v[h], lamp[slot], reinterpret_cast<const T*>(P.xl)[slot], unext, acc,
+                       rho, inv_rho);
     }
     __syncwarp();
 }
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
     __shared__ double red[kWarps][5];
     __shared__ uint64_t sbar[kWarps][2];
     __shared__ T inv_nu[kInvNu];
-    __shared__ int s_stop;
+    __shared__ int s_stop, s_chg;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
     Stage st{sdyn + (size_t)wid * 2 * kStageBytes, sbar[wid], 0u, 0u};
@@ -320,6 +322,10 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
     if (P.part && *(volatile long long*)&P.ctrl->stopped) return;      // partitioned: decided, no more sweeps
     const long long total0 = *(volatile long long*)&P.ctrl->total;
     const int4 tr0 = gw < P.n_tasks ? __ldg(P.tasks + gw) : make_int4(0, 0, 0, 0);
+    // the penalty in force: fixed, or (residual balancing, F2) the device copy in the control block
+    double rho_d = P.adapt_every ? *(volatile double*)&P.ctrl->rho_cur : P.rho;
+    T rho = (T)rho_d, inv_rho = P.adapt_every ? (T)(1.0 / rho_d) : (T)P.inv_rho;
+    unsigned long long bars2 = 0;
     long long it = 0;
     if (P.max_iter > 0) issue_task<T>(P, st, tr0, lane, false);
     while (it < P.max_iter) {
@@ -335,17 +341,17 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
             if (tr.w & kTaskPacked) {
                 const bool dir = tr.w & kTaskDirect;
                 if ((tr.w & 0xF) == 1) {
-                    if (dir) task_packed<1, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
-                    else task_packed<1, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
+                    if (dir) task_packed<1, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho);
+                    else task_packed<1, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho);
                 } else if constexpr (RMAX >= 2) {
-                    if (dir) task_packed<2, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
-                    else task_packed<2, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu);
+                    if (dir) task_packed<2, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho);
+                    else task_packed<2, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho);
                 }
             } else {
                 switch (tr.w & 0xF) {
-                    case 2: if constexpr (RMAX >= 2) task_full<2, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
-                    case 4: if constexpr (RMAX >= 4) task_full<4, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
-                    default: if constexpr (RMAX >= 8) task_full<8, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu); break;
+                    case 2: if constexpr (RMAX >= 2) task_full<2, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho); break;
+                    case 4: if constexpr (RMAX >= 4) task_full<4, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho); break;
+                    default: if constexpr (RMAX >= 8) task_full<8, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho); break;
                 }
             }
             tr = tr1;
@@ -387,15 +393,27 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
                     double* rs = P.xbuf + P.n_bnd + (size_t)P.rank * 8;   // the import kernel decides
                     for (int k = 0; k < 5; ++k) rs[k] = s[k];
                     __threadfence();
-                    st_release_u64(&P.ctrl->flag, ((unsigned long long)it << 2));
+                    st_release_u64(&P.ctrl->flag, ((unsigned long long)it << 3));
                     s_stop = 0;
+                    s_chg = 0;
                 } else if (lane == 0) {
-                    const double pres = sqrt(s[0]), dres = P.rho * sqrt(s[1]);
+                    const double pres = sqrt(s[0]), dres = rho_d * sqrt(s[1]);
                     const double ep = P.eps_rel * fmax(sqrt(s[2]), sqrt(s[3])), ed = P.eps_rel * sqrt(s[4]);
                     const int numeric = !(isfinite(s[0]) && isfinite(s[1]) && isfinite(s[2]) && isfinite(s[3]) && isfinite(s[4]));
                     const int conv = P.test && (pres <= ep) && (dres <= ed);
                     const int stop = conv || numeric;
                     DevCtrl* c = P.ctrl;
+                    int chg = 0;                               // residual balancing (F2): rho of the next sweep
+                    if (P.adapt_every && !stop && it < P.max_iter && ((total0 + it) % P.adapt_every) == 0) {
+                        double rn = rho_d;
+                        if (pres > P.adapt_mu * dres) rn = P.adapt_tau * rho_d;
+                        else if (dres > P.adapt_mu * pres) rn = rho_d / P.adapt_tau;
+                        if (rn != rho_d) {
+                            c->rho_cur = rn;
+                            c->rho_changes = c->rho_changes + 1;
+                            chg = 1;
+                        }
+                    }
                     if (P.trace_every > 0 && (it % P.trace_every) == 0) {
                         const long long row = it / P.trace_every - 1;
                         if (row < P.trace_cap) {
@@ -416,19 +434,31 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
                         c->numeric = numeric;
                     }
                     __threadfence();
-                    st_release_u64(&c->flag, ((unsigned long long)it << 2) | ((unsigned long long)stop << 1) |
-                                                 (unsigned long long)numeric);
+                    st_release_u64(&c->flag, ((unsigned long long)it << 3) | ((unsigned long long)chg << 2) |
+                                                 ((unsigned long long)stop << 1) | (unsigned long long)numeric);
                     s_stop = stop;
+                    s_chg = chg;
                 }
             } else if (lane == 0) {
                 unsigned long long f;
-                while (((f = ld_acquire_u64(&P.ctrl->flag)) >> 2) < (unsigned long long)it) __nanosleep(32);
+                while (((f = ld_acquire_u64(&P.ctrl->flag)) >> 3) < (unsigned long long)it) __nanosleep(32);
                 s_stop = (int)((f >> 1) & 1);
+                s_chg = (int)((f >> 2) & 1);
                 __threadfence();
             }
         }
         __syncthreads();
         if (s_stop) break;
+        if (s_chg) {        // rho changed: every u of the next sweep's buffer re-formed with it, then a barrier
+            rho_d = *(volatile double*)&P.ctrl->rho_cur;
+            rho = (T)rho_d;
+            inv_rho = (T)(1.0 / rho_d);
+            const T* xlp = reinterpret_cast<const T*>(P.xl);
+            const T* lmp = reinterpret_cast<const T*>(P.lam);
+            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_slots; i += gridDim.x * blockDim.x)
+                unext[i] = __ldcg(xlp + i) - __ldcg(lmp + i) * inv_rho;
+            dev::grid_sync(&P.ctrl->arrive2, (++bars2) * gridDim.x);
+        }
     }
     while (st.consumed < st.issued) {                          // drain the prefetch of a sweep not run
         mbar_wait(st.bar + (st.consumed & 1), (st.consumed >> 1) & 1);
@@ -490,6 +520,8 @@ __global__ void reset_kernel(DevProblem P) {
     if (i == 0) {
         P.ctrl->arrive = 0; P.ctrl->flag = 0; P.ctrl->total = 0; P.ctrl->iters = 0; P.ctrl->trace_rows = 0;
         P.ctrl->stopped = 0;
+        P.ctrl->rho_cur = P.rho;
+        P.ctrl->rho_changes = 0;
     }
 }
 
@@ -560,6 +592,7 @@ lopf_status query_grid(int rmax, int esz, int* grid, std::string& err) {
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(P.ctrl, 0, 2 * sizeof(unsigned long long), s);   // arrive, flag
+    if (e == cudaSuccess) e = cudaMemsetAsync(&P.ctrl->arrive2, 0, sizeof(unsigned long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(&P.ctrl->trace_rows, 0, sizeof(long long), s);
     if (e == cudaSuccess && P.max_iter > 0) {
         DevProblem Q = P;

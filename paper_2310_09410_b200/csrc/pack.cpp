@@ -263,11 +263,12 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     for (int64_t i = 0; i < P.n; ++i) {
         put(gbnd, 2 * i, P.lo[i]);
         put(gbnd, 2 * i + 1, P.hi[i]);
-        put(gcost, i, P.c[i] / opt.rho);
+        put(gcost, i, opt.adapt_every > 0 ? P.c[i] : P.c[i] / opt.rho);   // adaptive rho: c, divided on device
     }
     std::memcpy(at(L.off_objidx), obj_idx.data(), 4 * obj_idx.size());
     std::memcpy(at(L.off_objc), obj_c.data(), 8 * obj_c.size());
     init_state_image(P, L);
+    reinterpret_cast<DevCtrl*>(L.image.data() + L.off_ctrl)->rho_cur = opt.rho;   // the penalty in force at bind
     return LOPF_OK;
 }
 

@@ -44,7 +44,8 @@ class Network(C.Structure):
 class Options(C.Structure):
     _fields_ = [("rho", _f64), ("eps_rel", _f64), ("max_iter", _i64), ("trace_every", _i32), ("trace_cap", _i32),
                 ("single", _i32), ("kernel", _i32), ("block_threads", _i32), ("max_ctas", _i32), ("grid_cap", _i32),
-                ("reserved", _i32 * 2), ("precision", _i32)]
+                ("reserved", _i32 * 2), ("precision", _i32), ("adapt_every", _i32), ("reserved2", _i32),
+                ("adapt_mu", _f64), ("adapt_tau", _f64)]
 
 
 class Sizes(C.Structure):
@@ -86,6 +87,7 @@ def load_library(path: str = LIB_PATH):
         "lopf_solve_async": ([H, _i64, _i32, _vp], _i32),
         "lopf_result_get": ([H, _vp, C.POINTER(Result)], _i32),
         "lopf_fetch_async": ([H, _vp, _vp], _i32),
+        "lopf_get_rho": ([H, _vp, _vp, _vp], _i32),
         "lopf_get_decomposition": ([H] + [_vp] * 7, _i32),
         "lopf_get_consensus": ([H, _vp, _vp], _i32),
         "lopf_get_globals": ([H] + [_vp] * 6, _i32),
@@ -175,8 +177,9 @@ class Lopf:
     def setup(cls, feeder, rho: float = 100.0, eps_rel: float = 1e-3, max_iter: int = 1_000_000,
               trace_every: int = 0, trace_cap: int = 4096, single: bool = False, kernel: int = 0,
               grid_cap: int = 0, max_ctas: int = 0, diag_profile: bool = False,
-              precision: int = 64) -> "Lopf":
-        """lopf_setup; precision 32 selects the fp32 variant (the paper's GPU precision)."""
+              precision: int = 64, adapt_every: int = 0, adapt_mu: float = 0.0, adapt_tau: float = 0.0) -> "Lopf":
+        """lopf_setup; precision 32 selects the fp32 variant (the paper's GPU precision, PAPER.md:414);
+        adapt_every > 0 enables residual balancing of rho (reading F2)."""
         lib = load_library()
         o = Options()
         _check(lib.lopf_options_default(C.byref(o)), "lopf_options_default")
@@ -185,6 +188,7 @@ class Lopf:
         o.grid_cap, o.max_ctas = int(grid_cap), int(max_ctas)
         o.reserved[0] = int(bool(diag_profile))
         o.precision = int(precision)
+        o.adapt_every, o.adapt_mu, o.adapt_tau = int(adapt_every), float(adapt_mu), float(adapt_tau)
         net, keep = _network(feeder)
         h = _vp()
         _check(lib.lopf_setup(C.byref(net), C.byref(o), C.byref(h)), "lopf_setup")
@@ -317,6 +321,12 @@ class Lopf:
     def solve_async(self, max_iter: int, test: bool = True, stream=None):
         _check(load_library().lopf_solve_async(self._h, int(max_iter), int(bool(test)), _vp(_stream_handle(stream))),
                "lopf_solve_async")
+
+    def get_rho(self, stream=None):
+        """(rho in force, number of residual-balancing changes since the reset)."""
+        r, n = _f64(0.0), _i64(0)
+        _check(load_library().lopf_get_rho(self._h, _vp(_stream_handle(stream)), C.byref(r), C.byref(n)), "lopf_get_rho")
+        return r.value, n.value
 
     def fetch_async(self, host_buf, stream=None):
         """lopf_fetch_async into a host buffer of sizes.fetch_bytes bytes (a pinned torch uint8 tensor for a
