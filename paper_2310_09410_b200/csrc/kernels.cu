@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
                     const int stop = conv || numeric;
                     DevCtrl* c = P.ctrl;
                     int chg = 0;                               // residual balancing (F2): rho of the next sweep
-                    if (P.adapt_every && !stop && it < P.max_iter && ((total0 + it) % P.adapt_every) == 0) {
+                    if (P.adapt_every && !stop && ((total0 + it) % P.adapt_every) == 0) {
                         double rn = rho_d;
                         if (pres > P.adapt_mu * dres) rn = P.adapt_tau * rho_d;
                         else if (dres > P.adapt_mu * pres) rn = rho_d / P.adapt_tau;
