@@ -309,7 +309,7 @@ SHAPES = {
                   load_a=(0.0005, 0.002), n_extra3=0, delta_frac=0.0, n_caps=8),
 }
 
-SEEDS = {"13": 13, "123": 123, "8500": 8500}
+SEEDS = {"13": 13, "37": 37, "123": 123, "8500": 8500}
 
 
 def _sym3(rng, self_lo, self_hi, mut_lo, mut_hi):
@@ -477,10 +477,62 @@ def _add_load(fb: FeederBuilder, rng, bus: int, phases: int, conn: int, shape: S
     fb.load(bus, phases, conn, alpha, beta, a, b)
 
 
+def make_delta37(seed: int = 37) -> Feeder:
+    """IEEE37-shaped (Table II-IV column 2): a 3-wire, 3-phase feeder whose loads are all
+    delta-connected (VDLM-4 and VDLM-6..10).  Radial tree (reading C14) of 57 buses and
+    56 lines with exactly 16 leaves, so S = 57 + 56 - 16 = 97 (Table III); 30 three-phase delta loads (the 16
+    leaves and 14 internal buses) give sum m_s = 6 * 57 + 9 * 56 + 12 * 30 = 1206 rows (Table II, IV).
+    A trunk from the substation with 15 side branches (lengths multinomial), a regulator tap on the first
+    line, no capacitors, alpha, beta in {0, 1, 2}, a ~ U[0.01, 0.05], b = a tan(acos pf)."""
+    rng = np.random.default_rng(seed)
+    fb = FeederBuilder("ieee37-shaped")
+    root = fb.bus(ALL3, wmin=0.9025, wmax=1.1025)
+    fb.root = root
+    fb.gen(root, ALL3, -10.0, 10.0, -10.0, 10.0)
+    n_leaf, n_nodes = 16, 56
+    lengths = 1 + rng.multinomial(n_nodes - n_leaf, np.full(n_leaf, 1.0 / n_leaf))   # trunk + 15 branches
+    shape = Shape(n3=n_nodes, n1=0, n_lat=0, window=1, r3=(0.002, 0.008), r1=(0.004, 0.016), load_a=(0.01, 0.05),
+                  n_extra3=14, delta_frac=1.0, n_caps=0)
+
+    def line(par, b):
+        r = _sym3(rng, *shape.r3, 0.25, 0.4)
+        x = _sym3(rng, 2.0 * shape.r3[0], 3.0 * shape.r3[1], 0.35, 0.5)
+        fb.line(par, b, ALL3, r, x)
+
+    trunk, prev = [], root
+    for _ in range(int(lengths[0])):
+        b = fb.bus(ALL3)
+        line(prev, b)
+        trunk.append(b)
+        prev = b
+    leaves = [trunk[-1]]
+    internal = list(trunk[:-1])
+    for li in range(1, n_leaf):
+        prev = trunk[int(rng.integers(len(trunk) - 1))] if len(trunk) > 1 else root
+        for k in range(int(lengths[li])):
+            b = fb.bus(ALL3)
+            line(prev, b)
+            if k < lengths[li] - 1:
+                internal.append(b)
+            prev = b
+        leaves.append(prev)
+    tau = 0.98 if rng.uniform() < 0.5 else 1.02
+    fb.lines[0]["tau"] = [tau, tau, tau]
+    for b in leaves:
+        _add_load(fb, rng, b, ALL3, DELTA, shape)
+    for b in rng.choice(internal, shape.n_extra3, replace=False):
+        _add_load(fb, rng, int(b), ALL3, DELTA, shape)
+    f = fb.build()
+    f.meta = dict(shape="37", seed=seed)
+    return f
+
+
 def make_feeder(shape: str, seed: int | None = None) -> Feeder:
-    """The synthetic instance for configs 1-3 (shape '13', '123', '8500')."""
+    """The synthetic instance for configs 1-3 (shape '13', '123', '8500') and the IEEE37-shaped delta feeder."""
     if seed is None:
         seed = SEEDS[shape]
+    if shape == "37":
+        return make_delta37(seed)
     return make_radial(SHAPES[shape], seed, f"ieee{shape}-shaped")
 
 

@@ -105,7 +105,10 @@ typedef struct {
                               dres > adapt_mu pres.  Abar_s, bbar_s are rho-free, so only the scalar
                               changes, on the device, with no host round trip.  Streaming kernel only (kernel 0 picks
                               it; kernel 2, batch and partitioned handles are LOPF_E_ARG). */
-    int32_t reserved2;
+    int32_t coarse;        /* 0 / 1: component-wise subsystems.  B > 1: the coarse-partition regime
+                              (closed form for any S >= 1): consecutive runs of B
+                              component subsystems in depth-first order merged into one larger subsystem (kind 3,
+                              DESIGN.md reading C25).  n_s up to 256 (larger is LOPF_E_ARG at pack time). */
     double adapt_mu;       /* > 1 (0 = default 10) */
     double adapt_tau;      /* > 1 (0 = default 2) */
 } lopf_options;
@@ -225,7 +228,7 @@ lopf_status lopf_fetch_async(lopf_handle *h, void *cuda_stream, void *host_buf);
  * and the number of changes since the last reset / bind. */
 lopf_status lopf_get_rho(lopf_handle *h, void *cuda_stream, double *rho, int64_t *changes);
 
-/* Canonical decomposition: kind (0 BUS, 1 LINE, 2 LEAF), comp (bus or line index),
+/* Canonical decomposition: kind (0 BUS, 1 LINE, 2 LEAF, 3 COARSE run), comp (bus or line index, run index),
  * leaf_bus (-1 unless LEAF), m_s, n_s [S]; sub_ptr [S+1] copy offsets; copy_global [n_copies]. */
 lopf_status lopf_get_decomposition(const lopf_handle *h, int32_t *kind, int32_t *comp, int32_t *leaf_bus,
                                    int32_t *m_s, int32_t *n_s, int64_t *sub_ptr, int32_t *copy_global);

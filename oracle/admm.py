@@ -170,11 +170,11 @@ class OracleProblem:
 
 
 def build_problem(f: Feeder, rho: float = 100.0, eps_rel: float = 1e-3, single: bool = False,
-                  lp: LP | None = None) -> OracleProblem:
-    """LP (PAPER.md:206-227) -> decomposition (PAPER.md:441-445) -> precompute (PAPER.md:374-380).
-    Defaults rho = 100, eps_rel = 1e-3."""
+                  lp: LP | None = None, coarse: int = 0) -> OracleProblem:
+    """LP -> decomposition (coarse runs: reading C25) -> precompute
+    (PAPER.md:374-380).  Defaults rho = 100, eps_rel = 1e-3."""
     lp = lp if lp is not None else assemble_lp(f)
-    dec = decompose(f, lp, single=single)
+    dec = decompose(f, lp, single=single, coarse=coarse)
     ab, bb = [], []
     for s in range(dec.S):
         a, b = precompute(dec.A[s], dec.b[s])

@@ -21,7 +21,7 @@ import numpy as np
 from feedergen import Feeder
 from .lp import LP
 
-BUS, LINE, LEAF = 0, 1, 2
+BUS, LINE, LEAF, COARSE = 0, 1, 2, 3
 
 
 class DecompositionError(ValueError):
@@ -70,9 +70,73 @@ def leaves_of(f: Feeder) -> np.ndarray:
     return leaf
 
 
-def decompose(f: Feeder, lp: LP, single: bool = False) -> Decomposition:
+def dfs_components(f: Feeder, kinds, comps, leafb) -> list:
+    """Component subsystems in depth-first order from the root bus (reading C25): the root's subsystem, then
+    for each bus its incident lines in ascending index, each line's subsystem followed by the subtree behind
+    it (the far bus's subsystem first).  A LEAF subsystem (line + leaf bus) appears once."""
+    sub_of_bus, sub_of_line = {}, {}
+    for s, (k, c, lb) in enumerate(zip(kinds, comps, leafb)):
+        if k == BUS:
+            sub_of_bus[c] = s
+        else:
+            sub_of_line[c] = s
+            if k == LEAF:
+                sub_of_bus[lb] = s
+    adj = {i: [] for i in range(f.n_bus)}
+    for e in range(f.n_line):
+        adj[int(f.line_from[e])].append(e)
+        adj[int(f.line_to[e])].append(e)
+    order, seen_sub, seen_bus = [], set(), set()
+
+    def emit(s):
+        if s is not None and s not in seen_sub:
+            seen_sub.add(s)
+            order.append(s)
+
+    def visit(b):                                   # iterative DFS, explicit stack of (bus, next line position)
+        seen_bus.add(b)
+        emit(sub_of_bus.get(b))
+        stack = [[b, 0]]
+        while stack:
+            top = stack[-1]
+            lines = sorted(adj[top[0]])
+            if top[1] >= len(lines):
+                stack.pop()
+                continue
+            e = lines[top[1]]
+            top[1] += 1
+            o = int(f.line_to[e]) if int(f.line_from[e]) == top[0] else int(f.line_from[e])
+            emit(sub_of_line.get(e))
+            if o not in seen_bus:
+                seen_bus.add(o)
+                emit(sub_of_bus.get(o))
+                stack.append([o, 0])
+
+    visit(f.root_bus)
+    for b in range(f.n_bus):
+        if b not in seen_bus:
+            visit(b)
+    for s in range(len(kinds)):
+        emit(s)
+    return order
+
+
+def decompose(f: Feeder, lp: LP, single: bool = False, coarse: int = 0) -> Decomposition:
     """Component-wise decomposition with leaf merging; `single=True`
-    gives the S = 1 partition (all rows in one subsystem)."""
+    gives the S = 1 partition (all rows in one subsystem); `coarse=B` merges
+    consecutive runs of B component subsystems in depth-first order into one larger subsystem (the
+    coarse-partition regime of PAPER.md:245, 399-402, still closed-form for any S >= 1 (PAPER.md:63);
+    reading C25).  A coarse subsystem holds its members' rows in that order; kind COARSE, comp = run index."""
+    if coarse and coarse > 1 and not single:
+        base = decompose(f, lp)
+        order = dfs_components(f, list(base.kind), list(base.comp), list(base.leaf_bus))
+        runs = [order[i:i + coarse] for i in range(0, len(order), coarse)]
+        rows = [[r for s in run for r in base.rows[s]] for run in runs]
+        return _assemble(lp, [COARSE] * len(runs), list(range(len(runs))), [-1] * len(runs), rows)
+    return _component(f, lp, single)
+
+
+def _component(f: Feeder, lp: LP, single: bool) -> Decomposition:
     leaf = leaves_of(f)
     line_of_leaf = {}
     for e in range(f.n_line):
@@ -121,6 +185,12 @@ def decompose(f: Feeder, lp: LP, single: bool = False) -> Decomposition:
                 rows[s] = ([r for r in rows[s] if lp.rows[r].owner[0] == "line"]
                            + [r for r in rows[s] if lp.rows[r].owner[0] == "bus"])
 
+    return _assemble(lp, kinds, comps, leafb, rows)
+
+
+def _assemble(lp: LP, kinds, comps, leafb, rows) -> Decomposition:
+    """I_s = ascending columns touched by the rows of s (C11); dense A_s, b_s; copies; CSR; nu; orphans."""
+    S = len(kinds)
     cols, As, bs = [], [], []
     for s in range(S):
         touched = set()

@@ -108,6 +108,7 @@ static lopf_status check_precision(const lopf_options& o) {
     if (o.reserved[1] != 0)
         return fail(LOPF_E_ARG, "options.reserved[1] must be 0 (the phase-skip diagnostics are a build flag, LOPF_DIAG_SKIP)");
     if (o.adapt_every < 0) return fail(LOPF_E_ARG, "adapt_every must be >= 0");
+    if (o.coarse < 0) return fail(LOPF_E_ARG, "coarse must be >= 0");
     if (o.adapt_every > 0 && ((o.adapt_mu != 0 && !(o.adapt_mu > 1)) || (o.adapt_tau != 0 && !(o.adapt_tau > 1))))
         return fail(LOPF_E_ARG, "residual balancing needs adapt_mu > 1 and adapt_tau > 1");
     return LOPF_OK;
@@ -200,6 +201,7 @@ lopf_status lopf_setup_batch(const lopf_network* net, const lopf_options* opt, i
     if (o.max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
     if (n_scen <= 0 || !load_scale) return fail(LOPF_E_ARG, "n_scen must be > 0 with a load_scale array");
     if (o.adapt_every != 0) return fail(LOPF_E_ARG, "residual balancing is not available on batch handles");
+    if (o.coarse > 1) return fail(LOPF_E_ARG, "coarse partitions are not available on batch handles");
     if (n_scen > kBatchMaxScen)
         return fail(LOPF_E_ARG, "n_scen > " + std::to_string(kBatchMaxScen) + " per handle: shard the scenarios");
     if (check_precision(o) != LOPF_OK) return LOPF_E_ARG;
@@ -237,6 +239,7 @@ lopf_status lopf_setup_part(const lopf_network* net, const lopf_options* opt, in
     if (o.max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
     if (world < 1 || rank < 0 || rank >= world) return fail(LOPF_E_ARG, "need 0 <= rank < world");
     if (o.adapt_every != 0) return fail(LOPF_E_ARG, "residual balancing is not available on partitioned handles");
+    if (o.coarse > 1) return fail(LOPF_E_ARG, "coarse partitions are not available on partitioned handles");
     if (check_precision(o) != LOPF_OK) return LOPF_E_ARG;
     lopf_handle* h = new (std::nothrow) lopf_handle();
     if (!h) return fail(LOPF_E_ARG, "out of host memory");

@@ -17,7 +17,7 @@
 namespace lopf {
 
 enum Role : int8_t { PG = 0, QG, W, PB, QB, PD, QD, PF, QF, PT, QT };
-enum Kind : int32_t { BUS = 0, LINE = 1, LEAF = 2 };
+enum Kind : int32_t { BUS = 0, LINE = 1, LEAF = 2, COARSE = 3 };
 
 struct Var {
     int8_t role;

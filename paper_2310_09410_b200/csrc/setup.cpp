@@ -517,6 +517,23 @@ lopf_status build_canon(const Net& N, const lopf_options& opt, Canon& P, std::st
         }
     }
     P.S = (int64_t)P.kind.size();
+    // coarse partition (reading C25): consecutive runs of opt.coarse component
+    // subsystems in depth-first order become one subsystem holding their rows in that order
+    std::vector<std::vector<int64_t>> members;
+    std::vector<int32_t> ckind = P.kind, ccomp = P.comp, cleaf = P.leaf;
+    if (!opt.single && opt.coarse > 1) {
+        const std::vector<int64_t> order = dfs_order(N, P);
+        for (size_t i = 0; i < order.size(); i += (size_t)opt.coarse)
+            members.emplace_back(order.begin() + i, order.begin() + std::min(order.size(), i + (size_t)opt.coarse));
+        const int64_t S2 = (int64_t)members.size();
+        P.kind.assign(S2, COARSE);
+        P.comp.resize(S2);
+        for (int64_t s = 0; s < S2; ++s) P.comp[s] = (int32_t)s;
+        P.leaf.assign(S2, -1);
+        P.S = S2;
+    } else {
+        for (int64_t s = 0; s < P.S; ++s) members.push_back({s});
+    }
 
     // ---- per subsystem: rows, structural columns, dense A_s, b_s -----------------------------------
     std::vector<std::vector<RowB>> rows(P.S);
@@ -529,11 +546,15 @@ lopf_status build_canon(const Net& N, const lopf_options& opt, Canon& P, std::st
             for (int e = 0; e < N.n_line; ++e) B.line_rows(e, R);
             for (int i = 0; i < N.n_bus; ++i) B.bus_cols(i, Cs);
             for (int e = 0; e < N.n_line; ++e) B.line_cols(e, Cs);
-        } else if (P.kind[s] == BUS) {
-            B.bus_rows(P.comp[s], R); B.bus_cols(P.comp[s], Cs);
         } else {
-            B.line_rows(P.comp[s], R); B.line_cols(P.comp[s], Cs);
-            if (P.kind[s] == LEAF) { B.bus_rows(P.leaf[s], R); B.bus_cols(P.leaf[s], Cs); }
+            for (int64_t c : members[s]) {
+                if (ckind[c] == BUS) {
+                    B.bus_rows(ccomp[c], R); B.bus_cols(ccomp[c], Cs);
+                } else {
+                    B.line_rows(ccomp[c], R); B.line_cols(ccomp[c], Cs);
+                    if (ckind[c] == LEAF) { B.bus_rows(cleaf[c], R); B.bus_cols(cleaf[c], Cs); }
+                }
+            }
         }
         std::sort(Cs.begin(), Cs.end());
         Cs.erase(std::unique(Cs.begin(), Cs.end()), Cs.end());
@@ -604,7 +625,8 @@ lopf_status build_canon(const Net& N, const lopf_options& opt, Canon& P, std::st
     for (int64_t s = 0; s < P.S; ++s) {
         if (outs[s].status != 0) {
             std::string who = "subsystem " + std::to_string(s) + " (" +
-                              (P.kind[s] == BUS ? "bus " : P.kind[s] == LINE ? "line " : "leaf line ") +
+                              (P.kind[s] == BUS ? "bus " : P.kind[s] == LINE ? "line " : P.kind[s] == LEAF ? "leaf line "
+                                                                                                       : "coarse run ") +
                               std::to_string(P.comp[s]) + ")";
             if (outs[s].status == -1) { err = who + ": row references a column outside its structural set"; return LOPF_E_NETWORK; }
             err = who + (outs[s].status == LOPF_E_RANK ? ": A_s A_s^T is singular after row reduction"

@@ -44,7 +44,7 @@ class Network(C.Structure):
 class Options(C.Structure):
     _fields_ = [("rho", _f64), ("eps_rel", _f64), ("max_iter", _i64), ("trace_every", _i32), ("trace_cap", _i32),
                 ("single", _i32), ("kernel", _i32), ("block_threads", _i32), ("max_ctas", _i32), ("grid_cap", _i32),
-                ("reserved", _i32 * 2), ("precision", _i32), ("adapt_every", _i32), ("reserved2", _i32),
+                ("reserved", _i32 * 2), ("precision", _i32), ("adapt_every", _i32), ("coarse", _i32),
                 ("adapt_mu", _f64), ("adapt_tau", _f64)]
 
 
@@ -177,7 +177,8 @@ class Lopf:
     def setup(cls, feeder, rho: float = 100.0, eps_rel: float = 1e-3, max_iter: int = 1_000_000,
               trace_every: int = 0, trace_cap: int = 4096, single: bool = False, kernel: int = 0,
               grid_cap: int = 0, max_ctas: int = 0, diag_profile: bool = False,
-              precision: int = 64, adapt_every: int = 0, adapt_mu: float = 0.0, adapt_tau: float = 0.0) -> "Lopf":
+              precision: int = 64, adapt_every: int = 0, adapt_mu: float = 0.0, adapt_tau: float = 0.0,
+              coarse: int = 0) -> "Lopf":
         """lopf_setup; precision 32 selects the fp32 variant (the paper's GPU precision, PAPER.md:414);
         adapt_every > 0 enables residual balancing of rho (reading F2)."""
         lib = load_library()
@@ -189,6 +190,7 @@ class Lopf:
         o.reserved[0] = int(bool(diag_profile))
         o.precision = int(precision)
         o.adapt_every, o.adapt_mu, o.adapt_tau = int(adapt_every), float(adapt_mu), float(adapt_tau)
+        o.coarse = int(coarse)
         net, keep = _network(feeder)
         h = _vp()
         _check(lib.lopf_setup(C.byref(net), C.byref(o), C.byref(h)), "lopf_setup")

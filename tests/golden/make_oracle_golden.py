@@ -14,7 +14,7 @@ import feedergen as fg  # noqa: E402
 import oracle  # noqa: E402
 
 out = {"_note": "written by tests/golden/make_oracle_golden.py from oracle/ only", "configs": {}}
-CASES = {"13": lambda: fg.make_feeder("13"), "123": lambda: fg.make_feeder("123"),
+CASES = {"13": lambda: fg.make_feeder("13"), "37": lambda: fg.make_feeder("37"), "123": lambda: fg.make_feeder("123"),
          "8500": lambda: fg.make_feeder("8500"), "s4x13": lambda: fg.make_stitched(4, "13"),
          "s2x8500": lambda: fg.make_stitched(2, "8500")}
 for shape, make in CASES.items():
