@@ -57,7 +57,7 @@ typedef enum {
     LOPF_E_INFEASIBLE_SUB = 4, /* a subsystem's equality rows are inconsistent */
     LOPF_E_RANK = 5,           /* A_s A_s^T not positive definite even after row reduction */
     LOPF_E_CUDA = 6,           /* CUDA runtime error (message has the CUDA error string) */
-    LOPF_E_NCCL = 7,           /* reserved: multi-GPU partitioned mode */
+    LOPF_E_NCCL = 7,           /* NCCL failure in the library-owned communicator (lopf_part_nccl_*) */
     LOPF_E_NUMERIC = 8,        /* non-finite residual detected on the device */
     LOPF_E_STATE = 9           /* call out of order (e.g. solve before bind) */
 } lopf_status;
@@ -195,6 +195,30 @@ lopf_status lopf_part_info(const lopf_handle *h, int64_t *xbuf_offset, int64_t *
 lopf_status lopf_part_owner(const lopf_handle *h, int32_t *bus_owner, int32_t *copy_owner, int32_t *bidx);
 lopf_status lopf_part_sweep(lopf_handle *h, void *cuda_stream);
 lopf_status lopf_part_import(lopf_handle *h, void *cuda_stream);
+
+/* ---- partitioned mode with a device-initiated exchange ----------------
+ * One persistent launch per solve and rank, no host and no collective library in the loop: the kernel
+ * stores every boundary copy's u straight into each rank's exchange buffer (peer memory over NVLink /
+ * NVSwitch), the last CTA of a rank stores the rank's five residual sums the same way and then a sweep
+ * flag into every rank's flag array (release, system scope), waits for all ranks' flags (acquire), copies
+ * its ghost slots in and takes the (termination) decision on the rank-ordered sums -- identical on every
+ * rank, iterates bit-identical to the single-GPU streaming kernel.  Exchange buffers are double-buffered
+ * by sweep parity.  Each rank: lopf_part_p2p_info -> its arena offsets; peers' buffers are mapped with
+ * lopf_ipc_export / lopf_ipc_open (CUDA IPC, same node); lopf_part_connect(peer_xbuf[world],
+ * peer_flag[world]: device pointers valid in this process, [rank] = its own); lopf_reset on every rank and a
+ * host barrier; lopf_part_solve_p2p.  lopf_result_get then reports K, residuals and this rank's objective
+ * share.  Every rank's launch must be resident at the same time (one process per GPU). */
+lopf_status lopf_part_p2p_info(const lopf_handle *h, int64_t *xbuf_offset, int64_t *flag_offset);
+lopf_status lopf_part_connect(lopf_handle *h, const uint64_t *peer_xbuf, const uint64_t *peer_flag, void *cuda_stream);
+lopf_status lopf_part_solve_p2p(lopf_handle *h, int64_t max_iter, int32_t test, void *cuda_stream);
+/* All `world` ranks (hs[q] = rank q, bound on ONE GPU) as one cooperative launch (rank q = CTAs
+ * [q g, (q+1) g)), connected through local memory: the same kernel and protocol as lopf_part_solve_p2p,
+ * for testing the multi-rank path with fewer GPUs than ranks. */
+lopf_status lopf_part_emulate(lopf_handle *const *hs, int32_t world, int64_t max_iter, int32_t test, void *cuda_stream);
+/* CUDA IPC: out [72] = the cudaIpcMemHandle of the allocation holding dev_ptr + the offset of dev_ptr in
+ * it; lopf_ipc_open maps such a record into this process (closed when h is destroyed). */
+lopf_status lopf_ipc_export(const void *dev_ptr, void *out);
+lopf_status lopf_ipc_open(lopf_handle *h, const void *in, void **dev_ptr);
 
 /* Copy the packed problem into the caller's device arena (device pointer, >= device_bytes,
  * 256-byte aligned) on `stream`, and reset the iterate to the initial point of PAPER.md:495.

@@ -27,7 +27,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         return SO
     tmp = so + f".tmp{os.getpid()}"
     cmd = [NVCC, *[f"-D{d}" for d in defines], "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-O3,-Wall",
-           "-shared", "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES, "-lpthread"]
+           "-shared", "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES, "-lpthread", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

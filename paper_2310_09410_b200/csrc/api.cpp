@@ -2,6 +2,8 @@
 // launch orchestration and canonical-order getters.  No exception crosses this boundary.
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -29,6 +31,9 @@ struct lopf_handle {
     std::vector<ScenResult> scen_res;              // host copy of the last batch results
     PartSpec part;                                 // partitioned mode (lay.part != 0)
     uint32_t epoch = 0;                            // resident launches so far (exchange tag epoch)
+    std::vector<void*> ipc_open;                   // peer allocations opened by lopf_ipc_open (closed at destroy)
+    std::vector<uint64_t> peer_tab;                // [2 world] device pointers: exchange buffers, flag arrays
+    DevProblem p2p_arg{};                          // host copy of the p2p launch argument (kept for the async H2D)
     bool resident() const { return lay.kernel == 2; }
     bool parted() const { return lay.part != 0; }
     bool batch() const { return lay.kernel == 3; }
@@ -514,6 +519,20 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     P.xbuf = L.part ? (double*)(b + L.off_xbuf) : nullptr;
     P.s_exp = L.part ? (const int32_t*)(b + L.off_sexp) : nullptr;
     P.imp = L.part ? (const int32_t*)(b + L.off_imp) : nullptr;
+    P.p2p = 0;
+    P.xpar = 0;
+    P.xstride = (int64_t)L.n_bnd + 8 * (int64_t)L.world;
+    if (L.part) {                                  // peer tables: this rank's own entries (world 1 runs as is)
+        P.peer_xb = (double* const*)(b + L.off_peer);
+        P.peer_flag = (unsigned long long* const*)(b + L.off_peer + 8 * (size_t)L.world);
+        P.my_flag = (unsigned long long*)(b + L.off_pflag);
+        std::vector<uint64_t> tab(2 * (size_t)L.world, 0);
+        tab[L.rank] = (uint64_t)(uintptr_t)P.xbuf;
+        tab[L.world + L.rank] = (uint64_t)(uintptr_t)P.my_flag;
+        h->peer_tab = tab;
+        CUDA_TRY(cudaMemcpyAsync(b + L.off_peer, h->peer_tab.data(), 8 * h->peer_tab.size(), cudaMemcpyHostToDevice,
+                                 s), "peer table H2D");
+    }
     std::string err;
     int grid = 0;
     lopf_status st = query_grid(L.rmax, L.esz, &grid, err);
@@ -535,10 +554,151 @@ lopf_status lopf_reset(lopf_handle* h, void* stream) {
     lopf_status st = h->resident() ? launch_reset_resident(h->rp, stream, err)
                      : h->batch() ? launch_reset_batch(h->bp, stream, err)
                                   : launch_reset(h->dp, stream, err);
-    if (st == LOPF_OK && h->parted())
-        CUDA_TRY(cudaMemsetAsync(h->dp.xbuf, 0, sizeof(double) * ((size_t)h->lay.n_bnd + 8 * (size_t)h->lay.world),
-                                 (cudaStream_t)stream), "exchange clear");
+    if (st == LOPF_OK && h->parted()) {            // both exchange parities and the p2p sweep flags
+        CUDA_TRY(cudaMemsetAsync(h->dp.xbuf, 0, sizeof(double) * 2 * (size_t)h->dp.xstride, (cudaStream_t)stream),
+                 "exchange clear");
+        CUDA_TRY(cudaMemsetAsync(h->dp.my_flag, 0, 8 * (size_t)h->lay.world, (cudaStream_t)stream), "flag clear");
+    }
     return st == LOPF_OK ? LOPF_OK : fail(st, err);
+}
+
+lopf_status lopf_part_p2p_info(const lopf_handle* h, int64_t* xbuf_offset, int64_t* flag_offset) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->parted()) return fail(LOPF_E_STATE, "not a partitioned handle (lopf_setup_part)");
+    if (xbuf_offset) *xbuf_offset = (int64_t)h->lay.off_xbuf;
+    if (flag_offset) *flag_offset = (int64_t)h->lay.off_pflag;
+    return LOPF_OK;
+}
+
+lopf_status lopf_part_connect(lopf_handle* h, const uint64_t* peer_xbuf, const uint64_t* peer_flag, void* stream) {
+    if (!h || !peer_xbuf || !peer_flag) return fail(LOPF_E_ARG, "NULL argument");
+    if (!h->parted() || !h->bound) return fail(LOPF_E_STATE, "lopf_part_connect needs a bound partitioned handle");
+    const int W = h->lay.world;
+    for (int q = 0; q < W; ++q) {
+        if (!peer_xbuf[q] || !peer_flag[q]) return fail(LOPF_E_ARG, "peer pointer " + std::to_string(q) + " is NULL");
+        h->peer_tab[q] = peer_xbuf[q];
+        h->peer_tab[W + q] = peer_flag[q];
+    }
+    if (h->peer_tab[h->lay.rank] != (uint64_t)(uintptr_t)h->dp.xbuf)
+        return fail(LOPF_E_ARG, "peer_xbuf[rank] must be this handle's own exchange buffer");
+    CUDA_TRY(cudaMemcpyAsync((uint8_t*)h->arena + h->lay.off_peer, h->peer_tab.data(), 8 * h->peer_tab.size(),
+                             cudaMemcpyHostToDevice, (cudaStream_t)stream), "peer table H2D");
+    return LOPF_OK;
+}
+
+static lopf_status p2p_arg(lopf_handle* h, int64_t max_iter, int32_t test) {
+    if (!h || !h->parted() || !h->bound) return fail(LOPF_E_STATE, "p2p solve needs bound partitioned handles");
+    for (int q = 0; q < h->lay.world; ++q)
+        if (!h->peer_tab[q] || !h->peer_tab[h->lay.world + q])
+            return fail(LOPF_E_STATE, "rank " + std::to_string(h->lay.rank) + " is not connected to rank " +
+                                          std::to_string(q) + " (lopf_part_connect)");
+    h->p2p_arg = h->dp;
+    h->p2p_arg.p2p = 1;
+    h->p2p_arg.max_iter = max_iter;
+    h->p2p_arg.test = test ? 1 : 0;
+    return LOPF_OK;
+}
+
+lopf_status lopf_part_solve_p2p(lopf_handle* h, int64_t max_iter, int32_t test, void* stream) {
+    if (max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
+    lopf_status st = p2p_arg(h, max_iter, test);
+    if (st != LOPF_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    DevProblem* dev = (DevProblem*)((uint8_t*)h->arena + h->lay.off_parr);
+    CUDA_TRY(cudaMemcpyAsync(dev, &h->p2p_arg, sizeof(DevProblem), cudaMemcpyHostToDevice, s), "p2p argument H2D");
+    CUDA_TRY(cudaMemsetAsync(h->dp.ctrl, 0, 2 * sizeof(unsigned long long), s), "control clear");
+    CUDA_TRY(cudaMemsetAsync(&h->dp.ctrl->trace_rows, 0, sizeof(long long), s), "control clear");
+    CUDA_TRY(cudaEventRecord(h->ev0, s), "cudaEventRecord");
+    std::string err;
+    const int g = std::min(h->grid, p2p_max_group(h->lay.rmax, h->lay.esz, 1));
+    if (max_iter > 0) {
+        st = launch_p2p(dev, 1, g, h->lay.rmax, h->lay.esz, stream, err);
+        if (st != LOPF_OK) return fail(st, err);
+    }
+    CUDA_TRY(cudaEventRecord(h->ev1, s), "cudaEventRecord");
+    return LOPF_OK;
+}
+
+lopf_status lopf_part_emulate(lopf_handle* const* hs, int32_t world, int64_t max_iter, int32_t test, void* stream) {
+    if (!hs || world < 1) return fail(LOPF_E_ARG, "need world >= 1 handles");
+    if (max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
+    std::vector<uint64_t> xb(world), fl(world);
+    int rmax = 1, esz = 0;
+    for (int q = 0; q < world; ++q) {
+        lopf_handle* h = hs[q];
+        if (!h || !h->parted() || !h->bound || h->lay.world != world || h->lay.rank != q)
+            return fail(LOPF_E_ARG, "handle " + std::to_string(q) + " is not rank " + std::to_string(q) + " of a bound " +
+                                        std::to_string(world) + "-rank partition");
+        xb[q] = (uint64_t)(uintptr_t)h->dp.xbuf;
+        fl[q] = (uint64_t)(uintptr_t)h->dp.my_flag;
+        rmax = std::max(rmax, h->lay.rmax);
+        if (esz && esz != h->lay.esz) return fail(LOPF_E_ARG, "ranks of one emulation need the same precision");
+        esz = h->lay.esz;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<DevProblem> args(world);
+    for (int q = 0; q < world; ++q) {
+        lopf_status st = lopf_part_connect(hs[q], xb.data(), fl.data(), stream);
+        if (st != LOPF_OK) return st;
+        st = p2p_arg(hs[q], max_iter, test);
+        if (st != LOPF_OK) return st;
+        args[q] = hs[q]->p2p_arg;
+        CUDA_TRY(cudaMemsetAsync(hs[q]->dp.ctrl, 0, 2 * sizeof(unsigned long long), s), "control clear");
+    }
+    DevProblem* dev = (DevProblem*)((uint8_t*)hs[0]->arena + hs[0]->lay.off_parr);   // world entries
+    hs[0]->p2p_arg = args[0];
+    CUDA_TRY(cudaMemcpyAsync(dev, args.data(), sizeof(DevProblem) * world, cudaMemcpyHostToDevice, s), "p2p arguments H2D");
+    CUDA_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");             // `args` is a temporary
+    const int g = p2p_max_group(rmax, esz, world);
+    if (g < 1) return fail(LOPF_E_CUDA, "p2p emulation: no co-resident grid");
+    std::string err;
+    if (max_iter > 0) {
+        lopf_status st = launch_p2p(dev, world, g, rmax, esz, stream, err);
+        if (st != LOPF_OK) return fail(st, err);
+    }
+    return LOPF_OK;
+}
+
+// ---- CUDA IPC of a device allocation (for lopf_part_connect across processes on one node) -------------
+// The driver's cuMemGetAddressRange gives the allocation base of an arbitrary device pointer (a torch
+// tensor lives inside a caching-allocator block); libcuda is opened at first use so the library still
+// loads on machines without a driver.
+typedef int (*cuMemGetAddressRange_t)(unsigned long long*, size_t*, unsigned long long);
+static cuMemGetAddressRange_t get_range_fn() {
+    static cuMemGetAddressRange_t fn = nullptr;
+    if (!fn) {
+        void* lib = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+        if (lib) fn = (cuMemGetAddressRange_t)dlsym(lib, "cuMemGetAddressRange_v2");
+    }
+    return fn;
+}
+
+lopf_status lopf_ipc_export(const void* dev_ptr, void* out) {
+    if (!dev_ptr || !out) return fail(LOPF_E_ARG, "NULL argument");
+    cuMemGetAddressRange_t fn = get_range_fn();
+    if (!fn) return fail(LOPF_E_CUDA, "libcuda.so.1 / cuMemGetAddressRange not available");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0) return fail(LOPF_E_CUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t hd;
+    CUDA_TRY(cudaIpcGetMemHandle(&hd, (void*)(uintptr_t)base), "cudaIpcGetMemHandle");
+    std::memcpy(out, &hd, sizeof(hd));
+    const int64_t off = (int64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+    std::memcpy((char*)out + sizeof(hd), &off, 8);
+    return LOPF_OK;
+}
+
+lopf_status lopf_ipc_open(lopf_handle* h, const void* in, void** dev_ptr) {
+    if (!h || !in || !dev_ptr) return fail(LOPF_E_ARG, "NULL argument");
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, in, sizeof(hd));
+    int64_t off = 0;
+    std::memcpy(&off, (const char*)in + sizeof(hd), 8);
+    void* base = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    h->ipc_open.push_back(base);
+    *dev_ptr = (char*)base + off;
+    return LOPF_OK;
 }
 
 lopf_status lopf_solve_async(lopf_handle* h, int64_t max_iter, int32_t test, void* stream) {
@@ -882,6 +1042,7 @@ lopf_status lopf_get_profile(lopf_handle* h, void* stream, int64_t* buf, int64_t
 
 void lopf_destroy(lopf_handle* h) {
     if (!h) return;
+    for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
     if (h->registered) cudaHostUnregister(h->lay.image.data());
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);

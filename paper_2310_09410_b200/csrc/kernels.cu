@@ -142,7 +142,15 @@ __device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, 
         __stcs(reinterpret_cast<T*>(P.lam) + slot, ln);
         unext[slot] = un;
     }
-    if (inf & kInfoExport) __stcg(P.xbuf + __ldg(P.s_exp + slot), (double)un);   // partitioned: to the other ranks
+    if (inf & kInfoExport) {                                           // partitioned: to the other ranks
+        const int e = __ldg(P.s_exp + slot);
+        if (P.p2p) {                                                   // device-initiated: into every rank's
+            for (int q = 0; q < P.world; ++q)                          // exchange buffer of this sweep's parity
+                __stcg(P.peer_xb[q] + (size_t)P.xpar * P.xstride + e, (double)un);
+        } else {
+            __stcg(P.xbuf + e, (double)un);
+        }
+    }
     const T rr = v - xn, dx = xn - xo;
     acc[0] += (double)(rr * rr);
     acc[1] += (double)(dx * dx);
@@ -299,8 +307,24 @@ struct StreamWarps {
     static constexpr int value = RMAX > 2 ? kStreamWarpsWide : sizeof(T) == 8 ? kStreamWarpsF64 : kStreamWarpsF32;
 };
 
-template <int RMAX, class T>   // largest task width in the problem (RMAX > 2 only with n_s > 64: the S = 1 path)
-__global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stream_kernel(DevProblem P) {
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// The persistent sweep loop of the streaming kernel for CTA `cta` of `ncta` (one rank's grid).  P2P: the
+// partitioned mode with a device-initiated exchange: boundary copies' u go
+// straight into every rank's exchange buffer (peer memory over NVLink, or local memory when the ranks are
+// emulated on one GPU), the last CTA of each rank publishes the rank's residual sums the same way and a
+// per-rank sweep flag, waits for every rank's flag, copies its ghosts in and takes the (termination)
+// decision on the rank-ordered sums -- one launch per solve, no host, no NCCL.  `Pm` is writable (P2P: the
+// CTA's shared copy, whose exchange parity is updated per sweep).
+template <int RMAX, class T, bool P2P>
+__device__ __forceinline__ void stream_body(const DevProblem& P, DevProblem* Pm, const int cta, const int ncta) {
     constexpr int kWarps = StreamWarps<RMAX, T>::value;
     constexpr int kStageBytes = Stg<T>::kBytes;
     extern __shared__ __align__(128) char sdyn[];      // [kWarps][2][kStageBytes] stages, [kWarps][32*RMAX] d
@@ -309,7 +333,7 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
     __shared__ T inv_nu[kInvNu];
     __shared__ int s_stop, s_chg;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
+    const int gw = cta * kWarps + wid, nw = ncta * kWarps;
     Stage st{sdyn + (size_t)wid * 2 * kStageBytes, sbar[wid], 0u, 0u};
     T* dsm = reinterpret_cast<T*>(sdyn + (size_t)kWarps * 2 * kStageBytes) + (size_t)wid * 32 * RMAX;
     for (int i = threadIdx.x; i < kInvNu; i += blockDim.x) inv_nu[i] = i > 0 ? T(1) / (T)i : T(0);
@@ -319,7 +343,7 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (P.part && *(volatile long long*)&P.ctrl->stopped) return;      // partitioned: decided, no more sweeps
+    if (!P2P && P.part && *(volatile long long*)&P.ctrl->stopped) return;   // partitioned: decided, no more sweeps
     const long long total0 = *(volatile long long*)&P.ctrl->total;
     const int4 tr0 = gw < P.n_tasks ? __ldg(P.tasks + gw) : make_int4(0, 0, 0, 0);
     // the penalty in force: fixed, or (residual balancing, F2) the device copy in the control block
@@ -332,6 +356,10 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
         const long long t = total0 + it;
         const T* ucur = reinterpret_cast<const T*>((t & 1) ? P.u1 : P.u0);
         T* unext = reinterpret_cast<T*>((t & 1) ? P.u0 : P.u1);
+        if (P2P) {                                         // exchange parity of this sweep (read by finish_slot)
+            if (threadIdx.x == 0) Pm->xpar = (int)(t & 1);
+            __syncthreads();
+        }
         double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         int4 tr = tr0;
         int4 tr1 = gw + nw < P.n_tasks ? __ldg(P.tasks + gw + nw) : make_int4(0, 0, 0, 0);
@@ -372,24 +400,48 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
                 double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
                 for (int w = 0; w < kWarps; ++w)
                     for (int k = 0; k < 5; ++k) s[k] += red[w][k];
-                double* part = P.partial + (size_t)blockIdx.x * 8;
+                double* part = P.partial + (size_t)cta * 8;
                 for (int k = 0; k < 5; ++k) part[k] = s[k];
-                __threadfence();
+                if (P2P) __threadfence_system();               // this CTA's exports visible to the other ranks
+                else __threadfence();
                 const unsigned long long old = atomicAdd(&P.ctrl->arrive, 1ULL);
-                last = (old + 1 == (unsigned long long)it * gridDim.x);
+                last = (old + 1 == (unsigned long long)it * ncta);
             }
             last = __shfl_sync(kFull, last, 0);
             if (last) {                                        // reduce partials in block order
                 __threadfence();
                 double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-                for (int b = lane; b < (int)gridDim.x; b += 32)
+                for (int b = lane; b < ncta; b += 32)
                     for (int k = 0; k < 5; ++k) s[k] += __ldcg(P.partial + (size_t)b * 8 + k);
 #pragma unroll
                 for (int k = 0; k < 5; ++k) {
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) s[k] += __shfl_xor_sync(kFull, s[k], off);
                 }
-                if (lane == 0 && P.part) {             // partitioned: this rank's sums go to the exchange;
+                if (P2P) {
+                    // this rank's sums into every rank's buffer, then its flag "sweep t done" to every rank;
+                    // wait for all ranks' flags; ghosts in; the rank-ordered sums are then identical everywhere
+                    const size_t xo = (size_t)(t & 1) * P.xstride;
+                    if (lane < P.world) {
+                        double* rs = P.peer_xb[lane] + xo + P.n_bnd + (size_t)P.rank * 8;
+                        for (int k = 0; k < 5; ++k) rs[k] = s[k];
+                    }
+                    __syncwarp();
+                    __threadfence_system();
+                    if (lane < P.world) st_release_sys_u64(P.peer_flag[lane] + P.rank, (unsigned long long)(t + 1));
+                    if (lane < P.world)
+                        while (ld_acquire_sys_u64(P.my_flag + lane) < (unsigned long long)(t + 1)) {
+                        }
+                    __syncwarp();
+                    __threadfence();
+                    const double* xb = P.xbuf + xo;                 // this rank's buffer (P.xbuf = peer_xb[rank])
+                    for (int i = lane; i < P.n_imp; i += 32) unext[P.ghost0 + i] = (T)__ldcg(xb + __ldg(P.imp + i));
+                    for (int k = 0; k < 5; ++k) s[k] = 0.0;
+                    for (int r = 0; r < P.world; ++r)
+                        for (int k = 0; k < 5; ++k) s[k] += __ldcg(xb + P.n_bnd + (size_t)r * 8 + k);
+                    __syncwarp();
+                }
+                if (lane == 0 && P.part && !P2P) {             // partitioned: this rank's sums go to the exchange;
                     double* rs = P.xbuf + P.n_bnd + (size_t)P.rank * 8;   // the import kernel decides
                     for (int k = 0; k < 5; ++k) rs[k] = s[k];
                     __threadfence();
@@ -455,15 +507,34 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stre
             inv_rho = (T)(1.0 / rho_d);
             const T* xlp = reinterpret_cast<const T*>(P.xl);
             const T* lmp = reinterpret_cast<const T*>(P.lam);
-            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_slots; i += gridDim.x * blockDim.x)
+            for (int i = cta * blockDim.x + threadIdx.x; i < P.n_slots; i += ncta * blockDim.x)
                 unext[i] = __ldcg(xlp + i) - __ldcg(lmp + i) * inv_rho;
-            dev::grid_sync(&P.ctrl->arrive2, (++bars2) * gridDim.x);
+            dev::grid_sync(&P.ctrl->arrive2, (++bars2) * ncta);
         }
     }
     while (st.consumed < st.issued) {                          // drain the prefetch of a sweep not run
         mbar_wait(st.bar + (st.consumed & 1), (st.consumed >> 1) & 1);
         ++st.consumed;
     }
+}
+
+template <int RMAX, class T>   // largest task width in the problem (RMAX > 2 only with n_s > 64: the S = 1 path)
+__global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stream_kernel(DevProblem P) {
+    stream_body<RMAX, T, false>(P, nullptr, blockIdx.x, gridDim.x);
+}
+
+// Partitioned mode with the device-initiated exchange: CTA b runs rank (b / gsize)'s share; one rank per
+// GPU (gridDim = gsize), or every rank of an emulation on one GPU in one cooperative launch.
+template <int RMAX, class T>
+__global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_p2p_kernel(const DevProblem* parr, int gsize) {
+    __shared__ __align__(16) DevProblem sP;
+    {
+        const int* src = reinterpret_cast<const int*>(parr + blockIdx.x / gsize);
+        int* dst = reinterpret_cast<int*>(&sP);
+        for (int i = threadIdx.x; i < (int)(sizeof(DevProblem) / 4); i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    stream_body<RMAX, T, true>(sP, &sP, blockIdx.x % gsize, gsize);
 }
 
 // Partitioned mode, after the exchange-buffer allreduce of sweep t: the other ranks' boundary u into
@@ -604,6 +675,42 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
     return LOPF_OK;
 }
 
+
+template <class T>
+static const void* p2p_kernel_t(int rmax) {
+    return rmax <= 1 ? (const void*)admm_p2p_kernel<1, T>
+         : rmax <= 2 ? (const void*)admm_p2p_kernel<2, T>
+         : rmax <= 4 ? (const void*)admm_p2p_kernel<4, T>
+                     : (const void*)admm_p2p_kernel<8, T>;
+}
+
+// CTAs per rank of a p2p launch with `world_here` ranks on this GPU: every CTA of the launch co-resident
+int p2p_max_group(int rmax, int esz, int world_here) {
+    int dev = 0, sms = 0, per = 0;
+    const void* k = esz == 4 ? p2p_kernel_t<float>(rmax) : p2p_kernel_t<double>(rmax);
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem(rmax, esz)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, stream_block(rmax, esz), stream_smem(rmax, esz)) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return sms * per / world_here;
+}
+
+lopf_status launch_p2p(const DevProblem* parr_dev, int world_here, int gsize, int rmax, int esz, void* stream,
+                       std::string& err) {
+    const void* k = esz == 4 ? p2p_kernel_t<float>(rmax) : p2p_kernel_t<double>(rmax);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem(rmax, esz));
+    if (e == cudaSuccess) {
+        const DevProblem* a0 = parr_dev;
+        int g = gsize;
+        void* args[] = {&a0, &g};
+        e = cudaLaunchCooperativeKernel(k, dim3(world_here * gsize), dim3(stream_block(rmax, esz)), args,
+                                        stream_smem(rmax, esz), (cudaStream_t)stream);
+    }
+    if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
+    return LOPF_OK;
+}
 
 lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err) {
     const int nb = P.n_imp > 0 ? (P.n_imp + 255) / 256 : 1;

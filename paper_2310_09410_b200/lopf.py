@@ -106,6 +106,12 @@ def load_library(path: str = LIB_PATH):
         "lopf_part_owner": ([H, _vp, _vp, _vp], _i32),
         "lopf_part_sweep": ([H, _vp], _i32),
         "lopf_part_import": ([H, _vp], _i32),
+        "lopf_part_p2p_info": ([H, _vp, _vp], _i32),
+        "lopf_part_connect": ([H, _vp, _vp, _vp], _i32),
+        "lopf_part_solve_p2p": ([H, _i64, _i32, _vp], _i32),
+        "lopf_part_emulate": ([_vp, _i32, _i64, _i32, _vp], _i32),
+        "lopf_ipc_export": ([_vp, _vp], _i32),
+        "lopf_ipc_open": ([H, _vp, _vp], _i32),
         "lopf_destroy": ([H], None),
         "lopf_last_error": ([], C.c_char_p),
         "lopf_abi_version": ([], _i32),
@@ -258,6 +264,43 @@ class Lopf:
 
     def part_import(self, stream=None):
         _check(load_library().lopf_part_import(self._h, _vp(_stream_handle(stream))), "lopf_part_import")
+
+    # ---- device-initiated exchange ------------------------------------------------------------
+    def p2p_pointers(self):
+        """(exchange buffer, flag array) device addresses of this rank (valid in this process)."""
+        xo, fo = _i64(0), _i64(0)
+        _check(load_library().lopf_part_p2p_info(self._h, C.byref(xo), C.byref(fo)), "lopf_part_p2p_info")
+        base = self.arena.data_ptr()
+        return base + xo.value, base + fo.value
+
+    def part_connect(self, peer_xbuf, peer_flag, stream=None):
+        xb = np.ascontiguousarray(peer_xbuf, dtype=np.uint64)
+        fl = np.ascontiguousarray(peer_flag, dtype=np.uint64)
+        _check(load_library().lopf_part_connect(self._h, _ptr(xb), _ptr(fl), _vp(_stream_handle(stream))),
+               "lopf_part_connect")
+
+    def part_solve_p2p(self, max_iter: int, test: bool = True, stream=None):
+        _check(load_library().lopf_part_solve_p2p(self._h, int(max_iter), int(bool(test)), _vp(_stream_handle(stream))),
+               "lopf_part_solve_p2p")
+
+    @staticmethod
+    def part_emulate(handles, max_iter: int, test: bool = True, stream=None):
+        """All ranks (handles[q] = rank q, bound on this GPU) in one cooperative launch (lopf_part_emulate)."""
+        arr = (_vp * len(handles))(*[h._h.value for h in handles])
+        _check(load_library().lopf_part_emulate(arr, len(handles), int(max_iter), int(bool(test)),
+                                                _vp(_stream_handle(stream))), "lopf_part_emulate")
+
+    @staticmethod
+    def ipc_export(dev_ptr: int) -> bytes:
+        out = C.create_string_buffer(72)
+        _check(load_library().lopf_ipc_export(_vp(dev_ptr), out), "lopf_ipc_export")
+        return out.raw
+
+    def ipc_open(self, record: bytes) -> int:
+        p = _vp()
+        buf = C.create_string_buffer(bytes(record), 72)
+        _check(load_library().lopf_ipc_open(self._h, buf, C.byref(p)), "lopf_ipc_open")
+        return p.value
 
     def get_batch_results(self, stream=None) -> dict:
         ns = int(self.sizes.n_scen)

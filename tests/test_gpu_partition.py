@@ -111,3 +111,53 @@ def test_graph_captured_sweeps_with_nccl(torch_cuda):
     finally:
         if own:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("key,world,natural", [("s4x13", 2, True), ("s4x13", 4, True), ("123", 3, False),
+                                               ("s2x8500", 2, True), ("s2x8500", 4, False)])
+def test_p2p_emulation_equals_single_gpu(torch_cuda, key, world, natural):
+    """the device-initiated exchange (lopf_part_emulate: every rank's share in one cooperative
+    launch, exchanging through the same peer-store / flag protocol as one process per GPU) gives iterates
+    bit-identical to the single-GPU streaming kernel after fixed K, across launches (state, flags and
+    exchange parity carry over)."""
+    f = _feeder(key)
+    owner = fg.stitched_bus_owner(f, world) if natural else None
+    hs = _ranks(f, world, owner)
+    for h in hs:
+        h.reset()
+    single = Lopf.setup(f, kernel=1).bind("cuda")
+    done = 0
+    for k in (1, 7, 50):
+        Lopf.part_emulate(hs, k - done, test=False)
+        single.run(k - done)
+        done = k
+        for a, b in zip(_merged_state(hs), single.get_state()):
+            assert not np.isnan(a).any()
+            assert np.array_equal(a, b)
+    assert all(h.result_get().iters == 43 for h in hs)            # the last launch's sweeps
+
+
+@pytest.mark.parametrize("key,world", [("s4x13", 2), ("s2x8500", 2), ("s2x8500", 4)])
+def test_p2p_emulation_k_to_tolerance(torch_cuda, key, world):
+    f = _feeder(key)
+    g = GOLD[key]
+    hs = _ranks(f, world, fg.stitched_bus_owner(f, world) if world <= 2 else None)
+    for h in hs:
+        h.reset()
+    Lopf.part_emulate(hs, 1_000_000, test=True)
+    rs = [h.result_get() for h in hs]
+    assert all(r.outcome == CONVERGED and r.iters == g["iters"] for r in rs), [(r.outcome, r.iters) for r in rs]
+    assert abs(sum(r.objective for r in rs) - g["objective"]) <= 1e-6 * abs(g["objective"])
+    assert len({(r.pres, r.dres, r.eps_prim, r.eps_dual) for r in rs}) == 1        # one decision everywhere
+
+
+def test_p2p_single_rank_solve(torch_cuda):
+    """world = 1: lopf_part_solve_p2p runs without peers (its own tables) and equals the streaming kernel."""
+    f = _feeder("s2x8500")
+    h = Lopf.setup_part(f, 0, 1).bind("cuda")
+    h.reset()
+    h.part_solve_p2p(300, test=False)
+    s = Lopf.setup(f, kernel=1).bind("cuda")
+    s.run(300)
+    for a, b in zip(h.get_state(), s.get_state()):
+        assert np.array_equal(a, b)
