@@ -198,18 +198,20 @@ lopf_status lopf_part_import(lopf_handle *h, void *cuda_stream);
 
 /* ---- partitioned mode with a device-initiated exchange ----------------
  * One persistent launch per solve and rank, no host and no collective library in the loop: the kernel
- * stores every boundary copy's u straight into each rank's exchange buffer (peer memory over NVLink /
- * NVSwitch), the last CTA of a rank stores the rank's five residual sums the same way and then a sweep
- * flag into every rank's flag array (release, system scope), waits for all ranks' flags (acquire), copies
- * its ghost slots in and takes the (termination) decision on the rank-ordered sums -- identical on every
- * rank, iterates bit-identical to the single-GPU streaming kernel.  Exchange buffers are double-buffered
- * by sweep parity.  Each rank: lopf_part_p2p_info -> its arena offsets; peers' buffers are mapped with
- * lopf_ipc_export / lopf_ipc_open (CUDA IPC, same node); lopf_part_connect(peer_xbuf[world],
- * peer_flag[world]: device pointers valid in this process, [rank] = its own); lopf_reset on every rank and a
- * host barrier; lopf_part_solve_p2p.  lopf_result_get then reports K, residuals and this rank's objective
+ * stores every boundary copy's u as a tagged entry {u, sweep + 1} straight into each rank's entry buffer
+ * (peer memory over NVLink / NVSwitch), each entry ONE 128-bit system-scope store; the last CTA of a rank
+ * stores the rank's five residual sums the same way, then reads every rank's sums and its own ghost values,
+ * each when its tag says "this sweep", copies the ghosts in and takes the (termination) decision on the
+ * rank-ordered sums -- identical on every rank, iterates bit-identical to the single-GPU streaming kernel.
+ * No flags and no fences cross GPUs; entry buffers are double-buffered by sweep parity (a rank cannot run
+ * two sweeps ahead of a reader of its entries, because it waits for that reader's sums of the sweep in
+ * between).  Each rank: lopf_part_p2p_info -> its entry buffer (offset in the arena, bytes); peers'
+ * buffers are mapped with lopf_ipc_export / lopf_ipc_open (CUDA IPC, same node); lopf_part_connect(
+ * peer_entries[world]: device pointers valid in this process, [rank] = its own); lopf_reset on every rank
+ * and a host barrier; lopf_part_solve_p2p.  lopf_result_get reports K, residuals and this rank's objective
  * share.  Every rank's launch must be resident at the same time (one process per GPU). */
-lopf_status lopf_part_p2p_info(const lopf_handle *h, int64_t *xbuf_offset, int64_t *flag_offset);
-lopf_status lopf_part_connect(lopf_handle *h, const uint64_t *peer_xbuf, const uint64_t *peer_flag, void *cuda_stream);
+lopf_status lopf_part_p2p_info(const lopf_handle *h, int64_t *entry_offset, int64_t *entry_bytes);
+lopf_status lopf_part_connect(lopf_handle *h, const uint64_t *peer_entries, void *cuda_stream);
 lopf_status lopf_part_solve_p2p(lopf_handle *h, int64_t max_iter, int32_t test, void *cuda_stream);
 /* All `world` ranks (hs[q] = rank q, bound on ONE GPU) as one cooperative launch (rank q = CTAs
  * [q g, (q+1) g)), connected through local memory: the same kernel and protocol as lopf_part_solve_p2p,

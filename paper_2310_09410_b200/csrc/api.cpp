@@ -32,7 +32,7 @@ struct lopf_handle {
     PartSpec part;                                 // partitioned mode (lay.part != 0)
     uint32_t epoch = 0;                            // resident launches so far (exchange tag epoch)
     std::vector<void*> ipc_open;                   // peer allocations opened by lopf_ipc_open (closed at destroy)
-    std::vector<uint64_t> peer_tab;                // [2 world] device pointers: exchange buffers, flag arrays
+    std::vector<uint64_t> peer_tab;                // [world] device pointers of every rank's p2p entry buffer
     DevProblem p2p_arg{};                          // host copy of the p2p launch argument (kept for the async H2D)
     bool resident() const { return lay.kernel == 2; }
     bool parted() const { return lay.part != 0; }
@@ -520,15 +520,12 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     P.s_exp = L.part ? (const int32_t*)(b + L.off_sexp) : nullptr;
     P.imp = L.part ? (const int32_t*)(b + L.off_imp) : nullptr;
     P.p2p = 0;
-    P.xpar = 0;
     P.xstride = (int64_t)L.n_bnd + 8 * (int64_t)L.world;
-    if (L.part) {                                  // peer tables: this rank's own entries (world 1 runs as is)
-        P.peer_xb = (double* const*)(b + L.off_peer);
-        P.peer_flag = (unsigned long long* const*)(b + L.off_peer + 8 * (size_t)L.world);
-        P.my_flag = (unsigned long long*)(b + L.off_pflag);
-        std::vector<uint64_t> tab(2 * (size_t)L.world, 0);
-        tab[L.rank] = (uint64_t)(uintptr_t)P.xbuf;
-        tab[L.world + L.rank] = (uint64_t)(uintptr_t)P.my_flag;
+    if (L.part) {                                  // peer table: this rank's own entry (world 1 runs as is)
+        P.peer_xe = (double2* const*)(b + L.off_peer);
+        P.xent = (double2*)(b + L.off_xent);
+        std::vector<uint64_t> tab((size_t)L.world, 0);
+        tab[L.rank] = (uint64_t)(uintptr_t)P.xent;
         h->peer_tab = tab;
         CUDA_TRY(cudaMemcpyAsync(b + L.off_peer, h->peer_tab.data(), 8 * h->peer_tab.size(), cudaMemcpyHostToDevice,
                                  s), "peer table H2D");
@@ -555,32 +552,31 @@ lopf_status lopf_reset(lopf_handle* h, void* stream) {
                      : h->batch() ? launch_reset_batch(h->bp, stream, err)
                                   : launch_reset(h->dp, stream, err);
     if (st == LOPF_OK && h->parted()) {            // both exchange parities and the p2p sweep flags
-        CUDA_TRY(cudaMemsetAsync(h->dp.xbuf, 0, sizeof(double) * 2 * (size_t)h->dp.xstride, (cudaStream_t)stream),
+        CUDA_TRY(cudaMemsetAsync(h->dp.xbuf, 0, sizeof(double) * (size_t)h->dp.xstride, (cudaStream_t)stream),
                  "exchange clear");
-        CUDA_TRY(cudaMemsetAsync(h->dp.my_flag, 0, 8 * (size_t)h->lay.world, (cudaStream_t)stream), "flag clear");
+        CUDA_TRY(cudaMemsetAsync(h->dp.xent, 0, 16 * 2 * (size_t)h->dp.xstride, (cudaStream_t)stream), "entry clear");
     }
     return st == LOPF_OK ? LOPF_OK : fail(st, err);
 }
 
-lopf_status lopf_part_p2p_info(const lopf_handle* h, int64_t* xbuf_offset, int64_t* flag_offset) {
+lopf_status lopf_part_p2p_info(const lopf_handle* h, int64_t* entry_offset, int64_t* entry_bytes) {
     if (!h) return fail(LOPF_E_ARG, "NULL handle");
     if (!h->parted()) return fail(LOPF_E_STATE, "not a partitioned handle (lopf_setup_part)");
-    if (xbuf_offset) *xbuf_offset = (int64_t)h->lay.off_xbuf;
-    if (flag_offset) *flag_offset = (int64_t)h->lay.off_pflag;
+    if (entry_offset) *entry_offset = (int64_t)h->lay.off_xent;
+    if (entry_bytes) *entry_bytes = 16 * 2 * ((int64_t)h->lay.n_bnd + 8 * (int64_t)h->lay.world);
     return LOPF_OK;
 }
 
-lopf_status lopf_part_connect(lopf_handle* h, const uint64_t* peer_xbuf, const uint64_t* peer_flag, void* stream) {
-    if (!h || !peer_xbuf || !peer_flag) return fail(LOPF_E_ARG, "NULL argument");
+lopf_status lopf_part_connect(lopf_handle* h, const uint64_t* peer_entries, void* stream) {
+    if (!h || !peer_entries) return fail(LOPF_E_ARG, "NULL argument");
     if (!h->parted() || !h->bound) return fail(LOPF_E_STATE, "lopf_part_connect needs a bound partitioned handle");
     const int W = h->lay.world;
     for (int q = 0; q < W; ++q) {
-        if (!peer_xbuf[q] || !peer_flag[q]) return fail(LOPF_E_ARG, "peer pointer " + std::to_string(q) + " is NULL");
-        h->peer_tab[q] = peer_xbuf[q];
-        h->peer_tab[W + q] = peer_flag[q];
+        if (!peer_entries[q]) return fail(LOPF_E_ARG, "peer pointer " + std::to_string(q) + " is NULL");
+        h->peer_tab[q] = peer_entries[q];
     }
-    if (h->peer_tab[h->lay.rank] != (uint64_t)(uintptr_t)h->dp.xbuf)
-        return fail(LOPF_E_ARG, "peer_xbuf[rank] must be this handle's own exchange buffer");
+    if (h->peer_tab[h->lay.rank] != (uint64_t)(uintptr_t)h->dp.xent)
+        return fail(LOPF_E_ARG, "peer_entries[rank] must be this handle's own entry buffer");
     CUDA_TRY(cudaMemcpyAsync((uint8_t*)h->arena + h->lay.off_peer, h->peer_tab.data(), 8 * h->peer_tab.size(),
                              cudaMemcpyHostToDevice, (cudaStream_t)stream), "peer table H2D");
     return LOPF_OK;
@@ -589,7 +585,7 @@ lopf_status lopf_part_connect(lopf_handle* h, const uint64_t* peer_xbuf, const u
 static lopf_status p2p_arg(lopf_handle* h, int64_t max_iter, int32_t test) {
     if (!h || !h->parted() || !h->bound) return fail(LOPF_E_STATE, "p2p solve needs bound partitioned handles");
     for (int q = 0; q < h->lay.world; ++q)
-        if (!h->peer_tab[q] || !h->peer_tab[h->lay.world + q])
+        if (!h->peer_tab[q])
             return fail(LOPF_E_STATE, "rank " + std::to_string(h->lay.rank) + " is not connected to rank " +
                                           std::to_string(q) + " (lopf_part_connect)");
     h->p2p_arg = h->dp;
@@ -612,7 +608,7 @@ lopf_status lopf_part_solve_p2p(lopf_handle* h, int64_t max_iter, int32_t test, 
     std::string err;
     const int g = std::min(h->grid, p2p_max_group(h->lay.rmax, h->lay.esz, 1));
     if (max_iter > 0) {
-        st = launch_p2p(dev, 1, g, h->lay.rmax, h->lay.esz, stream, err);
+        st = launch_p2p(dev, &h->p2p_arg, 1, g, h->lay.rmax, h->lay.esz, stream, err);
         if (st != LOPF_OK) return fail(st, err);
     }
     CUDA_TRY(cudaEventRecord(h->ev1, s), "cudaEventRecord");
@@ -622,15 +618,14 @@ lopf_status lopf_part_solve_p2p(lopf_handle* h, int64_t max_iter, int32_t test, 
 lopf_status lopf_part_emulate(lopf_handle* const* hs, int32_t world, int64_t max_iter, int32_t test, void* stream) {
     if (!hs || world < 1) return fail(LOPF_E_ARG, "need world >= 1 handles");
     if (max_iter < 0) return fail(LOPF_E_ARG, "max_iter must be >= 0");
-    std::vector<uint64_t> xb(world), fl(world);
+    std::vector<uint64_t> xe(world);
     int rmax = 1, esz = 0;
     for (int q = 0; q < world; ++q) {
         lopf_handle* h = hs[q];
         if (!h || !h->parted() || !h->bound || h->lay.world != world || h->lay.rank != q)
             return fail(LOPF_E_ARG, "handle " + std::to_string(q) + " is not rank " + std::to_string(q) + " of a bound " +
                                         std::to_string(world) + "-rank partition");
-        xb[q] = (uint64_t)(uintptr_t)h->dp.xbuf;
-        fl[q] = (uint64_t)(uintptr_t)h->dp.my_flag;
+        xe[q] = (uint64_t)(uintptr_t)h->dp.xent;
         rmax = std::max(rmax, h->lay.rmax);
         if (esz && esz != h->lay.esz) return fail(LOPF_E_ARG, "ranks of one emulation need the same precision");
         esz = h->lay.esz;
@@ -638,7 +633,7 @@ lopf_status lopf_part_emulate(lopf_handle* const* hs, int32_t world, int64_t max
     cudaStream_t s = (cudaStream_t)stream;
     std::vector<DevProblem> args(world);
     for (int q = 0; q < world; ++q) {
-        lopf_status st = lopf_part_connect(hs[q], xb.data(), fl.data(), stream);
+        lopf_status st = lopf_part_connect(hs[q], xe.data(), stream);
         if (st != LOPF_OK) return st;
         st = p2p_arg(hs[q], max_iter, test);
         if (st != LOPF_OK) return st;
@@ -653,7 +648,7 @@ lopf_status lopf_part_emulate(lopf_handle* const* hs, int32_t world, int64_t max
     if (g < 1) return fail(LOPF_E_CUDA, "p2p emulation: no co-resident grid");
     std::string err;
     if (max_iter > 0) {
-        lopf_status st = launch_p2p(dev, world, g, rmax, esz, stream, err);
+        lopf_status st = launch_p2p(dev, nullptr, world, g, rmax, esz, stream, err);
         if (st != LOPF_OK) return fail(st, err);
     }
     return LOPF_OK;

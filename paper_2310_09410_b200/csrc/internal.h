@@ -141,12 +141,11 @@ struct DevProblem {                        // kernel argument (pointers into the
     const int32_t* s_exp;                  // [n_slots] exchange slot of an exported copy (kInfoExport)
     const int32_t* imp;                    // [n_imp] exchange slot feeding each ghost slot
     int32_t n_imp, ghost0;                 // ghost slots ghost0 .. ghost0 + n_imp - 1 (after the task slots)
-    // device-initiated exchange: every rank's exchange buffers [2][xstride] and sweep flags [world]
-    int32_t p2p, xpar;                     // xpar: parity of the sweep in flight (the CTA's shared copy)
-    int64_t xstride;                       // n_bnd + 8 world doubles per parity
-    double* const* peer_xb;                // [world] each rank's exchange buffer (this rank's at [rank])
-    unsigned long long* const* peer_flag;  // [world] each rank's flag array
-    unsigned long long* my_flag;           // [world] this rank's flags, written by the ranks
+    // device-initiated exchange: every rank's tagged exchange entries {value, sweep + 1} [2][xstride]
+    int32_t p2p, pad_p;
+    int64_t xstride;                       // n_bnd + 8 world entries per parity
+    double2* const* peer_xe;               // [world] each rank's entry buffer (this rank's at [rank])
+    double2* xent;                         // this rank's entry buffer
 };
 
 // ---- resident kernel (operators + iterate in shared memory) -----------------------------------
@@ -286,7 +285,7 @@ struct Layout {
     int32_t esz = 8;                      // streaming / batch: element size of the (T) arrays (8 fp64, 4 fp32)
     // partitioned mode
     int32_t part = 0, rank = 0, world = 1, n_bnd = 0, n_imp = 0, ghost0 = 0;
-    size_t off_sexp = 0, off_imp = 0, off_xbuf = 0, off_pflag = 0, off_peer = 0, off_parr = 0;
+    size_t off_sexp = 0, off_imp = 0, off_xbuf = 0, off_xent = 0, off_peer = 0, off_parr = 0;
     size_t off_tasks = 0, off_meta = 0, off_bbar = 0, off_xl = 0, off_lam = 0,
            off_u0 = 0, off_u1 = 0, off_x0 = 0, off_gpar = 0, off_gcost = 0, off_segptr = 0, off_segslot = 0, off_x = 0, off_abar = 0,
            off_partial = 0, off_ctrl = 0, off_trace = 0, off_objidx = 0, off_objc = 0;
@@ -365,7 +364,8 @@ int stream_block(int rmax, int esz);
 lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::string& err);
 lopf_status launch_reset(const DevProblem& P, void* stream, std::string& err);
 lopf_status launch_part_import(const DevProblem& P, void* stream, std::string& err);
-lopf_status launch_p2p(const DevProblem* parr_dev, int world_here, int gsize, int rmax, int esz, void* stream, std::string& err);
+lopf_status launch_p2p(const DevProblem* parr_dev, const DevProblem* one, int world_here, int gsize, int rmax, int esz,
+                       void* stream, std::string& err);
 int p2p_max_group(int rmax, int esz, int world_here);
 lopf_status launch_fetch(const DevCtrl* ctrl, const void* x, int64_t n, int esz, void* stage, void* stream, std::string& err);
 lopf_status query_grid(int rmax, int esz, int* grid, std::string& err);

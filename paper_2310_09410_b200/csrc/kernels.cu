@@ -99,6 +99,21 @@ __device__ __forceinline__ void issue_task(const DevProblem& P, Stage& st, const
     }
 }
 
+// A {value, tag} exchange entry, written and read as ONE 128-bit access at system scope (single-copy
+// atomic): a reader that sees the tag of sweep t also sees that sweep's value -- no fences, no flags.
+__device__ __forceinline__ void st_entry_sys(double2* p, const double v, const unsigned long long tag) {
+    asm volatile("{\n .reg .b128 x;\n mov.b128 x, {%1, %2};\n st.relaxed.sys.global.b128 [%0], x;\n}"
+                 ::"l"(p), "l"(__double_as_longlong(v)), "l"(tag) : "memory");
+}
+__device__ __forceinline__ double ld_entry_sys(const double2* p, const unsigned long long tag) {
+    unsigned long long lo, hi;
+    do {
+        asm volatile("{\n .reg .b128 x;\n ld.relaxed.sys.global.b128 x, [%2];\n mov.b128 {%0, %1}, x;\n}"
+                     : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
+    } while (hi != tag);
+    return __longlong_as_double(lo);
+}
+
 // a4 for one slot: the global's consensus value from the ping-pong copies (closed_1, rho restored)
 template <class T>
 __device__ __forceinline__ T consensus(const DevProblem& P, const int inf, const int g, const int4 nb,
@@ -133,7 +148,8 @@ __device__ __forceinline__ T consensus(const DevProblem& P, const int inf, const
 template <class T>
 __device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, const int slot, const T ax, const T bb,
                                             const T v, const T lam, const T xo, T* __restrict__ unext,
-                                            double (&acc)[5], const T rho, const T inv_rho, const bool val = true) {
+                                            double (&acc)[5], const T rho, const T inv_rho, const bool val = true,
+                                            const unsigned long long xtag = 0) {
     const T xn = fma(ax, inv_rho, bb);                                 // (1/rho) Abar d + bbar
     const T ln = lam + rho * (v - xn);                                 // ADMM-3
     const T un = xn - ln * inv_rho;                                    // next consensus input
@@ -144,9 +160,10 @@ __device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, 
     }
     if (inf & kInfoExport) {                                           // partitioned: to the other ranks
         const int e = __ldg(P.s_exp + slot);
-        if (P.p2p) {                                                   // device-initiated: into every rank's
-            for (int q = 0; q < P.world; ++q)                          // exchange buffer of this sweep's parity
-                __stcg(P.peer_xb[q] + (size_t)P.xpar * P.xstride + e, (double)un);
+        if (P.p2p) {                                                   // device-initiated: a tagged entry into
+            const size_t xo = unext == reinterpret_cast<T*>(P.u0) ? (size_t)P.xstride : 0;   // every rank's buffer
+            for (int q = 0; q < P.world; ++q)                          // of this sweep's parity (t & 1)
+                st_entry_sys(P.peer_xe[q] + xo + e, (double)un, xtag);
         } else {
             __stcg(P.xbuf + e, (double)un);
         }
@@ -167,7 +184,7 @@ template <int R, class T, int SRC>
 __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, const T* __restrict__ ucur,
                                             T* __restrict__ unext, double (&acc)[5], const int lane,
                                             T* __restrict__ dsm, Stage& st, const T* __restrict__ inv_nu,
-                                            const T rho, const T inv_rho) {
+                                            const T rho, const T inv_rho, const unsigned long long xtag) {
     constexpr int kStageBytes = Stg<T>::kBytes;
     const int b = st.consumed & 1;
     mbar_wait(st.bar + b, (st.consumed >> 1) & 1);
@@ -254,7 +271,7 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
         const T bb = (info[h] & kInfoBbar)
                          ? S[((unsigned)info[h] >> kInfoPoffShift) + ns[h] * (ns[h] + 1) / 2 + r[h]] : T(0);
         finish_slot<T>(P, info[h], tr.x + j, ax[h], bb, v[h], val ? s_lam[j] : T(0), val ? s_xl[j] : T(0), unext,
-                       acc, rho, inv_rho, val);
+                       acc, rho, inv_rho, val, xtag);
     }
     __syncwarp();
 }
@@ -265,7 +282,7 @@ template <int R, class T>
 __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, const T* __restrict__ ucur,
                                           T* __restrict__ unext, double (&acc)[5], const int lane,
                                           T* __restrict__ dsm, const T* __restrict__ inv_nu, const T rho,
-                                          const T inv_rho) {
+                                          const T inv_rho, const unsigned long long xtag) {
     const T* lamp = reinterpret_cast<const T*>(P.lam);
     T v[R], ax[R];
     int info[R];
@@ -297,7 +314,7 @@ __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, co
         const int slot = tr.x + h * 32 + lane;
         const T bb = (info[h] & kInfoBbar) ? __ldg(reinterpret_cast<const T*>(P.s_bbar) + slot) : T(0);
         finish_slot<T>(P, info[h], slot, ax[h], bb, v[h], lamp[slot], reinterpret_cast<const T*>(P.xl)[slot], unext, acc,
-                       rho, inv_rho);
+                       rho, inv_rho, true, xtag);
     }
     __syncwarp();
 }
@@ -307,24 +324,14 @@ struct StreamWarps {
     static constexpr int value = RMAX > 2 ? kStreamWarpsWide : sizeof(T) == 8 ? kStreamWarpsF64 : kStreamWarpsF32;
 };
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
 // The persistent sweep loop of the streaming kernel for CTA `cta` of `ncta` (one rank's grid).  P2P: the
 // partitioned mode with a device-initiated exchange: boundary copies' u go
-// straight into every rank's exchange buffer (peer memory over NVLink, or local memory when the ranks are
-// emulated on one GPU), the last CTA of each rank publishes the rank's residual sums the same way and a
-// per-rank sweep flag, waits for every rank's flag, copies its ghosts in and takes the (termination)
-// decision on the rank-ordered sums -- one launch per solve, no host, no NCCL.  `Pm` is writable (P2P: the
-// CTA's shared copy, whose exchange parity is updated per sweep).
+// straight into every rank's entry buffer as tagged 128-bit entries (peer memory over NVLink, or local
+// memory when the ranks are emulated on one GPU); the last CTA of each rank publishes the rank's residual
+// sums the same way, reads every rank's sums and its own ghosts when their tags say "this sweep", and
+// takes the (termination) decision on the rank-ordered sums -- one launch per solve, no host, no NCCL.
 template <int RMAX, class T, bool P2P>
-__device__ __forceinline__ void stream_body(const DevProblem& P, DevProblem* Pm, const int cta, const int ncta) {
+__device__ __forceinline__ void stream_body(const DevProblem& P, const int cta, const int ncta) {
     constexpr int kWarps = StreamWarps<RMAX, T>::value;
     constexpr int kStageBytes = Stg<T>::kBytes;
     extern __shared__ __align__(128) char sdyn[];      // [kWarps][2][kStageBytes] stages, [kWarps][32*RMAX] d
@@ -356,11 +363,8 @@ __device__ __forceinline__ void stream_body(const DevProblem& P, DevProblem* Pm,
         const long long t = total0 + it;
         const T* ucur = reinterpret_cast<const T*>((t & 1) ? P.u1 : P.u0);
         T* unext = reinterpret_cast<T*>((t & 1) ? P.u0 : P.u1);
-        if (P2P) {                                         // exchange parity of this sweep (read by finish_slot)
-            if (threadIdx.x == 0) Pm->xpar = (int)(t & 1);
-            __syncthreads();
-        }
         double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        const unsigned long long xtag = (unsigned long long)(t + 1);     // p2p exchange tag of this sweep
         int4 tr = tr0;
         int4 tr1 = gw + nw < P.n_tasks ? __ldg(P.tasks + gw + nw) : make_int4(0, 0, 0, 0);
         for (int task = gw; task < P.n_tasks; task += nw) {
@@ -369,17 +373,17 @@ __device__ __forceinline__ void stream_body(const DevProblem& P, DevProblem* Pm,
             if (tr.w & kTaskPacked) {
                 const bool dir = tr.w & kTaskDirect;
                 if ((tr.w & 0xF) == 1) {
-                    if (dir) task_packed<1, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho);
-                    else task_packed<1, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho);
+                    if (dir) task_packed<1, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
+                    else task_packed<1, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
                 } else if constexpr (RMAX >= 2) {
-                    if (dir) task_packed<2, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho);
-                    else task_packed<2, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho);
+                    if (dir) task_packed<2, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
+                    else task_packed<2, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
                 }
             } else {
                 switch (tr.w & 0xF) {
-                    case 2: if constexpr (RMAX >= 2) task_full<2, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho); break;
-                    case 4: if constexpr (RMAX >= 4) task_full<4, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho); break;
-                    default: if constexpr (RMAX >= 8) task_full<8, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho); break;
+                    case 2: if constexpr (RMAX >= 2) task_full<2, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho, xtag); break;
+                    case 4: if constexpr (RMAX >= 4) task_full<4, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho, xtag); break;
+                    default: if constexpr (RMAX >= 8) task_full<8, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho, xtag); break;
                 }
             }
             tr = tr1;
@@ -402,8 +406,7 @@ __device__ __forceinline__ void stream_body(const DevProblem& P, DevProblem* Pm,
                     for (int k = 0; k < 5; ++k) s[k] += red[w][k];
                 double* part = P.partial + (size_t)cta * 8;
                 for (int k = 0; k < 5; ++k) part[k] = s[k];
-                if (P2P) __threadfence_system();               // this CTA's exports visible to the other ranks
-                else __threadfence();
+                __threadfence();
                 const unsigned long long old = atomicAdd(&P.ctrl->arrive, 1ULL);
                 last = (old + 1 == (unsigned long long)it * ncta);
             }
@@ -418,28 +421,21 @@ __device__ __forceinline__ void stream_body(const DevProblem& P, DevProblem* Pm,
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) s[k] += __shfl_xor_sync(kFull, s[k], off);
                 }
-                if (P2P) {
-                    // this rank's sums into every rank's buffer, then its flag "sweep t done" to every rank;
-                    // wait for all ranks' flags; ghosts in; the rank-ordered sums are then identical everywhere
+                if (P2P && P.world > 1) {
+                    // this rank's five sums as tagged entries into every rank's buffer; then every rank's sums
+                    // and this rank's ghosts, each read when its tag says "sweep t" -- the rank-ordered sums
+                    // are then identical everywhere.  No flags, no fences: each entry is one 128-bit access.
                     const size_t xo = (size_t)(t & 1) * P.xstride;
-                    if (lane < P.world) {
-                        double* rs = P.peer_xb[lane] + xo + P.n_bnd + (size_t)P.rank * 8;
-                        for (int k = 0; k < 5; ++k) rs[k] = s[k];
-                    }
-                    __syncwarp();
-                    __threadfence_system();
-                    if (lane < P.world) st_release_sys_u64(P.peer_flag[lane] + P.rank, (unsigned long long)(t + 1));
-                    if (lane < P.world)
-                        while (ld_acquire_sys_u64(P.my_flag + lane) < (unsigned long long)(t + 1)) {
-                        }
-                    __syncwarp();
-                    __threadfence();
-                    const double* xb = P.xbuf + xo;                 // this rank's buffer (P.xbuf = peer_xb[rank])
-                    for (int i = lane; i < P.n_imp; i += 32) unext[P.ghost0 + i] = (T)__ldcg(xb + __ldg(P.imp + i));
+                    if (lane < 5)
+                        for (int q = 0; q < P.world; ++q)
+                            st_entry_sys(P.peer_xe[q] + xo + P.n_bnd + (size_t)P.rank * 8 + lane, s[lane], xtag);
+                    const double2* xe = P.xent + xo;                 // this rank's buffer
+                    for (int i = lane; i < P.n_imp; i += 32) unext[P.ghost0 + i] = (T)ld_entry_sys(xe + __ldg(P.imp + i), xtag);
                     for (int k = 0; k < 5; ++k) s[k] = 0.0;
                     for (int r = 0; r < P.world; ++r)
-                        for (int k = 0; k < 5; ++k) s[k] += __ldcg(xb + P.n_bnd + (size_t)r * 8 + k);
+                        for (int k = 0; k < 5; ++k) s[k] += ld_entry_sys(xe + P.n_bnd + (size_t)r * 8 + k, xtag);
                     __syncwarp();
+                    __threadfence();                                 // ghosts before the local release below
                 }
                 if (lane == 0 && P.part && !P2P) {             // partitioned: this rank's sums go to the exchange;
                     double* rs = P.xbuf + P.n_bnd + (size_t)P.rank * 8;   // the import kernel decides
@@ -520,13 +516,19 @@ __device__ __forceinline__ void stream_body(const DevProblem& P, DevProblem* Pm,
 
 template <int RMAX, class T>   // largest task width in the problem (RMAX > 2 only with n_s > 64: the S = 1 path)
 __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stream_kernel(DevProblem P) {
-    stream_body<RMAX, T, false>(P, nullptr, blockIdx.x, gridDim.x);
+    stream_body<RMAX, T, false>(P, blockIdx.x, gridDim.x);
 }
 
-// Partitioned mode with the device-initiated exchange: CTA b runs rank (b / gsize)'s share; one rank per
-// GPU (gridDim = gsize), or every rank of an emulation on one GPU in one cooperative launch.
+// Partitioned mode with the device-initiated exchange, one rank per GPU (one launch per rank).
 template <int RMAX, class T>
-__global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_p2p_kernel(const DevProblem* parr, int gsize) {
+__global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_p2p_kernel(DevProblem P) {
+    stream_body<RMAX, T, true>(P, blockIdx.x, gridDim.x);
+}
+
+// ... every rank of an emulation on one GPU in one cooperative launch: CTA b runs rank (b / gsize)'s share
+// from a shared-memory copy of that rank's argument.
+template <int RMAX, class T>
+__global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_p2p_emu_kernel(const DevProblem* parr, int gsize) {
     __shared__ __align__(16) DevProblem sP;
     {
         const int* src = reinterpret_cast<const int*>(parr + blockIdx.x / gsize);
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_p2p_
         for (int i = threadIdx.x; i < (int)(sizeof(DevProblem) / 4); i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
-    stream_body<RMAX, T, true>(sP, &sP, blockIdx.x % gsize, gsize);
+    stream_body<RMAX, T, true>(sP, blockIdx.x % gsize, gsize);
 }
 
 // Partitioned mode, after the exchange-buffer allreduce of sweep t: the other ranks' boundary u into
@@ -677,7 +679,12 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
 
 
 template <class T>
-static const void* p2p_kernel_t(int rmax) {
+static const void* p2p_kernel_t(int rmax, bool emu) {
+    if (emu)
+        return rmax <= 1 ? (const void*)admm_p2p_emu_kernel<1, T>
+             : rmax <= 2 ? (const void*)admm_p2p_emu_kernel<2, T>
+             : rmax <= 4 ? (const void*)admm_p2p_emu_kernel<4, T>
+                         : (const void*)admm_p2p_emu_kernel<8, T>;
     return rmax <= 1 ? (const void*)admm_p2p_kernel<1, T>
          : rmax <= 2 ? (const void*)admm_p2p_kernel<2, T>
          : rmax <= 4 ? (const void*)admm_p2p_kernel<4, T>
@@ -687,7 +694,7 @@ static const void* p2p_kernel_t(int rmax) {
 // CTAs per rank of a p2p launch with `world_here` ranks on this GPU: every CTA of the launch co-resident
 int p2p_max_group(int rmax, int esz, int world_here) {
     int dev = 0, sms = 0, per = 0;
-    const void* k = esz == 4 ? p2p_kernel_t<float>(rmax) : p2p_kernel_t<double>(rmax);
+    const void* k = esz == 4 ? p2p_kernel_t<float>(rmax, world_here > 1) : p2p_kernel_t<double>(rmax, world_here > 1);
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem(rmax, esz)) != cudaSuccess ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, stream_block(rmax, esz), stream_smem(rmax, esz)) != cudaSuccess) {
@@ -697,15 +704,18 @@ int p2p_max_group(int rmax, int esz, int world_here) {
     return sms * per / world_here;
 }
 
-lopf_status launch_p2p(const DevProblem* parr_dev, int world_here, int gsize, int rmax, int esz, void* stream,
-                       std::string& err) {
-    const void* k = esz == 4 ? p2p_kernel_t<float>(rmax) : p2p_kernel_t<double>(rmax);
+lopf_status launch_p2p(const DevProblem* parr_dev, const DevProblem* one, int world_here, int gsize, int rmax, int esz,
+                       void* stream, std::string& err) {
+    const bool emu = world_here > 1;
+    const void* k = esz == 4 ? p2p_kernel_t<float>(rmax, emu) : p2p_kernel_t<double>(rmax, emu);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem(rmax, esz));
     if (e == cudaSuccess) {
         const DevProblem* a0 = parr_dev;
         int g = gsize;
-        void* args[] = {&a0, &g};
-        e = cudaLaunchCooperativeKernel(k, dim3(world_here * gsize), dim3(stream_block(rmax, esz)), args,
+        DevProblem P = one ? *one : DevProblem{};
+        void* args_emu[] = {&a0, &g};
+        void* args_one[] = {&P};
+        e = cudaLaunchCooperativeKernel(k, dim3(world_here * gsize), dim3(stream_block(rmax, esz)), emu ? args_emu : args_one,
                                         stream_smem(rmax, esz), (cudaStream_t)stream);
     }
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }

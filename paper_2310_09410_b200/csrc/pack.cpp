@@ -168,9 +168,9 @@ lopf_status pack_streaming(const Net& N, const Canon& P, const lopf_options& opt
     if (part) {
         L.off_sexp = take(4 * NS);
         L.off_imp = take(4 * ghosts.size());
-        L.off_xbuf = take(8 * 2 * ((size_t)part->n_bnd + 8 * (size_t)part->world));   // [2 parities] (p2p; NCCL: [0])
-        L.off_pflag = take(8 * (size_t)part->world);                                  // per-rank sweep flags (p2p)
-        L.off_peer = take(16 * (size_t)part->world);                                  // peer_xb, peer_flag tables
+        L.off_xbuf = take(8 * ((size_t)part->n_bnd + 8 * (size_t)part->world));       // host-driven (NCCL) exchange
+        L.off_xent = take(16 * 2 * ((size_t)part->n_bnd + 8 * (size_t)part->world));  // p2p tagged entries [2 parities]
+        L.off_peer = take(8 * (size_t)part->world);                                   // p2p: every rank's entry buffer
         L.off_parr = take(sizeof(DevProblem) * (size_t)part->world);                  // p2p launch argument(s)
     }
     L.bytes = o;

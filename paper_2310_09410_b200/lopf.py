@@ -107,7 +107,7 @@ def load_library(path: str = LIB_PATH):
         "lopf_part_sweep": ([H, _vp], _i32),
         "lopf_part_import": ([H, _vp], _i32),
         "lopf_part_p2p_info": ([H, _vp, _vp], _i32),
-        "lopf_part_connect": ([H, _vp, _vp, _vp], _i32),
+        "lopf_part_connect": ([H, _vp, _vp], _i32),
         "lopf_part_solve_p2p": ([H, _i64, _i32, _vp], _i32),
         "lopf_part_emulate": ([_vp, _i32, _i64, _i32, _vp], _i32),
         "lopf_ipc_export": ([_vp, _vp], _i32),
@@ -266,18 +266,15 @@ class Lopf:
         _check(load_library().lopf_part_import(self._h, _vp(_stream_handle(stream))), "lopf_part_import")
 
     # ---- device-initiated exchange ------------------------------------------------------------
-    def p2p_pointers(self):
-        """(exchange buffer, flag array) device addresses of this rank (valid in this process)."""
-        xo, fo = _i64(0), _i64(0)
-        _check(load_library().lopf_part_p2p_info(self._h, C.byref(xo), C.byref(fo)), "lopf_part_p2p_info")
-        base = self.arena.data_ptr()
-        return base + xo.value, base + fo.value
+    def p2p_entries(self) -> int:
+        """Device address of this rank's p2p entry buffer (valid in this process)."""
+        xo, nb = _i64(0), _i64(0)
+        _check(load_library().lopf_part_p2p_info(self._h, C.byref(xo), C.byref(nb)), "lopf_part_p2p_info")
+        return self.arena.data_ptr() + xo.value
 
-    def part_connect(self, peer_xbuf, peer_flag, stream=None):
-        xb = np.ascontiguousarray(peer_xbuf, dtype=np.uint64)
-        fl = np.ascontiguousarray(peer_flag, dtype=np.uint64)
-        _check(load_library().lopf_part_connect(self._h, _ptr(xb), _ptr(fl), _vp(_stream_handle(stream))),
-               "lopf_part_connect")
+    def part_connect(self, peer_entries, stream=None):
+        xe = np.ascontiguousarray(peer_entries, dtype=np.uint64)
+        _check(load_library().lopf_part_connect(self._h, _ptr(xe), _vp(_stream_handle(stream))), "lopf_part_connect")
 
     def part_solve_p2p(self, max_iter: int, test: bool = True, stream=None):
         _check(load_library().lopf_part_solve_p2p(self._h, int(max_iter), int(bool(test)), _vp(_stream_handle(stream))),
