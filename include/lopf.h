@@ -196,6 +196,14 @@ lopf_status lopf_part_owner(const lopf_handle *h, int32_t *bus_owner, int32_t *c
 lopf_status lopf_part_sweep(lopf_handle *h, void *cuda_stream);
 lopf_status lopf_part_import(lopf_handle *h, void *cuda_stream);
 
+/* Host-driven partitioned sweeps with a library-owned NCCL communicator (libnccl.so.2 opened at first use;
+ * failures are LOPF_E_NCCL): rank 0 creates an id (128 bytes) and every rank passes the same bytes to
+ * lopf_part_nccl_init; lopf_part_step = lopf_part_sweep + ncclAllReduce(sum, fp64) of the exchange buffer on
+ * `stream` + lopf_part_import, all stream-ordered (capturable in a CUDA graph). */
+lopf_status lopf_nccl_unique_id(void *out128);
+lopf_status lopf_part_nccl_init(lopf_handle *h, const void *unique_id128);
+lopf_status lopf_part_step(lopf_handle *h, void *cuda_stream);
+
 /* ---- partitioned mode with a device-initiated exchange ----------------
  * One persistent launch per solve and rank, no host and no collective library in the loop: the kernel
  * stores every boundary copy's u as a tagged entry {u, sweep + 1} straight into each rank's entry buffer

@@ -34,6 +34,7 @@ struct lopf_handle {
     std::vector<void*> ipc_open;                   // peer allocations opened by lopf_ipc_open (closed at destroy)
     std::vector<uint64_t> peer_tab;                // [world] device pointers of every rank's p2p entry buffer
     DevProblem p2p_arg{};                          // host copy of the p2p launch argument (kept for the async H2D)
+    void* nccl_comm = nullptr;                     // library-owned NCCL communicator (lopf_part_nccl_init)
     bool resident() const { return lay.kernel == 2; }
     bool parted() const { return lay.part != 0; }
     bool batch() const { return lay.kernel == 3; }
@@ -654,6 +655,72 @@ lopf_status lopf_part_emulate(lopf_handle* const* hs, int32_t world, int64_t max
     return LOPF_OK;
 }
 
+// ---- library-owned NCCL communicator for the host-driven partitioned mode ------------------------------
+// libnccl.so.2 is opened at first use (the one torch has loaded, if any); its absence is LOPF_E_NCCL.
+struct NcclApi {
+    int (*get_unique_id)(void*) = nullptr;
+    int (*comm_init_rank)(void**, int, const void*, int) = nullptr;   // ncclUniqueId passed by value (128 B)
+    int (*all_reduce)(const void*, void*, size_t, int, int, void*, void*) = nullptr;
+    int (*comm_destroy)(void*) = nullptr;
+    const char* (*error_string)(int) = nullptr;
+    bool ok = false;
+};
+struct NcclId { char b[128]; };
+typedef int (*nccl_init_by_value_t)(void**, int, NcclId, int);
+static NcclApi& nccl() {
+    static NcclApi a;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (lib) {
+            a.get_unique_id = (int (*)(void*))dlsym(lib, "ncclGetUniqueId");
+            a.comm_init_rank = (int (*)(void**, int, const void*, int))dlsym(lib, "ncclCommInitRank");
+            a.all_reduce = (int (*)(const void*, void*, size_t, int, int, void*, void*))dlsym(lib, "ncclAllReduce");
+            a.comm_destroy = (int (*)(void*))dlsym(lib, "ncclCommDestroy");
+            a.error_string = (const char* (*)(int))dlsym(lib, "ncclGetErrorString");
+            a.ok = a.get_unique_id && a.comm_init_rank && a.all_reduce && a.comm_destroy && a.error_string;
+        }
+    }
+    return a;
+}
+static lopf_status nccl_fail(int r, const char* where) {
+    g_err = std::string("NCCL error in ") + where + ": " + (nccl().error_string ? nccl().error_string(r) : "?");
+    return LOPF_E_NCCL;
+}
+
+lopf_status lopf_nccl_unique_id(void* out) {
+    if (!out) return fail(LOPF_E_ARG, "NULL argument");
+    if (!nccl().ok) return fail(LOPF_E_NCCL, "libnccl.so.2 not available");
+    const int r = nccl().get_unique_id(out);
+    return r ? nccl_fail(r, "ncclGetUniqueId") : LOPF_OK;
+}
+
+lopf_status lopf_part_nccl_init(lopf_handle* h, const void* unique_id) {
+    if (!h || !unique_id) return fail(LOPF_E_ARG, "NULL argument");
+    if (!h->parted()) return fail(LOPF_E_STATE, "not a partitioned handle (lopf_setup_part)");
+    if (!nccl().ok) return fail(LOPF_E_NCCL, "libnccl.so.2 not available");
+    if (h->nccl_comm) return LOPF_OK;
+    NcclId id;
+    std::memcpy(id.b, unique_id, 128);
+    void* comm = nullptr;
+    const int r = ((nccl_init_by_value_t)(void*)nccl().comm_init_rank)(&comm, h->lay.world, id, h->lay.rank);
+    if (r) return nccl_fail(r, "ncclCommInitRank");
+    h->nccl_comm = comm;
+    return LOPF_OK;
+}
+
+lopf_status lopf_part_step(lopf_handle* h, void* stream) {
+    if (!h) return fail(LOPF_E_ARG, "NULL handle");
+    if (!h->nccl_comm) return fail(LOPF_E_STATE, "lopf_part_step needs lopf_part_nccl_init");
+    lopf_status st = lopf_part_sweep(h, stream);
+    if (st != LOPF_OK) return st;
+    const int r = nccl().all_reduce(h->dp.xbuf, h->dp.xbuf, (size_t)h->dp.xstride, /*ncclFloat64*/ 8, /*ncclSum*/ 0,
+                                    h->nccl_comm, stream);
+    if (r) return nccl_fail(r, "ncclAllReduce");
+    return lopf_part_import(h, stream);
+}
+
 // ---- CUDA IPC of a device allocation (for lopf_part_connect across processes on one node) -------------
 // The driver's cuMemGetAddressRange gives the allocation base of an arbitrary device pointer (a torch
 // tensor lives inside a caching-allocator block); libcuda is opened at first use so the library still
@@ -1038,6 +1105,7 @@ lopf_status lopf_get_profile(lopf_handle* h, void* stream, int64_t* buf, int64_t
 void lopf_destroy(lopf_handle* h) {
     if (!h) return;
     for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
+    if (h->nccl_comm && nccl().ok) nccl().comm_destroy(h->nccl_comm);
     if (h->registered) cudaHostUnregister(h->lay.image.data());
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);

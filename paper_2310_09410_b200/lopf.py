@@ -111,6 +111,9 @@ def load_library(path: str = LIB_PATH):
         "lopf_part_solve_p2p": ([H, _i64, _i32, _vp], _i32),
         "lopf_part_emulate": ([_vp, _i32, _i64, _i32, _vp], _i32),
         "lopf_ipc_export": ([_vp, _vp], _i32),
+        "lopf_nccl_unique_id": ([_vp], _i32),
+        "lopf_part_nccl_init": ([H, _vp], _i32),
+        "lopf_part_step": ([H, _vp], _i32),
         "lopf_ipc_open": ([H, _vp, _vp], _i32),
         "lopf_destroy": ([H], None),
         "lopf_last_error": ([], C.c_char_p),
@@ -286,6 +289,19 @@ class Lopf:
         arr = (_vp * len(handles))(*[h._h.value for h in handles])
         _check(load_library().lopf_part_emulate(arr, len(handles), int(max_iter), int(bool(test)),
                                                 _vp(_stream_handle(stream))), "lopf_part_emulate")
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        out = C.create_string_buffer(128)
+        _check(load_library().lopf_nccl_unique_id(out), "lopf_nccl_unique_id")
+        return out.raw
+
+    def part_nccl_init(self, unique_id: bytes):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(load_library().lopf_part_nccl_init(self._h, buf), "lopf_part_nccl_init")
+
+    def part_step(self, stream=None):
+        _check(load_library().lopf_part_step(self._h, _vp(_stream_handle(stream))), "lopf_part_step")
 
     @staticmethod
     def ipc_export(dev_ptr: int) -> bytes:

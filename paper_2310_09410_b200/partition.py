@@ -10,6 +10,8 @@ termination decision on the rank-ordered sums (identical everywhere) and clears 
 paper's own multi-GPU runs stage the same exchange through the host with MPI.
 
 PyTorch here is plumbing only (the arena tensor, the stream, the process group and its allreduce).
+Two more exchange modes: liblopf's own NCCL communicator (`exchange="nccl"`), and the
+device-initiated exchange over peer memory (`exchange="p2p"`) that needs no per-sweep launch.
 """
 from __future__ import annotations
 
@@ -20,16 +22,27 @@ from .lopf import CONVERGED, Lopf
 
 class PartitionedSolver:
     """This rank's share of a partitioned feeder.  All ranks construct it with the same feeder and
-    options; `solve` / `run` are collective calls."""
+    options; `solve` / `run` are collective calls.
+
+    exchange = "torch": per sweep lopf_part_sweep, torch.distributed.all_reduce of the exchange buffer,
+               lopf_part_import (the PyTorch NCCL communicator);
+               "nccl":  the same three steps inside liblopf with its own NCCL communicator (lopf_part_step;
+               the id is created on rank 0 and broadcast once through torch.distributed);
+               "p2p":   the device-initiated exchange: every rank's entry buffer mapped into every
+               process by CUDA IPC once, then ONE persistent launch per solve (lopf_part_solve_p2p) -- no host
+               and no collective library in the sweep loop."""
 
     def __init__(self, feeder, group=None, device=None, bus_owner=None, rank=None, world=None, graph_block=0,
-                 always_reduce=False, **opts):
+                 always_reduce=False, exchange="torch", **opts):
         """graph_block > 0: `sweeps` / `run` replay a CUDA graph of `graph_block` captured sweeps (launch,
         allreduce, import per sweep) instead of launching every sweep from the host.  always_reduce: run the
         allreduce even with one rank (tests the captured collective on a single GPU)."""
         import torch
         import torch.distributed as dist
+        if exchange not in ("torch", "nccl", "p2p"):
+            raise ValueError("exchange must be 'torch', 'nccl' or 'p2p'")
         self.group = group
+        self.exchange_mode = exchange
         self.graph_block = int(graph_block)
         self.always_reduce = bool(always_reduce)
         self._graph = None
@@ -41,6 +54,34 @@ class PartitionedSolver:
         self.h = Lopf.setup_part(feeder, self.rank, self.world, bus_owner=bus_owner, **opts)
         self.h.bind(device or (torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cuda"))
         self.xbuf = self.h.exchange()
+        if exchange == "nccl":
+            uid = [Lopf.nccl_unique_id() if self.rank == 0 else None]
+            if self.world > 1:
+                dist.broadcast_object_list(uid, src=0, group=self.group)
+            self.h.part_nccl_init(uid[0])
+        elif exchange == "p2p":
+            own = self.h.p2p_entries()
+            recs = [Lopf.ipc_export(own)]
+            if self.world > 1:
+                recs = [None] * self.world
+                dist.all_gather_object(recs, Lopf.ipc_export(own), group=self.group)
+            ptrs = [own if q == self.rank else self.h.ipc_open(recs[q]) for q in range(self.world)]
+            self.h.part_connect(ptrs)
+            torch.cuda.synchronize()
+
+    def _barrier(self):
+        import torch
+        torch.cuda.synchronize()
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier(group=self.group)
+
+    def solve_p2p(self, max_iter: int, test: bool = True, stream=None):
+        """exchange = "p2p": up to max_iter sweeps in one launch per rank (collective: every rank's launch
+        runs at the same time); returns this rank's lopf_result."""
+        self._barrier()                                  # every rank reset / connected before any launch
+        self.h.part_solve_p2p(max_iter, test, stream)
+        return self.h.result_get(stream)
 
     def _allreduce(self):
         if self.world > 1 or self.always_reduce:
@@ -59,9 +100,12 @@ class PartitionedSolver:
         else:
             ctx = torch.cuda.stream(stream)
         with ctx:                                     # everything on torch's current stream
-            self.h.part_sweep(None)
-            self._allreduce()
-            self.h.part_import(None)
+            if self.exchange_mode == "nccl":
+                self.h.part_step(None)
+            else:
+                self.h.part_sweep(None)
+                self._allreduce()
+                self.h.part_import(None)
 
     def reset(self, stream=None):
         self.h.reset(stream)
@@ -88,6 +132,9 @@ class PartitionedSolver:
 
     def sweeps(self, k: int, stream=None):
         """k sweeps on every rank (collective): graph replays of graph_block sweeps, then single sweeps."""
+        if self.exchange_mode == "p2p":
+            self.solve_p2p(k, False, stream)
+            return
         done = 0
         if self.graph_block > 0:
             g = self._captured()
@@ -100,6 +147,8 @@ class PartitionedSolver:
     def run(self, k: int, check_every: int = 64, stream=None):
         """Up to k sweeps, stopping early at (termination); polls the device result every
         `check_every` sweeps (the kernels become no-ops once the test has fired)."""
+        if self.exchange_mode == "p2p":
+            return self.solve_p2p(k, True, stream)
         if self.graph_block > 0:
             check_every = max(self.graph_block, check_every // self.graph_block * self.graph_block)
         done = 0

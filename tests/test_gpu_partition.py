@@ -161,3 +161,31 @@ def test_p2p_single_rank_solve(torch_cuda):
     s.run(300)
     for a, b in zip(h.get_state(), s.get_state()):
         assert np.array_equal(a, b)
+
+
+def test_library_owned_nccl_step(torch_cuda):
+    """exchange="nccl": liblopf's own NCCL communicator (one rank, so no kernel waits on another GPU):
+    lopf_part_step sweeps equal host-launched torch-allreduce sweeps bit for bit, eager and graph-captured."""
+    import socket
+
+    import torch.distributed as dist
+    from paper_2310_09410_b200.partition import PartitionedSolver
+    own = not dist.is_initialized()
+    if own:
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        f = _feeder("s4x13")
+        a = PartitionedSolver(f, rank=0, world=1, always_reduce=True)
+        b = PartitionedSolver(f, rank=0, world=1, exchange="nccl")
+        c = PartitionedSolver(f, rank=0, world=1, exchange="nccl", graph_block=20)
+        for s_ in (a, b, c):
+            s_.reset()
+            s_.sweeps(70)
+        for x, y, z in zip(a.h.get_state(), b.h.get_state(), c.h.get_state()):
+            assert np.array_equal(x, y) and np.array_equal(x, z)
+    finally:
+        if own:
+            dist.destroy_process_group()
