@@ -145,6 +145,9 @@ def main():
     ap.add_argument("--graph-block", type=int, default=50,
                     help="config 5 under torchrun: sweeps per captured CUDA graph (0 = host-launched sweeps)")
     ap.add_argument("--n-scen", type=int, default=4096, help="config 4: scenarios")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl", "torch"],
+                    help="config 5 under torchrun: device-initiated exchange over peer memory (one launch per solve), "
+                         "liblopf's NCCL communicator, or torch.distributed's allreduce (per-sweep launches)")
     args = ap.parse_args()
     if args.config == 5:
         return bench_stitched(args)
@@ -430,7 +433,8 @@ def bench_stitched(args):
         solver = None
     else:
         solver = PartitionedSolver(feeder, device=dev, bus_owner=fg.stitched_bus_owner(feeder, world), max_iter=100_000,
-                                   precision=args.precision, graph_block=args.graph_block)
+                                   precision=args.precision, graph_block=args.graph_block if args.exchange != "p2p" else 0,
+                                   exchange=args.exchange)
         h = solver.h
     setup_s = time.perf_counter() - t0
     sz = h.sizes
@@ -522,7 +526,9 @@ def bench_stitched(args):
             "config": {"workload": f"stitched {args.n_sub} x 8500-shaped feeder (BASELINE configs[4]): "
                                    f"{feeder.n_bus} buses, one scenario, {args.sweeps} sweeps per step (test off)",
                        "S": int(sz.S), "n": int(sz.n), "n_copies": int(sz.n_copies),
-                       "mode": "streaming kernel" if world == 1 else f"partitioned over {world} ranks (NCCL allreduce)",
+                       "mode": "streaming kernel" if world == 1 else
+                       (f"partitioned over {world} ranks, device-initiated exchange (tagged peer stores, one launch)"
+                        if args.exchange == "p2p" else f"partitioned over {world} ranks ({args.exchange} NCCL allreduce)"),
                        "iters_to_tolerance": k_tol, "converged": conv, "time_to_tolerance_ms": ttt_max,
                        "l2": "working set >> L2; flushed between steps anyway", "gen_s": round(gen_s, 1),
                        "setup_s": round(setup_s, 1)},
@@ -533,7 +539,7 @@ def bench_stitched(args):
             "e2e": {"value": e2e_steps * args.sweeps / e2e_max, "unit": "iterations/s",
                     "h2d_bytes_per_step": int(sz.upload_bytes), "d2h_bytes_per_step": int(8 * sz.n), "steps": e2e_steps},
             "clocks": clk.summary(),
-            "gpu_launches": args.steps * (1 if world == 1 else 2 * args.sweeps),
+            "gpu_launches": args.steps * (1 if world == 1 or args.exchange == "p2p" else 2 * args.sweeps),
         }
         print(json.dumps(out))
     if world > 1:

@@ -525,9 +525,8 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
     if (L.part) {                                  // peer table: this rank's own entry (world 1 runs as is)
         P.peer_xe = (double2* const*)(b + L.off_peer);
         P.xent = (double2*)(b + L.off_xent);
-        std::vector<uint64_t> tab((size_t)L.world, 0);
-        tab[L.rank] = (uint64_t)(uintptr_t)P.xent;
-        h->peer_tab = tab;
+        if (h->peer_tab.size() != (size_t)L.world) h->peer_tab.assign((size_t)L.world, 0);   // a re-bind keeps peers
+        h->peer_tab[L.rank] = (uint64_t)(uintptr_t)P.xent;
         CUDA_TRY(cudaMemcpyAsync(b + L.off_peer, h->peer_tab.data(), 8 * h->peer_tab.size(), cudaMemcpyHostToDevice,
                                  s), "peer table H2D");
     }

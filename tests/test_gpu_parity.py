@@ -56,7 +56,7 @@ def _check_state(h, ref):
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-@pytest.mark.parametrize("shape,ks", [("13", (1, 10, 100, 1000)), ("123", (1, 10, 1000)), ("8500", (1, 10, 200))])
+@pytest.mark.parametrize("shape,ks", [("13", (1, 10, 100, 1000)), ("123", (1, 10, 1000)), ("8500", (1, 10, 200, 1000))])
 def test_fixed_k_iterates(torch_cuda, shape, ks, kernel):
     f, p = _problem(shape)
     h = _solver(f, kernel=kernel)

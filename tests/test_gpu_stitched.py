@@ -107,3 +107,30 @@ def test_full_64x8500_properties(full_instance):
     h2.run(21)
     for a, b in zip(h2.get_state(), (x1, xl1, lam1)):
         assert np.array_equal(a, b)                                         # per-copy arithmetic is grid-independent
+
+
+def test_stitched_8x8500_oracle_k100_and_partitions():
+    """SURVEY §8(c) parity matrix, config 5: an 8 x 8500 stitched instance (1.32M copies) after K = 100
+    sweeps -- the streaming kernel against the oracle (1e-9 relative), and the partitioned mode with the
+    device-initiated exchange (2 and 4 ranks emulated in one launch) bit-identical to the streaming kernel."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2310_09410_b200 import Lopf
+    from paper_2310_09410_b200.partition import merge_owned
+    f = fg.make_stitched(8, "8500")
+    p = oracle.build_problem(f)
+    ref = oracle.run_k(p, 100)
+    h = Lopf.setup(f, kernel=1).bind("cuda")
+    h.run(100)
+    single = h.get_state()
+    for a, b in zip(single, (ref.x, ref.x_loc, ref.lam)):
+        assert float(np.abs(a - b).max() / max(1.0, np.abs(b).max())) <= 1e-9
+    for world in (2, 4):
+        hs = [Lopf.setup_part(f, r, world, bus_owner=fg.stitched_bus_owner(f, world)).bind("cuda") for r in range(world)]
+        for x in hs:
+            x.reset()
+        Lopf.part_emulate(hs, 100, test=False)
+        parts = [x.get_state() for x in hs]
+        for i in range(3):
+            assert np.array_equal(merge_owned([q[i] for q in parts]), single[i]), (world, i)
