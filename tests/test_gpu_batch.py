@@ -90,7 +90,9 @@ def test_full_4096_batch_sampled():
     r = h.get_batch_results()
     assert np.all(r["outcome"] == 0)
     samples = sorted(set(np.random.default_rng(64).choice(4096, 62, replace=False).tolist()) | {0, 4095})
-    with mp.get_context("fork").Pool(min(len(samples), max(1, os.cpu_count() or 1))) as pool:
+    # spawn, not fork: a fork of this process (CUDA context, BLAS thread pool) can leave the parent's BLAS
+    # deadlocked in a later linalg call
+    with mp.get_context("spawn").Pool(min(len(samples), max(1, os.cpu_count() or 1))) as pool:
         ref = pool.map(_oracle_solve, [(f, K[sc]) for sc in samples])
     for sc, (k, obj) in zip(samples, ref):
         assert int(r["iters"][sc]) == k, (sc, int(r["iters"][sc]), k)
