@@ -179,7 +179,7 @@ int64_t chunk_bytes(const Canon& P, const std::vector<int64_t>& subs, std::vecto
         for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) cnt[P.copy_global[k]] = 0;
     const int64_t NT = (int64_t)tasks.size();
     int64_t b = 0;
-    for (int64_t sz : {E * pool, E * NS, 4 * E * NG, 16 * NT, 4 * NS, 4 * NS, 4 * (NG + 1), 4 * NSEG, 4 * NG,
+    for (int64_t sz : {E * pool, E * NS, 4 * E * NG, 16 * NT, 4 * NS, 4 * NS, 8 * NG, 4 * NSEG, 4 * NG,
                        (int64_t)4 * 64, E * NS, E * NS, E * NS, E * NS, 2 * E * NG, E * (64 + kpad) * (kResBlock / 32)})
         b = a16(b + sz);
     return b;
@@ -217,13 +217,50 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     }
     if (G > max_ctas / (E == 8 ? 2 : 4)) G = max_ctas;   // large problems: use every SM
     std::vector<Chunk> chunks;
+    // span[p]: globals whose copies lie on both sides of a cut placed before DFS position p (each becomes a
+    // boundary global whose copies are exchanged through L2 every sweep).  A chunk ends where span is
+    // smallest within +-LOPF_RES_CUT_WINDOW of the balanced target, so cuts fall between weakly coupled
+    // subsystems (a 1-phase lateral) rather than inside the 3-phase primary.
+    std::vector<int64_t> span(P.S + 1, 0);
+    {
+        std::vector<int64_t> pos(P.S), first(P.n, P.S), last(P.n, -1);
+        for (int64_t i = 0; i < P.S; ++i) pos[order[i]] = i;
+        for (int64_t s = 0; s < P.S; ++s)
+            for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) {
+                const int32_t g = P.copy_global[k];
+                first[g] = std::min(first[g], pos[s]);
+                last[g] = std::max(last[g], pos[s]);
+            }
+        std::vector<int64_t> diff(P.S + 2, 0);
+        for (int64_t g = 0; g < P.n; ++g)
+            if (last[g] > first[g]) { diff[first[g] + 1] += 1; diff[last[g] + 1] -= 1; }
+        int64_t run = 0;
+        for (int64_t p = 0; p <= P.S; ++p) { run += diff[p]; span[p] = run; }
+    }
+#ifndef LOPF_RES_CUT_WINDOW
+#define LOPF_RES_CUT_WINDOW 0.0           // A/B (profiles/r02_ab_resident_cut.log): 0 4.55, 0.05 4.78, 0.08 4.70, 0.15 5.18 us/sweep
+#endif
+    const double win = LOPF_RES_CUT_WINDOW;
     auto cut = [&](int64_t T, int64_t cap) {
         chunks.assign(1, Chunk{});
         int64_t acc = 0;
-        for (int64_t s : order) {
-            if (acc > 0 && (acc + est[s] > T || acc + est[s] > cap)) { chunks.push_back(Chunk{}); acc = 0; }
-            chunks.back().subs.push_back(s);
-            acc += est[s];
+        size_t i = 0;
+        while (i < order.size()) {
+            // the end of this chunk: scan while the footprint stays within the window / cap
+            const int64_t lo = (int64_t)(T * (1.0 - win)), hi = std::min<int64_t>((int64_t)(T * (1.0 + win)), cap);
+            size_t j = i, best = i;
+            int64_t a = acc, best_span = -1;
+            while (j < order.size() && (a == 0 || a + est[order[j]] <= hi)) {
+                a += est[order[j]];
+                ++j;
+                if (a >= lo && (best_span < 0 || span[j] < best_span)) { best_span = span[j]; best = j; }
+            }
+            if (best_span < 0 || win <= 0) best = j;           // window empty (or off): greedy end
+            for (size_t q = i; q < best; ++q) chunks.back().subs.push_back(order[q]);
+            if (best >= order.size()) break;
+            chunks.push_back(Chunk{});
+            acc = 0;
+            i = best;
         }
     };
     bool done = false;
@@ -322,7 +359,7 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         h.off_tasks = o;    o = a16(o + 16 * NT);
         h.off_sinfo = o;    o = a16(o + 4 * NS);
         h.off_sexp = o;     o = a16(o + 4 * NS);
-        h.off_gsegoff = o;  o = a16(o + 4 * (NG + 1));
+        h.off_gsegoff = o;  o = a16(o + 8 * NG);                     // int2 descriptor per global
         h.off_gseg = o;     o = a16(o + 4 * NSEG);
         h.off_gown = o;     o = a16(o + 4 * NG);
         h.off_nbr = o;      o = a16(o + 4 * std::max<int64_t>(NNB, 64));
@@ -390,14 +427,19 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
             put(h.off_gpar, 4 * j + 1, 1.0 / nu);
             put(h.off_gpar, 4 * j + 2, P.lo[g]);
             put(h.off_gpar, 4 * j + 3, P.hi[g]);
-            segoff[j] = q;
+            const int32_t q0 = q;
+            int jx = 4, nbnd = 0;
             for (int64_t p = P.seg_ptr[g]; p < P.seg_ptr[g + 1]; ++p) {
                 const int32_t k = P.seg_copy[p];                 // canonical ascending copy order
-                seg[q++] = copy_chunk[k] == c ? (L.slot_of_copy[k] - slot_base) : -(1 + xidx[k]);
+                seg[q] = copy_chunk[k] == c ? (L.slot_of_copy[k] - slot_base) : -(1 + xidx[k]);
+                if (seg[q] < 0 && q - q0 < 4) { if (jx == 4) jx = q - q0; ++nbnd; }
+                ++q;
             }
+            if (q - q0 > 255) { err = "a global with more than 255 copies (resident kernel)"; return LOPF_E_ARG; }
+            segoff[2 * j] = q0;                                   // {first entry, nu | first boundary << 8 | several << 12}
+            segoff[2 * j + 1] = (q - q0) | (jx << 8) | (nbnd > 1 ? 1 << 12 : 0);
             gown[j] = copy_chunk[P.seg_copy[P.seg_ptr[g]]] == c ? g : -1;
         }
-        segoff[NG] = q;
         for (int32_t g : gl_list) gl_of[g] = -1;
         slot_base += (int32_t)NS;
     }

@@ -112,14 +112,17 @@ __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, doubl
     int info[2];
     // a4 for both rows without per-row branches (invalid rows read global 0 and are discarded), so the
     // SMEM dependency chains of the two rows interleave; only a boundary entry leaves the straight line
-    int gl[2], q0[2], nq[2], e[2][4];
+    int gl[2], q0[2], nq[2], e[2][4], jxm[2];
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         info[h] = Ii(C.sinfo, tr.x + h * 32 + lane);
         const bool val = info[h] & kResValid;
         gl[h] = val ? info[h] >> kResGlShift : 0;
-        q0[h] = Ii(C.gsegoff, gl[h]);
-        nq[h] = val ? Ii(C.gsegoff, gl[h] + 1) - q0[h] : 0;
+        // per-global descriptor {first entry, nu | first boundary position << 8 | several boundaries << 12}
+        const int2 gd = reinterpret_cast<const int2*>(sm + C.gsegoff)[gl[h]];
+        q0[h] = gd.x;
+        nq[h] = val ? (gd.y & 0xFF) : 0;
+        jxm[h] = val ? gd.y >> 8 : 4;
 #pragma unroll
         for (int j = 0; j < 4; ++j) e[h][j] = Ii(C.gseg, q0[h] + (j < nq[h] ? j : 0));
     }
@@ -129,11 +132,8 @@ __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, doubl
     unsigned long long xlo[2], xhi[2];
 #pragma unroll
     for (int h = 0; h < R; ++h) {
-        jx[h] = 4;
-        ex[h] = -1;
-#pragma unroll
-        for (int j = 3; j >= 0; --j)
-            if (j < nq[h] && e[h][j] < 0) { jx[h] = j; ex[h] = e[h][j]; }
+        jx[h] = jxm[h] & 0xF;
+        ex[h] = jx[h] == 0 ? e[h][0] : jx[h] == 1 ? e[h][1] : jx[h] == 2 ? e[h][2] : e[h][3];
         xlo[h] = 0ull;
         xhi[h] = C.tag_c;
         if (jx[h] < 4) ld_entry_once(C.xch_c + (-ex[h] - 1), xlo[h], xhi[h]);
@@ -149,7 +149,7 @@ __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, doubl
             if (j == jx[h]) {
                 while (xhi[h] != C.tag_c) ld_entry_once(C.xch_c + (-ex[h] - 1), xlo[h], xhi[h]);
                 u = (T)__longlong_as_double((long long)xlo[h]);
-            } else if (j < nq[h] && e[h][j] < 0) {
+            } else if ((jxm[h] & 0x10) && j < nq[h] && e[h][j] < 0) {      // a second boundary entry (rare)
                 u = (T)ld_entry(C.xch_c + (-e[h][j] - 1), C.tag_c);
             }
             if (j < nq[h]) sig[h] += u;                                  // canonical copy order
@@ -256,7 +256,14 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     C.inv_rho = (T)P.inv_rho;
     unsigned long long* pub = P.flags + (size_t)G * kFlagStride;       // CTAs x sweeps published
     const long long total0 = *(volatile long long*)&P.ctrl->total;
+#ifndef LOPF_RES_PROF
+#define LOPF_RES_PROF 0                           // 1: per-CTA phase counters (lopf_get_profile, diagnostics builds)
+#endif
+#ifdef LOPF_RES_TIMELINE
     const bool prof = P.prof != nullptr;
+#else
+    const bool prof = LOPF_RES_PROF && P.prof != nullptr;
+#endif
     __shared__ long long s_prof[3];
     if (tid == 0) s_prof[0] = s_prof[1] = s_prof[2] = 0;
 
@@ -367,7 +374,8 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                             if (!(inf & kResValid)) continue;
                             ++rows;
                             const int gl = inf >> kResGlShift;
-                            for (int q = Ii(C.gsegoff, gl); q < Ii(C.gsegoff, gl + 1); ++q) xr += Ii(C.gseg, q) < 0;
+                            const int2 gd = reinterpret_cast<const int2*>(sm + C.gsegoff)[gl];
+                            for (int q = gd.x; q < gd.x + (gd.y & 0xFF); ++q) xr += Ii(C.gseg, q) < 0;
                         }
                     }
                     for (int off = 16; off > 0; off >>= 1) {
