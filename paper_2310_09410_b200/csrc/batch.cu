@@ -37,7 +37,8 @@ using dev::kFull;
 #define LOPF_BATCH_CROWS 4                    // consensus rows whose gathers are issued together
 #endif
 #ifndef LOPF_BATCH_L2PF
-#define LOPF_BATCH_L2PF 1                     // per-subsystem lane-parallel L2 prefetch of x_s and the operator
+#define LOPF_BATCH_L2PF 1                     // per-subsystem lane-parallel L2 prefetch: 1 x_s, 2 the operator,
+                                              // 4 lambda, 8 the subsystem's own u rows
 #endif
 constexpr int BW = kBatchWarps;
 constexpr int CR = LOPF_BATCH_CROWS;
@@ -106,8 +107,18 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
         // lane-parallel L2 prefetch of the lines this subsystem streams from HBM (x_s read in the finish, the
         // per-scenario operator in the mat-vec), issued before the consensus so they arrive while it runs
         const char* xb = reinterpret_cast<const char*>(xlg - lane);
-        for (int e = lane; e < 2 * ns; e += 32) prefetch_l2_line(xb + (size_t)(32 * row0) * sizeof(T) + 128 * e);
-        if (var) {
+        const int xlines = (int)(ns * 32 * sizeof(T) / 128);
+        if (LOPF_BATCH_L2PF & 1)
+            for (int e = lane; e < xlines; e += 32) prefetch_l2_line(xb + (size_t)(32 * row0) * sizeof(T) + 128 * e);
+        if (LOPF_BATCH_L2PF & 4) {
+            const char* lb = reinterpret_cast<const char*>(lmg - lane);
+            for (int e = lane; e < xlines; e += 32) prefetch_l2_line(lb + (size_t)(32 * row0) * sizeof(T) + 128 * e);
+        }
+        if (LOPF_BATCH_L2PF & 8) {
+            const char* ub = reinterpret_cast<const char*>(ug - lane);
+            for (int e = lane; e < xlines; e += 32) prefetch_l2_line(ub + (size_t)(32 * row0) * sizeof(T) + 128 * e);
+        }
+        if ((LOPF_BATCH_L2PF & 2) && var) {
             const char* vb = reinterpret_cast<const char*>(V - lane);
             const int nl = (ns * (ns + 1) / 2 + ns) * (int)(32 * sizeof(T) / 128);
             for (int e = lane; e < nl; e += 32) prefetch_l2_line(vb + 128 * e);
@@ -315,7 +326,8 @@ __global__ void __launch_bounds__(BB, 1) admm_batch_kernel(BatchProblem B) {
             const bool act = sc < B.n_scen && __ldcg(B.stopped + sc) == 0;
             double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
             const double* pp = B.partial + (size_t)grp * NT * 160 + lane;
-            for (int k2 = 0; k2 < NT; ++k2)                      // task order: fixed
+#pragma unroll 8
+            for (int k2 = 0; k2 < NT; ++k2)                      // task order: fixed (loads run 8 tasks ahead)
 #pragma unroll
                 for (int k = 0; k < 5; ++k) s5[k] += __ldcg(pp + (size_t)k2 * 160 + k * 32);
             const double pres = sqrt(s5[0]), dres = B.rho * sqrt(s5[1]);
