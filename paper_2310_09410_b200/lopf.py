@@ -348,7 +348,10 @@ class Lopf:
 
     @property
     def sizes(self) -> Sizes:
-        return self.sizes_get()
+        """lopf_sizes_get, cached (the sizes are fixed at setup; grid and block once bound)."""
+        if self._sizes is None or (self._sizes.grid == 0 and self.arena is not None):
+            self._sizes = self.sizes_get()
+        return self._sizes
 
     # ---- device ---------------------------------------------------------------------------------
     def bind(self, device="cuda", stream=None, arena=None):
@@ -357,9 +360,12 @@ class Lopf:
         nbytes = int(self.sizes.device_bytes)
         if arena is None:
             arena = self.arena if self.arena is not None else torch.empty(nbytes, dtype=torch.uint8, device=device)
+        first = self.arena is None
         self.arena = arena
         _check(load_library().lopf_bind(self._h, _vp(arena.data_ptr()), arena.numel(), _vp(_stream_handle(stream))),
                "lopf_bind")
+        if first:
+            self._sizes = None                          # grid / block are known now
         return self
 
     def reset(self, stream=None):
@@ -393,12 +399,12 @@ class Lopf:
         _check(load_library().lopf_fetch_async(self._h, _vp(_stream_handle(stream)), _vp(ptr)), "lopf_fetch_async")
 
     @staticmethod
-    def decode_fetch(host_buf, n: int):
-        """(Result, x) from a buffer filled by fetch_async."""
+    def decode_fetch(host_buf, n: int, with_x: bool = True):
+        """(Result, x) from a buffer filled by fetch_async (x is None with with_x=False)."""
         raw = host_buf.numpy() if hasattr(host_buf, "numpy") else np.asarray(host_buf)
-        raw = np.ascontiguousarray(raw).view(np.uint8)
+        raw = raw.view(np.uint8)
         r = Result.from_buffer_copy(raw[: C.sizeof(Result)].tobytes())
-        x = raw[64: 64 + 8 * n].view(np.float64).copy()
+        x = raw[64: 64 + 8 * n].view(np.float64).copy() if with_x else None
         return r, x
 
     def result_get(self, stream=None) -> Result:
