@@ -73,3 +73,17 @@ def test_coarse(torch_cuda, make, B, kernel):
     o = oracle.solve(p)
     assert r.outcome == CONVERGED and o.converged
     assert r.iters == o.iters and abs(r.objective - o.objective) <= 1e-6 * abs(o.objective)
+
+
+def test_coarse_fp32(torch_cuda):
+    """Coarse runs in the fp32 variant against the oracle's binary32 loop on the same coarse decomposition,
+    within twice the forward-error bound K (n_max + nu_max + 4) 2^-24 (as tests/test_gpu_f32.py)."""
+    from paper_2310_09410_b200 import Lopf
+    f = fg.make_feeder("123")
+    p = oracle.build_problem(f, coarse=16)
+    h = Lopf.setup(f, coarse=16, precision=32).bind("cuda")
+    h.run(100)
+    ref = oracle.run_k_f32(p, 100)
+    tol = 2.0 * 100 * (int(p.dec.n_s().max()) + int(np.diff(p.dec.seg_ptr).max()) + 4) * 2.0 ** -24
+    x, xl, lam = h.get_state()
+    assert _rel(x, ref.x) <= tol and _rel(xl, ref.x_loc) <= tol and _rel(lam / 100.0, ref.lam / 100.0) <= tol

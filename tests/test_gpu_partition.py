@@ -33,8 +33,8 @@ def _feeder(key):
             "s2x8500": lambda: fg.make_stitched(2, "8500")}[key]()
 
 
-def _ranks(f, world, owner=None):
-    return [Lopf.setup_part(f, r, world, bus_owner=owner).bind("cuda") for r in range(world)]
+def _ranks(f, world, owner=None, precision=64):
+    return [Lopf.setup_part(f, r, world, bus_owner=owner, precision=precision).bind("cuda") for r in range(world)]
 
 
 def _merged_state(hs):
@@ -189,3 +189,17 @@ def test_library_owned_nccl_step(torch_cuda):
     finally:
         if own:
             dist.destroy_process_group()
+
+
+def test_p2p_emulation_fp32_equals_single_gpu(torch_cuda):
+    """The device-initiated exchange in the fp32 variant (reading F1): u travels widened to fp64 in the
+    tagged entries and is rounded back exactly, so 3 emulated ranks equal the fp32 streaming kernel bit for bit."""
+    f = _feeder("s4x13")
+    hs = _ranks(f, 3, None, precision=32)
+    for h in hs:
+        h.reset()
+    single = Lopf.setup(f, kernel=1, precision=32).bind("cuda")
+    Lopf.part_emulate(hs, 120, test=False)
+    single.run(120)
+    for a, b in zip(_merged_state(hs), single.get_state()):
+        assert np.array_equal(a, b)
