@@ -42,6 +42,9 @@ constexpr int kInvNu = 64;                 // SMEM table of 1 / nu (the host's 1
 // on that stage's mbarrier, one task ahead of the compute.
 // T = double (the parity path) or float (the paper's GPU precision; reading F1): the
 // operator block holds kPackBudget entries of T, then the per-slot inputs of 64 slots.
+// Compile-time variants of the sweep (template M): the device-initiated exchange, residual balancing.
+constexpr int kModeP2P = 1, kModeAdapt = 2;
+
 template <class T> struct Stg {
     static constexpr int kOffMeta = (int)sizeof(T) * kPackBudget;
     static constexpr int kOffLam = kOffMeta + (int)sizeof(SlotMeta) * 64;
@@ -115,12 +118,12 @@ __device__ __forceinline__ double ld_entry_sys(const double2* p, const unsigned 
 }
 
 // a4 for one slot: the global's consensus value from the ping-pong copies (closed_1, rho restored)
-template <class T>
+template <class T, int M>
 __device__ __forceinline__ T consensus(const DevProblem& P, const int inf, const int g, const int4 nb,
                                        const T* __restrict__ ucur, const T* __restrict__ inv_nu, const T rho) {
     const vec2_t<T> bd = __ldg(reinterpret_cast<const vec2_t<T>*>(P.gbnd) + g);        // {lo, hi}
     T cr = (inf & kInfoCost) ? __ldg(reinterpret_cast<const T*>(P.gcost) + g) : T(0);   // c / rho
-    if (P.adapt_every) cr = cr / rho;                                   // adaptive rho: gcost holds c
+    if constexpr ((M & kModeAdapt) != 0) cr = cr / rho;                // adaptive rho: gcost holds c
     T sigma, inv;
     if (inf & kInfoInline) {                               // nu <= 4: neighbour slots inline
         const int nu = (inf >> kInfoNuShift) & 0xF;
@@ -145,7 +148,7 @@ __device__ __forceinline__ T consensus(const DevProblem& P, const int inf, const
 }
 
 // a6 + a7 for one slot.  The five residual terms are formed in T and summed in fp64 (reading F1).
-template <class T>
+template <class T, int M>
 __device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, const int slot, const T ax, const T bb,
                                             const T v, const T lam, const T xo, T* __restrict__ unext,
                                             double (&acc)[5], const T rho, const T inv_rho, const bool val = true,
@@ -160,7 +163,7 @@ __device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, 
     }
     if (inf & kInfoExport) {                                           // partitioned: to the other ranks
         const int e = __ldg(P.s_exp + slot);
-        if (P.p2p) {                                                   // device-initiated: a tagged entry into
+        if constexpr ((M & kModeP2P) != 0) {                           // device-initiated: a tagged entry into
             const size_t xo = unext == reinterpret_cast<T*>(P.u0) ? (size_t)P.xstride : 0;   // every rank's buffer
             for (int q = 0; q < P.world; ++q)                          // of this sweep's parity (t & 1)
                 st_entry_sys(P.peer_xe[q] + xo + e, (double)un, xtag);
@@ -180,7 +183,7 @@ __device__ __forceinline__ void finish_slot(const DevProblem& P, const int inf, 
 // lone large subsystem (kTaskDirect), straight from the pool.
 // SRC: where the operator block is read -- 1 the pool (direct task), 2 the SMEM stage (shared-space
 // loads), 0 decided per task at run time (one code path: the batch kernel, whose registers are tighter)
-template <int R, class T, int SRC>
+template <int R, class T, int SRC, int M>
 __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, const T* __restrict__ ucur,
                                             T* __restrict__ unext, double (&acc)[5], const int lane,
                                             T* __restrict__ dsm, Stage& st, const T* __restrict__ inv_nu,
@@ -220,7 +223,7 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
         lo[h] = bd.x;
         hi[h] = bd.y;
         cr[h] = val && (info[h] & kInfoCost) ? __ldg(reinterpret_cast<const T*>(P.gcost) + g[h]) : T(0);
-        if (P.adapt_every) cr[h] = cr[h] / rho;                     // adaptive rho: gcost holds c
+        if constexpr ((M & kModeAdapt) != 0) cr[h] = cr[h] / rho;   // adaptive rho: gcost holds c
     }
 #pragma unroll
     for (int h = 0; h < R; ++h) {      // branch-free for the inline case (absent entries are exact zeros)
@@ -270,7 +273,7 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
         // b-bar follows the subsystem's triangle in the block when nonzero
         const T bb = (info[h] & kInfoBbar)
                          ? S[((unsigned)info[h] >> kInfoPoffShift) + ns[h] * (ns[h] + 1) / 2 + r[h]] : T(0);
-        finish_slot<T>(P, info[h], tr.x + j, ax[h], bb, v[h], val ? s_lam[j] : T(0), val ? s_xl[j] : T(0), unext,
+        finish_slot<T, M>(P, info[h], tr.x + j, ax[h], bb, v[h], val ? s_lam[j] : T(0), val ? s_xl[j] : T(0), unext,
                        acc, rho, inv_rho, val, xtag);
     }
     __syncwarp();
@@ -278,7 +281,7 @@ __device__ __forceinline__ void task_packed(const DevProblem& P, const int4 tr, 
 
 // Full task (one subsystem of n_s > 63, R = 2, 4 or 8): Abar as kmax columns of 32*R entries and the
 // per-slot inputs read straight from HBM.
-template <int R, class T>
+template <int R, class T, int M>
 __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, const T* __restrict__ ucur,
                                           T* __restrict__ unext, double (&acc)[5], const int lane,
                                           T* __restrict__ dsm, const T* __restrict__ inv_nu, const T rho,
@@ -294,7 +297,7 @@ __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, co
         T d = T(0);
         if (info[h] & kInfoValid) {
             const int2 n01 = __ldg(&P.s_meta[slot].n01), n23 = __ldg(&P.s_meta[slot].n23);
-            v[h] = consensus<T>(P, info[h], __ldg(&P.s_meta[slot].g), make_int4(n01.x, n01.y, n23.x, n23.y), ucur,
+            v[h] = consensus<T, M>(P, info[h], __ldg(&P.s_meta[slot].g), make_int4(n01.x, n01.y, n23.x, n23.y), ucur,
                                 inv_nu, rho);
             d = -rho * v[h] - lamp[slot];
         }
@@ -313,7 +316,7 @@ __device__ __forceinline__ void task_full(const DevProblem& P, const int4 tr, co
         if (!(info[h] & kInfoValid)) continue;
         const int slot = tr.x + h * 32 + lane;
         const T bb = (info[h] & kInfoBbar) ? __ldg(reinterpret_cast<const T*>(P.s_bbar) + slot) : T(0);
-        finish_slot<T>(P, info[h], slot, ax[h], bb, v[h], lamp[slot], reinterpret_cast<const T*>(P.xl)[slot], unext, acc,
+        finish_slot<T, M>(P, info[h], slot, ax[h], bb, v[h], lamp[slot], reinterpret_cast<const T*>(P.xl)[slot], unext, acc,
                        rho, inv_rho, true, xtag);
     }
     __syncwarp();
@@ -330,8 +333,9 @@ struct StreamWarps {
 // memory when the ranks are emulated on one GPU); the last CTA of each rank publishes the rank's residual
 // sums the same way, reads every rank's sums and its own ghosts when their tags say "this sweep", and
 // takes the (termination) decision on the rank-ordered sums -- one launch per solve, no host, no NCCL.
-template <int RMAX, class T, bool P2P>
+template <int RMAX, class T, int M>
 __device__ __forceinline__ void stream_body(const DevProblem& P, const int cta, const int ncta) {
+    constexpr bool P2P = (M & kModeP2P) != 0, ADAPT = (M & kModeAdapt) != 0;
     constexpr int kWarps = StreamWarps<RMAX, T>::value;
     constexpr int kStageBytes = Stg<T>::kBytes;
     extern __shared__ __align__(128) char sdyn[];      // [kWarps][2][kStageBytes] stages, [kWarps][32*RMAX] d
@@ -353,9 +357,10 @@ __device__ __forceinline__ void stream_body(const DevProblem& P, const int cta, 
     if (!P2P && P.part && *(volatile long long*)&P.ctrl->stopped) return;   // partitioned: decided, no more sweeps
     const long long total0 = *(volatile long long*)&P.ctrl->total;
     const int4 tr0 = gw < P.n_tasks ? __ldg(P.tasks + gw) : make_int4(0, 0, 0, 0);
-    // the penalty in force: fixed, or (residual balancing, F2) the device copy in the control block
-    double rho_d = P.adapt_every ? *(volatile double*)&P.ctrl->rho_cur : P.rho;
-    T rho = (T)rho_d, inv_rho = P.adapt_every ? (T)(1.0 / rho_d) : (T)P.inv_rho;
+    // the penalty in force: fixed (kernel parameters: no loop-carried registers under the 128-register
+    // cap), or (residual balancing, F2) the device copy in the control block
+    double rho_d = ADAPT ? *(volatile double*)&P.ctrl->rho_cur : P.rho;
+    T rho = (T)rho_d, inv_rho = ADAPT ? (T)(1.0 / rho_d) : (T)P.inv_rho;
     unsigned long long bars2 = 0;
     long long it = 0;
     if (P.max_iter > 0) issue_task<T>(P, st, tr0, lane, false);
@@ -373,17 +378,17 @@ __device__ __forceinline__ void stream_body(const DevProblem& P, const int cta, 
             if (tr.w & kTaskPacked) {
                 const bool dir = tr.w & kTaskDirect;
                 if ((tr.w & 0xF) == 1) {
-                    if (dir) task_packed<1, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
-                    else task_packed<1, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
+                    if (dir) task_packed<1, T, 1, M>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
+                    else task_packed<1, T, 2, M>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
                 } else if constexpr (RMAX >= 2) {
-                    if (dir) task_packed<2, T, 1>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
-                    else task_packed<2, T, 2>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
+                    if (dir) task_packed<2, T, 1, M>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
+                    else task_packed<2, T, 2, M>(P, tr, ucur, unext, acc, lane, dsm, st, inv_nu, rho, inv_rho, xtag);
                 }
             } else {
                 switch (tr.w & 0xF) {
-                    case 2: if constexpr (RMAX >= 2) task_full<2, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho, xtag); break;
-                    case 4: if constexpr (RMAX >= 4) task_full<4, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho, xtag); break;
-                    default: if constexpr (RMAX >= 8) task_full<8, T>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho, xtag); break;
+                    case 2: if constexpr (RMAX >= 2) task_full<2, T, M>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho, xtag); break;
+                    case 4: if constexpr (RMAX >= 4) task_full<4, T, M>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho, xtag); break;
+                    default: if constexpr (RMAX >= 8) task_full<8, T, M>(P, tr, ucur, unext, acc, lane, dsm, inv_nu, rho, inv_rho, xtag); break;
                 }
             }
             tr = tr1;
@@ -452,7 +457,7 @@ __device__ __forceinline__ void stream_body(const DevProblem& P, const int cta, 
                     const int stop = conv || numeric;
                     DevCtrl* c = P.ctrl;
                     int chg = 0;                               // residual balancing (F2): rho of the next sweep
-                    if (P.adapt_every && !stop && ((total0 + it) % P.adapt_every) == 0) {
+                    if (ADAPT && !stop && ((total0 + it) % P.adapt_every) == 0) {
                         double rn = rho_d;
                         if (pres > P.adapt_mu * dres) rn = P.adapt_tau * rho_d;
                         else if (dres > P.adapt_mu * pres) rn = rho_d / P.adapt_tau;
@@ -497,7 +502,7 @@ __device__ __forceinline__ void stream_body(const DevProblem& P, const int cta, 
         }
         __syncthreads();
         if (s_stop) break;
-        if (s_chg) {        // rho changed: every u of the next sweep's buffer re-formed with it, then a barrier
+        if (ADAPT && s_chg) {   // rho changed: every u of the next sweep's buffer re-formed with it, then a barrier
             rho_d = *(volatile double*)&P.ctrl->rho_cur;
             rho = (T)rho_d;
             inv_rho = (T)(1.0 / rho_d);
@@ -514,15 +519,16 @@ __device__ __forceinline__ void stream_body(const DevProblem& P, const int cta, 
     }
 }
 
-template <int RMAX, class T>   // largest task width in the problem (RMAX > 2 only with n_s > 64: the S = 1 path)
+// RMAX: largest task width in the problem (RMAX > 2 only with n_s > 64: the S = 1 path); ADAPT: residual balancing
+template <int RMAX, class T, bool ADAPT>
 __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_stream_kernel(DevProblem P) {
-    stream_body<RMAX, T, false>(P, blockIdx.x, gridDim.x);
+    stream_body<RMAX, T, ADAPT ? kModeAdapt : 0>(P, blockIdx.x, gridDim.x);
 }
 
 // Partitioned mode with the device-initiated exchange, one rank per GPU (one launch per rank).
 template <int RMAX, class T>
 __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_p2p_kernel(DevProblem P) {
-    stream_body<RMAX, T, true>(P, blockIdx.x, gridDim.x);
+    stream_body<RMAX, T, kModeP2P>(P, blockIdx.x, gridDim.x);
 }
 
 // ... every rank of an emulation on one GPU in one cooperative launch: CTA b runs rank (b / gsize)'s share
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(32 * StreamWarps<RMAX, T>::value, 1) admm_p2p_
         for (int i = threadIdx.x; i < (int)(sizeof(DevProblem) / 4); i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
-    stream_body<RMAX, T, true>(sP, blockIdx.x % gsize, gsize);
+    stream_body<RMAX, T, kModeP2P>(sP, blockIdx.x % gsize, gsize);
 }
 
 // Partitioned mode, after the exchange-buffer allreduce of sweep t: the other ranks' boundary u into
@@ -627,15 +633,16 @@ lopf_status launch_fetch(const DevCtrl* ctrl, const void* x, int64_t n, int esz,
     return LOPF_OK;
 }
 
-template <class T>
+template <class T, bool ADAPT>
 static const void* stream_kernel_t(int rmax) {
-    return rmax <= 1 ? (const void*)admm_stream_kernel<1, T>
-         : rmax <= 2 ? (const void*)admm_stream_kernel<2, T>
-         : rmax <= 4 ? (const void*)admm_stream_kernel<4, T>
-                     : (const void*)admm_stream_kernel<8, T>;
+    return rmax <= 1 ? (const void*)admm_stream_kernel<1, T, ADAPT>
+         : rmax <= 2 ? (const void*)admm_stream_kernel<2, T, ADAPT>
+         : rmax <= 4 ? (const void*)admm_stream_kernel<4, T, ADAPT>
+                     : (const void*)admm_stream_kernel<8, T, ADAPT>;
 }
-static const void* stream_kernel_for(int rmax, int esz) {
-    return esz == 4 ? stream_kernel_t<float>(rmax) : stream_kernel_t<double>(rmax);
+static const void* stream_kernel_for(int rmax, int esz, bool adapt) {
+    if (adapt) return esz == 4 ? stream_kernel_t<float, true>(rmax) : stream_kernel_t<double, true>(rmax);
+    return esz == 4 ? stream_kernel_t<float, false>(rmax) : stream_kernel_t<double, false>(rmax);
 }
 
 static int stream_smem(int rmax, int esz) {
@@ -650,10 +657,13 @@ int stream_block(int rmax, int esz) {
 
 lopf_status query_grid(int rmax, int esz, int* grid, std::string& err) {
     int dev = 0, sms = 0, per = 0;
-    const void* k = stream_kernel_for(rmax, esz);
+    const void* k = stream_kernel_for(rmax, esz, false);
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem(rmax, esz));
+    if (e == cudaSuccess)          // the residual-balancing variant launches with the same block and SMEM
+        e = cudaFuncSetAttribute(stream_kernel_for(rmax, esz, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 stream_smem(rmax, esz));
     if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, stream_block(rmax, esz), stream_smem(rmax, esz));
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
@@ -670,7 +680,7 @@ lopf_status launch_solve(const DevProblem& P, int grid, void* stream, std::strin
     if (e == cudaSuccess && P.max_iter > 0) {
         DevProblem Q = P;
         void* args[] = {&Q};
-        e = cudaLaunchCooperativeKernel(stream_kernel_for(P.rmax, P.esz), dim3(grid), dim3(stream_block(P.rmax, P.esz)), args,
+        e = cudaLaunchCooperativeKernel(stream_kernel_for(P.rmax, P.esz, P.adapt_every > 0), dim3(grid), dim3(stream_block(P.rmax, P.esz)), args,
                                         stream_smem(P.rmax, P.esz), s);
     }
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
