@@ -158,24 +158,31 @@ struct DevProblem {                        // kernel argument (pointers into the
 constexpr int kResBlock = LOPF_RES_BLOCK;     // worker warps + 1 reducer warp (768: 80 registers, no spills)
 constexpr int kResSmemBudget = 222 * 1024;    // dynamic SMEM per CTA (227 KB usable on sm_100, minus static)
 // sinfo: base (bits 0-5, first slot of the subsystem in its task) | valid (bit 6) | first (bit 7: this slot
-// is the canonical first copy of a global whose x this CTA outputs) | n_s (bits 8-14) | gl (bits 15-31)
+// is the canonical first copy of a global whose x this CTA outputs) | consensus flags of the slot's global
+// (bit 14) | gl (bits 15-31).  Every copy a CTA reads has an SMEM slot: its own copies [0, n_slots), the
+// zero slot n_slots (x = lambda = 0), and a ghost slot per copy owned by another CTA (x = u imported from the
+// exchange buffer by each task that reads it, lambda = 0).  A global with nu <= 4 has a record grec of the
+// slots of its copies in canonical order, padded with the zero slot; one with nu > 4 ("slow") has gxb =
+// {first entry, nu} of its slot list in gseg.
 constexpr int kResValid = 1 << 6;
 constexpr int kResFirst = 1 << 7;
-constexpr int kResNsShift = 8;
+constexpr int kResSlow = 1 << 14;             // nu > 4: the global's list in gseg
 constexpr int kResGlShift = 15;
 
 struct CtaHdr {                               // 128 B, one per CTA
-    int32_t n_tasks, n_slots, n_glob, n_seg, n_nbr;
+    int32_t n_tasks, n_slots, n_glob, n_seg, n_ghost;
     int32_t blob_bytes, smem_bytes;
     // blob (global and SMEM): constant part then the state (x_s, lambda of sweep parity 0)
-    int32_t off_abar, off_bbar, off_gpar, off_tasks, off_sinfo, off_sexp, off_gsegoff, off_gseg, off_gown,
-        off_nbr, off_xl0, off_lam0;
+    int32_t off_abar, off_bbar, off_gpar, off_tasks, off_sinfo, off_sexp, off_grec, off_gxb, off_gseg,
+        off_gimp, off_xl0, off_lam0;
+    int32_t off_gown;                         // blob only, past blob_bytes (read from global memory at exit)
     // SMEM only (after the blob)
     int32_t off_xl1, off_lam1, off_xout, off_dst, dst_stride;
     int32_t slot_base;
     long long blob_off;
-    int32_t pad[2];
+    int32_t pad[1];
 };
+static_assert(sizeof(CtaHdr) <= 128, "CtaHdr is loaded by the first 32 threads");
 
 struct ResProblem {                           // resident kernel argument
     const CtaHdr* hdr;

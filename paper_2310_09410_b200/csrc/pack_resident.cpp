@@ -13,6 +13,8 @@
 //    CTAs, indices into the global exchange buffer (only boundary copies are exchanged).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 
@@ -148,7 +150,13 @@ void split_tasks(const Canon& P, std::vector<TaskR>& tasks, const std::vector<in
         }
         const int extra = (int)bins.size() - 1;
         if (!ok || extra > idle) continue;
-        int64_t grow = 32 * per_slot * ((int64_t)bins.size() - 2);     // 32 slots per R = 1 task (64 before)
+        int64_t xr_t = 0;                                 // remote-copy reads of the task: bounds the extra
+        for (int64_t s : t.subs)                          // import entries of each new bin
+            for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) {
+                const int32_t g = P.copy_global[k];
+                for (int64_t q = P.seg_ptr[g]; q < P.seg_ptr[g + 1]; ++q) xr_t += copy_chunk[P.seg_copy[q]] != c;
+            }
+        int64_t grow = 32 * per_slot * ((int64_t)bins.size() - 2) + 8 * xr_t * extra;   // 32 slots per R = 1 task
         for (auto& b : bins) grow += E * 32 * b.kmax;
         grow -= E * 64 * t.kmax;
         if (grow > smem_room) continue;
@@ -164,23 +172,42 @@ void split_tasks(const Canon& P, std::vector<TaskR>& tasks, const std::vector<in
     tasks.swap(out);
 }
 
-// exact SMEM bytes of a chunk (blob + xg scratch); mirrors the blob layout built below
+// exact SMEM bytes of a chunk; mirrors the blob layout built below.  Ghost slots: one per copy owned by
+// another chunk of a global this chunk touches (nu - copies here); import entries: per task, the remote
+// copies of the globals of its rows.
 int64_t chunk_bytes(const Canon& P, const std::vector<int64_t>& subs, std::vector<int32_t>& cnt, const int64_t E) {
     auto tasks = make_tasks(P, subs);
-    int64_t NS = 0, pool = 0, NG = 0, NSEG = 0;
+    int64_t NS = 0, pool = 0, NG = 0, NSEG = 0, NGH = 0, NIMP = 0;
     int kpad = 0;
     for (auto& t : tasks) { NS += 64; pool += (int64_t)t.kmax * 64; kpad = std::max(kpad, t.kmax); }
+    std::vector<int32_t> touched;
     for (int64_t s : subs)
         for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) {
             const int32_t g = P.copy_global[k];
-            if (cnt[g]++ == 0) { ++NG; NSEG += P.seg_ptr[g + 1] - P.seg_ptr[g]; }
+            if (cnt[g]++ == 0) { ++NG; touched.push_back(g); }
         }
-    for (int64_t s : subs)
-        for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) cnt[P.copy_global[k]] = 0;
-    const int64_t NT = (int64_t)tasks.size();
+    for (int32_t g : touched) {
+        const int64_t nu = P.seg_ptr[g + 1] - P.seg_ptr[g];
+        NGH += nu - cnt[g];
+        if (nu > 4) NSEG += nu;
+    }
+    for (auto& t : tasks) {                                      // distinct globals per task (cnt < 0: seen)
+        std::vector<int32_t> seen;
+        for (int64_t s : t.subs)
+            for (int64_t k = P.sub_ptr[s]; k < P.sub_ptr[s + 1]; ++k) {
+                const int32_t g = P.copy_global[k];
+                if (cnt[g] < 0) continue;
+                NIMP += (P.seg_ptr[g + 1] - P.seg_ptr[g]) - cnt[g];
+                cnt[g] = -cnt[g];
+                seen.push_back(g);
+            }
+        for (int32_t g : seen) cnt[g] = -cnt[g];
+    }
+    for (int32_t g : touched) cnt[g] = 0;
+    const int64_t NT = (int64_t)tasks.size(), NX = NS + 1 + NGH;
     int64_t b = 0;
-    for (int64_t sz : {E * pool, E * NS, 4 * E * NG, 16 * NT, 4 * NS, 4 * NS, 8 * NG, 4 * NSEG, 4 * NG,
-                       (int64_t)4 * 64, E * NS, E * NS, E * NS, E * NS, 2 * E * NG, E * (64 + kpad) * (kResBlock / 32)})
+    for (int64_t sz : {E * pool, E * NS, 4 * E * NG, 16 * NT, 4 * NS, 4 * NS, 16 * NG, 8 * NG, 4 * NSEG, 8 * NIMP,
+                       E * NX, E * NX, E * NX, E * NX, 2 * E * NG, E * (64 + kpad) * (kResBlock / 32)})
         b = a16(b + sz);
     return b;
 }
@@ -340,18 +367,42 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
             }
         const int64_t NG = (int64_t)gl_list.size();
         if (NG >= (1 << (31 - kResGlShift))) { err = "too many globals in one CTA chunk"; return LOPF_E_ARG; }
+        // own slots [0, NS), the zero slot NS, ghost slots NS + 1 + i: one per copy owned by another chunk
+        // (its u imported from the exchange buffer by every task that reads it, x = u and lambda = 0)
+        std::map<int32_t, int32_t> ghost;                            // remote copy -> ghost slot
         int64_t NSEG = 0;
-        for (int32_t g : gl_list) NSEG += P.seg_ptr[g + 1] - P.seg_ptr[g];
-        const int64_t NT = (int64_t)tasks.size();
-        // neighbour CTAs: owners of the remote copies this chunk's segments read
-        std::vector<int32_t> nbrs;
-        for (int32_t g : gl_list)
+        for (int64_t j = 0; j < NG; ++j) {
+            const int32_t g = gl_list[j];
+            const int64_t nu = P.seg_ptr[g + 1] - P.seg_ptr[g];
+            if (nu > 255) { err = "a global with more than 255 copies (resident kernel)"; return LOPF_E_ARG; }
+            if (nu > 4) NSEG += nu;
             for (int64_t p = P.seg_ptr[g]; p < P.seg_ptr[g + 1]; ++p) {
-                const int32_t oc = copy_chunk[P.seg_copy[p]];
-                if (oc != c && std::find(nbrs.begin(), nbrs.end(), oc) == nbrs.end()) nbrs.push_back(oc);
+                const int32_t k = P.seg_copy[p];
+                if (copy_chunk[k] != c) ghost.emplace(k, (int32_t)(NS + 1 + (int64_t)ghost.size()));
             }
-        std::sort(nbrs.begin(), nbrs.end());
-        const int64_t NNB = (int64_t)nbrs.size();
+        }
+        const int64_t NGH = (int64_t)ghost.size(), NX = NS + 1 + NGH;
+        // per task: the remote copies of the globals its rows read (each imported once per task)
+        std::vector<int2> imp;
+        for (size_t t = 0; t < tasks.size(); ++t) {
+            const int32_t i0 = (int32_t)imp.size();
+            std::vector<int32_t> seen;
+            for (int64_t s : tasks[t].subs)
+                for (int r = 0; r < P.n_s[s]; ++r) {
+                    const int32_t g = P.copy_global[P.sub_ptr[s] + r];
+                    if (std::find(seen.begin(), seen.end(), g) != seen.end()) continue;
+                    seen.push_back(g);
+                    for (int64_t p = P.seg_ptr[g]; p < P.seg_ptr[g + 1]; ++p) {
+                        const int32_t k = P.seg_copy[p];
+                        if (copy_chunk[k] != c) imp.push_back(make_int2(xidx[k], ghost.at(k)));
+                    }
+                }
+            const int32_t n = (int32_t)imp.size() - i0;
+            if (n > 255 || i0 >= (1 << 19)) { err = "too many boundary imports in one resident task"; return LOPF_E_ARG; }
+            trec[t].w = tasks[t].R | (n << 4) | (i0 << 12);
+        }
+        const int64_t NIMP = (int64_t)imp.size();
+        const int64_t NT = (int64_t)tasks.size();
         int32_t o = 0;
         h.off_abar = o;     o = a16(o + E * pool);
         h.off_bbar = o;     o = a16(o + E * NS);
@@ -359,33 +410,35 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
         h.off_tasks = o;    o = a16(o + 16 * NT);
         h.off_sinfo = o;    o = a16(o + 4 * NS);
         h.off_sexp = o;     o = a16(o + 4 * NS);
-        h.off_gsegoff = o;  o = a16(o + 8 * NG);                     // int2 descriptor per global
+        h.off_grec = o;     o = a16(o + 16 * NG);                    // int4 per global: SMEM slots of 4 copies
+        h.off_gxb = o;      o = a16(o + 8 * NG);                     // int2 per global: {first entry, nu} if nu > 4
         h.off_gseg = o;     o = a16(o + 4 * NSEG);
-        h.off_gown = o;     o = a16(o + 4 * NG);
-        h.off_nbr = o;      o = a16(o + 4 * std::max<int64_t>(NNB, 64));
-        h.off_xl0 = o;      o = a16(o + E * NS);
-        h.off_lam0 = o;     o = a16(o + E * NS);
+        h.off_gimp = o;     o = a16(o + 8 * NIMP);                   // int2 per import: {exchange index, ghost slot}
+        h.off_xl0 = o;      o = a16(o + E * NX);
+        h.off_lam0 = o;     o = a16(o + E * NX);
         h.blob_bytes = o;
-        h.off_xl1 = o;      o = a16(o + E * NS);
-        h.off_lam1 = o;     o = a16(o + E * NS);
+        h.off_gown = o;                                              // blob only (not copied to SMEM)
+        const int32_t blob_alloc = a16(o + 4 * NG);
+        h.off_xl1 = o;      o = a16(o + E * NX);
+        h.off_lam1 = o;     o = a16(o + E * NX);
         h.off_xout = o;     o = a16(o + 2 * E * NG);
         h.off_dst = o;      o = a16(o + E * (64 + kpad) * (kResBlock / 32));   // d staging; tail stays 0
         h.dst_stride = 64 + kpad;
         h.smem_bytes = o;
         if (h.smem_bytes > kResSmemBudget) { err = "internal: chunk exceeds the SMEM budget"; return LOPF_E_ARG; }
         h.n_tasks = (int32_t)NT; h.n_slots = (int32_t)NS; h.n_glob = (int32_t)NG; h.n_seg = (int32_t)NSEG;
-        h.n_nbr = (int32_t)NNB;
+        h.n_ghost = (int32_t)NGH;
         h.slot_base = slot_base;
         max_smem = std::max(max_smem, h.smem_bytes);
         std::vector<uint8_t>& blob = B[c].blob;
-        blob.assign(h.blob_bytes, 0);
+        blob.assign(blob_alloc, 0);
         auto put = [&](int32_t off, size_t i, double v) {          // (T) arrays: fp64, or rounded once to fp32
             if (E == 8) reinterpret_cast<double*>(blob.data() + off)[i] = v;
             else reinterpret_cast<float*>(blob.data() + off)[i] = (float)v;
         };
         auto I = [&](int32_t off) { return (int32_t*)(blob.data() + off); };
         std::memcpy(blob.data() + h.off_tasks, trec.data(), 16 * NT);
-        std::memcpy(blob.data() + h.off_nbr, nbrs.data(), 4 * NNB);
+        std::memcpy(blob.data() + h.off_gimp, imp.data(), 8 * NIMP);
 
         int32_t* sinfo = I(h.off_sinfo);
         int32_t* sexp = I(h.off_sexp);
@@ -404,7 +457,8 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
                     const int64_t copy = P.sub_ptr[s] + r;
                     const int32_t g = P.copy_global[copy];
                     const bool first = P.seg_copy[P.seg_ptr[g]] == copy;     // canonical first copy: writes x_g
-                    sinfo[slot] = (base & 0x3F) | kResValid | (first ? kResFirst : 0) | (ns << kResNsShift) |
+                    const int64_t nu = P.seg_ptr[g + 1] - P.seg_ptr[g];
+                    sinfo[slot] = (base & 0x3F) | kResValid | (first ? kResFirst : 0) | (nu > 4 ? kResSlow : 0) |
                                   (gl_of[g] << kResGlShift);
                     sexp[slot] = xidx[copy];
                     put(h.off_bbar, slot, P.bbar[copy]);
@@ -416,29 +470,37 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
             }
         }
 
-        int32_t* segoff = I(h.off_gsegoff);
+        int32_t* grec = I(h.off_grec);
+        int32_t* gxb = I(h.off_gxb);
         int32_t* seg = I(h.off_gseg);
         int32_t* gown = I(h.off_gown);
         int32_t q = 0;
         for (int64_t j = 0; j < NG; ++j) {
             const int32_t g = gl_list[j];
-            const double nu = (double)(P.seg_ptr[g + 1] - P.seg_ptr[g]);
+            const int64_t nu = P.seg_ptr[g + 1] - P.seg_ptr[g];
             put(h.off_gpar, 4 * j, P.c[g] / opt.rho);
-            put(h.off_gpar, 4 * j + 1, 1.0 / nu);
+            put(h.off_gpar, 4 * j + 1, 1.0 / (double)nu);
             put(h.off_gpar, 4 * j + 2, P.lo[g]);
             put(h.off_gpar, 4 * j + 3, P.hi[g]);
-            const int32_t q0 = q;
-            int jx = 4, nbnd = 0;
-            for (int64_t p = P.seg_ptr[g]; p < P.seg_ptr[g + 1]; ++p) {
-                const int32_t k = P.seg_copy[p];                 // canonical ascending copy order
-                seg[q] = copy_chunk[k] == c ? (L.slot_of_copy[k] - slot_base) : -(1 + xidx[k]);
-                if (seg[q] < 0 && q - q0 < 4) { if (jx == 4) jx = q - q0; ++nbnd; }
-                ++q;
+            auto smem_slot = [&](int32_t k) { return copy_chunk[k] == c ? L.slot_of_copy[k] - slot_base : ghost.at(k); };
+            for (int k = 0; k < 4; ++k) grec[4 * j + k] = (int32_t)NS;           // the zero slot
+            gxb[2 * j] = gxb[2 * j + 1] = 0;
+            if (nu > 4) {                                        // the whole list, canonical order
+                gxb[2 * j] = q;
+                gxb[2 * j + 1] = (int32_t)nu;
+                for (int64_t p = P.seg_ptr[g]; p < P.seg_ptr[g + 1]; ++p) seg[q++] = smem_slot(P.seg_copy[p]);
+            } else {
+                for (int64_t p = P.seg_ptr[g]; p < P.seg_ptr[g + 1]; ++p)      // canonical ascending copy order
+                    grec[4 * j + (p - P.seg_ptr[g])] = smem_slot(P.seg_copy[p]);
             }
-            if (q - q0 > 255) { err = "a global with more than 255 copies (resident kernel)"; return LOPF_E_ARG; }
-            segoff[2 * j] = q0;                                   // {first entry, nu | first boundary << 8 | several << 12}
-            segoff[2 * j + 1] = (q - q0) | (jx << 8) | (nbnd > 1 ? 1 << 12 : 0);
             gown[j] = copy_chunk[P.seg_copy[P.seg_ptr[g]]] == c ? g : -1;
+        }
+        if (std::getenv("LOPF_PACK_DEBUG")) {           // diagnostics: one line per CTA chunk
+            int nsl = 0, nexp = 0, kmx = 0, imx = 0;
+            for (int64_t i = 0; i < NS; ++i) { nsl += (sinfo[i] & kResSlow) != 0; nexp += sexp[i] >= 0; }
+            for (size_t t = 0; t < tasks.size(); ++t) { kmx = std::max(kmx, tasks[t].kmax); imx = std::max(imx, (trec[t].w >> 4) & 0xFF); }
+            std::fprintf(stderr, "cta %d tasks %d slots %d glob %d smem %d ghost %d imp %d impmax %d slow %d exp %d kmax %d margin %.3f\n",
+                         c, (int)NT, (int)NS, (int)NG, h.smem_bytes, (int)NGH, (int)NIMP, imx, nsl, nexp, kmx, margin);
         }
         for (int32_t g : gl_list) gl_of[g] = -1;
         slot_base += (int32_t)NS;

@@ -71,7 +71,7 @@ __device__ __forceinline__ int Ii(int off, int i) { return reinterpret_cast<cons
 
 template <class T>                                 // T: element type of the SMEM state (fp64, or fp32: reading F1)
 struct Ctx {                                       // byte offsets into SMEM + the two exchange slots
-    int sinfo, sexp, sabar, sbbar, gsegoff, gseg, gpar;
+    int sinfo, sexp, sabar, sbbar, grec, gxb, gseg, gimp, gpar;
     int xl_c, lam_c, xl_n, lam_n, xout_n, dst;
     const double2* xch_c;                          // {u, tag} entries of state t / t+1 (u widened to fp64)
     double2* xch_n;
@@ -97,68 +97,60 @@ __device__ __forceinline__ void ld_entry_once(const double2* p, unsigned long lo
                  : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
 }
 
-// value of one consensus-segment entry: u of an own copy (SMEM) or of a boundary copy (exchange buffer)
+// u of the copy in SMEM slot e (own, ghost or zero slot)
 template <class T>
-__device__ __forceinline__ T seg_u(const Ctx<T>& C, const int e) {
-    return e >= 0 ? u_of<T>(Dt<T>(C.xl_c, e), Dt<T>(C.lam_c, e), C.inv_rho) : (T)ld_entry(C.xch_c + (-e - 1), C.tag_c);
+__device__ __forceinline__ T u_at(const Ctx<T>& C, const int e) {
+    return u_of<T>(Dt<T>(C.xl_c, e), Dt<T>(C.lam_c, e), C.inv_rho);
 }
 
-// one task of 32R rows (tr.w = R): lane l owns rows l (and l + 32 when R = 2: two dependency chains)
+// one task of 32R rows (tr.w = R | imports << 4 | first import << 12): lane l owns rows l (and l + 32 when R = 2: two dependency chains)
 template <int R, class T>
 __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, double (&acc)[5], const int lane) {
     constexpr int E = sizeof(T);
     using T2 = typename V2<T>::type;
+    // boundary values first: the u of every copy owned by another CTA that this task's rows read, from the
+    // exchange buffer into the CTA's ghost slots (x = u, lambda = 0).  All entries of the task are requested
+    // before any is waited on (one L2 round trip), each lane spinning until its entry's tag says "state t".
+    {
+        const int nimp = (tr.w >> 4) & 0xFF, i0 = tr.w >> 12;
+        if (nimp > 0) {
+            const int2* im = reinterpret_cast<const int2*>(sm + C.gimp) + i0;
+            const int2 a = lane < nimp ? im[lane] : make_int2(0, 0);
+            const int2 b = lane + 32 < nimp ? im[lane + 32] : make_int2(0, 0);
+            unsigned long long alo = 0, ahi = C.tag_c, blo = 0, bhi = C.tag_c;
+            if (lane < nimp) ld_entry_once(C.xch_c + a.x, alo, ahi);
+            if (lane + 32 < nimp) ld_entry_once(C.xch_c + b.x, blo, bhi);
+            for (int i = lane + 64; i < nimp; i += 32) {              // (> 64 imports: rare)
+                const int2 c = im[i];
+                Dt<T>(C.xl_c, c.y) = (T)ld_entry(C.xch_c + c.x, C.tag_c);
+            }
+            while (ahi != C.tag_c) ld_entry_once(C.xch_c + a.x, alo, ahi);
+            while (bhi != C.tag_c) ld_entry_once(C.xch_c + b.x, blo, bhi);
+            if (lane < nimp) Dt<T>(C.xl_c, a.y) = (T)__longlong_as_double((long long)alo);
+            if (lane + 32 < nimp) Dt<T>(C.xl_c, b.y) = (T)__longlong_as_double((long long)blo);
+            __syncwarp();
+        }
+    }
     T v[2], lam[2], xo[2];
-    int info[2];
-    // a4 for both rows without per-row branches (invalid rows read global 0 and are discarded), so the
-    // SMEM dependency chains of the two rows interleave; only a boundary entry leaves the straight line
-    int gl[2], q0[2], nq[2], e[2][4], jxm[2];
-#pragma unroll
-    for (int h = 0; h < R; ++h) {
-        info[h] = Ii(C.sinfo, tr.x + h * 32 + lane);
-        const bool val = info[h] & kResValid;
-        gl[h] = val ? info[h] >> kResGlShift : 0;
-        // per-global descriptor {first entry, nu | first boundary position << 8 | several boundaries << 12}
-        const int2 gd = reinterpret_cast<const int2*>(sm + C.gsegoff)[gl[h]];
-        q0[h] = gd.x;
-        nq[h] = val ? (gd.y & 0xFF) : 0;
-        jxm[h] = val ? gd.y >> 8 : 4;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) e[h][j] = Ii(C.gseg, q0[h] + (j < nq[h] ? j : 0));
-    }
-    // the first boundary entry of each row is requested before any is consumed (one L2 round trip for
-    // both rows instead of one per row; a second boundary entry of a row, rare, is read on its own)
-    int jx[2], ex[2];
-    unsigned long long xlo[2], xhi[2];
-#pragma unroll
-    for (int h = 0; h < R; ++h) {
-        jx[h] = jxm[h] & 0xF;
-        ex[h] = jx[h] == 0 ? e[h][0] : jx[h] == 1 ? e[h][1] : jx[h] == 2 ? e[h][2] : e[h][3];
-        xlo[h] = 0ull;
-        xhi[h] = C.tag_c;
-        if (jx[h] < 4) ld_entry_once(C.xch_c + (-ex[h] - 1), xlo[h], xhi[h]);
-    }
+    int info[2], gl[2];
+    // a4 for both rows, straight-line from SMEM: the four entries of the global's record (own, ghost or zero
+    // slots) summed in canonical copy order; nu > 4 walks the global's slot list
     T sig[2];
 #pragma unroll
     for (int h = 0; h < R; ++h) {
-        sig[h] = T(0);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int ee = e[h][j] >= 0 ? e[h][j] : 0;
-            T u = u_of<T>(Dt<T>(C.xl_c, ee), Dt<T>(C.lam_c, ee), C.inv_rho);
-            if (j == jx[h]) {
-                while (xhi[h] != C.tag_c) ld_entry_once(C.xch_c + (-ex[h] - 1), xlo[h], xhi[h]);
-                u = (T)__longlong_as_double((long long)xlo[h]);
-            } else if ((jxm[h] & 0x10) && j < nq[h] && e[h][j] < 0) {      // a second boundary entry (rare)
-                u = (T)ld_entry(C.xch_c + (-e[h][j] - 1), C.tag_c);
-            }
-            if (j < nq[h]) sig[h] += u;                                  // canonical copy order
+        info[h] = Ii(C.sinfo, tr.x + h * 32 + lane);
+        gl[h] = info[h] >> kResGlShift;                                  // an empty row: global 0, discarded
+        const int4 rc = reinterpret_cast<const int4*>(sm + C.grec)[gl[h]];
+        sig[h] = ((u_at<T>(C, rc.x) + u_at<T>(C, rc.y)) + u_at<T>(C, rc.z)) + u_at<T>(C, rc.w);
+        if (info[h] & kResSlow) {
+            const int2 sl = reinterpret_cast<const int2*>(sm + C.gxb)[gl[h]];   // {first entry, nu}
+            sig[h] = T(0);
+            for (int q = 0; q < sl.y; ++q) sig[h] += u_at<T>(C, Ii(C.gseg, sl.x + q));
         }
     }
 #pragma unroll
     for (int h = 0; h < R; ++h) {
         const int slot = tr.x + h * 32 + lane;
-        for (int q = 4; q < nq[h]; ++q) sig[h] += seg_u<T>(C, Ii(C.gseg, q0[h] + q));
         const T2 g0 = reinterpret_cast<const T2*>(sm + C.gpar)[2 * gl[h]];       // {c/rho, 1/nu}
         const T2 g1 = reinterpret_cast<const T2*>(sm + C.gpar)[2 * gl[h] + 1];   // {lo, hi}
         const T xg = fmin(fmax((sig[h] - g0.x) * g0.y, g1.x), g1.y);   // IEEE +-inf = no clamp
@@ -248,9 +240,13 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     const int NS = H.n_slots, NG = H.n_glob, NT = H.n_tasks;
     const int dst_stride = H.dst_stride;                              // 64 + largest task width, doubles
     for (int i = tid; i < RW * dst_stride; i += RB) Dt<T>(H.off_dst, i) = T(0);   // zero tail of the d staging
+    for (int i = NS + tid; i <= NS + H.n_ghost; i += RB) {       // zero and ghost slots of parity 1
+        Dt<T>(H.off_xl1, i) = T(0);
+        Dt<T>(H.off_lam1, i) = T(0);
+    }
     Ctx<T> C;
     C.sinfo = H.off_sinfo; C.sexp = H.off_sexp; C.sabar = H.off_abar; C.sbbar = H.off_bbar;
-    C.gsegoff = H.off_gsegoff; C.gseg = H.off_gseg; C.gpar = H.off_gpar;
+    C.grec = H.off_grec; C.gxb = H.off_gxb; C.gseg = H.off_gseg; C.gimp = H.off_gimp; C.gpar = H.off_gpar;
     C.dst = H.off_dst + E * wid * dst_stride;
     C.rho = (T)P.rho;
     C.inv_rho = (T)P.inv_rho;
@@ -359,7 +355,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                 C.tag_n = tag_of(t + 1);
                 for (int task = wid; task < NT; task += NWORK) {
                     const int4 tr = reinterpret_cast<const int4*>(sm + H.off_tasks)[task];
-                    if (tr.w == 1) task_sweep<1, T>(C, tr, acc, lane);
+                    if ((tr.w & 0xF) == 1) task_sweep<1, T>(C, tr, acc, lane);
                     else task_sweep<2, T>(C, tr, acc, lane);
                 }
 #if LOPF_RES_TIMELINE == 2
@@ -369,13 +365,11 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                         const int4 tr = reinterpret_cast<const int4*>(sm + H.off_tasks)[task];
                         km = km > tr.y ? km : tr.y;
                         ++nt;
-                        for (int h = 0; h < (tr.w == 1 ? 1 : 2); ++h) {
+                        for (int h = 0; h < ((tr.w & 0xF) == 1 ? 1 : 2); ++h) {
                             const int inf = Ii(C.sinfo, tr.x + h * 32 + lane);
                             if (!(inf & kResValid)) continue;
                             ++rows;
-                            const int gl = inf >> kResGlShift;
-                            const int2 gd = reinterpret_cast<const int2*>(sm + C.gsegoff)[gl];
-                            for (int q = gd.x; q < gd.x + (gd.y & 0xFF); ++q) xr += Ii(C.gseg, q) < 0;
+                            xr += (inf & kResSlow) != 0;
                         }
                     }
                     for (int off = 16; off > 0; off >>= 1) {
@@ -411,8 +405,9 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
             __stcg(gl + i, Dt<T>(olm, i));
         }
     }
+    const int* gown = reinterpret_cast<const int*>(blob + H.off_gown);  // global memory (not staged in SMEM)
     for (int j = tid; j < NG; j += RB) {
-        const int g = Ii(H.off_gown, j);
+        const int g = __ldg(gown + j);
         if (g >= 0) __stcg(reinterpret_cast<T*>(P.x) + g, Dt<T>(H.off_xout, fin * NG + j));
     }
 #if !LOPF_RES_TIMELINE
