@@ -343,7 +343,10 @@ lopf_status pack_resident(const Net& N, const Canon& P, const lopf_options& opt,
     std::vector<int32_t> gl_of(P.n, -1);
     for (int c = 0; c < L.G; ++c) {
         auto tasks = make_tasks(P, chunks[c].subs);
-        if (L.G <= 16)          // small feeders only: 123 shape 3.43 -> 3.31 us/sweep, 8500 shape 4.53 -> 4.73
+#ifndef LOPF_RES_SPLIT_MAXG
+#define LOPF_RES_SPLIT_MAXG 16
+#endif
+        if (L.G <= LOPF_RES_SPLIT_MAXG)   // round 1: 123 shape 3.43 -> 3.31 us/sweep, 8500 shape 4.53 -> 4.73
             split_tasks(P, tasks, copy_chunk, c, kResBlock / 32 - 1,
                         kResSmemBudget - 512 - chunk_bytes(P, chunks[c].subs, cnt, E), E);
         CtaHdr& h = B[c].h;

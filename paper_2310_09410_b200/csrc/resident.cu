@@ -5,19 +5,20 @@
 // the iterate then stays on chip for the whole solve, ping-ponged by sweep parity.  Iteration t
 // (state t known) computes sweep t+1:
 //   workers (all warps but one), one lane per row slot of a packed task:
+//     import: the u of every copy owned by another CTA that the task reads, from the exchange buffer
+//         (16-byte {u, tag} entries, spinning until the tag says "state t") into the CTA's ghost slots
 //     a4  x_g = clamp((sum_{k in seg(g)} u_k - c_g/rho) / nu_g, lo_g, hi_g)   (closed_1, rho restored;
-//         PAPER.md:305-310, reading C1) in canonical copy order; u_k = x_k - lambda_k/rho is formed from
-//         SMEM for this CTA's copies; a boundary copy (owned by another CTA) is read from the exchange
-//         buffer as a 16-byte {u, tag} entry, spinning until its tag says "state t"
+//         PAPER.md:305-310, reading C1) in canonical copy order, u_k = x_k - lambda_k/rho from SMEM
 //     a5  d = -rho v - lambda, x_s = (1/rho) Abar_s d + bbar_s                  (closed_2)
 //     a6  lambda_s += rho (v - x_s)                                            (ADMM-3)
 //         each exported copy's u goes out at once as {u, tag of state t+1}; five residual sums per lane
 //   reducer (1 warp), concurrently: publishes this CTA's residual partials of sweep t (summed by the
-//     workers in iteration t-1), waits until every CTA has, reduces them in CTA order and takes the
-//     (termination) decision for sweep t, identical in every CTA.
+//     workers in iteration t-1) as parity-signed 16-byte entries; CTA 0's reducer gathers them all,
+//     reduces them in CTA order, takes the (termination) decision for sweep t and
+//     publishes it as one tagged entry, which every other reducer waits for.
 //   one CTA barrier; a stop at t discards the speculative sweep t+1 (state t is the other buffer).
-// No flags, fences or grid barrier inside the loop: a CTA waits only for the boundary values it reads,
-// each entry written by one 128-bit store (value and tag travel together).  Two parity slots suffice:
+// No flags, fences or grid barrier inside the loop: a CTA waits only for the values it reads, each
+// entry written by one 128-bit store (value and tag travel together).  Two parity slots suffice:
 // the copy of a shared global that a CTA writes for state t+2 depends on every copy of that global at
 // state t+1, and those are written only after their owners have read the state-t entries.  Tags
 // carry the launch number, so entries from earlier launches never match.
@@ -43,6 +44,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef LOPF_DIAG_SKIP
 #define LOPF_DIAG_SKIP 0                   // diagnostics builds only: bit 1 skips the update work (sync cost alone)
 #endif
+#ifndef LOPF_RES_CLAMP_SEL
+#define LOPF_RES_CLAMP_SEL 1
+#endif
 #ifndef LOPF_RES_SLEEP
 #define LOPF_RES_SLEEP 20                  // reducer poll back-off (ns)
 #endif
@@ -50,8 +54,6 @@ constexpr int kUnroll = LOPF_RES_UNROLL;
 constexpr int kPer = 5;                    // flags / partials per reducer lane per round (G <= 160 in one round)
 
 __device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p) { return dev::ld_acquire_u64(p); }
-__device__ __forceinline__ unsigned long long ld_rlx(const unsigned long long* p) { return dev::ld_relaxed_u64(p); }
-using dev::fence_acq_rel;
 using dev::warp_sum5;
 
 // consensus input u = x_s - lambda / rho, formed with the same rounding wherever it is needed
@@ -90,6 +92,23 @@ __device__ __forceinline__ double ld_entry(const double2* p, const unsigned long
                      : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
     } while (hi != tag);
     return __longlong_as_double(lo);
+}
+
+// raw 128-bit entry access (single-copy atomic at gpu scope)
+__device__ __forceinline__ void st_pair(double2* p, const unsigned long long lo, const unsigned long long hi) {
+    asm volatile("{\n .reg .b128 v;\n mov.b128 v, {%1, %2};\n st.relaxed.gpu.global.b128 [%0], v;\n}"
+                 ::"l"(p), "l"(lo), "l"(hi) : "memory");
+}
+__device__ __forceinline__ void ld_pair(const double2* p, unsigned long long& lo, unsigned long long& hi) {
+    asm volatile("{\n .reg .b128 v;\n ld.relaxed.gpu.global.b128 v, [%2];\n mov.b128 {%0, %1}, v;\n}"
+                 : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
+}
+// residual partial (>= 0 or NaN) with the sweep parity bit in its sign bit, and back
+__device__ __forceinline__ unsigned long long enc_par(const double v, const unsigned long long par) {
+    return ((unsigned long long)__double_as_longlong(v) & ~(1ull << 63)) | par;
+}
+__device__ __forceinline__ double dec_par(const unsigned long long b) {
+    return __longlong_as_double((long long)(b & ~(1ull << 63)));
 }
 
 __device__ __forceinline__ void ld_entry_once(const double2* p, unsigned long long& lo, unsigned long long& hi) {
@@ -153,7 +172,15 @@ __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, doubl
         const int slot = tr.x + h * 32 + lane;
         const T2 g0 = reinterpret_cast<const T2*>(sm + C.gpar)[2 * gl[h]];       // {c/rho, 1/nu}
         const T2 g1 = reinterpret_cast<const T2*>(sm + C.gpar)[2 * gl[h] + 1];   // {lo, hi}
-        const T xg = fmin(fmax((sig[h] - g0.x) * g0.y, g1.x), g1.y);   // IEEE +-inf = no clamp
+        // clamp to [lo, hi] with the semantics of fmin(fmax(y, lo), hi) (a NaN y gives lo; IEEE +-inf = no
+        // clamp) in two compare-selects
+        const T y = (sig[h] - g0.x) * g0.y;
+#if LOPF_RES_CLAMP_SEL
+        const T ylo = y > g1.x ? y : g1.x;
+        const T xg = ylo < g1.y ? ylo : g1.y;
+#else
+        const T xg = fmin(fmax(y, g1.x), g1.y);
+#endif
         const bool val = info[h] & kResValid;
         if (val && (info[h] & kResFirst)) Dt<T>(C.xout_n, gl[h]) = xg;
         v[h] = val ? xg : T(0);
@@ -199,10 +226,12 @@ __device__ __forceinline__ void task_sweep(const Ctx<T>& C, const int4 tr, doubl
     }
 }
 
-constexpr int kFlagStride = 32;                    // one flag per 256-byte line (no L2 hot spot)
 
 #if LOPF_RES_TIMELINE == 1   // diagnostics build: per-warp clock64 events of CTA G/2, sweeps 500..502, into P.prof
-#define TL(e) do { if (P.prof && cta == G / 2 && t >= 500 && t < 503 && lane == 0) \
+#ifndef LOPF_RES_TL_CTA
+#define LOPF_RES_TL_CTA (G / 2)
+#endif
+#define TL(e) do { if (P.prof && cta == LOPF_RES_TL_CTA && t >= 500 && t < 503 && lane == 0) \
     P.prof[((t - 500) * RW + wid) * 8 + (e)] = clock64(); } while (0)
 #elif LOPF_RES_TIMELINE == 2  // every CTA, sweeps 500..503: cycles from each warp's loop top to its work end
                               // (event 1; slot = warp) and, for warp 0, to the end-of-iteration barrier (slot 31)
@@ -250,7 +279,7 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
     C.dst = H.off_dst + E * wid * dst_stride;
     C.rho = (T)P.rho;
     C.inv_rho = (T)P.inv_rho;
-    unsigned long long* pub = P.flags + (size_t)G * kFlagStride;       // CTAs x sweeps published
+    double2* dec = reinterpret_cast<double2*>(P.flags);                  // {decision bits, tag of sweep t}
     const long long total0 = *(volatile long long*)&P.ctrl->total;
 #ifndef LOPF_RES_PROF
 #define LOPF_RES_PROF 0                           // 1: per-CTA phase counters (lopf_get_profile, diagnostics builds)
@@ -283,53 +312,88 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
         TL(0);
         if (wid == RED) {
             if (t >= 1) {
-                // this CTA's residual partials of sweep t (the workers' sums of iteration t-1), then the
-                // decision for sweep t once every CTA has published its own
-                if (lane < 5) {
-                    double sk = 0.0;
-                    for (int w = 0; w < NWORK; ++w) sk += red[cur][w][lane];
-                    __stcg(P.partial + (size_t)(t & 3) * G * 8 + (size_t)cta * 8 + lane, sk);
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    fence_acq_rel();                   // release: partials before the published count
-                    asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pub) : "memory");
-                }
-                const unsigned long long need = (unsigned long long)G * (unsigned long long)t;
-                while (ld_rlx(pub) < need) __nanosleep(LOPF_RES_SLEEP);
-                __syncwarp();
-                fence_acq_rel();
-                double ps[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-                const double* part = P.partial + (size_t)(t & 3) * G * 8;
-                for (int b0 = 0; b0 < G; b0 += 32 * kPer) {
-                    double pv[kPer][5];
+                // this CTA's residual partials of sweep t (the workers' sums of iteration t-1), published as
+                // three 16-byte entries {s0, s1} {s2, s3} {s4, s4} in slot u & 3 (u = t - 1: publications are
+                // numbered from 0 in each launch); the sign bit of each (non-negative) value carries (u >> 2) & 1,
+                // so the reader tells this publication from the one four earlier with no flag and no fence (each
+                // entry is one 128-bit access).  The launch fills the slots with sign bit 1: u = 0..3 never match
+                // them, and u >= 4 finds its slot written at least once before (per-location coherence).
+                const long long u = t - 1;
+                const int slot = (int)(u & 3);
+                const unsigned long long par = (unsigned long long)((u >> 2) & 1) << 63;
+                double2* part = reinterpret_cast<double2*>(P.partial) + (size_t)slot * G * 4;
+                {
+                    double sk = 0.0;                   // four interleaved chains, combined in a fixed order
+                    if (lane < 5) {
+                        double q4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                    for (int j = 0; j < kPer; ++j) {
-                        const int b = b0 + j * 32 + lane;
-#pragma unroll
-                        for (int k = 0; k < 5; ++k) pv[j][k] = b < G ? __ldcg(part + (size_t)b * 8 + k) : 0.0;
+                        for (int w = 0; w < NWORK; ++w) q4[w & 3] += red[cur][w][lane];
+                        sk = (q4[0] + q4[1]) + (q4[2] + q4[3]);
                     }
+                    const double a = __shfl_sync(kFull, sk, 2 * lane < 5 ? 2 * lane : 4);
+                    const double b = __shfl_sync(kFull, sk, 2 * lane + 1 < 5 ? 2 * lane + 1 : 4);
+                    if (lane < 3) st_pair(part + (size_t)cta * 4 + lane, enc_par(a, par), enc_par(b, par));
+                }
+                TL(3);
+                // the decision: CTA 0's reducer gathers every CTA's entries (lane l: CTAs l, l + 32, ...), sums
+                // them in CTA order per lane then across lanes (fixed order), decides and publishes one tagged
+                // entry; every other CTA's reducer waits for that entry
+                double ps[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+                if (cta == 0) {
+                    unsigned long long ev[kPer][3][2];
+                    unsigned pend = 0;                 // entries of this lane still to be (re)read
+#pragma unroll
+                    for (int j = 0; j < kPer; ++j)
+                        if (j * 32 + lane < G) pend |= 7u << (3 * j);
 #pragma unroll
                     for (int j = 0; j < kPer; ++j)
 #pragma unroll
-                        for (int k = 0; k < 5; ++k) ps[k] += pv[j][k];     // CTA order per lane: fixed
-                }
+                        for (int e = 0; e < 3; ++e) { ev[j][e][0] = par; ev[j][e][1] = par; }
+                    while (pend) {                     // every stale entry re-requested together: one round trip
 #pragma unroll
-                for (int k = 0; k < 5; ++k) {
+                        for (int j = 0; j < kPer; ++j)
 #pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) ps[k] += __shfl_xor_sync(kFull, ps[k], off);
+                            for (int e = 0; e < 3; ++e)
+                                if (pend >> (3 * j + e) & 1) ld_pair(part + (size_t)(j * 32 + lane) * 4 + e, ev[j][e][0], ev[j][e][1]);
+#pragma unroll
+                        for (int j = 0; j < kPer; ++j)
+#pragma unroll
+                            for (int e = 0; e < 3; ++e)
+                                if (!(((ev[j][e][0] ^ par) | (ev[j][e][1] ^ par)) >> 63)) pend &= ~(1u << (3 * j + e));
+                    }
+                    TL(4);
+#pragma unroll
+                    for (int j = 0; j < kPer; ++j)
+#pragma unroll
+                        for (int k = 0; k < 5; ++k) ps[k] += dec_par(ev[j][k >> 1][k & 1]);   // CTA order per lane
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) {
+#pragma unroll
+                        for (int off = 16; off > 0; off >>= 1) ps[k] += __shfl_xor_sync(kFull, ps[k], off);
+                    }
                 }
-                if (lane == 0) {
-                    const double pres = sqrt(ps[0]), dres = P.rho * sqrt(ps[1]);
-                    const double ep = P.eps_rel * fmax(sqrt(ps[2]), sqrt(ps[3])), ed = P.eps_rel * sqrt(ps[4]);
-                    const int num = !(isfinite(ps[0]) && isfinite(ps[1]) && isfinite(ps[2]) && isfinite(ps[3]) &&
-                                      isfinite(ps[4]));
+                // the five square roots one per lane (every lane holds all five sums after the butterfly)
+                double rt = 0.0;
+                bool fin = true;
+                if (cta == 0) {
+                    const double mine = lane == 0 ? ps[0] : lane == 1 ? ps[1] : lane == 2 ? ps[2] : lane == 3 ? ps[3] : ps[4];
+                    rt = sqrt(mine);
+                    fin = __all_sync(kFull, lane >= 5 || isfinite(mine));
+                }
+                const double r1 = __shfl_sync(kFull, rt, 1), r2 = __shfl_sync(kFull, rt, 2);
+                const double r3 = __shfl_sync(kFull, rt, 3), r4 = __shfl_sync(kFull, rt, 4);
+                if (lane == 0 && cta == 0) {
+                    const double pres = rt, dres = P.rho * r1;
+                    const double ep = P.eps_rel * fmax(r2, r3), ed = P.eps_rel * r4;
+                    const int num = !fin;
                     const int conv = P.test && pres <= ep && dres <= ed;
                     const int q = (int)(t & 1);
                     s_res[q][0] = pres; s_res[q][1] = dres; s_res[q][2] = ep; s_res[q][3] = ed;
                     s_conv[q] = conv; s_num[q] = num;
                     s_stop[q] = conv || num || t >= P.max_iter;
-                    if (cta == 0 && P.trace_every > 0 && (t % P.trace_every) == 0) {
+                    TL(5);
+                    st_pair(dec, (unsigned long long)(s_stop[q] | (conv << 1) | (num << 2)), tag_of(t));   // decision of t
+                    if (P.trace_every > 0 && (t % P.trace_every) == 0) {
                         const long long row = t / P.trace_every - 1;
                         if (row < P.trace_cap) {
                             double* tr = P.trace + row * 5;
@@ -337,6 +401,18 @@ __global__ void __launch_bounds__(RB, 1) admm_resident_kernel(ResProblem P) {
                             P.ctrl->trace_rows = row + 1;
                         }
                     }
+                } else if (lane == 0 && cta != 0) {
+                    unsigned long long bits, tg;
+                    ld_pair(dec, bits, tg);
+                    while (tg != tag_of(t)) {
+                        if (LOPF_RES_SLEEP > 0) __nanosleep(LOPF_RES_SLEEP);
+                        ld_pair(dec, bits, tg);
+                    }
+                    TL(5);
+                    const int q = (int)(t & 1);
+                    s_stop[q] = (int)(bits & 1);
+                    s_conv[q] = (int)((bits >> 1) & 1);
+                    s_num[q] = (int)((bits >> 2) & 1);
                 }
             }
             TL(1);
@@ -494,6 +570,9 @@ lopf_status launch_resident(const ResProblem& P, void* stream, std::string& err)
     if (e == cudaSuccess) e = cudaMemsetAsync(P.ctrl, 0, 2 * sizeof(unsigned long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(&P.ctrl->trace_rows, 0, sizeof(long long), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(P.flags, 0, sizeof(unsigned long long) * 32 * (P.G + 1), s);
+    // partial entries: all sign bits set, i.e. "sweep parity 1", which the first sweeps (parity 0) never match
+    // and later sweeps only meet after their slot was written at parity 0 (per-location coherence)
+    if (e == cudaSuccess) e = cudaMemsetAsync(P.partial, 0xFF, sizeof(double) * 8 * 4 * P.G, s);
     if (e == cudaSuccess && P.max_iter > 0) {
         ResProblem Q = P;
         void* args[] = {&Q};
