@@ -1,7 +1,12 @@
-"""Build liblopf.so in-tree for sm_100a (nvcc; host C++ + CUDA in one shared library)."""
+"""Build liblopf.so in-tree for sm_100a (nvcc; host C++ + CUDA in one shared library).
+
+Every source compiles to its own object (in parallel, under build/<variant>/), then one nvcc link;
+`force` recompiles everything, otherwise an object is rebuilt when its source or a header is newer."""
+import hashlib
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -25,19 +30,46 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     so = out or SO
     if not force and out is None and not _stale():
         return SO
+    tag = hashlib.sha1(" ".join(sorted(defines)).encode()).hexdigest()[:10] if defines else "default"
+    objdir = os.path.join(ROOT, "build", tag)
+    os.makedirs(objdir, exist_ok=True)
+    flags = [*[f"-D{d}" for d in defines], "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v", "-Xcompiler",
+             "-fPIC,-O3,-Wall", "-I", os.path.join(ROOT, "include")]
+    hdr_t = max(os.path.getmtime(p) for p in HEADERS + [__file__])
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(src)):
+            return obj, None
+        res = subprocess.run([NVCC, *flags, "-c", src, "-o", obj + ".tmp"], capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError(f"nvcc failed compiling {os.path.basename(src)}")
+        os.replace(obj + ".tmp", obj)
+        return obj, res.stderr
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        done = list(ex.map(compile_one, SOURCES))
     tmp = so + f".tmp{os.getpid()}"
-    cmd = [NVCC, *[f"-D{d}" for d in defines], "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-O3,-Wall",
-           "-shared", "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES, "-lpthread", "-ldl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    res = subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *[o for o, _ in done], "-lpthread", "-ldl"],
+                         capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building liblopf.so")
+        raise RuntimeError("nvcc failed linking liblopf.so")
+    report = "".join(r for _, r in done if r)
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write(report)
     os.replace(tmp, so)
-    if out is None:
-        with open(os.path.join(HERE, "ptxas_report.txt"), "w") as fh:
-            fh.write(res.stderr)
+    if out is None and report:
+        # ptxas lines of the objects rebuilt now; the others keep their previous entries
+        path = os.path.join(HERE, "ptxas_report.txt")
+        old = open(path).read() if os.path.exists(path) else ""
+        rebuilt = {os.path.basename(s) for s, (_, r) in zip(SOURCES, done) if r}
+        names = {os.path.basename(s) for s in SOURCES}
+        keep = [blk for blk in old.split("\n### ") if blk and blk.split("\n", 1)[0].strip("# ") in names - rebuilt]
+        new = [f"{os.path.basename(s)}\n{r}" for s, (_, r) in zip(SOURCES, done) if r]
+        with open(path, "w") as fh:
+            fh.write("".join("### " + b.lstrip("# ") + ("\n" if not b.endswith("\n") else "") for b in keep + new))
     return so
 
 

@@ -8,14 +8,16 @@
 // subsystem s the warp computes, for its 32 scenarios at once,
 //   a4  x_g = clamp((sum_{k in seg(g)} u_k - c_g/rho) / nu_g, lo_g, hi_g) for each row (closed_1, rho
 //       restored, reading C1), canonical copy order; d = -rho v - lambda staged in SMEM [row][lane]
-//   a5  y = Abar_s d, four rows at a time (k ascending, FMA); Abar_s from the shared dense pool (uniform
-//       loads) or, for a load subsystem, the scenario's packed upper triangle ([entry][lane], coalesced)
+//   a5  y = Abar_s d, one row quad at a time (k ascending, FMA); Abar_s from the shared pool (row quads
+//       [k][4], one 4-wide uniform load per column) or, for a load subsystem, the scenario's quad-block
+//       upper layout ([entry][lane], coalesced, every operand at an immediate offset of one block pointer)
 //   a6  x_s = y / rho + bbar_s, lambda += rho (v - x_s), u = x_s - lambda / rho     (closed_2, ADMM-3)
 //   a7  five residual sums per lane (scenario), written per item
-// The ACTIVE items of a sweep (groups with a scenario still running, times tasks) are cut into one
-// contiguous chunk per warp by a per-task cost weight.  Grid barrier; one warp per active group then
-// sums each scenario's item partials in task order (deterministic) and takes its decision; converged
-// scenarios freeze (their lanes stop storing), a group leaves the item list when all 32 have; grid barrier.
+// The ACTIVE items of a sweep (groups with a scenario still running, times tasks) are handed out one at a
+// time from an atomic counter, costliest tasks first.  Grid barrier; one warp per active group then sums
+// each scenario's item partials in task order (deterministic whichever warp ran an item) and takes its
+// decision; converged scenarios freeze (their lanes stop storing), a group leaves the item list when all
+// 32 have; grid barrier.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -30,9 +32,6 @@ namespace {
 using dev::grid_sync;
 using dev::kFull;
 
-#ifndef LOPF_BATCH_KUNROLL
-#define LOPF_BATCH_KUNROLL 4                  // mat-vec column unroll (operator loads in flight: 4 rows x this)
-#endif
 #ifndef LOPF_BATCH_CROWS
 #define LOPF_BATCH_CROWS 4                    // consensus rows whose gathers are issued together
 #endif
@@ -42,24 +41,20 @@ using dev::kFull;
 #endif
 constexpr int BW = kBatchWarps;
 constexpr int CR = LOPF_BATCH_CROWS;
-constexpr int KU = LOPF_BATCH_KUNROLL;
 constexpr int BB = 32 * BW;
 
 template <class T> struct V2;                 // {c/rho, lo}, {hi, 1/nu} per global
 template <> struct V2<double> { using type = double2; };
 template <> struct V2<float> { using type = float2; };
 
-// first item (active-group rank * NT + task) whose start weight (rank * WS + wpre[task]) is >= w
-__device__ __forceinline__ long long item_at(const long long* __restrict__ wpre, const int NT, const long long WS,
-                                             const long long w) {
-    const long long ar = w / WS, rem = w - ar * WS;
-    if (rem == 0) return ar * NT;
-    int lo = 1, hi = NT;                       // smallest t with wpre[t] >= rem (wpre[NT] = WS > rem)
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(wpre + mid) >= rem) hi = mid; else lo = mid + 1;
-    }
-    return ar * NT + lo;
+// four consecutive T of a 4-aligned address, same for every lane (uniform 16-byte loads)
+__device__ __forceinline__ void ld4_uniform(const double* p, double (&a)[4]) {
+    const double2 lo = __ldg(reinterpret_cast<const double2*>(p)), hi = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    a[0] = lo.x; a[1] = lo.y; a[2] = hi.x; a[3] = hi.y;
+}
+__device__ __forceinline__ void ld4_uniform(const float* p, float (&a)[4]) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
 }
 
 __device__ __forceinline__ void prefetch_l2_line(const void* p) {
@@ -120,7 +115,7 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
         }
         if ((LOPF_BATCH_L2PF & 2) && var) {
             const char* vb = reinterpret_cast<const char*>(V - lane);
-            const int nl = (ns * (ns + 1) / 2 + ns) * (int)(32 * sizeof(T) / 128);
+            const int nl = (batch_var_entries(ns) + ns) * (int)(32 * sizeof(T) / 128);
             for (int e = lane; e < nl; e += 32) prefetch_l2_line(vb + 128 * e);
         }
     }
@@ -175,37 +170,88 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
         }
         __syncwarp();                                                   // the row records are restaged
     }
-    // a5-a7, four rows at a time: y_r = sum_k Abar[r][k] d_k with k ascending
+    // a5-a7, one row quad at a time: y_r = sum_k Abar[r][k] d_k with k ascending (zero entries past n_s add
+    // nothing; d past n_s reads a finite value: staged zeros, or the clamped last row for BIG)
+    const int nq = (ns + 3) >> 2, nsp = nq << 2;
     const T* __restrict__ A = reinterpret_cast<const T*>(B.spool) + (var ? 0 : sm.z);
-    for (int r0 = 0; r0 < ns; r0 += 4) {
-        int rr[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) rr[i] = min(r0 + i, ns - 1);        // rows past n_s: discarded
+    if (!BIG) {
+        __syncwarp();
+        for (int k = ns; k < nsp; ++k) dd[k * 32] = T(0);
+        __syncwarp();
+    }
+    auto dk_at = [&](const int k) -> T {
+        if (BIG) return __ldcg(dd + min(k, ns - 1) * 32);
+        return dd[k * 32];
+    };
+    for (int q = 0; q < nq; ++q) {
         T y[4] = {T(0), T(0), T(0), T(0)};
-        if (var) {
+        if (var && !LOPF_BATCH_VQB) {
             // packed upper triangle, row-major: (i, j >= i) at i n - i (i - 1) / 2 + j - i; row r reads
             // (min(r, k), max(r, k)): the walk steps by n - k - 1 while k < r, then by 1
-            int p[4];
+            int p[4], rq[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) p[i] = rr[i];
-#pragma unroll KU
+            for (int i = 0; i < 4; ++i) p[i] = rq[i] = min(4 * q + i, ns - 1);
+#pragma unroll 4
             for (int k = 0; k < ns; ++k) {
-                const T dk = BIG ? __ldcg(dd + k * 32) : dd[k * 32];
+                const T dk = dk_at(k);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     y[i] = fma(__ldg(V + 32 * p[i]), dk, y[i]);
-                    p[i] += k < rr[i] ? ns - k - 1 : 1;
+                    p[i] += k < rq[i] ? ns - k - 1 : 1;
                 }
             }
-        } else {
-#pragma unroll KU
-            for (int k = 0; k < ns; ++k) {                              // Abar is exactly symmetric: A[k][r]
-                const T dk = BIG ? __ldcg(dd + k * 32) : dd[k * 32];
-                const T* __restrict__ Ak = A + k * ns;
+        } else if (var) {
+            // quad-block upper layout: block q' at Q(q') = sum_{p < q'} 4 (nsp - 4p) entries; for k < 4q the
+            // entry (r = 4q + i, k = 4q' + j) is the stored (k, r): block q', column 4q + i, row j
+            int Q = 0;
+            for (int qp = 0; qp < q; ++qp) {
+                const T* __restrict__ Bp = V + 32 * (Q + 16 * (q - qp));
+                T dj[4], a[4][4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) y[i] = fma(__ldg(Ak + rr[i]), dk, y[i]);
+                for (int j = 0; j < 4; ++j) dj[j] = dk_at(4 * qp + j);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) a[i][j] = __ldg(Bp + 32 * (4 * i + j));
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) y[i] = fma(a[i][j], dj[j], y[i]);
+                Q += 4 * (nsp - 4 * qp);
+            }
+            const T* __restrict__ Bq = V + 32 * Q;                          // block q: column k at 4 (k - 4q)
+            for (int k = 4 * q; k < nsp; k += 4, Bq += 32 * 16) {
+                T dj[4], a[4][4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dj[j] = dk_at(k + j);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) a[i][j] = __ldg(Bq + 32 * (4 * j + i));
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) y[i] = fma(a[i][j], dj[j], y[i]);
+            }
+        } else {
+            // row quad q: [k][4] over the padded width, one 4-wide uniform load per column
+            const T* __restrict__ Aq = A + q * nsp * 4;
+            for (int k = 0; k < nsp; k += 4, Aq += 16) {
+                T dj[4], a[4][4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dj[j] = dk_at(k + j);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) ld4_uniform(Aq + 4 * j, a[j]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) y[i] = fma(a[j][i], dj[j], y[i]);
             }
         }
+        const int r0 = 4 * q;
+        int rr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) rr[i] = min(r0 + i, ns - 1);        // rows past n_s: discarded
         T vv[4], lam[4], xo[4], bb[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {                                   // the four rows' loads first
@@ -213,7 +259,7 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
             vv[i] = __ldcg(ung + at);
             lam[i] = __ldcg(lmg + at);
             xo[i] = __ldcg(xlg + at);
-            bb[i] = (sm.w & kBBbar) ? __ldg(V + 32 * (ns * (ns + 1) / 2 + rr[i])) : T(0);
+            bb[i] = (sm.w & kBBbar) ? __ldg(V + 32 * (batch_var_entries(ns) + rr[i])) : T(0);
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -270,7 +316,6 @@ __global__ void __launch_bounds__(BB, 1) admm_batch_kernel(BatchProblem B) {
     const long long total0 = *(volatile long long*)&B.ctrl->total;
     const int NT = B.n_tasks, NG = B.n_grp;
     unsigned long long bars = 0;
-    const long long WS = __ldg(B.wpre + NT);
     long long it = 0;
     while (it < B.max_iter) {
         const long long t = total0 + it;
@@ -293,32 +338,31 @@ __global__ void __launch_bounds__(BB, 1) admm_batch_kernel(BatchProblem B) {
         __syncthreads();
         const int NA = s_na;
         if (NA == 0) break;                             // every scenario has stopped (same view in every CTA)
-        // warp gw takes the active items (active group rank * NT + task, group-major) whose start weight
-        // lies in [gw, gw + 1) WT / nw: consecutive tasks of one group, cost-balanced
         const long long NI = (long long)NA * NT;
-        const long long WT = (long long)NA * WS;
-        long long a = item_at(B.wpre, NT, WS, (WT * gw + nw - 1) / nw);
-        const long long a_end = item_at(B.wpre, NT, WS, (WT * (gw + 1) + nw - 1) / nw);
-        if (a >= a_end) a = NI;
-        int cur = -1;
-        bool act = false;
+        // dynamic hand-out: item i = (task torder[i / NA], active group i % NA), costliest tasks first; lane 0
+        // claims the next item while the warp computes the current one.  The partials land per (group, task),
+        // so the result does not depend on which warp ran an item.
+        unsigned long long* ictr = B.cnt + 1 + (it & 1);
+        long long a = 0;
+        if (lane == 0) a = (long long)atomicAdd(ictr, 1ULL);
+        a = __shfl_sync(kFull, a, 0);
         while (a < NI) {
-            const long long an = a + 1 < a_end ? a + 1 : NI;
-            const int ag = (int)(a / NT), task = (int)(a - (long long)ag * NT);
-            const int grp = s_gl[ag];
-            if (grp != cur) {
-                cur = grp;
-                const int sc = grp * 32 + lane;
-                act = sc < B.n_scen && __ldcg(B.stopped + sc) == 0;
-            }
+            long long nxt = 0;
+            if (lane == 0) nxt = (long long)atomicAdd(ictr, 1ULL);
+            const long long tq = a / NA;
+            const int grp = s_gl[(int)(a - tq * NA)], task = __ldg(B.torder + tq);
+            const int sc = grp * 32 + lane;
+            const bool act = sc < B.n_scen && __ldcg(B.stopped + sc) == 0;
             double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
             batch_item<T>(B, grp, task, ucur, unext, W, lane, act, acc);
             double* pp = B.partial + ((size_t)grp * NT + task) * 5 * 32 + lane;
 #pragma unroll
             for (int k = 0; k < 5; ++k) __stcg(pp + k * 32, acc[k]);
-            a = an;
+            a = __shfl_sync(kFull, nxt, 0);
         }
         grid_sync(B.cnt, (++bars) * gridDim.x);
+        if (blockIdx.x == 0 && threadIdx.x == 0) B.cnt[1 + ((it + 1) & 1)] = 0ULL;   // next sweep's counter (seen
+                                                                                    // after the second barrier)
         // per-scenario (termination): warp per active group, lane = scenario
         uint32_t* gnext = B.gact + (size_t)((it + 1) & 1) * NG;
         for (int ag = gw; ag < NA; ag += nw) {
@@ -447,7 +491,7 @@ lopf_status launch_batch(const BatchProblem& B, int grid, void* stream, std::str
     const void* k = batch_kernel_for(B.esz);
     const int smem = batch_smem(B.ns_max, B.esz);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) e = cudaMemsetAsync(B.cnt, 0, sizeof(unsigned long long), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(B.cnt, 0, 3 * sizeof(unsigned long long), s);
     if (e == cudaSuccess) {
         batch_gact_kernel<<<(B.n_grp + 255) / 256, 256, 0, s>>>(B);
         e = cudaGetLastError();

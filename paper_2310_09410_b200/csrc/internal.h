@@ -231,6 +231,19 @@ struct alignas(8) BRow {                       // 24 B per row (copy)
 static_assert(sizeof(BRow) == 24, "BRow is 24 bytes");
 constexpr int kBVar = 1;                       // BSub.flags: per-scenario operator (the subsystem holds a load)
 constexpr int kBBbar = 2;                      // ... with a nonzero b-bar after the triangle
+// Per-scenario operator entries of an n_s-row subsystem in the quad-block upper layout (pack_batch.cpp):
+// block q (rows 4q..4q+3) holds 4 entries for every column k in [4q, 4 ceil(n_s / 4)).
+#ifdef __CUDACC__
+#define LOPF_HD __host__ __device__
+#else
+#define LOPF_HD
+#endif
+#ifndef LOPF_BATCH_VQB
+#define LOPF_BATCH_VQB 1                       // 1: quad-block upper layout; 0: packed upper triangle, row-major
+#endif
+LOPF_HD constexpr int batch_var_entries(int ns) {
+    return LOPF_BATCH_VQB ? 8 * ((ns + 3) / 4) * ((ns + 3) / 4 + 1) : ns * (ns + 1) / 2;
+}
 struct BSub {                                  // 16 B per subsystem (DFS order)
     int32_t row0, ns, op, flags;               // op: shared dense Abar offset (T entries) or var-pool entry offset
 };
@@ -260,6 +273,7 @@ struct BatchProblem {
     uint32_t* gact;                            // [2][n_grp] group has an active scenario, by sweep parity
     unsigned long long* cnt;                   // barrier arrivals
     const long long* wpre;                     // [n_tasks + 1] prefix of the per-task cost weights (work split)
+    const int32_t* torder;                     // [n_tasks] tasks by decreasing cost weight (dynamic hand-out order)
     const int32_t* obj_idx;
     const double* obj_c;
     DevCtrl* ctrl;
@@ -271,7 +285,7 @@ struct BatchProblem {
 constexpr int kBatchMaxScen = 8192;            // scenarios per batch handle
 constexpr int kBatchMaxGrp = kBatchMaxScen / 32;
 #ifndef LOPF_BATCH_WARPS
-#define LOPF_BATCH_WARPS 20
+#define LOPF_BATCH_WARPS 24
 #endif
 constexpr int kBatchWarps = LOPF_BATCH_WARPS;  // warps per CTA of the batch kernel
 #ifndef LOPF_BATCH_DMAX
@@ -311,7 +325,8 @@ struct Layout {
     // batch kernel (config 4, lane = scenario)
     int32_t n_scen = 0, n_grp = 0, ns_max = 0, n_rows = 0, n_bsub = 0, ve = 0;
     size_t off_brow = 0, off_bsub = 0, off_btask = 0, off_bseg = 0, off_bspool = 0, off_bvpool = 0, off_bpart = 0,
-           off_bres = 0, off_bstop = 0, off_bgact = 0, off_bcnt = 0, off_bwpre = 0, off_bstage = 0, off_bdscr = 0;
+           off_bres = 0, off_bstop = 0, off_bgact = 0, off_bcnt = 0, off_bwpre = 0, off_bstage = 0, off_bdscr = 0,
+           off_btorder = 0;
     size_t image_bytes = 0;                // bytes of `image` uploaded by bind (0: the whole arena); the rest is
                                            // device state initialised by the reset kernels
     size_t off_fetch = 0;                  // staging of lopf_fetch_async (result record + x as fp64), after the image

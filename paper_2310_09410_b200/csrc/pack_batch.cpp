@@ -64,15 +64,24 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     for (int64_t s : order) {
         const int ns = P.n_s[s];
         BSub b{r0, ns, 0, 0};
+        const int nq = (ns + 3) / 4, nsp = 4 * nq;
         if (bo.vidx[s] >= 0) {
             b.flags = kBVar | kBBbar;
             b.op = (int32_t)ve;
             var_op[s] = ve;
-            ve += (int64_t)ns * (ns + 1) / 2 + ns;
+            ve += batch_var_entries(ns) + ns;
         } else {
             if (has_b[s]) { err = "batch mode: a subsystem without a load has a nonzero b-bar"; return LOPF_E_ARG; }
+            // row quads, each [k][4] over the padded width (zero rows and columns past n_s): the four rows'
+            // entries of one column are one 4-wide uniform load
             b.op = (int32_t)spool.size();
-            spool.insert(spool.end(), P.abar.begin() + P.abar_ptr[s], P.abar.begin() + P.abar_ptr[s + 1]);
+            const double* A = &P.abar[P.abar_ptr[s]];
+            for (int q = 0; q < nq; ++q)
+                for (int k = 0; k < nsp; ++k)
+                    for (int i = 0; i < 4; ++i) {
+                        const int r = 4 * q + i;
+                        spool.push_back(r < ns && k < ns ? A[(size_t)r * ns + k] : 0.0);
+                    }
         }
         subs.push_back(b);
         r0 += ns;
@@ -90,7 +99,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
             w += 16 + 12 * ns + ns * ns * ((subs[i].flags & kBVar) ? 2 : 1);
             t.row1 += subs[i].ns;
             if (subs[i].flags & kBVar) {                           // var entries are assigned in DFS order
-                const int32_t e1 = subs[i].op + (int32_t)(ns * (ns + 1) / 2 + ns);
+                const int32_t e1 = subs[i].op + (int32_t)(batch_var_entries((int)ns) + ns);
                 if (t.vop0 < 0) t.vop0 = subs[i].op;
                 t.vop1 = e1;
             }
@@ -101,6 +110,10 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
         wpre.push_back(wpre.back() + w);
     }
     const int64_t NT = (int64_t)tasks.size();
+    std::vector<int32_t> torder(NT);
+    for (int64_t t = 0; t < NT; ++t) torder[t] = (int32_t)t;
+    std::stable_sort(torder.begin(), torder.end(),
+                     [&](int32_t a, int32_t b) { return wpre[a + 1] - wpre[a] > wpre[b + 1] - wpre[b]; });
 
     // ---- arena -----------------------------------------------------------------------------------
     std::vector<int32_t> obj_idx;
@@ -131,6 +144,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     L.off_bspool = take(E * spool.size());
     L.off_x0 = take(E * (size_t)nr);
     L.off_bwpre = take(8 * (size_t)(NT + 1));
+    L.off_btorder = take(4 * (size_t)NT);
     L.off_objidx = take(4 * obj_idx.size());
     L.off_objc = take(8 * obj_c.size());
     L.off_bvpool = take(E * (size_t)NG * ve * 32);
@@ -174,6 +188,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     for (size_t i = 0; i < spool.size(); ++i) put(img + L.off_bspool, i, spool[i]);
     for (int64_t k = 0; k < P.nc; ++k) put(img + L.off_x0, row_of_copy[k], P.x0[k]);
     std::memcpy(img + L.off_bwpre, wpre.data(), 8 * wpre.size());
+    std::memcpy(img + L.off_btorder, torder.data(), 4 * torder.size());
     std::memcpy(img + L.off_objidx, obj_idx.data(), 4 * obj_idx.size());
     std::memcpy(img + L.off_objc, obj_c.data(), 8 * obj_c.size());
     // per-scenario operators: [group][entry][lane]; padding lanes of the last group stay zero
@@ -186,9 +201,20 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
             const double* A = &bo.abar[(size_t)sc * bo.VA + bo.va_off[v]];
             const double* b = &bo.bbar[(size_t)sc * bo.VB + bo.vb_off[v]];
             const size_t base = ((size_t)(sc >> 5) * ve + op) * 32 + (sc & 31);
+            // quad-block upper layout: block q holds, for each column k in [4q, nsp), the entries of rows
+            // 4q..4q+3 (zero past n_s); then b-bar
+            const int nq = (ns + 3) / 4, nsp = 4 * nq;
             int64_t e = 0;
-            for (int i = 0; i < ns; ++i)
-                for (int j = i; j < ns; ++j, ++e) put(vp, base + 32 * (size_t)e, A[(size_t)i * ns + j]);
+            if (!LOPF_BATCH_VQB)
+                for (int i = 0; i < ns; ++i)
+                    for (int j = i; j < ns; ++j, ++e) put(vp, base + 32 * (size_t)e, A[(size_t)i * ns + j]);
+            else
+            for (int q = 0; q < nq; ++q)
+                for (int k = 4 * q; k < nsp; ++k)
+                    for (int i = 0; i < 4; ++i, ++e) {
+                        const int r = 4 * q + i;
+                        put(vp, base + 32 * (size_t)e, r < ns && k < ns ? A[(size_t)r * ns + k] : 0.0);
+                    }
             for (int i = 0; i < ns; ++i, ++e) put(vp, base + 32 * (size_t)e, b[i]);
         }
     }
