@@ -36,8 +36,8 @@ using dev::kFull;
 #define LOPF_BATCH_CROWS 4                    // consensus rows whose gathers are issued together
 #endif
 #ifndef LOPF_BATCH_L2PF
-#define LOPF_BATCH_L2PF 1                     // per-subsystem lane-parallel L2 prefetch: 1 x_s, 2 the operator,
-                                              // 4 lambda, 8 the subsystem's own u rows
+#define LOPF_BATCH_L2PF 1                     // per-subsystem lane-parallel L2 prefetch (fp64 only: fp32 A/B 291 ->
+                                              // 235 us without it): 1 x_s, 2 the operator, 4 lambda, 8 own u rows
 #endif
 constexpr int BW = kBatchWarps;
 constexpr int CR = LOPF_BATCH_CROWS;
@@ -46,6 +46,51 @@ constexpr int BB = 32 * BW;
 template <class T> struct V2;                 // {c/rho, lo}, {hi, 1/nu} per global
 template <> struct V2<double> { using type = double2; };
 template <> struct V2<float> { using type = float2; };
+
+#ifndef LOPF_BATCH_EVICT
+#define LOPF_BATCH_EVICT 1                    // L2 evict_first on last-use loads and on every state store: 1 fp32
+#endif                                        // only (fp64 A/B: DRAM 1.54 -> 1.44 GB per sweep, time +0.5%), 2 both
+
+// L2 eviction hints: a line's last use in a sweep (and every store of the state, read again only a sweep
+// = ~1 GB of traffic later) is marked evict_first, so the L2 keeps the lines a sweep re-reads soon
+// (lambda and the parked v of the current subsystem, neighbouring u, the shared operators).
+__device__ __forceinline__ unsigned long long pol_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_last(const double* p, unsigned long long pol) {
+    if (LOPF_BATCH_EVICT != 2) return __ldcg(p);
+    double v;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_last(const float* p, unsigned long long pol) {
+    if (!LOPF_BATCH_EVICT) return __ldcg(p);
+    float v;
+    asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_op(const double* p, unsigned long long pol) {
+    if (LOPF_BATCH_EVICT != 2) return __ldg(p);
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_op(const float* p, unsigned long long pol) {
+    if (!LOPF_BATCH_EVICT) return __ldg(p);
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_first(double* p, double v, unsigned long long pol) {
+    if (LOPF_BATCH_EVICT != 2) { __stcg(p, v); return; }
+    asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_first(float* p, float v, unsigned long long pol) {
+    if (!LOPF_BATCH_EVICT) { __stcg(p, v); return; }
+    asm volatile("st.global.cg.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
 
 // four consecutive T of a 4-aligned address, same for every lane (uniform 16-byte loads)
 __device__ __forceinline__ void ld4_uniform(const double* p, double (&a)[4]) {
@@ -86,6 +131,7 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
                                           const int lane, const bool act, double (&acc)[5], const size_t grp) {
     using T2 = typename V2<T>::type;
     const T rho = (T)B.rho, inv_rho = (T)B.inv_rho;
+    const unsigned long long pf = pol_first();
     // this group's lane views: element (row r) at [32 r] (32-bit indices on 64-bit bases)
     const T* __restrict__ ug = ucur + gb * 32 + lane;
     T* __restrict__ ung = unext + gb * 32 + lane;
@@ -98,7 +144,7 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
     T* __restrict__ dd = BIG ? reinterpret_cast<T*>(B.dscr) + (gb + row0) * 32 + lane : W.d + lane;   // d_r at dd[32 r]
     const bool var = sm.w & kBVar;
     const T* __restrict__ V = reinterpret_cast<const T*>(B.vpool) + (grp * B.ve + (var ? sm.z : 0)) * 32 + lane;
-    if (LOPF_BATCH_L2PF) {
+    if (LOPF_BATCH_L2PF && sizeof(T) == 8) {
         // lane-parallel L2 prefetch of the lines this subsystem streams from HBM (x_s read in the finish, the
         // per-scenario operator in the mat-vec), issued before the consensus so they arrive while it runs
         const char* xb = reinterpret_cast<const char*>(xlg - lane);
@@ -161,7 +207,7 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
                 }
                 const T v = fmin(fmax((sig - mp[0]) * mp[3], mp[1]), mp[2]);   // IEEE +-inf = no clamp
                 const int at = 32 * (row0 + c0 + r + i);
-                if (act && (inf & kBFirst)) __stcg(xg + 32 * g, v);
+                if (act && (inf & kBFirst)) st_first(xg + 32 * g, v, pf);
                 const T d = -rho * v - lm[i];
                 if (BIG) __stcg(dd + (c0 + r + i) * 32, d);
                 else dd[(c0 + r + i) * 32] = d;
@@ -196,7 +242,7 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
                 const T dk = dk_at(k);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    y[i] = fma(__ldg(V + 32 * p[i]), dk, y[i]);
+                    y[i] = fma(ld_op(V + 32 * p[i], pf), dk, y[i]);
                     p[i] += k < rq[i] ? ns - k - 1 : 1;
                 }
             }
@@ -212,7 +258,7 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) a[i][j] = __ldg(Bp + 32 * (4 * i + j));
+                    for (int j = 0; j < 4; ++j) a[i][j] = ld_op(Bp + 32 * (4 * i + j), pf);
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -227,7 +273,7 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) a[i][j] = __ldg(Bq + 32 * (4 * j + i));
+                    for (int i = 0; i < 4; ++i) a[i][j] = ld_op(Bq + 32 * (4 * j + i), pf);
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -256,10 +302,10 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
 #pragma unroll
         for (int i = 0; i < 4; ++i) {                                   // the four rows' loads first
             const int at = 32 * (row0 + rr[i]);
-            vv[i] = __ldcg(ung + at);
-            lam[i] = __ldcg(lmg + at);
-            xo[i] = __ldcg(xlg + at);
-            bb[i] = (sm.w & kBBbar) ? __ldg(V + 32 * (batch_var_entries(ns) + rr[i])) : T(0);
+            vv[i] = ld_last(ung + at, pf);
+            lam[i] = ld_last(lmg + at, pf);
+            xo[i] = ld_last(xlg + at, pf);
+            bb[i] = (sm.w & kBBbar) ? ld_op(V + 32 * (batch_var_entries(ns) + rr[i]), pf) : T(0);
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -270,9 +316,9 @@ __device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, 
             const T ln = lam[i] + rho * (v - xn);                       // ADMM-3
             const T un = xn - ln * inv_rho;                             // next consensus input
             if (act) {
-                __stcg(xlg + at, xn);
-                __stcg(lmg + at, ln);
-                __stcg(ung + at, un);
+                st_first(xlg + at, xn, pf);
+                st_first(lmg + at, ln, pf);
+                st_first(ung + at, un, pf);
                 const T rs = v - xn, dx = xn - xo[i];                   // terms in T, sums in fp64 (F1)
                 acc[0] += (double)(rs * rs);
                 acc[1] += (double)(dx * dx);
