@@ -478,19 +478,47 @@ def bench_stitched(args):
     ttt_ms = a.elapsed_time(b)
     k_tol = int(r.iters)
     conv = int(r.outcome) == CONVERGED
-    # end to end: upload the packed problem from pinned host memory, --sweeps sweeps, x back
-    e2e_steps = 3
-    barrier()
-    t = time.perf_counter()
-    for _ in range(e2e_steps):
-        h.bind(dev)
-        if solver is None:
-            h.run(args.sweeps)
-        else:
+    # end to end: upload the packed problem from pinned host memory, --sweeps sweeps, x back.  N = 1: stream-
+    # ordered like config 3 -- two handles on two streams, step i+1's upload (lopf_bind) on the copy engine
+    # while step i solves (lopf_solve_async, test off), result record + x into pinned host memory
+    # (lopf_fetch_async); the host waits only for step i-2's fetch.  N > 1: bind, sweeps, get_x per step.
+    e2e_steps = 4 if solver is None else 3
+    if solver is None:
+        h2 = Lopf.setup(feeder, kernel=1, max_iter=100_000, precision=args.precision).bind(dev)
+        hs, ss = (h, h2), (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        fb = int(h.sizes.fetch_bytes)
+        bufs = [torch.empty(fb, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
+        pending = [False, False]
+        torch.cuda.synchronize(dev)
+        barrier()
+        t = time.perf_counter()
+        for i in range(e2e_steps):
+            j = i % 2
+            if pending[j]:
+                done[j].synchronize()
+                _r, x = Lopf.decode_fetch(bufs[j], int(sz.n))
+            with torch.cuda.stream(ss[j]):
+                hs[j].bind(dev, stream=ss[j])
+                hs[j].solve_async(args.sweeps, False, stream=ss[j])
+                hs[j].fetch_async(bufs[j], stream=ss[j])
+                done[j].record(ss[j])
+            pending[j] = True
+        for j in range(2):
+            if pending[j]:
+                done[j].synchronize()
+                _r, x = Lopf.decode_fetch(bufs[j], int(sz.n))
+        e2e_s = time.perf_counter() - t
+        del h2
+    else:
+        barrier()
+        t = time.perf_counter()
+        for _ in range(e2e_steps):
+            h.bind(dev)
             solver.sweeps(args.sweeps)
-        x = h.get_x()
-    torch.cuda.synchronize(dev)
-    e2e_s = time.perf_counter() - t
+            x = h.get_x()
+        torch.cuda.synchronize(dev)
+        e2e_s = time.perf_counter() - t
     allv = _max_over_ranks(world, dev, dev_ms, e2e_s, ttt_ms)
     max_ms, e2e_max, ttt_max = float(allv[:, 0].max()), float(allv[:, 1].max()), float(allv[:, 2].max())
     value = args.steps * args.sweeps / (max_ms / 1e3)
@@ -537,7 +565,10 @@ def bench_stitched(args):
                          "alg_bytes_per_sweep": int(sz.alg_bytes), "us_per_sweep": us},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_steps * args.sweeps / e2e_max, "unit": "iterations/s",
-                    "h2d_bytes_per_step": int(sz.upload_bytes), "d2h_bytes_per_step": int(8 * sz.n), "steps": e2e_steps},
+                    "h2d_bytes_per_step": int(sz.upload_bytes),
+                    "d2h_bytes_per_step": int(sz.fetch_bytes) if world == 1 else int(8 * sz.n), "steps": e2e_steps,
+                    "pipeline": ("2 handles x 2 streams: bind (H2D) / solve_async / fetch_async (D2H), no per-step sync"
+                                 if world == 1 else "bind, sweeps, get_x per step")},
             "clocks": clk.summary(),
             "gpu_launches": args.steps * (1 if world == 1 or args.exchange == "p2p" else 2 * args.sweeps),
         }
