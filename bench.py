@@ -685,7 +685,8 @@ def bench_batch(args):
                        "mean_iters": float(allv[:, 3].sum()) / args.n_scen, "time_to_tolerance_ms": max_ms / args.steps,
                        "l2": "flushed between steps (512 MiB write)", "setup_s": round(setup_s, 1)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": peak_src, "kernel": "admm_batch_kernel",
+                         "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "admm_batch_kernel" if args.precision == 32 else "admm_batch_team_kernel",
                          "alg_bytes_per_batch_sweep": int(sz.alg_bytes), "active_fraction": active,
                          "us_per_batch_sweep": us_per_batch_sweep},
             "cpu_baseline": cpu,

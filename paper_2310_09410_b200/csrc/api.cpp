@@ -348,9 +348,10 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
     }
     const int64_t E = h->lay.esz;           // 8 (fp64) or 4 (fp32 variant): the (T) arrays
     sz->alg_bytes = E * (psym + nbbar + 6 * P.nc + 4 * P.n + h->lay.n_obj) + 4 * (2 * P.nc + P.n + 1);
-    if (h->batch()) {                       // per batch sweep: shared operators once, the rest per scenario
-        const int64_t ns = h->lay.n_scen;
-        sz->alg_bytes = E * ((psym - psym_var) + ns * (psym_var + nbbar + 6 * P.nc + 4 * P.n + h->lay.n_obj)) +
+    if (h->batch()) {                       // per batch sweep: what all scenarios share once (the operators of the
+        const int64_t ns = h->lay.n_scen;   // subsystems without a load, lo, hi, c), per scenario the rest: its
+        sz->alg_bytes = E * ((psym - psym_var) + 2 * P.n + h->lay.n_obj +     // operators and b-bar, the
+                             ns * (psym_var + nbbar + 6 * P.nc + 2 * P.n)) +   // 6 N_c iterate terms, x (w + r)
                         4 * (2 * P.nc + P.n + 1);
     }
     sz->kernel = h->lay.kernel;
@@ -361,7 +362,7 @@ lopf_status lopf_sizes_get(const lopf_handle* h, lopf_sizes* sz) {
         sz->reserved[1] = h->lay.max_smem;
     }
     sz->grid = h->resident() ? h->lay.G : h->grid;
-    sz->block = h->resident() ? kResBlock : h->batch() ? batch_block() : stream_block(h->lay.rmax, h->lay.esz);
+    sz->block = h->resident() ? kResBlock : h->batch() ? batch_block(h->lay.task_rows_max, h->lay.esz) : stream_block(h->lay.rmax, h->lay.esz);
     sz->n_scen = h->batch() ? h->lay.n_scen : 0;
     sz->upload_bytes = (int64_t)h->lay.image.size();
     sz->fetch_bytes = (h->batch() || h->parted()) ? 0 : (int64_t)(64 + 8 * h->cp.n);
@@ -395,6 +396,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         B.n_tasks = (int32_t)L.n_tasks;
         B.ve = L.ve;
         B.ns_max = L.ns_max;
+        B.trmax = L.task_rows_max;
         B.esz = L.esz;
         B.n_obj = (int32_t)L.n_obj;
         B.n = h->cp.n;
@@ -412,7 +414,6 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         B.u1 = b + L.off_u1;
         B.x = b + L.off_x;
         B.partial = (double*)(b + L.off_bpart);
-        B.dscr = b + L.off_bdscr;
         B.res = (ScenResult*)(b + L.off_bres);
         B.stopped = (int32_t*)(b + L.off_bstop);
         B.gact = (uint32_t*)(b + L.off_bgact);
@@ -430,7 +431,7 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         h->dp.ctrl = B.ctrl;
         std::string err;
         int grid = 0;
-        lopf_status st = query_batch_grid(L.ns_max, L.esz, &grid, err);
+        lopf_status st = query_batch_grid(L.task_rows_max, L.esz, &grid, err);
         if (st != LOPF_OK) return fail(st, err);
         h->grid = grid;
         st = launch_reset_batch(B, stream, err);

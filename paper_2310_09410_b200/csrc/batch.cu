@@ -4,22 +4,24 @@
 // Lane = scenario.  Scenarios form groups of 32 and every per-scenario array is [group][entry][32], so a
 // warp instruction moves one 256-byte line for 32 scenarios while everything structural -- rows, segment
 // lists, bounds, the operators of subsystems without a load -- is the same address for all 32 lanes
-// (uniform loads).  A work item is (group, task), a task a depth-first run of subsystems; per item and
-// subsystem s the warp computes, for its 32 scenarios at once,
+// (uniform loads).  A work item is (group, task), a task a depth-first run of subsystems, run by a team of
+// kTeamWarps warps (see the kernel below); per item and subsystem s the team computes, for its 32
+// scenarios at once,
 //   a4  x_g = clamp((sum_{k in seg(g)} u_k - c_g/rho) / nu_g, lo_g, hi_g) for each row (closed_1, rho
-//       restored, reading C1), canonical copy order; d = -rho v - lambda staged in SMEM [row][lane]
+//       restored, reading C1), canonical copy order; d = -rho v - lambda staged in team SMEM [row][lane]
 //   a5  y = Abar_s d, one row quad at a time (k ascending, FMA); Abar_s from the shared pool (row quads
 //       [k][4], one 4-wide uniform load per column) or, for a load subsystem, the scenario's quad-block
 //       upper layout ([entry][lane], coalesced, every operand at an immediate offset of one block pointer)
 //   a6  x_s = y / rho + bbar_s, lambda += rho (v - x_s), u = x_s - lambda / rho     (closed_2, ADMM-3)
 //   a7  five residual sums per lane (scenario), written per item
 // The ACTIVE items of a sweep (groups with a scenario still running, times tasks) are handed out one at a
-// time from an atomic counter, costliest tasks first.  Grid barrier; one warp per active group then sums
+// time from an atomic counter, costliest tasks first, to the teams.  Grid barrier; one warp per active group then sums
 // each scenario's item partials in task order (deterministic whichever warp ran an item) and takes its
 // decision; converged scenarios freeze (their lanes stop storing), a group leaves the item list when all
 // 32 have; grid barrier.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "device.cuh"
@@ -35,13 +37,27 @@ using dev::kFull;
 #ifndef LOPF_BATCH_CROWS
 #define LOPF_BATCH_CROWS 4                    // consensus rows whose gathers are issued together
 #endif
-#ifndef LOPF_BATCH_L2PF
-#define LOPF_BATCH_L2PF 1                     // per-subsystem lane-parallel L2 prefetch (fp64 only: fp32 A/B 291 ->
-                                              // 235 us without it): 1 x_s, 2 the operator, 4 lambda, 8 own u rows
+#ifndef LOPF_BATCH_TW
+#define LOPF_BATCH_TW 4                       // warps per team
 #endif
-constexpr int BW = kBatchWarps;
+#ifndef LOPF_BATCH_TEAMS
+#define LOPF_BATCH_TEAMS 6                    // most teams per CTA (fewer when the task rows need more SMEM)
+#endif
+#ifndef LOPF_BATCH_VPARK
+#define LOPF_BATCH_VPARK 1                    // team kernel: 1 parks v in u-next (L2), 0 in team SMEM
+#endif
+#ifndef LOPF_BATCH_BPF
+#define LOPF_BATCH_BPF 15                     // team kernel bulk L2 prefetch at item start, of the current item: 1
+#endif                                        // operators, 2 x_s rows, 4 lambda rows, 8 u rows; bits 4-7 the same
+                                              // of the next item
+#ifndef LOPF_BATCH_JH
+#define LOPF_BATCH_JH 4                       // operator columns per load batch of the per-scenario mat-vec (4 or 2)
+#endif
 constexpr int CR = LOPF_BATCH_CROWS;
-constexpr int BB = 32 * BW;
+constexpr int JH = LOPF_BATCH_JH;
+constexpr int kTeamWarps = LOPF_BATCH_TW;
+constexpr int kTeamMax = LOPF_BATCH_TEAMS;
+constexpr int kSmemBudget = 232448 - 2048;    // opt-in dynamic SMEM per block minus the static arrays
 
 template <class T> struct V2;                 // {c/rho, lo}, {hi, 1/nu} per global
 template <> struct V2<double> { using type = double2; };
@@ -102,345 +118,444 @@ __device__ __forceinline__ void ld4_uniform(const float* p, float (&a)[4]) {
     a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
 }
 
-__device__ __forceinline__ void prefetch_l2_line(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+// ---- per-row / per-quad arithmetic ---------------------------------------------------------------
+
+// Consensus (a4, closed_1 with rho restored, reading C1) of up to CR rows whose records sit at mi + 6 i,
+// mp + 4 i (i < cnt) and whose own rows are self0 + i: every gather of the CR rows is issued first, then
+// x_g = clamp((sum_k u_k - c/rho) / nu, lo, hi) in ascending canonical copy order; x stored by the first
+// copy; put(i, v, d) receives v = x_g and d = -rho v - lambda of row i.
+template <class T, class Put>
+__device__ __forceinline__ void consensus_group(const BatchProblem& B, const int* mi0, const T* mp0, const int cnt,
+                                                const int self0, const T* __restrict__ ug, const T* __restrict__ lmg,
+                                                T* __restrict__ xg, const bool act, const unsigned long long pf, Put put) {
+    const T rho = (T)B.rho;
+    T ua[CR][4], lm[CR];
+#pragma unroll
+    for (int i = 0; i < CR; ++i) {                                      // every load of CR rows first
+        const int rr = min(i, cnt - 1);
+        const int* mi = mi0 + rr * 6;
+        const int inf = mi[1];
+        const bool inl = inf & kBInline;
+        const int nu = inl ? (inf >> kBNuShift) & 0xFF : 0;
+        const int self = self0 + rr;
+        ua[i][0] = __ldcg(ug + 32 * (inl ? mi[2] : self));
+        ua[i][1] = nu > 1 ? __ldcg(ug + 32 * mi[3]) : T(0);
+        ua[i][2] = nu > 2 ? __ldcg(ug + 32 * mi[4]) : T(0);
+        ua[i][3] = nu > 3 ? __ldcg(ug + 32 * mi[5]) : T(0);
+        lm[i] = __ldcg(lmg + 32 * self);
+    }
+#pragma unroll
+    for (int i = 0; i < CR; ++i) {
+        if (i >= cnt) break;
+        const int* mi = mi0 + i * 6;
+        const T* mp = mp0 + i * 4;
+        const int g = mi[0], inf = mi[1];
+        T sig = ((ua[i][0] + ua[i][1]) + ua[i][2]) + ua[i][3];           // ascending canonical copy order
+        if (!(inf & kBInline)) {                                        // nu > 4 (rare): the segment list
+            sig = T(0);
+            for (int q = 0; q < mi[3]; ++q) sig += __ldcg(ug + 32 * __ldg(B.seg_rows + mi[2] + q));
+        }
+        const T v = fmin(fmax((sig - mp[0]) * mp[3], mp[1]), mp[2]);       // IEEE +-inf = no clamp
+        if (act && (inf & kBFirst)) st_first(xg + 32 * g, v, pf);
+        put(i, v, -rho * v - lm[i]);
+    }
 }
 
-// Per-warp shared memory: d of the current subsystem [kBatchDMax][32] (a subsystem with more rows keeps
-// its d in the global scratch `dscr` instead, an L2-resident [group][row][32] array), and the records of
-// up to 32 rows ({g, info, n0..n3} and {c/rho, lo, hi, 1/nu}) staged by one coalesced load per lane, so
-// the row loop reads its uniform metadata with shared-memory broadcasts instead of dependent global loads.
-template <class T>
-struct WarpSmem {
-    T* d;                                      // [kBatchDMax][32]
-    int* mi;                                   // [32][6]
-    T* mp;                                     // [32][4]
-};
-template <class T>
-__host__ __device__ constexpr int warp_smem_bytes() {
-    return kBatchDMax * 32 * (int)sizeof(T) + 32 * 6 * 4 + 32 * 4 * (int)sizeof(T);
-}
-
-// One subsystem of a (group, task) item for the 32 scenarios of the group (lane = scenario; `act`: the
-// lane's scenario is running -- frozen or padding lanes compute but store nothing and add nothing).  Every
-// loop keeps many independent loads in flight: four rows' gathers at a time, the mat-vec's operator loads
-// of four rows x four columns, the four rows' finish loads.  BIG: d in the global scratch.
-template <class T, bool BIG>
-__device__ __forceinline__ void batch_sub(const BatchProblem& B, const int4 sm, const size_t gb,
-                                          const T* __restrict__ ucur, T* __restrict__ unext, const WarpSmem<T>& W,
-                                          const int lane, const bool act, double (&acc)[5], const size_t grp) {
-    using T2 = typename V2<T>::type;
-    const T rho = (T)B.rho, inv_rho = (T)B.inv_rho;
-    const unsigned long long pf = pol_first();
-    // this group's lane views: element (row r) at [32 r] (32-bit indices on 64-bit bases)
-    const T* __restrict__ ug = ucur + gb * 32 + lane;
-    T* __restrict__ ung = unext + gb * 32 + lane;
-    T* __restrict__ xlg = reinterpret_cast<T*>(B.xl) + gb * 32 + lane;
-    T* __restrict__ lmg = reinterpret_cast<T*>(B.lam) + gb * 32 + lane;
-    T* __restrict__ xg = reinterpret_cast<T*>(B.x) + grp * B.n * 32 + lane;
-    const T2* __restrict__ gpar = reinterpret_cast<const T2*>(B.gpar);
-    const int2* __restrict__ rows = reinterpret_cast<const int2*>(B.rows);
-    const int row0 = sm.x, ns = sm.y;
-    T* __restrict__ dd = BIG ? reinterpret_cast<T*>(B.dscr) + (gb + row0) * 32 + lane : W.d + lane;   // d_r at dd[32 r]
+// a5 for row quad q of subsystem sm: y_i = sum_k Abar[4q + i][k] d_k, k ascending (zero entries past n_s
+// add nothing; dk(k) for k in [n_s, 4 nq) must return a finite value).  V: the group's per-scenario pool
+// at the subsystem (lane view), A: the shared pool.
+template <class T, class DK>
+__device__ __forceinline__ void matvec_quad(const int4 sm, const T* __restrict__ V, const T* __restrict__ A,
+                                            const int q, const unsigned long long pf, DK dk, T (&y)[4]) {
+    const int ns = sm.y, nq = (ns + 3) >> 2, nsp = nq << 2;
     const bool var = sm.w & kBVar;
-    const T* __restrict__ V = reinterpret_cast<const T*>(B.vpool) + (grp * B.ve + (var ? sm.z : 0)) * 32 + lane;
-    if (LOPF_BATCH_L2PF && sizeof(T) == 8) {
-        // lane-parallel L2 prefetch of the lines this subsystem streams from HBM (x_s read in the finish, the
-        // per-scenario operator in the mat-vec), issued before the consensus so they arrive while it runs
-        const char* xb = reinterpret_cast<const char*>(xlg - lane);
-        const int xlines = (int)(ns * 32 * sizeof(T) / 128);
-        if (LOPF_BATCH_L2PF & 1)
-            for (int e = lane; e < xlines; e += 32) prefetch_l2_line(xb + (size_t)(32 * row0) * sizeof(T) + 128 * e);
-        if (LOPF_BATCH_L2PF & 4) {
-            const char* lb = reinterpret_cast<const char*>(lmg - lane);
-            for (int e = lane; e < xlines; e += 32) prefetch_l2_line(lb + (size_t)(32 * row0) * sizeof(T) + 128 * e);
-        }
-        if (LOPF_BATCH_L2PF & 8) {
-            const char* ub = reinterpret_cast<const char*>(ug - lane);
-            for (int e = lane; e < xlines; e += 32) prefetch_l2_line(ub + (size_t)(32 * row0) * sizeof(T) + 128 * e);
-        }
-        if ((LOPF_BATCH_L2PF & 2) && var) {
-            const char* vb = reinterpret_cast<const char*>(V - lane);
-            const int nl = (batch_var_entries(ns) + ns) * (int)(32 * sizeof(T) / 128);
-            for (int e = lane; e < nl; e += 32) prefetch_l2_line(vb + 128 * e);
-        }
-    }
-    // a4: consensus of every row's global, 32 rows per chunk; v parked in unext (replaced by u below)
-    for (int c0 = 0; c0 < ns; c0 += 32) {
-        const int nrow = min(32, ns - c0);
-        if (lane < nrow) {                                              // lane l stages row c0 + l's records
-            const int row = row0 + c0 + lane;
-            const int2 a = __ldg(rows + 3 * row), b = __ldg(rows + 3 * row + 1), c = __ldg(rows + 3 * row + 2);
-            int* mi = W.mi + lane * 6;
-            mi[0] = a.x; mi[1] = a.y; mi[2] = b.x; mi[3] = b.y; mi[4] = c.x; mi[5] = c.y;
-            const T2 p0 = __ldg(gpar + 2 * a.x), p1 = __ldg(gpar + 2 * a.x + 1);
-            T* mp = W.mp + lane * 4;
-            mp[0] = p0.x; mp[1] = p0.y; mp[2] = p1.x; mp[3] = p1.y;
-        }
-        __syncwarp();
-        for (int r = 0; r < nrow; r += CR) {
-            T ua[CR][4], lm[CR];
 #pragma unroll
-            for (int i = 0; i < CR; ++i) {                              // every load of CR rows first
-                const int rr = min(r + i, nrow - 1);
-                const int* mi = W.mi + rr * 6;
-                const int inf = mi[1];
-                const bool inl = inf & kBInline;
-                const int nu = inl ? (inf >> kBNuShift) & 0xFF : 0;
-                const int self = row0 + c0 + rr;
-                ua[i][0] = __ldcg(ug + 32 * (inl ? mi[2] : self));
-                ua[i][1] = nu > 1 ? __ldcg(ug + 32 * mi[3]) : T(0);
-                ua[i][2] = nu > 2 ? __ldcg(ug + 32 * mi[4]) : T(0);
-                ua[i][3] = nu > 3 ? __ldcg(ug + 32 * mi[5]) : T(0);
-                lm[i] = __ldcg(lmg + 32 * self);
-            }
+    for (int i = 0; i < 4; ++i) y[i] = T(0);
+    if (var && !LOPF_BATCH_VQB) {
+        // packed upper triangle, row-major: (i, j >= i) at i n - i (i - 1) / 2 + j - i; row r reads
+        // (min(r, k), max(r, k)): the walk steps by n - k - 1 while k < r, then by 1
+        int p[4], rq[4];
 #pragma unroll
-            for (int i = 0; i < CR; ++i) {
-                if (r + i >= nrow) break;
-                const int* mi = W.mi + (r + i) * 6;
-                const T* mp = W.mp + (r + i) * 4;
-                const int g = mi[0], inf = mi[1];
-                T sig = ((ua[i][0] + ua[i][1]) + ua[i][2]) + ua[i][3];   // ascending canonical copy order
-                if (!(inf & kBInline)) {                                // nu > 4 (rare): the segment list
-                    sig = T(0);
-                    for (int q = 0; q < mi[3]; ++q) sig += __ldcg(ug + 32 * __ldg(B.seg_rows + mi[2] + q));
-                }
-                const T v = fmin(fmax((sig - mp[0]) * mp[3], mp[1]), mp[2]);   // IEEE +-inf = no clamp
-                const int at = 32 * (row0 + c0 + r + i);
-                if (act && (inf & kBFirst)) st_first(xg + 32 * g, v, pf);
-                const T d = -rho * v - lm[i];
-                if (BIG) __stcg(dd + (c0 + r + i) * 32, d);
-                else dd[(c0 + r + i) * 32] = d;
-                if (act) __stcg(ung + at, v);
-            }
-        }
-        __syncwarp();                                                   // the row records are restaged
-    }
-    // a5-a7, one row quad at a time: y_r = sum_k Abar[r][k] d_k with k ascending (zero entries past n_s add
-    // nothing; d past n_s reads a finite value: staged zeros, or the clamped last row for BIG)
-    const int nq = (ns + 3) >> 2, nsp = nq << 2;
-    const T* __restrict__ A = reinterpret_cast<const T*>(B.spool) + (var ? 0 : sm.z);
-    if (!BIG) {
-        __syncwarp();
-        for (int k = ns; k < nsp; ++k) dd[k * 32] = T(0);
-        __syncwarp();
-    }
-    auto dk_at = [&](const int k) -> T {
-        if (BIG) return __ldcg(dd + min(k, ns - 1) * 32);
-        return dd[k * 32];
-    };
-    for (int q = 0; q < nq; ++q) {
-        T y[4] = {T(0), T(0), T(0), T(0)};
-        if (var && !LOPF_BATCH_VQB) {
-            // packed upper triangle, row-major: (i, j >= i) at i n - i (i - 1) / 2 + j - i; row r reads
-            // (min(r, k), max(r, k)): the walk steps by n - k - 1 while k < r, then by 1
-            int p[4], rq[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) p[i] = rq[i] = min(4 * q + i, ns - 1);
+        for (int i = 0; i < 4; ++i) p[i] = rq[i] = min(4 * q + i, ns - 1);
 #pragma unroll 4
-            for (int k = 0; k < ns; ++k) {
-                const T dk = dk_at(k);
+        for (int k = 0; k < ns; ++k) {
+            const T dkv = dk(k);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    y[i] = fma(ld_op(V + 32 * p[i], pf), dk, y[i]);
-                    p[i] += k < rq[i] ? ns - k - 1 : 1;
-                }
+            for (int i = 0; i < 4; ++i) {
+                y[i] = fma(ld_op(V + 32 * p[i], pf), dkv, y[i]);
+                p[i] += k < rq[i] ? ns - k - 1 : 1;
             }
-        } else if (var) {
-            // quad-block upper layout: block q' at Q(q') = sum_{p < q'} 4 (nsp - 4p) entries; for k < 4q the
-            // entry (r = 4q + i, k = 4q' + j) is the stored (k, r): block q', column 4q + i, row j
-            int Q = 0;
-            for (int qp = 0; qp < q; ++qp) {
-                const T* __restrict__ Bp = V + 32 * (Q + 16 * (q - qp));
-                T dj[4], a[4][4];
+        }
+    } else if (var) {
+        // quad-block upper layout: block q' at Q(q') = sum_{p < q'} 4 (nsp - 4p) entries; for k < 4q the
+        // entry (r = 4q + i, k = 4q' + j) is the stored (k, r): block q', column 4q + i, row j.  The 16
+        // operands of a 4 x 4 block are loaded JH columns at a time (JH = 4: all at once; 2: fewer registers)
+        int Q = 0;
+        for (int qp = 0; qp < q; ++qp) {
+            const T* __restrict__ Bp = V + 32 * (Q + 16 * (q - qp));
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dj[j] = dk_at(4 * qp + j);
+            for (int j0 = 0; j0 < 4; j0 += JH) {
+                T dj[JH], a[4][JH];
+#pragma unroll
+                for (int j = 0; j < JH; ++j) dj[j] = dk(4 * qp + j0 + j);
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) a[i][j] = ld_op(Bp + 32 * (4 * i + j), pf);
+                    for (int j = 0; j < JH; ++j) a[i][j] = ld_op(Bp + 32 * (4 * i + j0 + j), pf);
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) y[i] = fma(a[i][j], dj[j], y[i]);
-                Q += 4 * (nsp - 4 * qp);
-            }
-            const T* __restrict__ Bq = V + 32 * Q;                          // block q: column k at 4 (k - 4q)
-            for (int k = 4 * q; k < nsp; k += 4, Bq += 32 * 16) {
-                T dj[4], a[4][4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) dj[j] = dk_at(k + j);
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) a[i][j] = ld_op(Bq + 32 * (4 * j + i), pf);
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < JH; ++j)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) y[i] = fma(a[i][j], dj[j], y[i]);
             }
-        } else {
-            // row quad q: [k][4] over the padded width, one 4-wide uniform load per column
-            const T* __restrict__ Aq = A + q * nsp * 4;
-            for (int k = 0; k < nsp; k += 4, Aq += 16) {
-                T dj[4], a[4][4];
+            Q += 4 * (nsp - 4 * qp);
+        }
+        const T* __restrict__ Bq = V + 32 * Q;                          // block q: column k at 4 (k - 4q)
+        for (int k = 4 * q; k < nsp; k += 4, Bq += 32 * 16) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dj[j] = dk_at(k + j);
+            for (int j0 = 0; j0 < 4; j0 += JH) {
+                T dj[JH], a[4][JH];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) ld4_uniform(Aq + 4 * j, a[j]);
+                for (int j = 0; j < JH; ++j) dj[j] = dk(k + j0 + j);
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < JH; ++j)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) y[i] = fma(a[j][i], dj[j], y[i]);
+                    for (int i = 0; i < 4; ++i) a[i][j] = ld_op(Bq + 32 * (4 * (j0 + j) + i), pf);
+#pragma unroll
+                for (int j = 0; j < JH; ++j)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) y[i] = fma(a[i][j], dj[j], y[i]);
             }
         }
-        const int r0 = 4 * q;
-        int rr[4];
+    } else {
+        // row quad q: [k][4] over the padded width, one 4-wide uniform load per column
+        const T* __restrict__ Aq = A + q * nsp * 4;
+        for (int k = 0; k < nsp; k += 4, Aq += 16) {
+            T dj[4], a[4][4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) rr[i] = min(r0 + i, ns - 1);        // rows past n_s: discarded
-        T vv[4], lam[4], xo[4], bb[4];
+            for (int j = 0; j < 4; ++j) dj[j] = dk(k + j);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {                                   // the four rows' loads first
-            const int at = 32 * (row0 + rr[i]);
-            vv[i] = ld_last(ung + at, pf);
-            lam[i] = ld_last(lmg + at, pf);
-            xo[i] = ld_last(xlg + at, pf);
-            bb[i] = (sm.w & kBBbar) ? ld_op(V + 32 * (batch_var_entries(ns) + rr[i]), pf) : T(0);
-        }
+            for (int j = 0; j < 4; ++j) ld4_uniform(Aq + 4 * j, a[j]);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            if (r0 + i >= ns) break;
-            const int at = 32 * (row0 + r0 + i);
-            const T xn = fma(y[i], inv_rho, bb[i]);                     // (1/rho) Abar d + bbar
-            const T v = vv[i];
-            const T ln = lam[i] + rho * (v - xn);                       // ADMM-3
-            const T un = xn - ln * inv_rho;                             // next consensus input
-            if (act) {
-                st_first(xlg + at, xn, pf);
-                st_first(lmg + at, ln, pf);
-                st_first(ung + at, un, pf);
-                const T rs = v - xn, dx = xn - xo[i];                   // terms in T, sums in fp64 (F1)
-                acc[0] += (double)(rs * rs);
-                acc[1] += (double)(dx * dx);
-                acc[2] += (double)(v * v);
-                acc[3] += (double)(xn * xn);
-                acc[4] += (double)(ln * ln);
-            }
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) y[i] = fma(a[j][i], dj[j], y[i]);
         }
     }
-    __syncwarp();                                                       // d is reused by the next subsystem
 }
 
+// a6-a7 for row quad q of subsystem sm (rows past n_s discarded): x_s = y / rho + bbar, lambda += rho (v -
+// x_s) (ADMM-3), u = x_s - lambda / rho; five residual sums per lane (terms in T, sums in fp64, F1).  vof(r)
+// returns the row's consensus value v (parked in u-next or staged in SMEM).
+template <class T, class VOF>
+__device__ __forceinline__ void finish_quad(const BatchProblem& B, const int4 sm, const T* __restrict__ V, const int q,
+                                            const T (&y)[4], T* __restrict__ ung, T* __restrict__ lmg,
+                                            T* __restrict__ xlg, const bool act, const unsigned long long pf, VOF vof,
+                                            double (&acc)[5]) {
+    const T rho = (T)B.rho, inv_rho = (T)B.inv_rho;
+    const int row0 = sm.x, ns = sm.y, r0 = 4 * q;
+    int rr[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rr[i] = min(r0 + i, ns - 1);
+    T vv[4], lam[4], xo[4], bb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {                                       // the four rows' loads first
+        const int at = 32 * (row0 + rr[i]);
+        vv[i] = vof(rr[i]);
+        lam[i] = ld_last(lmg + at, pf);
+        xo[i] = ld_last(xlg + at, pf);
+        bb[i] = (sm.w & kBBbar) ? ld_op(V + 32 * (batch_var_entries(ns) + rr[i]), pf) : T(0);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (r0 + i >= ns) break;
+        const int at = 32 * (row0 + r0 + i);
+        const T xn = fma(y[i], inv_rho, bb[i]);                         // (1/rho) Abar d + bbar
+        const T v = vv[i];
+        const T ln = lam[i] + rho * (v - xn);                           // ADMM-3
+        const T un = xn - ln * inv_rho;                                 // next consensus input
+        if (act) {
+            st_first(xlg + at, xn, pf);
+            st_first(lmg + at, ln, pf);
+            st_first(ung + at, un, pf);
+            const T rs = v - xn, dx = xn - xo[i];
+            acc[0] += (double)(rs * rs);
+            acc[1] += (double)(dx * dx);
+            acc[2] += (double)(v * v);
+            acc[3] += (double)(xn * xn);
+            acc[4] += (double)(ln * ln);
+        }
+    }
+}
+
+// Stage the records of row `row` ({g, info, n0..n3} and {c/rho, lo, hi, 1/nu}) at mi[6], mp[4].
 template <class T>
-__device__ __forceinline__ void batch_item(const BatchProblem& B, const int grp, const int task,
-                                           const T* __restrict__ ucur, T* __restrict__ unext, const WarpSmem<T>& W,
-                                           const int lane, const bool act, double (&acc)[5]) {
+__device__ __forceinline__ void stage_record(const BatchProblem& B, const int row, int* mi, T* mp) {
+    using T2 = typename V2<T>::type;
+    const int2* __restrict__ rows = reinterpret_cast<const int2*>(B.rows);
+    const T2* __restrict__ gpar = reinterpret_cast<const T2*>(B.gpar);
+    const int2 a = __ldg(rows + 3 * row), b = __ldg(rows + 3 * row + 1), c = __ldg(rows + 3 * row + 2);
+    mi[0] = a.x; mi[1] = a.y; mi[2] = b.x; mi[3] = b.y; mi[4] = c.x; mi[5] = c.y;
+    const T2 p0 = __ldg(gpar + 2 * a.x), p1 = __ldg(gpar + 2 * a.x + 1);
+    mp[0] = p0.x; mp[1] = p0.y; mp[2] = p1.x; mp[3] = p1.y;
+}
+
+// The lane views of group grp: element (row r) at [32 r] (32-bit indices on 64-bit bases).
+template <class T>
+struct LaneViews {
+    const T* ug;
+    T *ung, *xlg, *lmg, *xg;
+    const T* V;                                        // per-scenario pool of the group
+    __device__ __forceinline__ LaneViews(const BatchProblem& B, const T* ucur, T* unext, const int grp, const int lane) {
+        const size_t gb = (size_t)grp * B.n_rows;
+        ug = ucur + gb * 32 + lane;
+        ung = unext + gb * 32 + lane;
+        xlg = reinterpret_cast<T*>(B.xl) + gb * 32 + lane;
+        lmg = reinterpret_cast<T*>(B.lam) + gb * 32 + lane;
+        xg = reinterpret_cast<T*>(B.x) + (size_t)grp * B.n * 32 + lane;
+        V = reinterpret_cast<const T*>(B.vpool) + (size_t)grp * B.ve * 32 + lane;
+    }
+};
+
+// Sweep prologue (every CTA): the active groups of this sweep into s_gl (ascending), their count into
+// s_na; CTA 0 clears the next sweep's flags.
+__device__ __forceinline__ int batch_active_groups(const BatchProblem& B, const long long it, int* s_gl, int* s_na) {
+    const int lane = threadIdx.x & 31, NG = B.n_grp;
+    const uint32_t* gcur = B.gact + (size_t)(it & 1) * NG;
+    if (threadIdx.x < 32) {
+        int run = 0;
+        for (int g0 = 0; g0 < NG; g0 += 32) {
+            const int g = g0 + lane;
+            const bool a = g < NG && __ldcg(gcur + g) != 0u;
+            const unsigned m = __ballot_sync(kFull, a);
+            if (a) s_gl[run + __popc(m & ((1u << lane) - 1u))] = g;
+            run += __popc(m);
+        }
+        if (lane == 0) *s_na = run;
+    }
+    if (blockIdx.x == 0)
+        for (int g = threadIdx.x; g < NG; g += blockDim.x) B.gact[(size_t)((it + 1) & 1) * NG + g] = 0u;
+    __syncthreads();
+    return *s_na;
+}
+
+// Per-scenario (termination), after the sweep's grid barrier: warp gw (of nw) per active
+// group, lane = scenario; the item partials summed in task order (fixed whichever warp ran an item).
+template <class T>
+__device__ __forceinline__ void batch_decide(const BatchProblem& B, const int* s_gl, const int NA, const long long it,
+                                             const long long t, const int gw, const int nw) {
+    const int lane = threadIdx.x & 31, NT = B.n_tasks;
+    uint32_t* gnext = B.gact + (size_t)((it + 1) & 1) * B.n_grp;
+    for (int ag = gw; ag < NA; ag += nw) {
+        const int grp = s_gl[ag], sc = grp * 32 + lane;
+        const bool act = sc < B.n_scen && __ldcg(B.stopped + sc) == 0;
+        double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        const double* pp = B.partial + (size_t)grp * NT * 160 + lane;
+#pragma unroll 8
+        for (int k2 = 0; k2 < NT; ++k2)                          // task order: fixed (loads run 8 tasks ahead)
+#pragma unroll
+            for (int k = 0; k < 5; ++k) s5[k] += __ldcg(pp + (size_t)k2 * 160 + k * 32);
+        const double pres = sqrt(s5[0]), dres = B.rho * sqrt(s5[1]);
+        const double ep = B.eps_rel * fmax(sqrt(s5[2]), sqrt(s5[3])), ed = B.eps_rel * sqrt(s5[4]);
+        const int num = !(isfinite(s5[0]) && isfinite(s5[1]) && isfinite(s5[2]) && isfinite(s5[3]) && isfinite(s5[4]));
+        const int conv = B.test && pres <= ep && dres <= ed;
+        const bool fin = conv || num || it + 1 == B.max_iter;
+        if (act) {
+            ScenResult& R = B.res[sc];
+            R.iters = it + 1;
+            R.total = t + 1;
+            R.res[0] = pres; R.res[1] = dres; R.res[2] = ep; R.res[3] = ed;
+            R.status = conv ? 1 : num ? 3 : (fin ? 2 : 0);
+            if (fin) {
+                double obj = 0.0;
+                const T* xs = reinterpret_cast<const T*>(B.x) + (size_t)grp * B.n * 32 + lane;
+                for (int j = 0; j < B.n_obj; ++j) obj += B.obj_c[j] * (double)__ldcg(xs + (size_t)B.obj_idx[j] * 32);
+                R.objective = obj;
+            }
+            if (conv || num) B.stopped[sc] = 1;
+        }
+        if (__any_sync(kFull, act && !(conv || num)) && lane == 0) gnext[grp] = 1u;
+    }
+}
+
+// ---- the batch kernel -----------------------------------------------------------------------------
+// A (group, task) item is run by a TEAM of kTeamWarps warps that share its rows through SMEM: the team
+// stages the task's row records, splits the consensus rows (four-row groups round robin over its warps;
+// d and v of every row of the task into team SMEM), then splits the mat-vec + finish units (subsystem,
+// row quad) round robin.  An item therefore completes ~kTeamWarps times sooner than with one warp per item
+// and the L2 lines it touches twice (lambda, the u it gathers) are re-read moments later instead of after
+// ~2 L2 turnovers; v no longer round-trips through memory.  At item start one lane issues bulk L2
+// prefetches of the item's contiguous per-scenario inputs (x_s rows, lambda rows, the task's operators).
+// Residual sums: per warp over its units in order, then warp 0 + 1 + ... in order (deterministic whichever
+// team ran the item).
+constexpr int TW = kTeamWarps;
+constexpr int kTeamThreads = 32 * TW;
+
+constexpr bool kVPark = LOPF_BATCH_VPARK;        // v parked in u-next (L2) instead of team SMEM
+// named barriers: 1 + team (the team), 1 + kTeamMax + team (the residual hand-over, when ids remain)
+constexpr bool kRedArrive = 2 * kTeamMax + 1 <= 16;
+
+// rows per team buffer: the task's rows + 4 zero rows (d past the last row)
+__host__ __device__ constexpr int team_rows_alloc(int trmax) { return trmax + 4; }
+__host__ __device__ constexpr int team_smem_bytes(int trmax, int esz) {
+    // D (and Vv) [TRA][32] T, the residual area [TW - 1][5][32] double, mp [TRA][4] T, mi [TRA][6] int
+    return team_rows_alloc(trmax) * ((kVPark ? 1 : 2) * 32 * esz + 4 * esz + 24) + (TW - 1) * 5 * 32 * 8;
+}
+
+__device__ __forceinline__ void team_bar(const int team) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(kTeamThreads) : "memory");
+}
+__device__ __forceinline__ void red_arrive(const int team) {
+    if (kRedArrive) asm volatile("bar.arrive %0, %1;" ::"r"(1 + kTeamMax + team), "r"(kTeamThreads) : "memory");
+    else team_bar(team);
+}
+__device__ __forceinline__ void red_wait(const int team) {
+    if (kRedArrive) asm volatile("bar.sync %0, %1;" ::"r"(1 + kTeamMax + team), "r"(kTeamThreads) : "memory");
+    else team_bar(team);
+}
+__device__ __forceinline__ void prefetch_bulk_l2(const void* p, const unsigned bytes) {
+    if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Bulk L2 prefetch of item (grp, task)'s contiguous per-scenario inputs: `what` bits 1 the task's
+// operators, 2 x_s rows, 4 lambda rows, 8 u rows (the gathers' own rows).
+template <class T>
+__device__ __forceinline__ void team_prefetch(const BatchProblem& B, const T* ucur, const int grp, const int task,
+                                              const int what) {
     const int4 tk = __ldg(reinterpret_cast<const int4*>(B.tasks) + 2 * task);
-    const size_t gb = (size_t)grp * B.n_rows;                        // first row of this group
-    for (int s = tk.x; s < tk.y; ++s) {
-        const int4 sm = __ldg(reinterpret_cast<const int4*>(B.subs) + s);   // {row0, ns, op, flags}
-        if (sm.y <= kBatchDMax) batch_sub<T, false>(B, sm, gb, ucur, unext, W, lane, act, acc, grp);
-        else batch_sub<T, true>(B, sm, gb, ucur, unext, W, lane, act, acc, grp);
-    }
+    const int4 tv = __ldg(reinterpret_cast<const int4*>(B.tasks) + 2 * task + 1);
+    const size_t gb = (size_t)grp * B.n_rows, rb = (size_t)(tk.w - tk.z) * 32 * sizeof(T);
+    if (what & 1)
+        prefetch_bulk_l2(reinterpret_cast<const T*>(B.vpool) + ((size_t)grp * B.ve + tv.x) * 32,
+                         (unsigned)((size_t)(tv.y - tv.x) * 32 * sizeof(T)));
+    if (what & 2) prefetch_bulk_l2(reinterpret_cast<const T*>(B.xl) + (gb + tk.z) * 32, (unsigned)rb);
+    if (what & 4) prefetch_bulk_l2(reinterpret_cast<const T*>(B.lam) + (gb + tk.z) * 32, (unsigned)rb);
+    if (what & 8) prefetch_bulk_l2(ucur + (gb + tk.z) * 32, (unsigned)rb);
 }
 
 template <class T>
-__global__ void __launch_bounds__(BB, 1) admm_batch_kernel(BatchProblem B) {
+__global__ void __launch_bounds__(kTeamThreads * kTeamMax, 1) admm_batch_team_kernel(BatchProblem B) {
     extern __shared__ __align__(16) unsigned char bsm[];
     __shared__ int s_gl[kBatchMaxGrp];                  // active groups of this sweep, ascending
     __shared__ int s_na;
+    __shared__ long long s_item[kTeamMax][2];           // a team's current / next item (claim double buffer)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int gw = blockIdx.x * BW + wid, nw = gridDim.x * BW;
-    WarpSmem<T> W;
+    const int team = wid / TW, wt = wid - team * TW, tid = wt * 32 + lane;
+    const int nwarp = blockDim.x >> 5;
+    const int gw = blockIdx.x * nwarp + wid, nw = gridDim.x * nwarp;
+    const int TRA = team_rows_alloc(B.trmax);
+    T *D, *Vv, *mp;
+    int* mi;
+    double* red;
     {
-        unsigned char* base = bsm + (size_t)wid * warp_smem_bytes<T>();
-        W.d = reinterpret_cast<T*>(base);
-        unsigned char* meta = base + kBatchDMax * 32 * sizeof(T);
-        W.mp = reinterpret_cast<T*>(meta);
-        W.mi = reinterpret_cast<int*>(meta + 32 * 4 * sizeof(T));
+        unsigned char* base = bsm + (size_t)team * team_smem_bytes(B.trmax, (int)sizeof(T));
+        D = reinterpret_cast<T*>(base);
+        Vv = D + (kVPark ? 0 : TRA * 32);
+        red = reinterpret_cast<double*>(Vv + TRA * 32);  // [TW - 1][5][32]
+        mp = reinterpret_cast<T*>(red + (TW - 1) * 5 * 32);
+        mi = reinterpret_cast<int*>(mp + TRA * 4);
     }
+    const unsigned long long pf = pol_first();
     const long long total0 = *(volatile long long*)&B.ctrl->total;
-    const int NT = B.n_tasks, NG = B.n_grp;
+    const int NT = B.n_tasks;
     unsigned long long bars = 0;
     long long it = 0;
     while (it < B.max_iter) {
         const long long t = total0 + it;
         const T* ucur = reinterpret_cast<const T*>((t & 1) ? B.u1 : B.u0);
         T* unext = reinterpret_cast<T*>((t & 1) ? B.u0 : B.u1);
-        const uint32_t* gcur = B.gact + (size_t)(it & 1) * NG;
-        if (wid == 0) {
-            int run = 0;
-            for (int g0 = 0; g0 < NG; g0 += 32) {
-                const int g = g0 + lane;
-                const bool a = g < NG && __ldcg(gcur + g) != 0u;
-                const unsigned m = __ballot_sync(kFull, a);
-                if (a) s_gl[run + __popc(m & ((1u << lane) - 1u))] = g;
-                run += __popc(m);
-            }
-            if (lane == 0) s_na = run;
-        }
-        if (blockIdx.x == 0)
-            for (int g = threadIdx.x; g < NG; g += blockDim.x) B.gact[(size_t)((it + 1) & 1) * NG + g] = 0u;
-        __syncthreads();
-        const int NA = s_na;
+        const int NA = batch_active_groups(B, it, s_gl, &s_na);
         if (NA == 0) break;                             // every scenario has stopped (same view in every CTA)
         const long long NI = (long long)NA * NT;
-        // dynamic hand-out: item i = (task torder[i / NA], active group i % NA), costliest tasks first; lane 0
-        // claims the next item while the warp computes the current one.  The partials land per (group, task),
-        // so the result does not depend on which warp ran an item.
+        // dynamic hand-out as in the warp kernel, per team: item i = (task torder[i / NA], active group
+        // i % NA), costliest tasks first; the leader claims the next item while the team runs the current one
         unsigned long long* ictr = B.cnt + 1 + (it & 1);
-        long long a = 0;
-        if (lane == 0) a = (long long)atomicAdd(ictr, 1ULL);
-        a = __shfl_sync(kFull, a, 0);
+        if (tid == 0) s_item[team][0] = (long long)atomicAdd(ictr, 1ULL);
+        team_bar(team);
+        long long a = s_item[team][0];
+        int par = 0;
         while (a < NI) {
-            long long nxt = 0;
-            if (lane == 0) nxt = (long long)atomicAdd(ictr, 1ULL);
             const long long tq = a / NA;
             const int grp = s_gl[(int)(a - tq * NA)], task = __ldg(B.torder + tq);
+            if (tid == 0) {
+                const long long nx = (long long)atomicAdd(ictr, 1ULL);
+                s_item[team][par ^ 1] = nx;
+                team_prefetch<T>(B, ucur, grp, task, LOPF_BATCH_BPF & 15);
+                if ((LOPF_BATCH_BPF >> 4) && nx < NI) {
+                    const long long nq = nx / NA;
+                    team_prefetch<T>(B, ucur, s_gl[(int)(nx - nq * NA)], __ldg(B.torder + nq), LOPF_BATCH_BPF >> 4);
+                }
+            }
             const int sc = grp * 32 + lane;
             const bool act = sc < B.n_scen && __ldcg(B.stopped + sc) == 0;
+            const LaneViews<T> L(B, ucur, unext, grp, lane);
+            const int4 tk = __ldg(reinterpret_cast<const int4*>(B.tasks) + 2 * task);   // {sub0, sub1, row0, row1}
+            const int R0 = tk.z, nr = tk.w - tk.z;
+            // each warp stages the records of its own consensus rows (row r on warp (r / 4) mod TW), so the
+            // slots a warp writes are only ever read by that warp: no team barrier before the consensus
+            for (int k = lane; ; k += 32) {
+                const int r = 4 * (wt + TW * (k >> 2)) + (k & 3);
+                if (r >= nr + 3) break;
+                if (r < nr) stage_record<T>(B, R0 + r, mi + 6 * r, mp + 4 * r);
+            }
+            if (wt == 0)
+                for (int e = lane; e < 4 * 32; e += 32) D[nr * 32 + e] = T(0);   // d past the last row: 0
+            __syncwarp();
+            // a4: four-row groups round robin over the team's warps; d (and v) of every row into SMEM
+            for (int c = 4 * wt; c < nr; c += 4 * TW)
+                consensus_group<T>(B, mi + 6 * c, mp + 4 * c, min(CR, nr - c), R0 + c, L.ug, L.lmg, L.xg, act, pf,
+                                   [&](const int i, const T v, const T d) {
+                                       D[(c + i) * 32 + lane] = d;
+                                       if (kVPark) {
+                                           if (act) __stcg(L.ung + 32 * (R0 + c + i), v);
+                                       } else {
+                                           Vv[(c + i) * 32 + lane] = v;
+                                       }
+                                   });
+            team_bar(team);
+            // a5-a7: units (subsystem, row quad) of the task in order, unit j on warp j mod TW
             double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            batch_item<T>(B, grp, task, ucur, unext, W, lane, act, acc);
-            double* pp = B.partial + ((size_t)grp * NT + task) * 5 * 32 + lane;
+            int j0 = 0;
+            for (int s = tk.x; s < tk.y; ++s) {
+                const int4 sm = __ldg(reinterpret_cast<const int4*>(B.subs) + s);   // {row0, ns, op, flags}
+                const int nq = (sm.y + 3) >> 2, l0 = sm.x - R0;
+                const bool var = sm.w & kBVar;
+                const T* __restrict__ V = L.V + (var ? 32 * (size_t)sm.z : 0);
+                const T* __restrict__ A = reinterpret_cast<const T*>(B.spool) + (var ? 0 : sm.z);
+                const T* Ds = D + l0 * 32 + lane;
+                const T* Vs = Vv + l0 * 32 + lane;
+                for (int q = (wt - j0 % TW + TW) % TW; q < nq; q += TW) {
+                    T y[4];
+                    matvec_quad<T>(sm, V, A, q, pf, [&](const int k) { return Ds[k * 32]; }, y);
+                    finish_quad<T>(B, sm, V, q, y, L.ung, L.lmg, L.xlg, act, pf,
+                                   [&](const int r) {
+                                       return kVPark ? ld_last(L.ung + 32 * (sm.x + r), pf) : Vs[r * 32];
+                                   },
+                                   acc);
+                }
+                j0 += nq;
+            }
+            team_bar(team);                              // every unit done: D and Vv are free for the next item
+            if (wt > 0) {
 #pragma unroll
-            for (int k = 0; k < 5; ++k) __stcg(pp + k * 32, acc[k]);
-            a = __shfl_sync(kFull, nxt, 0);
+                for (int k = 0; k < 5; ++k) red[((wt - 1) * 5 + k) * 32 + lane] = acc[k];
+                red_arrive(team);
+            } else {
+                red_wait(team);
+                double* pp = B.partial + ((size_t)grp * NT + task) * 5 * 32 + lane;
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    double s = acc[k];
+                    for (int w = 1; w < TW; ++w) s += red[((w - 1) * 5 + k) * 32 + lane];
+                    __stcg(pp + k * 32, s);
+                }
+            }
+            a = s_item[team][par ^ 1];
+            par ^= 1;
         }
         grid_sync(B.cnt, (++bars) * gridDim.x);
         if (blockIdx.x == 0 && threadIdx.x == 0) B.cnt[1 + ((it + 1) & 1)] = 0ULL;   // next sweep's counter (seen
                                                                                     // after the second barrier)
-        // per-scenario (termination): warp per active group, lane = scenario
-        uint32_t* gnext = B.gact + (size_t)((it + 1) & 1) * NG;
-        for (int ag = gw; ag < NA; ag += nw) {
-            const int grp = s_gl[ag], sc = grp * 32 + lane;
-            const bool act = sc < B.n_scen && __ldcg(B.stopped + sc) == 0;
-            double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            const double* pp = B.partial + (size_t)grp * NT * 160 + lane;
-#pragma unroll 8
-            for (int k2 = 0; k2 < NT; ++k2)                      // task order: fixed (loads run 8 tasks ahead)
-#pragma unroll
-                for (int k = 0; k < 5; ++k) s5[k] += __ldcg(pp + (size_t)k2 * 160 + k * 32);
-            const double pres = sqrt(s5[0]), dres = B.rho * sqrt(s5[1]);
-            const double ep = B.eps_rel * fmax(sqrt(s5[2]), sqrt(s5[3])), ed = B.eps_rel * sqrt(s5[4]);
-            const int num = !(isfinite(s5[0]) && isfinite(s5[1]) && isfinite(s5[2]) && isfinite(s5[3]) && isfinite(s5[4]));
-            const int conv = B.test && pres <= ep && dres <= ed;
-            const bool fin = conv || num || it + 1 == B.max_iter;
-            if (act) {
-                ScenResult& R = B.res[sc];
-                R.iters = it + 1;
-                R.total = t + 1;
-                R.res[0] = pres; R.res[1] = dres; R.res[2] = ep; R.res[3] = ed;
-                R.status = conv ? 1 : num ? 3 : (fin ? 2 : 0);
-                if (fin) {
-                    double obj = 0.0;
-                    const T* xs = reinterpret_cast<const T*>(B.x) + (size_t)grp * B.n * 32 + lane;
-                    for (int j = 0; j < B.n_obj; ++j) obj += B.obj_c[j] * (double)__ldcg(xs + (size_t)B.obj_idx[j] * 32);
-                    R.objective = obj;
-                }
-                if (conv || num) B.stopped[sc] = 1;
-            }
-            if (__any_sync(kFull, act && !(conv || num)) && lane == 0) gnext[grp] = 1u;
-        }
+        batch_decide<T>(B, s_gl, NA, it, t, gw, nw);
         grid_sync(B.cnt, (++bars) * gridDim.x);
         ++it;
     }
@@ -506,26 +621,27 @@ __global__ void gather_scen_kernel(BatchProblem B, int32_t scen) {
 }
 
 const void* batch_kernel_for(int esz) {
-    return esz == 4 ? (const void*)admm_batch_kernel<float> : (const void*)admm_batch_kernel<double>;
+    return esz == 4 ? (const void*)admm_batch_team_kernel<float> : (const void*)admm_batch_team_kernel<double>;
 }
 
 }  // namespace
 
-int batch_block() { return BB; }
-
-int batch_smem(int ns_max, int esz) {
-    (void)ns_max;
-    return BW * (esz == 4 ? warp_smem_bytes<float>() : warp_smem_bytes<double>());
+static int batch_teams(int trmax, int esz) {
+    const int per = team_smem_bytes(trmax, esz);
+    return std::max(1, std::min(kTeamMax, kSmemBudget / per));
 }
+int batch_block(int trmax, int esz) { return kTeamThreads * batch_teams(trmax, esz); }
+int batch_smem(int trmax, int esz) { return batch_teams(trmax, esz) * team_smem_bytes(trmax, esz); }
 
-lopf_status query_batch_grid(int ns_max, int esz, int* grid, std::string& err) {
+lopf_status query_batch_grid(int trmax, int esz, int* grid, std::string& err) {
     int dev = 0, sms = 0, per = 0;
     const void* k = batch_kernel_for(esz);
-    const int smem = batch_smem(ns_max, esz);
+    const int smem = batch_smem(trmax, esz);
+    if (smem > kSmemBudget) { err = "batch kernel: the largest task needs more shared memory than a CTA has"; return LOPF_E_ARG; }
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, BB, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, batch_block(trmax, esz), smem);
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     if (per < 1) { err = "batch kernel cannot be resident (occupancy 0)"; return LOPF_E_CUDA; }
     *grid = sms * per;
@@ -535,7 +651,7 @@ lopf_status query_batch_grid(int ns_max, int esz, int* grid, std::string& err) {
 lopf_status launch_batch(const BatchProblem& B, int grid, void* stream, std::string& err) {
     cudaStream_t s = (cudaStream_t)stream;
     const void* k = batch_kernel_for(B.esz);
-    const int smem = batch_smem(B.ns_max, B.esz);
+    const int smem = batch_smem(B.trmax, B.esz);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) e = cudaMemsetAsync(B.cnt, 0, 3 * sizeof(unsigned long long), s);
     if (e == cudaSuccess) {
@@ -545,7 +661,7 @@ lopf_status launch_batch(const BatchProblem& B, int grid, void* stream, std::str
     if (e == cudaSuccess && B.max_iter > 0) {
         BatchProblem C = B;
         void* args[] = {&C};
-        e = cudaLaunchCooperativeKernel(k, dim3(grid), dim3(BB), args, smem, s);
+        e = cudaLaunchCooperativeKernel(k, dim3(grid), dim3(batch_block(B.trmax, B.esz)), args, smem, s);
     }
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     return LOPF_OK;

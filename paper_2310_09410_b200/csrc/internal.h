@@ -267,7 +267,6 @@ struct BatchProblem {
     void *xl, *lam, *u0, *u1;                  // (T) [group][n_rows][32]
     void* x;                                   // (T) [group][n][32]
     double* partial;                           // [group][n_tasks][5][32] residual sums per item
-    void* dscr;                                // (T) [group][n_rows][32] d of subsystems with n_s > kBatchDMax
     ScenResult* res;                           // [n_scen]
     int32_t* stopped;                          // [n_scen] converged / non-finite: frozen
     uint32_t* gact;                            // [2][n_grp] group has an active scenario, by sweep parity
@@ -280,20 +279,12 @@ struct BatchProblem {
     double* stage;                             // gather staging for the per-scenario getters
     double rho, inv_rho, eps_rel;
     long long max_iter;
-    int32_t test, pad;
+    int32_t test, trmax;                       // trmax: rows of the largest task
 };
 constexpr int kBatchMaxScen = 8192;            // scenarios per batch handle
 constexpr int kBatchMaxGrp = kBatchMaxScen / 32;
-#ifndef LOPF_BATCH_WARPS
-#define LOPF_BATCH_WARPS 24
-#endif
-constexpr int kBatchWarps = LOPF_BATCH_WARPS;  // warps per CTA of the batch kernel
-#ifndef LOPF_BATCH_DMAX
-#define LOPF_BATCH_DMAX 24
-#endif
-constexpr int kBatchDMax = LOPF_BATCH_DMAX;    // subsystems with more rows stage d in the global scratch
 #ifndef LOPF_BATCH_TASK_ROWS
-#define LOPF_BATCH_TASK_ROWS 32
+#define LOPF_BATCH_TASK_ROWS 48
 #endif
 constexpr int kBatchTaskRows = LOPF_BATCH_TASK_ROWS;   // rows per task (target; whole subsystems)
 
@@ -324,8 +315,9 @@ struct Layout {
     std::vector<int32_t> tsub_ptr, tsub_s, tsub_poff;
     // batch kernel (config 4, lane = scenario)
     int32_t n_scen = 0, n_grp = 0, ns_max = 0, n_rows = 0, n_bsub = 0, ve = 0;
+    int32_t task_rows_max = 0;             // rows of the largest task (team kernel SMEM)
     size_t off_brow = 0, off_bsub = 0, off_btask = 0, off_bseg = 0, off_bspool = 0, off_bvpool = 0, off_bpart = 0,
-           off_bres = 0, off_bstop = 0, off_bgact = 0, off_bcnt = 0, off_bwpre = 0, off_bstage = 0, off_bdscr = 0,
+           off_bres = 0, off_bstop = 0, off_bgact = 0, off_bcnt = 0, off_bwpre = 0, off_bstage = 0,
            off_btorder = 0;
     size_t image_bytes = 0;                // bytes of `image` uploaded by bind (0: the whole arena); the rest is
                                            // device state initialised by the reset kernels
@@ -396,9 +388,9 @@ lopf_status launch_reset_resident(const ResProblem& P, void* stream, std::string
 lopf_status launch_gather_resident(const ResProblem& P, void* stage, void* stream, std::string& err);
 lopf_status resident_capacity(int* sms, int* smem_optin, std::string& err);
 // batch.cu
-int batch_block();
-int batch_smem(int ns_max, int esz);
-lopf_status query_batch_grid(int ns_max, int esz, int* grid, std::string& err);
+int batch_block(int trmax, int esz);
+int batch_smem(int trmax, int esz);
+lopf_status query_batch_grid(int trmax, int esz, int* grid, std::string& err);
 lopf_status launch_batch(const BatchProblem& B, int grid, void* stream, std::string& err);
 lopf_status launch_reset_batch(const BatchProblem& B, void* stream, std::string& err);
 lopf_status launch_gather_scen(const BatchProblem& B, int32_t scen, void* stream, std::string& err);

@@ -110,6 +110,8 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
         wpre.push_back(wpre.back() + w);
     }
     const int64_t NT = (int64_t)tasks.size();
+    int32_t trmax = 1;
+    for (const BTask& t : tasks) trmax = std::max(trmax, t.row1 - t.row0);
     std::vector<int32_t> torder(NT);
     for (int64_t t = 0; t < NT; ++t) torder[t] = (int32_t)t;
     std::stable_sort(torder.begin(), torder.end(),
@@ -123,6 +125,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     L.n_scen = NSC;
     L.n_grp = NG;
     L.ns_max = ns_max;
+    L.task_rows_max = trmax;
     L.n_rows = nr;
     L.n_bsub = (int32_t)subs.size();
     L.ve = (int32_t)ve;
@@ -157,9 +160,6 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     L.off_u1 = take(per);
     L.off_x = take(E * (size_t)NG * P.n * 32);
     L.off_bpart = take(8 * 160 * (size_t)NG * NT);
-    bool big = false;
-    for (int64_t s = 0; s < P.S; ++s) big |= P.n_s[s] > kBatchDMax;
-    L.off_bdscr = take(big ? per : 0);
     L.off_bres = take(sizeof(ScenResult) * (size_t)NSC);
     L.off_bstop = take(4 * (size_t)NSC);
     L.off_bgact = take(4 * 2 * (size_t)NG);

@@ -147,6 +147,27 @@ def test_kernel_selection():
         Lopf.setup(fg.make_feeder("8500"), kernel=2, max_ctas=16)        # does not fit 16 CTAs
 
 
+def test_batch_byte_model():
+    """Batch alg_bytes: the operators of subsystems without a load, lo / hi (2 n) and c are
+    shared by every scenario and counted once; per scenario its load subsystems' packed A-bar and b-bar,
+    the 6 N_c iterate terms and x (write + read, 2 n)."""
+    f = fg.make_feeder("123")
+    n_scen = 64
+    p = oracle.build_problem(f)
+    s1 = Lopf.setup(f).sizes
+    sb = Lopf.setup_batch(f, fg.scenario_scales(f, n_scen)).sizes
+    ns = p.dec.n_s()
+    has_load = [bool(np.any(p.dec.b[i] != 0)) for i in range(p.dec.S)]
+    psym_var = int(sum(n * (n + 1) // 2 for n, v in zip(ns, has_load) if v))
+    nb = int(sum(n for n, v in zip(ns, has_load) if v))
+    psym = int((ns * (ns + 1) // 2).sum())
+    nobj = int((p.lp.c != 0).sum())
+    per_scen = psym_var + nb + 6 * p.dec.n_copies + 2 * p.lp.n
+    shared = (psym - psym_var) + 2 * p.lp.n + nobj
+    assert sb.alg_bytes == 8 * (shared + n_scen * per_scen) + 4 * (2 * p.dec.n_copies + p.lp.n + 1)
+    assert sb.alg_bytes < n_scen * s1.alg_bytes
+
+
 def test_precision_option():
     """fp32 variant (reading F1): every kernel has an fp32 layout with half the (T) bytes of the byte model
     and a smaller arena; an unknown precision is LOPF_E_ARG."""

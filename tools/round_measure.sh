@@ -20,7 +20,7 @@ timeout 120 python tools/ncu_resident.py 862 > ${o}_res_plain.log 2>&1 && \
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:admm_resident_kernel --launch-skip 1 -c 1 \
   -o ${o}_res python tools/ncu_resident.py 862 > ${o}_ncu_res.log 2>&1
 timeout 200 python tools/batch_time.py 4096 20 1 > ${o}_batch_plain.log 2>&1 && \
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:admm_batch_kernel -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:admm_batch -c 1 \
   -o ${o}_batch python tools/batch_time.py 4096 20 1 > ${o}_ncu_batch.log 2>&1
 timeout 400 python tools/ncu_stitched.py 50 > ${o}_stitched_plain.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:admm_stream_kernel --launch-skip 1 -c 1 \
