@@ -420,6 +420,8 @@ lopf_status lopf_bind(lopf_handle* h, void* arena, size_t bytes, void* stream) {
         B.cnt = (unsigned long long*)(b + L.off_bcnt);
         B.wpre = (const long long*)(b + L.off_bwpre);
         B.torder = (const int32_t*)(b + L.off_btorder);
+        B.tunit_ptr = (const int32_t*)(b + L.off_btunp);
+        B.tunits = (const int32_t*)(b + L.off_btun);
         B.obj_idx = (const int32_t*)(b + L.off_objidx);
         B.obj_c = (const double*)(b + L.off_objc);
         B.ctrl = (DevCtrl*)(b + L.off_ctrl);

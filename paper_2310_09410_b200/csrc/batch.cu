@@ -37,9 +37,6 @@ using dev::kFull;
 #ifndef LOPF_BATCH_CROWS
 #define LOPF_BATCH_CROWS 4                    // consensus rows whose gathers are issued together
 #endif
-#ifndef LOPF_BATCH_TW
-#define LOPF_BATCH_TW 4                       // warps per team
-#endif
 #ifndef LOPF_BATCH_TEAMS
 #define LOPF_BATCH_TEAMS 6                    // most teams per CTA (fewer when the task rows need more SMEM)
 #endif
@@ -55,7 +52,7 @@ using dev::kFull;
 #endif
 constexpr int CR = LOPF_BATCH_CROWS;
 constexpr int JH = LOPF_BATCH_JH;
-constexpr int kTeamWarps = LOPF_BATCH_TW;
+constexpr int kTeamWarps = kBatchTeamWarps;
 constexpr int kTeamMax = LOPF_BATCH_TEAMS;
 constexpr int kSmemBudget = 232448 - 2048;    // opt-in dynamic SMEM per block minus the static arrays
 
@@ -380,11 +377,12 @@ __device__ __forceinline__ void batch_decide(const BatchProblem& B, const int* s
 // ---- the batch kernel -----------------------------------------------------------------------------
 // A (group, task) item is run by a TEAM of kTeamWarps warps that share its rows through SMEM: the team
 // stages the task's row records, splits the consensus rows (four-row groups round robin over its warps;
-// d and v of every row of the task into team SMEM), then splits the mat-vec + finish units (subsystem,
-// row quad) round robin.  An item therefore completes ~kTeamWarps times sooner than with one warp per item
-// and the L2 lines it touches twice (lambda, the u it gathers) are re-read moments later instead of after
-// ~2 L2 turnovers; v no longer round-trips through memory.  At item start one lane issues bulk L2
-// prefetches of the item's contiguous per-scenario inputs (x_s rows, lambda rows, the task's operators).
+// d of every row of the task into team SMEM, v parked in u-next), then splits the mat-vec + finish units (subsystem,
+// row quad) as the packer assigned them (longest first onto the least-loaded warp).  An item therefore
+// completes ~kTeamWarps times sooner than with one warp per item, and the L2 lines it touches twice
+// (lambda, the parked v, the u it gathers) are re-read moments later instead of after ~2 L2 turnovers.
+// When the item is claimed one lane issues bulk L2 prefetches of its contiguous per-scenario inputs (the
+// task's operators, x_s, lambda and u rows).
 // Residual sums: per warp over its units in order, then warp 0 + 1 + ... in order (deterministic whichever
 // team ran the item).
 constexpr int TW = kTeamWarps;
@@ -512,27 +510,25 @@ __global__ void __launch_bounds__(kTeamThreads * kTeamMax, 1) admm_batch_team_ke
                                        }
                                    });
             team_bar(team);
-            // a5-a7: units (subsystem, row quad) of the task in order, unit j on warp j mod TW
+            // a5-a7: the units (subsystem, row quad) the packer gave this warp (cost-balanced), ascending
             double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            int j0 = 0;
-            for (int s = tk.x; s < tk.y; ++s) {
-                const int4 sm = __ldg(reinterpret_cast<const int4*>(B.subs) + s);   // {row0, ns, op, flags}
-                const int nq = (sm.y + 3) >> 2, l0 = sm.x - R0;
+            const int u1 = __ldg(B.tunit_ptr + task * TW + wt + 1);
+            for (int u = __ldg(B.tunit_ptr + task * TW + wt); u < u1; ++u) {
+                const int code = __ldg(B.tunits + u), q = code & 0xFF;
+                const int4 sm = __ldg(reinterpret_cast<const int4*>(B.subs) + tk.x + (code >> 8));   // {row0, ns, op, flags}
+                const int l0 = sm.x - R0;
                 const bool var = sm.w & kBVar;
                 const T* __restrict__ V = L.V + (var ? 32 * (size_t)sm.z : 0);
                 const T* __restrict__ A = reinterpret_cast<const T*>(B.spool) + (var ? 0 : sm.z);
                 const T* Ds = D + l0 * 32 + lane;
                 const T* Vs = Vv + l0 * 32 + lane;
-                for (int q = (wt - j0 % TW + TW) % TW; q < nq; q += TW) {
-                    T y[4];
-                    matvec_quad<T>(sm, V, A, q, pf, [&](const int k) { return Ds[k * 32]; }, y);
-                    finish_quad<T>(B, sm, V, q, y, L.ung, L.lmg, L.xlg, act, pf,
-                                   [&](const int r) {
-                                       return kVPark ? ld_last(L.ung + 32 * (sm.x + r), pf) : Vs[r * 32];
-                                   },
-                                   acc);
-                }
-                j0 += nq;
+                T y[4];
+                matvec_quad<T>(sm, V, A, q, pf, [&](const int k) { return Ds[k * 32]; }, y);
+                finish_quad<T>(B, sm, V, q, y, L.ung, L.lmg, L.xlg, act, pf,
+                               [&](const int r) {
+                                   return kVPark ? ld_last(L.ung + 32 * (sm.x + r), pf) : Vs[r * 32];
+                               },
+                               acc);
             }
             team_bar(team);                              // every unit done: D and Vv are free for the next item
             if (wt > 0) {

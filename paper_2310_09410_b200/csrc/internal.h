@@ -273,6 +273,8 @@ struct BatchProblem {
     unsigned long long* cnt;                   // barrier arrivals
     const long long* wpre;                     // [n_tasks + 1] prefix of the per-task cost weights (work split)
     const int32_t* torder;                     // [n_tasks] tasks by decreasing cost weight (dynamic hand-out order)
+    const int32_t* tunit_ptr;                  // [n_tasks * kBatchTeamWarps + 1] each (task, team warp)'s units
+    const int32_t* tunits;                     // unit = (subsystem - task.sub0) << 8 | row quad, per warp ascending
     const int32_t* obj_idx;
     const double* obj_c;
     DevCtrl* ctrl;
@@ -287,6 +289,13 @@ constexpr int kBatchMaxGrp = kBatchMaxScen / 32;
 #define LOPF_BATCH_TASK_ROWS 48
 #endif
 constexpr int kBatchTaskRows = LOPF_BATCH_TASK_ROWS;   // rows per task (target; whole subsystems)
+#ifndef LOPF_BATCH_TW
+#define LOPF_BATCH_TW 4
+#endif
+constexpr int kBatchTeamWarps = LOPF_BATCH_TW;          // warps per team of the batch kernel
+#ifndef LOPF_BATCH_LPT
+#define LOPF_BATCH_LPT 1                               // units to team warps: 1 cost-balanced (LPT), 0 round robin
+#endif
 
 // Arena layout: byte offsets of every array (all 256-byte aligned).
 struct Layout {
@@ -318,7 +327,7 @@ struct Layout {
     int32_t task_rows_max = 0;             // rows of the largest task (team kernel SMEM)
     size_t off_brow = 0, off_bsub = 0, off_btask = 0, off_bseg = 0, off_bspool = 0, off_bvpool = 0, off_bpart = 0,
            off_bres = 0, off_bstop = 0, off_bgact = 0, off_bcnt = 0, off_bwpre = 0, off_bstage = 0,
-           off_btorder = 0;
+           off_btorder = 0, off_btunp = 0, off_btun = 0;
     size_t image_bytes = 0;                // bytes of `image` uploaded by bind (0: the whole arena); the rest is
                                            // device state initialised by the reset kernels
     size_t off_fetch = 0;                  // staging of lopf_fetch_async (result record + x as fp64), after the image

@@ -117,6 +117,37 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     std::stable_sort(torder.begin(), torder.end(),
                      [&](int32_t a, int32_t b) { return wpre[a + 1] - wpre[a] > wpre[b + 1] - wpre[b]; });
 
+    // unit (subsystem, row quad) -> team warp: longest processing time first on a cost model of the loads
+    // a unit issues (a per-scenario operator row quad reads nq 4 x 4 blocks of coalesced lines, a shared one
+    // nq 4 x 4 uniform loads) plus its finish; each warp then runs its units in ascending order
+    const int TW = kBatchTeamWarps;
+    std::vector<int32_t> tunp(1, 0), tun;
+    for (const BTask& t : tasks) {
+        std::vector<std::pair<long long, int32_t>> units;             // (cost, code)
+        for (int32_t s = t.sub0; s < t.sub1; ++s) {
+            const int nq = (subs[s].ns + 3) / 4;
+            const long long c = ((subs[s].flags & kBVar) ? 16LL : 4LL) * nq + 12;
+            for (int q = 0; q < nq; ++q) units.push_back({c, ((s - t.sub0) << 8) | q});
+        }
+        std::vector<std::vector<int32_t>> per(TW);
+        std::vector<long long> load(TW, 0);
+        std::vector<size_t> ord(units.size());
+        for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+        if (LOPF_BATCH_LPT)
+            std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return units[a].first > units[b].first; });
+        for (size_t k = 0; k < ord.size(); ++k) {
+            int w = (int)(k % TW);                                     // round robin (LOPF_BATCH_LPT = 0)
+            if (LOPF_BATCH_LPT) w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+            per[w].push_back(units[ord[k]].second);
+            load[w] += units[ord[k]].first;
+        }
+        for (int w = 0; w < TW; ++w) {
+            std::sort(per[w].begin(), per[w].end());
+            tun.insert(tun.end(), per[w].begin(), per[w].end());
+            tunp.push_back((int32_t)tun.size());
+        }
+    }
+
     // ---- arena -----------------------------------------------------------------------------------
     std::vector<int32_t> obj_idx;
     std::vector<double> obj_c;
@@ -148,6 +179,8 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     L.off_x0 = take(E * (size_t)nr);
     L.off_bwpre = take(8 * (size_t)(NT + 1));
     L.off_btorder = take(4 * (size_t)NT);
+    L.off_btunp = take(4 * tunp.size());
+    L.off_btun = take(4 * tun.size());
     L.off_objidx = take(4 * obj_idx.size());
     L.off_objc = take(8 * obj_c.size());
     L.off_bvpool = take(E * (size_t)NG * ve * 32);
@@ -189,6 +222,8 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     for (int64_t k = 0; k < P.nc; ++k) put(img + L.off_x0, row_of_copy[k], P.x0[k]);
     std::memcpy(img + L.off_bwpre, wpre.data(), 8 * wpre.size());
     std::memcpy(img + L.off_btorder, torder.data(), 4 * torder.size());
+    std::memcpy(img + L.off_btunp, tunp.data(), 4 * tunp.size());
+    std::memcpy(img + L.off_btun, tun.data(), 4 * tun.size());
     std::memcpy(img + L.off_objidx, obj_idx.data(), 4 * obj_idx.size());
     std::memcpy(img + L.off_objc, obj_c.data(), 8 * obj_c.size());
     // per-scenario operators: [group][entry][lane]; padding lanes of the last group stay zero
