@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(kTeamThreads * kTeamMax, 1) admm_batch_team_ke
                 for (int e = lane; e < 4 * 32; e += 32) D[nr * 32 + e] = T(0);   // d past the last row: 0
             __syncwarp();
             // a4: four-row groups round robin over the team's warps; d (and v) of every row into SMEM
-            for (int c = 4 * wt; c < nr; c += 4 * TW)
+            for (int c = 4 * wt; c < nr; c += 4 * TW) {
                 consensus_group<T>(B, mi + 6 * c, mp + 4 * c, min(CR, nr - c), R0 + c, L.ug, L.lmg, L.xg, act, pf,
                                    [&](const int i, const T v, const T d) {
                                        D[(c + i) * 32 + lane] = d;
@@ -509,6 +509,7 @@ __global__ void __launch_bounds__(kTeamThreads * kTeamMax, 1) admm_batch_team_ke
                                            Vv[(c + i) * 32 + lane] = v;
                                        }
                                    });
+            }
             team_bar(team);
             // a5-a7: the units (subsystem, row quad) the packer gave this warp (cost-balanced), ascending
             double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -629,6 +630,10 @@ static int batch_teams(int trmax, int esz) {
 int batch_block(int trmax, int esz) { return kTeamThreads * batch_teams(trmax, esz); }
 int batch_smem(int trmax, int esz) { return batch_teams(trmax, esz) * team_smem_bytes(trmax, esz); }
 
+static cudaError_t set_smem_attrs(const void* k, int smem) {
+    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
 lopf_status query_batch_grid(int trmax, int esz, int* grid, std::string& err) {
     int dev = 0, sms = 0, per = 0;
     const void* k = batch_kernel_for(esz);
@@ -636,7 +641,7 @@ lopf_status query_batch_grid(int trmax, int esz, int* grid, std::string& err) {
     if (smem > kSmemBudget) { err = "batch kernel: the largest task needs more shared memory than a CTA has"; return LOPF_E_ARG; }
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = set_smem_attrs(k, smem);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, batch_block(trmax, esz), smem);
     if (e != cudaSuccess) { err = std::string("CUDA: ") + cudaGetErrorString(e); return LOPF_E_CUDA; }
     if (per < 1) { err = "batch kernel cannot be resident (occupancy 0)"; return LOPF_E_CUDA; }
@@ -648,7 +653,7 @@ lopf_status launch_batch(const BatchProblem& B, int grid, void* stream, std::str
     cudaStream_t s = (cudaStream_t)stream;
     const void* k = batch_kernel_for(B.esz);
     const int smem = batch_smem(B.trmax, B.esz);
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = set_smem_attrs(k, smem);
     if (e == cudaSuccess) e = cudaMemsetAsync(B.cnt, 0, 3 * sizeof(unsigned long long), s);
     if (e == cudaSuccess) {
         batch_gact_kernel<<<(B.n_grp + 255) / 256, 256, 0, s>>>(B);

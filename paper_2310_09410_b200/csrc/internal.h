@@ -286,9 +286,13 @@ struct BatchProblem {
 constexpr int kBatchMaxScen = 8192;            // scenarios per batch handle
 constexpr int kBatchMaxGrp = kBatchMaxScen / 32;
 #ifndef LOPF_BATCH_TASK_ROWS
-#define LOPF_BATCH_TASK_ROWS 48
+#define LOPF_BATCH_TASK_ROWS 40
 #endif
-constexpr int kBatchTaskRows = LOPF_BATCH_TASK_ROWS;   // rows per task (target; whole subsystems)
+#ifndef LOPF_BATCH_TASK_ROWS32
+#define LOPF_BATCH_TASK_ROWS32 48
+#endif
+constexpr int kBatchTaskRows = LOPF_BATCH_TASK_ROWS;     // rows per task (target; whole subsystems), fp64
+constexpr int kBatchTaskRows32 = LOPF_BATCH_TASK_ROWS32; // the same for the fp32 variant (A/B: 40 / 48 best)
 #ifndef LOPF_BATCH_TW
 #define LOPF_BATCH_TW 4
 #endif

@@ -7,7 +7,7 @@
 // {c/rho, lo, hi, 1/nu} of every global and the dense Abar of every subsystem without a load.  Per
 // scenario: the packed upper triangle and b-bar of every subsystem that holds a load (its A_s depends on
 // the load level through VDLM-1/2), and the iterate.  Tasks are depth-first runs of
-// whole subsystems of about kBatchTaskRows rows; a work item is (group, task).
+// whole subsystems of about kBatchTaskRows (fp32: kBatchTaskRows32) rows; a work item is (group, task).
 #include <algorithm>
 #include <cstring>
 
@@ -87,14 +87,15 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
         r0 += ns;
     }
     if ((int64_t)NG * ve * 32 * E > ((int64_t)1 << 40)) { err = "batch: per-scenario operators too large"; return LOPF_E_ARG; }
-    // tasks: DFS runs of whole subsystems of ~kBatchTaskRows rows; cost weight = consensus rows + the
+    // tasks: DFS runs of whole subsystems of ~trows rows; cost weight = consensus rows + the
     // mat-vec entries (a per-scenario operator entry is a coalesced line, a shared one a uniform load)
     std::vector<BTask> tasks;
+    const int trows = E == 8 ? kBatchTaskRows : kBatchTaskRows32;
     std::vector<long long> wpre(1, 0);
     for (size_t i = 0; i < subs.size();) {
         BTask t{(int32_t)i, (int32_t)i, subs[i].row0, subs[i].row0, -1, -1, {0, 0}};
         long long w = 0;
-        while (i < subs.size() && (t.row1 - t.row0 < kBatchTaskRows || t.sub1 == t.sub0)) {
+        while (i < subs.size() && (t.row1 - t.row0 < trows || t.sub1 == t.sub0)) {
             const long long ns = subs[i].ns;
             w += 16 + 12 * ns + ns * ns * ((subs[i].flags & kBVar) ? 2 : 1);
             t.row1 += subs[i].ns;
