@@ -144,3 +144,31 @@ def test_batch_handle_rejects_single_problem_state_calls(batch):
     with pytest.raises(LopfError) as e:
         h.get_state()
     assert STATUS[e.value.status] == "LOPF_E_STATE"
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_batch_repeat_bit_identical(precision):
+    """Race stress for the team kernel: items are claimed dynamically, so which team and SM
+    run an item changes from launch to launch; the team's SMEM hand-overs (d rows, the residual partials by
+    bar.arrive / bar.sync) and the L2-parked v must still give the same bits.  512 scenarios, 400 sweeps
+    run twice from reset (the second time as 150 + 250 across launches): every scenario's outcome,
+    residuals and objective, and the iterate of sampled scenarios, are bit-identical."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2310_09410_b200 import Lopf
+    f = fg.make_feeder("123")
+    K = fg.scenario_scales(f, 512, seed=77)
+    h = Lopf.setup_batch(f, K, eps_rel=1e-2, precision=precision).bind("cuda")
+    h.run(400, test=True)
+    r1 = h.get_batch_results()
+    s1 = {sc: h.get_state_scen(sc) for sc in (0, 100, 511)}
+    h.reset()
+    h.run(150, test=True)
+    h.run(250, test=True)
+    r2 = h.get_batch_results()
+    for key in ("outcome", "res", "objective"):
+        assert np.array_equal(r1[key], r2[key]), key
+    for sc, st in s1.items():
+        for a, b in zip(h.get_state_scen(sc), st):
+            assert np.array_equal(a, b), sc
