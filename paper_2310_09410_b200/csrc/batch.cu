@@ -34,9 +34,6 @@ namespace {
 using dev::grid_sync;
 using dev::kFull;
 
-#ifndef LOPF_BATCH_CROWS
-#define LOPF_BATCH_CROWS 4                    // consensus rows whose gathers are issued together
-#endif
 #ifndef LOPF_BATCH_TEAMS
 #define LOPF_BATCH_TEAMS 6                    // most teams per CTA (fewer when the task rows need more SMEM)
 #endif
@@ -50,7 +47,9 @@ using dev::kFull;
 #ifndef LOPF_BATCH_JH
 #define LOPF_BATCH_JH 4                       // operator columns per load batch of the per-scenario mat-vec (4 or 2)
 #endif
-constexpr int CR = LOPF_BATCH_CROWS;
+constexpr int CR = 4;                         // consensus rows per group (gathers issued together); the team
+                                              // splits a task's rows in groups of exactly CR
+static_assert(CR == 4, "the team kernel stages and splits rows in four-row groups");
 constexpr int JH = LOPF_BATCH_JH;
 constexpr int kTeamWarps = kBatchTeamWarps;
 constexpr int kTeamMax = LOPF_BATCH_TEAMS;
@@ -499,7 +498,7 @@ __global__ void __launch_bounds__(kTeamThreads * kTeamMax, 1) admm_batch_team_ke
                 for (int e = lane; e < 4 * 32; e += 32) D[nr * 32 + e] = T(0);   // d past the last row: 0
             __syncwarp();
             // a4: four-row groups round robin over the team's warps; d (and v) of every row into SMEM
-            for (int c = 4 * wt; c < nr; c += 4 * TW) {
+            for (int c = CR * wt; c < nr; c += CR * TW) {
                 consensus_group<T>(B, mi + 6 * c, mp + 4 * c, min(CR, nr - c), R0 + c, L.ug, L.lmg, L.xg, act, pf,
                                    [&](const int i, const T v, const T d) {
                                        D[(c + i) * 32 + lane] = d;
