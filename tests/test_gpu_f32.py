@@ -134,3 +134,33 @@ def test_f32_batch_fixed_k(torch_cuda):
         tol = _bound(p, 100)
         assert _rel(x, o.x) <= tol and _rel(xl, o.x_loc) <= tol and _rel(lam / 100.0, o.lam / 100.0) <= tol, sc
 
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_f32_residual_trace_fig2(torch_cuda, kernel):
+    """Fig. 2 analogue (the paper's fp32 GPU residual traces track its fp64 CPU
+    ones).  The fp32 GPU trace of (pres, dres, eps_prim, eps_dual) every 50 sweeps over 3000 sweeps of the
+    13-shape stays within the rounding bound of the fp64 oracle's trace: every element of the two
+    trajectories differs by at most _bound(k) * scale (the bound the fixed-K test pins), so a norm over
+    N_c rows differs by at most sqrt(N_c) times that per vector -- pres = ||v - x_s|| by 2 of them, dres =
+    rho ||x_s - x_s_prev|| by 2 rho, eps = eps_rel max(||v||, ||x_s||) by eps_rel."""
+    from paper_2310_09410_b200 import Lopf
+    f, p = _problem("13")
+    K, every, rho, eps_rel = 3000, 50, 100.0, 1e-3
+    h = Lopf.setup(f, precision=32, kernel=kernel, trace_every=every, max_iter=K).bind("cuda")
+    h.solve()
+    tr = h.get_trace()
+    o = oracle.solve(p, max_iter=K, trace_every=every)
+    assert tr.shape[0] == o.trace.shape[0] == K // every
+    scale = max(1.0, float(np.abs(oracle.run_k(p, K).x_loc).max()))
+    root_n = np.sqrt(p.dec.n_copies)
+    worst = 0.0
+    for row, ref in zip(tr, o.trace):
+        t = int(row[0])
+        e = root_n * _bound(p, t) * scale
+        lim = np.array([2 * e, 2 * rho * e, eps_rel * e, eps_rel * rho * e])
+        dev = np.abs(row[1:] - ref)
+        assert np.all(dev <= lim), (t, dev, lim)
+        worst = max(worst, float((dev / np.maximum(np.abs(ref), 1e-300))[:2].max()))
+    # and the traces are close in relative terms over the whole window (the Fig. 2 reading)
+    assert worst <= 0.05, worst
