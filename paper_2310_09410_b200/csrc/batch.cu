@@ -167,7 +167,7 @@ __device__ __forceinline__ void matvec_quad(const int4 sm, const T* __restrict__
     const bool var = sm.w & kBVar;
 #pragma unroll
     for (int i = 0; i < 4; ++i) y[i] = T(0);
-    if (var && !LOPF_BATCH_VQB) {
+    if (var && !batch_vqb((int)sizeof(T))) {
         // packed upper triangle, row-major: (i, j >= i) at i n - i (i - 1) / 2 + j - i; row r reads
         // (min(r, k), max(r, k)): the walk steps by n - k - 1 while k < r, then by 1
         int p[4], rq[4];
@@ -259,7 +259,7 @@ __device__ __forceinline__ void finish_quad(const BatchProblem& B, const int4 sm
         vv[i] = vof(rr[i]);
         lam[i] = ld_last(lmg + at, pf);
         xo[i] = ld_last(xlg + at, pf);
-        bb[i] = (sm.w & kBBbar) ? ld_op(V + 32 * (batch_var_entries(ns) + rr[i]), pf) : T(0);
+        bb[i] = (sm.w & kBBbar) ? ld_op(V + 32 * (batch_var_entries(ns, batch_vqb((int)sizeof(T))) + rr[i]), pf) : T(0);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {

@@ -23,6 +23,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
     L.kernel = 3;
     const int64_t E = opt.precision == 32 ? 4 : 8;            // (T) element size (fp32 variant: reading F1)
     L.esz = (int32_t)E;
+    const bool vqb = batch_vqb((int)E);                        // per-scenario operator layout (internal.h)
     int ns_max = 1;
     for (int64_t s = 0; s < P.S; ++s) ns_max = std::max(ns_max, P.n_s[s]);
     if (ns_max > 255) { err = "batch mode supports n_s <= 255"; return LOPF_E_ARG; }
@@ -69,7 +70,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
             b.flags = kBVar | kBBbar;
             b.op = (int32_t)ve;
             var_op[s] = ve;
-            ve += batch_var_entries(ns) + ns;
+            ve += batch_var_entries(ns, vqb) + ns;
         } else {
             if (has_b[s]) { err = "batch mode: a subsystem without a load has a nonzero b-bar"; return LOPF_E_ARG; }
             // row quads, each [k][4] over the padded width (zero rows and columns past n_s): the four rows'
@@ -100,7 +101,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
             w += 16 + 12 * ns + ns * ns * ((subs[i].flags & kBVar) ? 2 : 1);
             t.row1 += subs[i].ns;
             if (subs[i].flags & kBVar) {                           // var entries are assigned in DFS order
-                const int32_t e1 = subs[i].op + (int32_t)(batch_var_entries((int)ns) + ns);
+                const int32_t e1 = subs[i].op + (int32_t)(batch_var_entries((int)ns, vqb) + ns);
                 if (t.vop0 < 0) t.vop0 = subs[i].op;
                 t.vop1 = e1;
             }
@@ -241,7 +242,7 @@ lopf_status pack_batch(const Net& N, const Canon& P, const BatchOps& bo, const l
             // 4q..4q+3 (zero past n_s); then b-bar
             const int nq = (ns + 3) / 4, nsp = 4 * nq;
             int64_t e = 0;
-            if (!LOPF_BATCH_VQB)
+            if (!vqb)
                 for (int i = 0; i < ns; ++i)
                     for (int j = i; j < ns; ++j, ++e) put(vp, base + 32 * (size_t)e, A[(size_t)i * ns + j]);
             else
