@@ -116,8 +116,9 @@ typedef struct {
 typedef struct {
     int64_t S, n, m, n_copies, p_sym, n_tasks, n_slots, device_bytes;
     int64_t abar_doubles;  /* entries (fp64 or fp32, see precision) of the packed operator pool */
-    int64_t alg_bytes;     /* algorithmic bytes per iteration (DESIGN.md §5 byte model) */
-    int32_t kernel;        /* kernel actually selected (1 streaming, 2 resident) */
+    int64_t alg_bytes;     /* algorithmic bytes per iteration (DESIGN.md §4.6 byte model; a batch handle: per
+                              batch sweep, what the scenarios share counted once) */
+    int32_t kernel;        /* kernel actually selected (1 streaming, 2 resident, 3 batch) */
     int32_t grid;          /* CTAs of the persistent launch (known after bind) */
     int32_t block;         /* threads per CTA */
     int32_t max_ns, max_ms;
